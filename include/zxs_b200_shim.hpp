@@ -1,0 +1,89 @@
+// zxs_b200_shim.hpp — reference-side adapter: zxsim::CompiledSampler -> C ABI.
+//
+// Include this from code that already links the reference front-end
+// (proj/include/zxsim/*.hpp). It keeps the reference's signatures so callers
+// such as tools/zxsim.cpp:149-163 switch by namespace only:
+//
+//   zxsim::sample_detectors(cs, shots, opt)      (sampler.hpp:57-58)
+//     -> zxsim_b200::sample_detectors(cs, shots, opt)
+//
+// and re-raises C-ABI status codes as the reference's exception classes
+// (std::invalid_argument / std::runtime_error). There is no CPU
+// fallback: without a GPU the call throws.
+#pragma once
+
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <tuple>
+
+#include "zxs_b200.h"
+#include "zxs_b200_flatten.hpp"
+#include "zxs_flat.hpp"
+#include "zxsim/compile.hpp"
+#include "zxsim/sampler.hpp"
+
+namespace zxsim_b200 {
+
+inline void raise_status(zxs_status st) {
+    if (st == ZXS_OK) return;
+    std::string msg = zxs_last_error();
+    if (st == ZXS_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+}
+
+// RAII handle over one uploaded sampler.
+class Sampler {
+  public:
+    Sampler(const zxsim::CompiledSampler &cs, int device = 0) {
+        zxs::FlatModel flat = flatten(cs);
+        zxs_model_desc d = flat.desc();
+        raise_status(zxs_sampler_create(&d, device, &s_));
+    }
+    explicit Sampler(const zxs::FlatModel &flat, int device = 0) {
+        zxs_model_desc d = flat.desc();
+        raise_status(zxs_sampler_create(&d, device, &s_));
+    }
+    ~Sampler() { zxs_sampler_destroy(s_); }
+    Sampler(const Sampler &) = delete;
+    Sampler &operator=(const Sampler &) = delete;
+    zxs_sampler *get() const { return s_; }
+
+    zxsim::SampleRecord sample(zxs_mode mode, size_t shots, uint64_t seed) const {
+        zxs_sampler_info info;
+        raise_status(zxs_sampler_get_info(s_, &info));
+        zxsim::SampleRecord rec;
+        rec.shots = shots;
+        rec.width = info.num_outputs;
+        size_t words = (shots + 63) / 64;
+        std::vector<uint64_t> flat(static_cast<size_t>(info.num_outputs) * words);
+        raise_status(zxs_sample(s_, mode, seed, 0, shots, flat.data(), nullptr));
+        rec.columns.assign(info.num_outputs, std::vector<uint64_t>(words));
+        for (uint32_t o = 0; o < info.num_outputs; o++) {
+            std::memcpy(rec.columns[o].data(), flat.data() + o * words, words * 8);
+        }
+        return rec;
+    }
+
+  private:
+    zxs_sampler *s_ = nullptr;
+};
+
+// Drop-in replacements for sampler.hpp:57-60. `opt.batch_size`, `threads`,
+// `sparse_threshold` and `force_dense` are accepted and ignored: the device
+// always runs the dense path over the whole shot range, whose bits equal the
+// reference's dense path for any batch split (sampler.cpp:82, 91, 268-284).
+inline zxsim::SampleRecord sample_detectors(const zxsim::CompiledSampler &cs, size_t shots,
+                                            const zxsim::SamplerOptions &opt) {
+    Sampler s(cs);
+    return s.sample(ZXS_MODE_DETECTORS, shots, opt.seed);
+}
+
+inline zxsim::SampleRecord sample_measurements(const zxsim::CompiledSampler &cs, size_t shots,
+                                               const zxsim::SamplerOptions &opt) {
+    Sampler s(cs);
+    return s.sample(ZXS_MODE_MEASUREMENTS, shots, opt.seed);
+}
+
+}  // namespace zxsim_b200

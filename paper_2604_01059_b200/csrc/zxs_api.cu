@@ -1,0 +1,888 @@
+// zxs_api.cu — C-ABI implementation (include/zxs_b200.h): model upload and
+// kernel launches. Host-side preprocessing turns the reference's
+// floating-point draw rules into exact integer thresholds:
+//
+//   single mechanism  fire iff u < p              (sampler.cpp:272)
+//   joint mechanism   first o with u < sum_{j<=o} table[j], else 0
+//                                                  (sampler.cpp:283-293)
+//
+// with u = k * 2^-53 and k = r01 >> 11 (rng.hpp:35-37). Since scaling by a
+// power of two is exact, u < x  <=>  k < ceil(x * 2^53) =: T(x), and
+// k < T  <=>  r01 <= T * 2^11 - 1 =: lim. The cumulative sums are formed
+// with the same sequential double additions as the reference, so the integer
+// compare on the device reproduces every draw bit for bit. Outcomes that can
+// never be first (T not above the running maximum) are dropped, as are
+// mechanisms that cannot change f; their Philox streams are keyed by the
+// reference's mechanism index, so dropping them changes no other draw.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "zxs_b200.h"
+#include "zxs_kernels.cuh"
+
+using zxs_dev::DevModel;
+using zxs_dev::Factor;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct ZxsError {
+    zxs_status status;
+    std::string msg;
+};
+
+[[noreturn]] void fail(zxs_status st, const std::string &msg) { throw ZxsError{st, msg}; }
+
+void cuda_check(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) {
+        zxs_status st = e == cudaErrorMemoryAllocation ? ZXS_OUT_OF_MEMORY : ZXS_CUDA_ERROR;
+        fail(st, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+#define CK(x) cuda_check((x), #x)
+
+template <typename F>
+zxs_status guarded(F &&f) {
+    try {
+        f();
+        return ZXS_OK;
+    } catch (const ZxsError &e) {
+        g_last_error = e.msg;
+        return e.status;
+    } catch (const std::bad_alloc &) {
+        g_last_error = "host allocation failed";
+        return ZXS_OUT_OF_MEMORY;
+    } catch (const std::exception &e) {
+        g_last_error = e.what();
+        return ZXS_RUNTIME_ERROR;
+    }
+}
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        CK(cudaGetDevice(&prev));
+        if (prev != dev) CK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+uint64_t threshold_of(double x) {
+    if (!(x > 0.0)) return 0;                      // u < x never holds (also NaN)
+    if (x >= 1.0) return uint64_t(1) << 53;        // u < x always holds
+    return static_cast<uint64_t>(std::ceil(std::ldexp(x, 53)));
+}
+
+uint64_t lim_of(uint64_t T) {  // T in [1, 2^53]
+    return (T << 11) - 1;      // T = 2^53 wraps to 2^64 - 1: always fires
+}
+
+struct Arena {
+    std::vector<char> host;
+    template <typename T>
+    size_t add(const T *data, size_t n) {
+        size_t off = (host.size() + 255) & ~size_t(255);
+        host.resize(off + n * sizeof(T));
+        if (n) std::memcpy(host.data() + off, data, n * sizeof(T));
+        return off;
+    }
+    template <typename T>
+    size_t add(const std::vector<T> &v) {
+        return add(v.data(), v.size());
+    }
+};
+
+}  // namespace
+
+struct zxs_sampler {
+    int device = 0;
+    uint32_t mode = 0;
+    int fw_template = 1;
+    DevModel m{};
+    zxs_sampler_info info{};
+    bool all_outputs_covered = true;
+    uint32_t num_tensors = 0;
+    std::vector<uint32_t> tensor_width;
+    std::vector<uint32_t> comp_out_begin, comp_tensor_begin, comp_outputs;
+    std::vector<uint32_t> direct_out;
+    char *dev_model = nullptr;
+    size_t dev_model_bytes = 0;
+    const uint4 *mechs = nullptr;
+    const ulonglong2 *entries = nullptr;
+    unsigned long long *dev_err = nullptr;  // [2]
+    cudaStream_t stream = nullptr, copy_stream = nullptr;
+    cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
+    char *scratch = nullptr;
+    size_t scratch_bytes = 0;
+    int sm_count = 148;
+    int blocks_per_sm = 1;
+    std::mutex mu;
+
+    char *scratch_get(size_t bytes) {
+        if (bytes > scratch_bytes) {
+            if (scratch) CK(cudaFree(scratch));
+            scratch = nullptr;
+            scratch_bytes = 0;
+            CK(cudaMalloc(&scratch, bytes));
+            scratch_bytes = bytes;
+        }
+        return scratch;
+    }
+};
+
+namespace {
+
+template <int FW>
+const void *kernel_ptr() {
+    return reinterpret_cast<const void *>(&zxs_dev::shot_kernel<FW>);
+}
+
+const void *shot_kernel_for(int fw) {
+    switch (fw) {
+        case 1: return kernel_ptr<1>();
+        case 2: return kernel_ptr<2>();
+        case 4: return kernel_ptr<4>();
+        case 8: return kernel_ptr<8>();
+        case 16: return kernel_ptr<16>();
+    }
+    fail(ZXS_UNSUPPORTED, "f_width above 1024 is not supported");
+}
+
+constexpr int kThreads = 256;
+
+size_t shot_smem_bytes(const zxs_sampler *s) {
+    return size_t(s->m.num_outputs) * 8 + size_t(kThreads / 32) * s->m.col_stride * 4;
+}
+
+void validate_csr(const char *name, const uint32_t *b, size_t n, size_t total) {
+    if (!b) fail(ZXS_INVALID_ARGUMENT, std::string(name) + " is null");
+    if (b[0] != 0) fail(ZXS_INVALID_ARGUMENT, std::string(name) + "[0] != 0");
+    for (size_t i = 0; i < n; i++) {
+        if (b[i + 1] < b[i]) fail(ZXS_INVALID_ARGUMENT, std::string(name) + " not monotone");
+    }
+    if (total != SIZE_MAX && b[n] != total) fail(ZXS_INVALID_ARGUMENT, std::string(name) + " total mismatch");
+}
+void validate_csr64(const char *name, const uint64_t *b, size_t n) {
+    if (!b) fail(ZXS_INVALID_ARGUMENT, std::string(name) + " is null");
+    if (b[0] != 0) fail(ZXS_INVALID_ARGUMENT, std::string(name) + "[0] != 0");
+    for (size_t i = 0; i < n; i++) {
+        if (b[i + 1] < b[i]) fail(ZXS_INVALID_ARGUMENT, std::string(name) + " not monotone");
+    }
+}
+
+void build(zxs_sampler *s, const zxs_model_desc *d) {
+    if (!d) fail(ZXS_INVALID_ARGUMENT, "null model");
+    if (d->abi_version != ZXS_ABI_VERSION) fail(ZXS_INVALID_ARGUMENT, "model ABI version mismatch");
+    if (d->mode > 1) fail(ZXS_INVALID_ARGUMENT, "bad mode");
+    const uint32_t fwid = d->f_width;
+    if (fwid > 1024) fail(ZXS_UNSUPPORTED, "f_width above 1024 is not supported");
+    const int fw_need = std::max(1, int((fwid + 63) / 64));
+    int FW = 1;
+    while (FW < fw_need) FW *= 2;
+    s->fw_template = FW;
+    s->mode = d->mode;
+
+    // ---- error model -> scan entries
+    validate_csr("mech_vec_begin", d->mech_vec_begin, d->num_mechanisms, d->num_vectors);
+    validate_csr("vec_bit_begin", d->vec_bit_begin, d->num_vectors, SIZE_MAX);
+    validate_csr("mech_table_begin", d->mech_table_begin, d->num_mechanisms, SIZE_MAX);
+    auto vec_mask = [&](uint32_t v, std::vector<uint64_t> &mask) {
+        for (uint32_t i = d->vec_bit_begin[v]; i < d->vec_bit_begin[v + 1]; i++) {
+            uint32_t b = d->vec_bits[i];
+            if (b >= fwid) fail(ZXS_INVALID_ARGUMENT, "f_vector bit out of range");
+            mask[b >> 6] ^= uint64_t(1) << (b & 63);
+        }
+    };
+    std::map<std::vector<uint64_t>, uint32_t> flipsets;
+    std::vector<uint64_t> flip_masks;
+    auto flip_id = [&](const std::vector<uint64_t> &mask) -> uint32_t {
+        bool any = false;
+        for (uint64_t w : mask) any |= w != 0;
+        if (!any) return zxs_dev::kNoFlip;
+        auto it = flipsets.find(mask);
+        if (it != flipsets.end()) return it->second;
+        uint32_t id = static_cast<uint32_t>(flipsets.size());
+        flipsets.emplace(mask, id);
+        flip_masks.insert(flip_masks.end(), mask.begin(), mask.end());
+        return id;
+    };
+    std::vector<uint4> mechs;
+    std::vector<ulonglong2> entries;
+    for (uint32_t mi = 0; mi < d->num_mechanisms; mi++) {
+        uint32_t v0 = d->mech_vec_begin[mi], nv = d->mech_vec_begin[mi + 1] - v0;
+        std::vector<std::pair<uint64_t, uint32_t>> scan;  // (lim, flip)
+        if (nv == 1) {
+            // single: fire iff u < probability (sampler.cpp:269-280)
+            uint64_t T = threshold_of(d->mech_probability[mi]);
+            std::vector<uint64_t> mask(FW, 0);
+            vec_mask(v0, mask);
+            uint32_t fid = flip_id(mask);
+            if (T > 0 && fid != zxs_dev::kNoFlip) scan.push_back({lim_of(T), fid});
+        } else if (nv > 1) {
+            // joint: inverse CDF over the table (sampler.cpp:281-302)
+            uint32_t t0 = d->mech_table_begin[mi], t1 = d->mech_table_begin[mi + 1];
+            if (nv > 31) fail(ZXS_UNSUPPORTED, "joint mechanism with more than 31 vectors");
+            double acc = 0.0;
+            uint64_t best = 0;
+            bool effect = false;
+            for (uint32_t o = 0; o < t1 - t0; o++) {
+                acc += d->table[t0 + o];
+                uint64_t T = threshold_of(acc);
+                if (T <= best) continue;  // can never be the first hit
+                best = T;
+                std::vector<uint64_t> mask(FW, 0);
+                for (uint32_t b = 0; b < nv; b++) {
+                    if ((uint64_t(o) >> b) & 1) vec_mask(v0 + b, mask);
+                }
+                uint32_t fid = flip_id(mask);
+                effect |= fid != zxs_dev::kNoFlip;
+                scan.push_back({lim_of(T), fid});
+                if (T == (uint64_t(1) << 53)) break;  // every later entry is unreachable
+            }
+            // Trailing no-flip entries behave like the no-hit fallback (outcome 0).
+            while (!scan.empty() && scan.back().second == zxs_dev::kNoFlip) scan.pop_back();
+            if (!effect) scan.clear();
+        }
+        if (scan.empty()) continue;
+        uint4 md;
+        md.x = mi;  // Philox stream = reference mechanism index (sampler.cpp:268)
+        md.y = static_cast<uint32_t>(entries.size());
+        for (auto &e : scan) entries.push_back(make_ulonglong2(e.first, e.second));
+        md.z = static_cast<uint32_t>(entries.size());
+        md.w = 0;
+        mechs.push_back(md);
+    }
+    if (flip_masks.empty()) flip_masks.assign(FW, 0);
+    std::vector<uint64_t> base(FW, 0);
+    for (uint32_t i = 0; i < d->num_base_offset; i++) {
+        uint32_t b = d->base_offset[i];
+        if (b >= fwid) fail(ZXS_INVALID_ARGUMENT, "base_offset bit out of range");
+        base[b >> 6] |= uint64_t(1) << (b & 63);
+    }
+
+    // ---- direct outputs
+    validate_csr("direct_bit_begin", d->direct_bit_begin, d->num_direct, SIZE_MAX);
+    std::vector<uint8_t> covered(d->num_outputs, 0);
+    std::vector<uint32_t> direct_out(d->num_direct), direct_bits;
+    for (uint32_t i = 0; i < d->num_direct; i++) {
+        uint32_t o = d->direct_output[i];
+        if (o >= d->num_outputs || covered[o]) fail(ZXS_INVALID_ARGUMENT, "bad direct output index");
+        covered[o] = 1;
+        direct_out[i] = o | (d->direct_flip_const[i] ? 0x80000000u : 0u);
+        for (uint32_t b = d->direct_bit_begin[i]; b < d->direct_bit_begin[i + 1]; b++) {
+            if (d->direct_bits[b] >= fwid) fail(ZXS_INVALID_ARGUMENT, "direct f bit out of range");
+            direct_bits.push_back(d->direct_bits[b]);
+        }
+    }
+    std::vector<uint32_t> direct_bit_begin(d->direct_bit_begin, d->direct_bit_begin + d->num_direct + 1);
+
+    // ---- components and chain tensors
+    validate_csr("comp_out_begin", d->comp_out_begin, d->num_components, SIZE_MAX);
+    validate_csr("comp_tensor_begin", d->comp_tensor_begin, d->num_components, d->num_tensors);
+    validate_csr64("tensor_term_begin", d->tensor_term_begin, d->num_tensors);
+    validate_csr64("term_factor_begin", d->term_factor_begin, d->num_terms);
+    validate_csr64("factor_u_begin", d->factor_u_begin, d->num_factors);
+    validate_csr64("factor_v_begin", d->factor_v_begin, d->num_factors);
+    if (d->tensor_term_begin[d->num_tensors] != d->num_terms ||
+        d->term_factor_begin[d->num_terms] != d->num_factors) {
+        fail(ZXS_INVALID_ARGUMENT, "tensor/term totals mismatch");
+    }
+    if (d->num_terms >= (uint64_t(1) << 32) || d->num_factors >= (uint64_t(1) << 32)) {
+        fail(ZXS_UNSUPPORTED, "more than 2^32 terms or factors");
+    }
+    uint32_t max_chain = 0;
+    std::vector<uint32_t> comp_outputs;
+    for (uint32_t c = 0; c < d->num_components; c++) {
+        uint32_t n = d->comp_out_begin[c + 1] - d->comp_out_begin[c];
+        if (d->comp_tensor_begin[c + 1] - d->comp_tensor_begin[c] != n + 1) {
+            fail(ZXS_INVALID_ARGUMENT, "component needs normalization + one marginal per output");
+        }
+        if (n >= 4096) fail(ZXS_UNSUPPORTED, "component chain longer than 4095");
+        max_chain = std::max(max_chain, n);
+        for (uint32_t i = d->comp_out_begin[c]; i < d->comp_out_begin[c + 1]; i++) {
+            uint32_t o = d->comp_outputs[i];
+            if (o >= d->num_outputs || covered[o]) fail(ZXS_INVALID_ARGUMENT, "bad component output index");
+            covered[o] = 1;
+            comp_outputs.push_back(o);
+        }
+        for (uint32_t t = d->comp_tensor_begin[c]; t < d->comp_tensor_begin[c + 1]; t++) {
+            if (d->tensor_param_width[t] > fwid + n) {
+                fail(ZXS_INVALID_ARGUMENT, "eval_batch: parameter width mismatch");
+            }
+        }
+    }
+    s->all_outputs_covered = std::all_of(covered.begin(), covered.end(), [](uint8_t c) { return c != 0; });
+    std::vector<uint32_t> tensor_term_begin(d->num_tensors + 1), term_factor_begin(d->num_terms + 1);
+    for (uint32_t t = 0; t <= d->num_tensors; t++) tensor_term_begin[t] = uint32_t(d->tensor_term_begin[t]);
+    for (uint64_t t = 0; t <= d->num_terms; t++) term_factor_begin[t] = uint32_t(d->term_factor_begin[t]);
+    std::vector<double2> term_c(d->num_terms);
+    for (uint64_t t = 0; t < d->num_terms; t++) term_c[t] = make_double2(d->term_c[2 * t], d->term_c[2 * t + 1]);
+    std::vector<Factor> factors(d->num_factors);
+    std::vector<uint16_t> selectors;
+    selectors.reserve(d->factor_u_begin[d->num_factors] + d->factor_v_begin[d->num_factors]);
+    std::vector<uint32_t> factor_width(d->num_factors, 0);
+    for (uint32_t t = 0; t < d->num_tensors; t++) {
+        for (uint64_t term = d->tensor_term_begin[t]; term < d->tensor_term_begin[t + 1]; term++) {
+            for (uint64_t k = d->term_factor_begin[term]; k < d->term_factor_begin[term + 1]; k++) {
+                factor_width[k] = d->tensor_param_width[t];
+            }
+        }
+    }
+    uint64_t nsel = 0;
+    for (uint64_t k = 0; k < d->num_factors; k++) {
+        Factor fr;
+        fr.sel = static_cast<uint32_t>(selectors.size());
+        uint64_t u0 = d->factor_u_begin[k], u1 = d->factor_u_begin[k + 1];
+        uint64_t v0 = d->factor_v_begin[k], v1 = d->factor_v_begin[k + 1];
+        if (u1 - u0 > 65535 || v1 - v0 > 65535) fail(ZXS_UNSUPPORTED, "selector too long");
+        fr.nu = uint16_t(u1 - u0);
+        fr.nv = uint16_t(v1 - v0);
+        for (uint64_t i = u0; i < u1; i++) {
+            if (d->factor_u_bits[i] >= factor_width[k]) fail(ZXS_INVALID_ARGUMENT, "eval_batch: parameter width mismatch");
+            selectors.push_back(uint16_t(d->factor_u_bits[i]));
+        }
+        for (uint64_t i = v0; i < v1; i++) {
+            if (d->factor_v_bits[i] >= factor_width[k]) fail(ZXS_INVALID_ARGUMENT, "eval_batch: parameter width mismatch");
+            selectors.push_back(uint16_t(d->factor_v_bits[i]));
+        }
+        nsel += (u1 - u0) + (v1 - v0);
+        if (d->factor_table[k] >= d->num_h_tables) fail(ZXS_INVALID_ARGUMENT, "h table index out of range");
+        fr.table = d->factor_table[k];
+        fr.pad = 0;
+        factors[k] = fr;
+    }
+    if (selectors.empty()) selectors.push_back(0);
+    std::vector<double2> h(4 * std::max<uint32_t>(1, d->num_h_tables), make_double2(0, 0));
+    bool monomial = true;
+    for (uint32_t t = 0; t < d->num_h_tables; t++) {
+        for (int ab = 0; ab < 4; ab++) {
+            double re = d->h_table[8 * t + 2 * ab], im = d->h_table[8 * t + 2 * ab + 1];
+            h[4 * t + ab] = make_double2(re, im);
+            // Clifford monomial check: 0 or 2^(m/2) w^k within 1e-9
+            double mag = std::hypot(re, im);
+            if (mag > 1e-9) {
+                double lm = std::log2(mag) * 2.0;
+                double ang = std::atan2(im, re) / (M_PI / 4);
+                if (std::fabs(lm - std::round(lm)) > 1e-9 || std::fabs(ang - std::round(ang)) > 1e-9) monomial = false;
+            }
+        }
+    }
+
+    // ---- device upload
+    Arena ar;
+    size_t o_mechs = ar.add(mechs.empty() ? std::vector<uint4>(1, make_uint4(0, 0, 0, 0)) : mechs);
+    size_t o_entries = ar.add(entries.empty() ? std::vector<ulonglong2>(1, make_ulonglong2(0, 0)) : entries);
+    size_t o_flip = ar.add(flip_masks);
+    size_t o_base = ar.add(base);
+    std::vector<uint32_t> direct_out_pad = direct_out.empty() ? std::vector<uint32_t>(1, 0) : direct_out;
+    size_t o_dout = ar.add(direct_out_pad);
+    size_t o_dbb = ar.add(direct_bit_begin);
+    std::vector<uint32_t> direct_bits_pad = direct_bits.empty() ? std::vector<uint32_t>(1, 0) : direct_bits;
+    size_t o_dbits = ar.add(direct_bits_pad);
+    std::vector<uint32_t> cob(d->comp_out_begin, d->comp_out_begin + d->num_components + 1);
+    std::vector<uint32_t> ctb(d->comp_tensor_begin, d->comp_tensor_begin + d->num_components + 1);
+    size_t o_cob = ar.add(cob);
+    std::vector<uint32_t> comp_outputs_pad = comp_outputs.empty() ? std::vector<uint32_t>(1, 0) : comp_outputs;
+    size_t o_co = ar.add(comp_outputs_pad);
+    size_t o_ctb = ar.add(ctb);
+    size_t o_ttb = ar.add(tensor_term_begin);
+    std::vector<double2> term_c_pad = term_c.empty() ? std::vector<double2>(1, make_double2(0, 0)) : term_c;
+    size_t o_tc = ar.add(term_c_pad);
+    size_t o_tfb = ar.add(term_factor_begin);
+    std::vector<Factor> factors_pad = factors.empty() ? std::vector<Factor>(1, Factor{}) : factors;
+    size_t o_fac = ar.add(factors_pad);
+    size_t o_sel = ar.add(selectors);
+    size_t o_h = ar.add(h);
+
+    CK(cudaMalloc(&s->dev_model, ar.host.size()));
+    s->dev_model_bytes = ar.host.size();
+    CK(cudaMemcpy(s->dev_model, ar.host.data(), ar.host.size(), cudaMemcpyHostToDevice));
+    char *b = s->dev_model;
+    DevModel &m = s->m;
+    m.f_width = fwid;
+    m.fw = FW;
+    m.num_outputs = d->num_outputs;
+    m.num_mech = static_cast<uint32_t>(mechs.size());
+    m.num_direct = d->num_direct;
+    m.num_components = d->num_components;
+    m.max_chain = max_chain;
+    uint32_t cs = std::max((fwid + 31) & ~31u, fwid + max_chain);
+    m.col_stride = (cs + 3) & ~3u;
+    if (m.col_stride == 0) m.col_stride = 4;
+    s->mechs = reinterpret_cast<const uint4 *>(b + o_mechs);
+    s->entries = reinterpret_cast<const ulonglong2 *>(b + o_entries);
+    m.flip_mask = reinterpret_cast<const uint64_t *>(b + o_flip);
+    m.base_offset = reinterpret_cast<const uint64_t *>(b + o_base);
+    m.direct_out = reinterpret_cast<const uint32_t *>(b + o_dout);
+    m.direct_bit_begin = reinterpret_cast<const uint32_t *>(b + o_dbb);
+    m.direct_bits = reinterpret_cast<const uint32_t *>(b + o_dbits);
+    m.comp_out_begin = reinterpret_cast<const uint32_t *>(b + o_cob);
+    m.comp_outputs = reinterpret_cast<const uint32_t *>(b + o_co);
+    m.comp_tensor_begin = reinterpret_cast<const uint32_t *>(b + o_ctb);
+    m.tensor_term_begin = reinterpret_cast<const uint32_t *>(b + o_ttb);
+    m.term_c = reinterpret_cast<const double2 *>(b + o_tc);
+    m.term_factor_begin = reinterpret_cast<const uint32_t *>(b + o_tfb);
+    m.factors = reinterpret_cast<const Factor *>(b + o_fac);
+    m.selectors = reinterpret_cast<const uint16_t *>(b + o_sel);
+    m.h_table = reinterpret_cast<const double2 *>(b + o_h);
+    m.mech_entry_begin = nullptr;
+    m.mech_stream = nullptr;
+    m.entry_lim = nullptr;
+    m.entry_flip = nullptr;
+
+    s->num_tensors = d->num_tensors;
+    s->tensor_width.assign(d->tensor_param_width, d->tensor_param_width + d->num_tensors);
+    s->comp_out_begin = cob;
+    s->comp_tensor_begin = ctb;
+    s->comp_outputs = comp_outputs;
+    s->direct_out = direct_out;
+
+    zxs_sampler_info &in = s->info;
+    in.mode = d->mode;
+    in.num_outputs = d->num_outputs;
+    in.num_detectors = d->num_detectors;
+    in.num_observables = d->num_observables;
+    in.f_width = fwid;
+    in.num_mechanisms = d->num_mechanisms;
+    in.num_direct = d->num_direct;
+    in.num_components = d->num_components;
+    in.max_chain = max_chain;
+    in.fwords = FW;
+    in.num_terms = d->num_terms;
+    in.num_factors = d->num_factors;
+    in.num_selector_bits = nsel;
+    uint64_t chain_total = comp_outputs.size();
+    in.philox_blocks_per_shot = d->num_mechanisms + chain_total;
+    in.device_bytes = ar.host.size();
+    in.device = s->device;
+    in.monomial = monomial ? 1 : 0;
+
+    CK(cudaMalloc(&s->dev_err, 2 * sizeof(unsigned long long)));
+    unsigned long long init[2] = {0, ~0ull};
+    CK(cudaMemcpy(s->dev_err, init, sizeof(init), cudaMemcpyHostToDevice));
+    CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; i++) {
+        CK(cudaEventCreateWithFlags(&s->ev_done[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&s->ev_copied[i], cudaEventDisableTiming));
+    }
+    CK(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, s->device));
+    const void *kern = shot_kernel_for(FW);
+    size_t smem = shot_smem_bytes(s);
+    if (smem > 48 * 1024) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    }
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->blocks_per_sm, kern, kThreads, smem));
+    if (s->blocks_per_sm < 1) fail(ZXS_UNSUPPORTED, "shot kernel does not fit on an SM");
+}
+
+void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
+    a.m = s->m;
+    a.mechs = s->mechs;
+    a.entries = s->entries;
+    a.err = s->dev_err;
+    // Even tile count: the u64 word holding the last shots is written in full.
+    uint64_t words64 = (a.shots + 63) / 64;
+    a.n_tiles = 2 * words64;
+    if (a.n_tiles == 0) return;
+    uint64_t want = (a.n_tiles + kThreads / 32 - 1) / (kThreads / 32);
+    uint64_t cap = uint64_t(s->sm_count) * s->blocks_per_sm;
+    unsigned grid = unsigned(std::min(want, cap));
+    size_t smem = shot_smem_bytes(s);
+    void *args[] = {&a};
+    CK(cudaLaunchKernel(shot_kernel_for(s->fw_template), dim3(grid), dim3(kThreads), args, smem, st));
+}
+
+void check_ratio_error(zxs_sampler *s, cudaStream_t st) {
+    unsigned long long h[2];
+    CK(cudaMemcpyAsync(h, s->dev_err, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h[0]) {
+        unsigned long long init[2] = {0, ~0ull};
+        CK(cudaMemcpy(s->dev_err, init, sizeof(init), cudaMemcpyHostToDevice));
+        // sampler.cpp:86-89
+        fail(ZXS_RUNTIME_ERROR, "autoregressive ratio outside [0, 1]: numeric breakdown");
+    }
+}
+
+void check_mode(const zxs_sampler *s, uint32_t expected) {
+    if (expected != s->mode) {  // sampler.cpp:308-309, 316-317
+        fail(ZXS_INVALID_ARGUMENT, s->mode == ZXS_MODE_MEASUREMENTS ? "sampler was compiled in measurement mode"
+                                                                     : "sampler was compiled in detector mode");
+    }
+}
+
+cudaStream_t pick(zxs_sampler *s, void *stream) {
+    return stream ? reinterpret_cast<cudaStream_t>(stream) : s->stream;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *zxs_last_error(void) { return g_last_error.c_str(); }
+uint32_t zxs_abi_version(void) { return ZXS_ABI_VERSION; }
+
+zxs_status zxs_sampler_create(const zxs_model_desc *desc, int device, zxs_sampler **out) {
+    return guarded([&] {
+        if (!out) fail(ZXS_INVALID_ARGUMENT, "null output handle");
+        *out = nullptr;
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess || n == 0) fail(ZXS_CUDA_ERROR, "no CUDA device available (the sampler has no CPU fallback)");
+        if (device < 0 || device >= n) fail(ZXS_INVALID_ARGUMENT, "device ordinal out of range");
+        DeviceGuard g(device);
+        auto *s = new zxs_sampler;
+        s->device = device;
+        try {
+            build(s, desc);
+        } catch (...) {
+            zxs_sampler_destroy(s);
+            throw;
+        }
+        *out = s;
+    });
+}
+
+void zxs_sampler_destroy(zxs_sampler *s) {
+    if (!s) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(s->device);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    if (s->copy_stream) cudaStreamSynchronize(s->copy_stream);
+    for (int i = 0; i < 2; i++) {
+        if (s->ev_done[i]) cudaEventDestroy(s->ev_done[i]);
+        if (s->ev_copied[i]) cudaEventDestroy(s->ev_copied[i]);
+    }
+    if (s->stream) cudaStreamDestroy(s->stream);
+    if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
+    if (s->dev_model) cudaFree(s->dev_model);
+    if (s->dev_err) cudaFree(s->dev_err);
+    if (s->scratch) cudaFree(s->scratch);
+    if (prev >= 0) cudaSetDevice(prev);
+    delete s;
+}
+
+zxs_status zxs_sampler_get_info(const zxs_sampler *s, zxs_sampler_info *info) {
+    return guarded([&] {
+        if (!s || !info) fail(ZXS_INVALID_ARGUMENT, "null argument");
+        *info = s->info;
+    });
+}
+
+zxs_status zxs_sample_device(zxs_sampler *s, uint64_t seed, uint64_t first_shot, uint64_t shots,
+                             uint64_t *dev_columns, uint64_t ld_words, uint64_t *dev_counts, void *stream) {
+    return guarded([&] {
+        if (!s) fail(ZXS_INVALID_ARGUMENT, "null sampler");
+        if (dev_columns && ld_words < (shots + 63) / 64) fail(ZXS_INVALID_ARGUMENT, "ld_words < ceil(shots/64)");
+        DeviceGuard g(s->device);
+        cudaStream_t st = pick(s, stream);
+        if (dev_columns && !s->all_outputs_covered) {
+            CK(cudaMemsetAsync(dev_columns, 0, size_t(s->m.num_outputs) * ld_words * 8, st));
+        }
+        zxs_dev::LaunchArgs a{};
+        a.seed = seed;
+        a.first_shot = first_shot;
+        a.shots = shots;
+        a.out32 = reinterpret_cast<uint32_t *>(dev_columns);
+        a.ld32 = 2 * ld_words;
+        a.counts = reinterpret_cast<unsigned long long *>(dev_counts);
+        launch_shots(s, a, st);
+        CK(cudaGetLastError());
+    });
+}
+
+zxs_status zxs_count_device(zxs_sampler *s, uint64_t seed, uint64_t first_shot, uint64_t shots,
+                            uint64_t *dev_counts, void *stream) {
+    if (!dev_counts) {
+        g_last_error = "null counts";
+        return ZXS_INVALID_ARGUMENT;
+    }
+    return zxs_sample_device(s, seed, first_shot, shots, nullptr, 0, dev_counts, stream);
+}
+
+zxs_status zxs_check_errors(zxs_sampler *s, void *stream) {
+    return guarded([&] {
+        if (!s) fail(ZXS_INVALID_ARGUMENT, "null sampler");
+        DeviceGuard g(s->device);
+        check_ratio_error(s, pick(s, stream));
+    });
+}
+
+zxs_status zxs_count(zxs_sampler *s, uint64_t seed, uint64_t first_shot, uint64_t shots, uint64_t *host_counts,
+                     void *stream) {
+    return guarded([&] {
+        if (!s || !host_counts) fail(ZXS_INVALID_ARGUMENT, "null argument");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard g(s->device);
+        cudaStream_t st = pick(s, stream);
+        size_t bytes = size_t(s->m.num_outputs) * 8;
+        auto *dc = reinterpret_cast<unsigned long long *>(s->scratch_get(std::max<size_t>(bytes, 8)));
+        CK(cudaMemsetAsync(dc, 0, bytes, st));
+        zxs_dev::LaunchArgs a{};
+        a.seed = seed;
+        a.first_shot = first_shot;
+        a.shots = shots;
+        a.counts = dc;
+        launch_shots(s, a, st);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(host_counts, dc, bytes, cudaMemcpyDeviceToHost, st));
+        check_ratio_error(s, st);
+    });
+}
+
+// Host-buffer sampling: chunks of shots are sampled into two device buffers
+// in turn; each chunk's columns are copied into the caller's column-major
+// record on a second stream while the next chunk is sampled.
+zxs_status zxs_sample(zxs_sampler *s, uint32_t expected_mode, uint64_t seed, uint64_t first_shot, uint64_t shots,
+                      uint64_t *host_columns, void *stream) {
+    return guarded([&] {
+        if (!s) fail(ZXS_INVALID_ARGUMENT, "null sampler");
+        check_mode(s, expected_mode);
+        if (shots == 0) return;
+        if (!host_columns) fail(ZXS_INVALID_ARGUMENT, "null output");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard g(s->device);
+        cudaStream_t st = pick(s, stream);
+        const uint64_t words = (shots + 63) / 64;
+        const uint32_t nout = s->m.num_outputs;
+        if (nout == 0) {
+            check_ratio_error(s, st);
+            return;
+        }
+        // chunk: multiple of 64 shots, ~64 MiB of output per buffer
+        uint64_t chunk_words = std::max<uint64_t>(1, (uint64_t(64) << 20) / (8ull * nout));
+        chunk_words = std::min(chunk_words, words);
+        const size_t buf_bytes = size_t(chunk_words) * nout * 8;
+        char *scratch = s->scratch_get(2 * buf_bytes);
+        uint64_t nchunks = (words + chunk_words - 1) / chunk_words;
+        for (uint64_t c = 0; c < nchunks; c++) {
+            int bi = int(c & 1);
+            uint64_t w0 = c * chunk_words;
+            uint64_t cw = std::min(chunk_words, words - w0);
+            uint64_t cshots = std::min<uint64_t>(cw * 64, shots - w0 * 64);
+            auto *buf = reinterpret_cast<uint64_t *>(scratch + bi * buf_bytes);
+            if (c >= 2) CK(cudaStreamWaitEvent(st, s->ev_copied[bi], 0));
+            if (!s->all_outputs_covered) CK(cudaMemsetAsync(buf, 0, size_t(cw) * nout * 8, st));
+            zxs_dev::LaunchArgs a{};
+            a.seed = seed;
+            a.first_shot = first_shot + w0 * 64;
+            a.shots = cshots;
+            a.out32 = reinterpret_cast<uint32_t *>(buf);
+            a.ld32 = 2 * cw;
+            launch_shots(s, a, st);
+            CK(cudaGetLastError());
+            CK(cudaEventRecord(s->ev_done[bi], st));
+            CK(cudaStreamWaitEvent(s->copy_stream, s->ev_done[bi], 0));
+            CK(cudaMemcpy2DAsync(host_columns + w0, words * 8, buf, cw * 8, cw * 8, nout, cudaMemcpyDeviceToHost,
+                                 s->copy_stream));
+            CK(cudaEventRecord(s->ev_copied[bi], s->copy_stream));
+        }
+        CK(cudaStreamSynchronize(s->copy_stream));
+        check_ratio_error(s, st);
+    });
+}
+
+zxs_status zxs_sample_error_batch(zxs_sampler *s, uint64_t seed, uint64_t first_shot, uint64_t shots,
+                                  uint64_t *host_fcols) {
+    return guarded([&] {
+        if (!s) fail(ZXS_INVALID_ARGUMENT, "null sampler");
+        if (shots == 0 || s->m.f_width == 0) return;
+        if (!host_fcols) fail(ZXS_INVALID_ARGUMENT, "null output");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard g(s->device);
+        cudaStream_t st = s->stream;
+        const uint64_t words = (shots + 63) / 64;
+        size_t bytes = size_t(words) * s->m.f_width * 8;
+        auto *buf = reinterpret_cast<uint32_t *>(s->scratch_get(bytes));
+        zxs_dev::LaunchArgs a{};
+        a.seed = seed;
+        a.first_shot = first_shot;
+        a.shots = shots;
+        a.fcols_out = buf;
+        a.fcols_ld32 = 2 * words;
+        launch_shots(s, a, st);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(host_fcols, buf, bytes, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    });
+}
+
+zxs_status zxs_sample_given_f(zxs_sampler *s, uint64_t seed, uint64_t first_shot, uint64_t shots,
+                              const uint64_t *host_fcols, const double *host_uniforms, uint64_t *host_columns) {
+    return guarded([&] {
+        if (!s) fail(ZXS_INVALID_ARGUMENT, "null sampler");
+        if (shots == 0) return;
+        if (!host_columns || (!host_fcols && s->m.f_width)) fail(ZXS_INVALID_ARGUMENT, "null argument");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard g(s->device);
+        cudaStream_t st = s->stream;
+        const uint64_t words = (shots + 63) / 64;
+        const uint32_t nout = s->m.num_outputs;
+        size_t fbytes = size_t(words) * s->m.f_width * 8;
+        size_t obytes = size_t(words) * nout * 8;
+        size_t npos = s->comp_outputs.size();
+        size_t ubytes = host_uniforms ? npos * shots * 8 : 0;
+        auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+        char *base = s->scratch_get(al(fbytes) + al(obytes) + al(ubytes) + 256);
+        auto *df = reinterpret_cast<uint32_t *>(base);
+        auto *dout = reinterpret_cast<uint32_t *>(base + al(fbytes));
+        auto *du = reinterpret_cast<double *>(base + al(fbytes) + al(obytes));
+        if (fbytes) CK(cudaMemcpyAsync(df, host_fcols, fbytes, cudaMemcpyHostToDevice, st));
+        if (ubytes) CK(cudaMemcpyAsync(du, host_uniforms, ubytes, cudaMemcpyHostToDevice, st));
+        if (obytes) CK(cudaMemsetAsync(dout, 0, obytes, st));
+        zxs_dev::LaunchArgs a{};
+        a.seed = seed;
+        a.first_shot = first_shot;
+        a.shots = shots;
+        a.fcols_in = df;
+        a.fcols_ld32 = 2 * words;
+        a.uniforms = host_uniforms ? du : nullptr;
+        a.uniforms_ld = shots;
+        a.out32 = dout;
+        a.ld32 = 2 * words;
+        launch_shots(s, a, st);
+        CK(cudaGetLastError());
+        if (obytes) CK(cudaMemcpyAsync(host_columns, dout, obytes, cudaMemcpyDeviceToHost, st));
+        check_ratio_error(s, st);
+    });
+}
+
+namespace {
+void eval_on_device(zxs_sampler *s, uint32_t tensor, const uint64_t *host_params, uint32_t param_cols,
+                    uint64_t shots, double *host_values, double *max_imag) {
+    const uint64_t words = (shots + 63) / 64;
+    cudaStream_t st = s->stream;
+    size_t pbytes = size_t(words) * param_cols * 8;
+    size_t vbytes = size_t(shots) * 8;
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    char *base = s->scratch_get(al(pbytes) + al(vbytes) + 256);
+    auto *dp = reinterpret_cast<uint32_t *>(base);
+    auto *dv = reinterpret_cast<double *>(base + al(pbytes));
+    auto *dmi = reinterpret_cast<unsigned long long *>(base + al(pbytes) + al(vbytes));
+    if (pbytes) CK(cudaMemcpyAsync(dp, host_params, pbytes, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(dmi, 0, 8, st));
+    uint32_t col_stride = std::max<uint32_t>(4, (param_cols + 3) & ~3u);
+    uint64_t n_tiles = 2 * words;
+    unsigned grid = unsigned(std::min<uint64_t>((n_tiles + 7) / 8, uint64_t(s->sm_count) * 8));
+    size_t smem = size_t(8) * col_stride * 4;
+    if (smem > 48 * 1024) {
+        CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(&zxs_dev::eval_kernel),
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    }
+    zxs_dev::eval_kernel<<<grid, kThreads, smem, st>>>(s->m, tensor, dp, 2 * words, param_cols, col_stride, shots,
+                                                       n_tiles, dv, dmi);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(host_values, dv, vbytes, cudaMemcpyDeviceToHost, st));
+    unsigned long long mib = 0;
+    CK(cudaMemcpyAsync(&mib, dmi, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (max_imag) std::memcpy(max_imag, &mib, 8);
+}
+}  // namespace
+
+zxs_status zxs_eval_batch(zxs_sampler *s, uint32_t component, uint32_t chain_pos, const uint64_t *host_params,
+                          uint32_t param_cols, uint64_t shots, double *host_values, double *max_imag_ratio) {
+    return guarded([&] {
+        if (!s) fail(ZXS_INVALID_ARGUMENT, "null sampler");
+        if (component >= s->comp_out_begin.size() - 1) fail(ZXS_INVALID_ARGUMENT, "component out of range");
+        uint32_t n = s->comp_out_begin[component + 1] - s->comp_out_begin[component];
+        if (chain_pos > n) fail(ZXS_INVALID_ARGUMENT, "chain position out of range");
+        uint32_t t = s->comp_tensor_begin[component] + chain_pos;
+        if (param_cols < s->tensor_width[t]) fail(ZXS_INVALID_ARGUMENT, "eval_batch: parameter width mismatch");
+        if (max_imag_ratio) *max_imag_ratio = 0.0;
+        if (shots == 0) return;
+        if (!host_params || !host_values) fail(ZXS_INVALID_ARGUMENT, "null argument");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard g(s->device);
+        eval_on_device(s, t, host_params, param_cols, shots, host_values, max_imag_ratio);
+    });
+}
+
+// probability_of_at (sampler.cpp:360-368) -> outcome_probability_given
+// (sampler.cpp:324-356), every eval on the device.
+zxs_status zxs_probability_of_at(zxs_sampler *s, const uint8_t *outcome, uint32_t n_outcome,
+                                 const uint8_t *f_assignment, uint32_t n_f, double *out) {
+    return guarded([&] {
+        if (!s || !out || (!outcome && n_outcome) || (!f_assignment && n_f)) fail(ZXS_INVALID_ARGUMENT, "null argument");
+        if (n_outcome != s->m.num_outputs) fail(ZXS_INVALID_ARGUMENT, "outcome length must match the output count");
+        if (n_f != s->m.f_width) fail(ZXS_INVALID_ARGUMENT, "f assignment length must match f_width");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard g(s->device);
+        // f = f_assignment ^ base_offset
+        std::vector<uint64_t> base(s->fw_template);
+        CK(cudaMemcpy(base.data(), s->m.base_offset, base.size() * 8, cudaMemcpyDeviceToHost));
+        std::vector<uint8_t> f(n_f);
+        for (uint32_t i = 0; i < n_f; i++) f[i] = (f_assignment[i] ^ uint8_t((base[i >> 6] >> (i & 63)) & 1)) & 1;
+        // direct outputs
+        std::vector<uint32_t> dbb(s->m.num_direct + 1), dbits;
+        CK(cudaMemcpy(dbb.data(), s->m.direct_bit_begin, dbb.size() * 4, cudaMemcpyDeviceToHost));
+        dbits.resize(std::max<uint32_t>(1, dbb.back()));
+        CK(cudaMemcpy(dbits.data(), s->m.direct_bits, dbits.size() * 4, cudaMemcpyDeviceToHost));
+        for (uint32_t d = 0; d < s->m.num_direct; d++) {
+            uint32_t od = s->direct_out[d];
+            bool bit = (od >> 31) != 0;
+            for (uint32_t b = dbb[d]; b < dbb[d + 1]; b++) bit ^= f[dbits[b]] != 0;
+            if (bit != (outcome[od & 0x7fffffffu] != 0)) {
+                *out = 0.0;
+                return;
+            }
+        }
+        double p = 1.0;
+        for (size_t c = 0; c + 1 < s->comp_out_begin.size(); c++) {
+            uint32_t n = s->comp_out_begin[c + 1] - s->comp_out_begin[c];
+            uint32_t cols = s->m.f_width + n;
+            std::vector<uint64_t> params(std::max<uint32_t>(cols, 1), 0);
+            for (uint32_t i = 0; i < s->m.f_width; i++) params[i] = f[i];
+            double norm = 0.0;
+            eval_on_device(s, s->comp_tensor_begin[c], params.data(), cols, 1, &norm, nullptr);
+            if (!(norm > 0.0)) fail(ZXS_RUNTIME_ERROR, "component normalization is not positive");
+            double prev = norm;
+            for (uint32_t pos = 0; pos < n; pos++) {
+                double p0 = 0.0;
+                eval_on_device(s, s->comp_tensor_begin[c] + 1 + pos, params.data(), cols, 1, &p0, nullptr);
+                bool bit = outcome[s->comp_outputs[s->comp_out_begin[c] + pos]] != 0;
+                prev = bit ? prev - p0 : p0;
+                params[s->m.f_width + pos] = bit ? 1 : 0;
+            }
+            p *= prev / norm;
+        }
+        *out = p;
+    });
+}
+
+zxs_status zxs_philox_uniform(int device, uint64_t seed, uint32_t stream, uint64_t first_index, uint64_t n,
+                              double *host_out) {
+    return guarded([&] {
+        if (n == 0) return;
+        if (!host_out) fail(ZXS_INVALID_ARGUMENT, "null output");
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) fail(ZXS_CUDA_ERROR, "no CUDA device available");
+        DeviceGuard g(device);
+        double *d = nullptr;
+        CK(cudaMalloc(&d, n * 8));
+        unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, 4096));
+        zxs_dev::philox_kernel<<<grid, 256>>>(seed, stream, first_index, n, d);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaMemcpy(host_out, d, n * 8, cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        CK(e);
+    });
+}
+
+}  // extern "C"

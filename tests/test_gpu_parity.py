@@ -1,0 +1,197 @@
+"""Parity of the sm_100a path against the reference (run on a B200).
+
+Bit-exact gates (integer/bit work and the reference's FP64 arithmetic order):
+  * sampled detector/observable records == the reference's sample_detectors /
+    sample_measurements (goldens from the unmodified reference, every fixture,
+    up to 1e6 shots, shot ranges starting anywhere incl. across 2^32),
+  * f-columns == sample_error_batch,
+  * eval_batch values == the reference's, bit for bit (FP64 without FMA),
+  * injected noise + injected uniforms: run_batch == oracle,
+  * Philox uniforms == reference uniform_at,
+  * counts == popcounts of the records; any shard split gives the same bits.
+Marginal probabilities: probability_of_at within 1e-12 relative (target in
+BASELINE.json is 1e-6).
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import fixture_names, golden_path
+from oracle import coracle, refdriver
+
+pytestmark = pytest.mark.gpu
+
+import paper_2604_01059_b200 as zx  # noqa: E402
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, np.uint64).tobytes()).hexdigest()
+
+
+_cache = {}
+
+
+def model(name):
+    if name not in _cache:
+        _cache[name] = zx.CompiledSampler.load(golden_path(name))
+    return _cache[name]
+
+
+def sample(cs, shots, seed, first_shot=0):
+    opt = zx.SamplerOptions(seed=seed)
+    f = zx.sample_detectors if cs.mode == zx.MODE_DETECTORS else zx.sample_measurements
+    return f(cs, shots, opt, first_shot=first_shot).columns
+
+
+@pytest.mark.parametrize("name", fixture_names())
+def test_records_match_reference_goldens(name, goldens):
+    cs = model(name)
+    for s in goldens[name]["samples"]:
+        cols = sample(cs, s["shots"], s["seed"], s["first_shot"])
+        assert sha(cols) == s["sha256"], (name, s)
+
+
+@pytest.mark.parametrize("name", fixture_names())
+def test_error_batch_matches_reference(name, goldens):
+    cs = model(name)
+    for f in goldens[name]["fcols"]:
+        fc = zx.sample_error_batch(cs, f["seed"], f["first_shot"], f["shots"])
+        assert sha(fc) == f["sha256"], (name, f)
+
+
+@pytest.mark.parametrize("name", ["c2_surface_d3_xmem_t", "c4_color_d5_rz3", "surface_d3_xmem_rz5",
+                                  "surface_d3_xmem_9t", "oracle_mix_4", "random_02", "h_t_h_m"])
+def test_eval_batch_bit_exact(name):
+    cs = model(name)
+    orc = coracle.OracleModel.load(golden_path(name))
+    a = orc.arrays
+    rng = np.random.default_rng(17)
+    shots = 1000 if name != "surface_d3_xmem_9t" else 200
+    for c in range(a["comp_out_begin"].size - 1):
+        n = int(a["comp_out_begin"][c + 1] - a["comp_out_begin"][c])
+        params = rng.integers(0, 2**63, size=(orc.f_width + n, (shots + 63) // 64), dtype=np.uint64)
+        for pos in range(n + 1):
+            t = int(a["comp_tensor_begin"][c]) + pos
+            v_dev = zx.eval_batch(cs, c, pos, params, shots)
+            v_orc, mi = orc.eval_batch(t, params, shots)
+            assert np.array_equal(v_dev.values.view(np.uint64), v_orc.view(np.uint64)), (name, c, pos)
+            assert v_dev.max_imag_ratio == pytest.approx(mi, rel=1e-12, abs=1e-300)
+
+
+@pytest.mark.parametrize("name", ["c2_surface_d3_xmem_t", "c4_color_d5_rz3", "surface_d3_xmem_rz5", "random_05"])
+def test_injected_noise_and_uniforms(name):
+    """Bit-exact under injected noise configurations and uniform draws."""
+    cs = model(name)
+    orc = coracle.OracleModel.load(golden_path(name))
+    rng = np.random.default_rng(23)
+    shots = 3000
+    f = rng.integers(0, 2**63, size=(orc.f_width, (shots + 63) // 64), dtype=np.uint64)
+    f[:, -1] &= np.uint64((1 << (shots & 63)) - 1)
+    u = rng.random((orc.num_positions, shots))
+    try:
+        expect = orc.sample(shots, 0, fcols=f, uniforms=u)
+    except RuntimeError:
+        with pytest.raises(RuntimeError, match="numeric breakdown"):
+            zx.sample_given_f(cs, f, shots, uniforms=u)
+        return
+    assert np.array_equal(zx.sample_given_f(cs, f, shots, uniforms=u), expect)
+    # injected noise with the Philox autoregressive draws
+    assert np.array_equal(zx.sample_given_f(cs, f, shots, seed=9, first_shot=77),
+                          orc.sample(shots, 9, first_shot=77, fcols=f))
+
+
+def test_philox_matches_reference(goldens):
+    for p in goldens["_philox"]:
+        assert zx.philox_uniform(p["seed"], p["stream"], p["index"], 1)[0] == p["u"]
+    first = 2**32 - 500
+    dev = zx.philox_uniform(12345, 0x80000003, first, 1000)
+    ref = np.array([coracle.uniform_at(12345, 0x80000003, first + i) for i in range(1000)])
+    assert np.array_equal(dev.view(np.uint64), ref.view(np.uint64))
+
+
+@pytest.mark.skipif(not refdriver.available(), reason="reference library not present")
+@pytest.mark.parametrize("name", ["c2_surface_d3_xmem_t", "c4_color_d5_rz3", "oracle_mix_1", "norm_sum",
+                                  "random_02", "random_05"])
+def test_probability_of_at(name):
+    cs = model(name)
+    ref = refdriver.RefModel.load(golden_path(name))
+    rng = np.random.default_rng(1)
+    for _ in range(20):
+        outcome = rng.integers(0, 2, cs.num_outputs).astype(np.uint8)
+        f = rng.integers(0, 2, cs.f_width).astype(np.uint8)
+        try:
+            want = ref.probability_of_at(outcome, f)
+        except RuntimeError:
+            with pytest.raises(RuntimeError):
+                zx.probability_of_at(cs, outcome, f)
+            continue
+        got = zx.probability_of_at(cs, outcome, f)
+        assert got == pytest.approx(want, rel=1e-12, abs=1e-300)
+
+
+@pytest.mark.skipif(not refdriver.available(), reason="reference library not present")
+def test_large_d7_against_reference():
+    """Config 5 (d=7, 7 rounds): 2^20 shots from shot 2^32-2^19 vs the reference."""
+    cs = model("c5_surface_d7_r7")
+    ref = refdriver.RefModel.load(golden_path("c5_surface_d7_r7"))
+    first, shots = 2**32 - 2**19, 2**20
+    assert np.array_equal(sample(cs, shots, 3, first), ref.sample_rb(shots, 3, first_shot=first))
+
+
+def test_counts_and_shard_invariance():
+    """Full-size properties: any split of the shot range gives the same bits
+    and counts add up (the multi-GPU sharding contract)."""
+    cs = model("c2_surface_d3_xmem_t")
+    shots = 1 << 22
+    whole = sample(cs, shots, 5)
+    counts = zx.count_outputs(cs, shots, seed=5)
+    pc = np.unpackbits(whole.view(np.uint8), axis=1).sum(axis=1)
+    assert np.array_equal(counts, pc.astype(np.uint64))
+    half = shots // 2
+    a = sample(cs, half, 5, 0)
+    b = sample(cs, half, 5, half)
+    assert np.array_equal(np.concatenate([a, b], axis=1), whole)
+    c3 = [zx.count_outputs(cs, n, seed=5, first_shot=f) for f, n in ((0, 1000), (1000, shots - 1000))]
+    assert np.array_equal(c3[0] + c3[1], counts)
+
+
+def test_sample_device_strided_and_counts():
+    import torch
+    cs = model("c4_color_d5_rz3")
+    shots, ld = 100_000, 2000
+    cols = torch.zeros((cs.num_outputs, ld), dtype=torch.int64, device="cuda")
+    counts = torch.zeros(cs.num_outputs, dtype=torch.int64, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    cs.sample_device(3, 0, shots, cols.data_ptr(), ld, counts.data_ptr(), stream)
+    cs.check_errors(stream)
+    words = (shots + 63) // 64
+    got = cols.cpu().numpy().view(np.uint64)
+    assert np.array_equal(got[:, :words], sample(cs, shots, 3))
+    assert not got[:, words:].any()
+    assert np.array_equal(counts.cpu().numpy().view(np.uint64), zx.count_outputs(cs, shots, seed=3))
+
+
+def test_mode_mismatch_raises_like_reference():
+    with pytest.raises(ValueError, match="sampler was compiled in detector mode"):
+        zx.sample_measurements(model("c2_surface_d3_xmem_t"), 10)
+    with pytest.raises(ValueError, match="sampler was compiled in measurement mode"):
+        zx.sample_detectors(model("h_t_h_m"), 10)
+
+
+def test_ratio_breakdown_raises_like_reference():
+    from paper_2604_01059_b200 import zxs_format
+    a = zxs_format.load(golden_path("h_t_h_m"))
+    t = int(a["tensor_term_begin"][1])
+    a["term_c"][2 * t: 2 * int(a["tensor_term_begin"][2])] *= 10.0  # marginal > normalization
+    cs = zx.CompiledSampler(a)
+    with pytest.raises(RuntimeError, match="autoregressive ratio outside"):
+        zx.sample_measurements(cs, 100, zx.SamplerOptions(seed=1))
+
+
+def test_empty_and_tiny_ranges():
+    cs = model("c2_surface_d3_xmem_t")
+    assert sample(cs, 0, 1).shape == (25, 0)
+    orc = coracle.OracleModel.load(golden_path("c2_surface_d3_xmem_t"))
+    for shots, first in ((1, 0), (31, 5), (33, 2**32 - 7), (64, 64), (65, 1)):
+        assert np.array_equal(sample(cs, shots, 4, first), orc.sample(shots, 4, first))

@@ -150,7 +150,7 @@ zxs_status zxs_sampler_get_info(const zxs_sampler *s, zxs_sampler_info *info);
  * index), so any split of the shot range gives the same bits).
  * `expected_mode` reproduces the reference's mode check (sampler.cpp:308-317).
  * host_columns: [num_outputs][ceil(shots/64)] uint64, written in full.
- * stream: a cudaStream_t or NULL (the sampler's own stream). Synchronous.
+ * stream: a cudaStream_t, or NULL for the sampler's own stream. Synchronous.
  */
 zxs_status zxs_sample(zxs_sampler *s, uint32_t expected_mode, uint64_t seed,
                       uint64_t first_shot, uint64_t shots, uint64_t *host_columns,
@@ -160,8 +160,9 @@ zxs_status zxs_sample(zxs_sampler *s, uint32_t expected_mode, uint64_t seed,
  * Device-resident variant: dev_columns is device memory [num_outputs][ld_words]
  * uint64 with ld_words >= ceil(shots/64). dev_counts (nullable, device,
  * [num_outputs] uint64) is incremented by the per-output number of set bits.
- * Asynchronous on `stream`; errors in the autoregressive ratio check are
- * reported by the next zxs_check_errors / synchronous call.
+ * Asynchronous on `stream` (a cudaStream_t; NULL is the legacy default
+ * stream). Errors in the autoregressive ratio check are reported by the next
+ * zxs_check_errors / synchronous call.
  */
 zxs_status zxs_sample_device(zxs_sampler *s, uint64_t seed, uint64_t first_shot,
                              uint64_t shots, uint64_t *dev_columns, uint64_t ld_words,

@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <stdexcept>
@@ -121,8 +122,12 @@ struct zxs_sampler {
     std::vector<uint32_t> direct_out;
     char *dev_model = nullptr;
     size_t dev_model_bytes = 0;
-    const uint4 *mechs = nullptr;
-    const ulonglong2 *entries = nullptr;
+    bool param_mechs = true;
+    std::unique_ptr<zxs_dev::MechTable<zxs_dev::kParamMechs>> mech_table;
+    const zxs_dev::MechRec *mech_global = nullptr;
+    const uint32_t *ext_begin = nullptr;
+    const ulonglong2 *ext = nullptr;
+    uint32_t dead_mechanisms = 0;
     unsigned long long *dev_err = nullptr;  // [2]
     cudaStream_t stream = nullptr, copy_stream = nullptr;
     cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
@@ -147,17 +152,18 @@ struct zxs_sampler {
 namespace {
 
 template <int FW>
-const void *kernel_ptr() {
-    return reinterpret_cast<const void *>(&zxs_dev::shot_kernel<FW>);
+const void *kernel_ptr(bool param_mechs) {
+    return param_mechs ? reinterpret_cast<const void *>(&zxs_dev::shot_kernel<FW, true>)
+                       : reinterpret_cast<const void *>(&zxs_dev::shot_kernel<FW, false>);
 }
 
-const void *shot_kernel_for(int fw) {
+const void *shot_kernel_for(int fw, bool param_mechs) {
     switch (fw) {
-        case 1: return kernel_ptr<1>();
-        case 2: return kernel_ptr<2>();
-        case 4: return kernel_ptr<4>();
-        case 8: return kernel_ptr<8>();
-        case 16: return kernel_ptr<16>();
+        case 1: return kernel_ptr<1>(param_mechs);
+        case 2: return kernel_ptr<2>(param_mechs);
+        case 4: return kernel_ptr<4>(param_mechs);
+        case 8: return kernel_ptr<8>(param_mechs);
+        case 16: return kernel_ptr<16>(param_mechs);
     }
     fail(ZXS_UNSUPPORTED, "f_width above 1024 is not supported");
 }
@@ -165,7 +171,7 @@ const void *shot_kernel_for(int fw) {
 constexpr int kThreads = 256;
 
 size_t shot_smem_bytes(const zxs_sampler *s) {
-    return size_t(s->m.num_outputs) * 8 + size_t(kThreads / 32) * s->m.col_stride * 4;
+    return size_t(s->m.num_outputs) * 8 + size_t(zxs_dev::kS) * s->m.col_stride * 4;  // one warp per CTA
 }
 
 void validate_csr(const char *name, const uint32_t *b, size_t n, size_t total) {
@@ -220,8 +226,10 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         flip_masks.insert(flip_masks.end(), mask.begin(), mask.end());
         return id;
     };
-    std::vector<uint4> mechs;
-    std::vector<ulonglong2> entries;
+    std::vector<zxs_dev::MechRec> recs;
+    std::vector<uint32_t> ext_begin;
+    std::vector<ulonglong2> ext;
+    uint32_t dead = 0;
     for (uint32_t mi = 0; mi < d->num_mechanisms; mi++) {
         uint32_t v0 = d->mech_vec_begin[mi], nv = d->mech_vec_begin[mi + 1] - v0;
         std::vector<std::pair<uint64_t, uint32_t>> scan;  // (lim, flip)
@@ -257,14 +265,21 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
             while (!scan.empty() && scan.back().second == zxs_dev::kNoFlip) scan.pop_back();
             if (!effect) scan.clear();
         }
-        if (scan.empty()) continue;
-        uint4 md;
-        md.x = mi;  // Philox stream = reference mechanism index (sampler.cpp:268)
-        md.y = static_cast<uint32_t>(entries.size());
-        for (auto &e : scan) entries.push_back(make_ulonglong2(e.first, e.second));
-        md.z = static_cast<uint32_t>(entries.size());
-        md.w = 0;
-        mechs.push_back(md);
+        // Record index = Philox stream = reference mechanism index (sampler.cpp:268).
+        zxs_dev::MechRec rec;
+        ext_begin.push_back(static_cast<uint32_t>(ext.size()));
+        if (scan.empty()) {
+            rec.lim0 = 0;  // never fires
+            rec.flip0 = zxs_dev::kNoFlip;
+            rec.n_extra = 0;
+            dead++;
+        } else {
+            rec.lim0 = scan[0].first;
+            rec.flip0 = scan[0].second;
+            rec.n_extra = static_cast<uint32_t>(scan.size() - 1);
+            for (size_t e = 1; e < scan.size(); e++) ext.push_back(make_ulonglong2(scan[e].first, scan[e].second));
+        }
+        recs.push_back(rec);
     }
     if (flip_masks.empty()) flip_masks.assign(FW, 0);
     std::vector<uint64_t> base(FW, 0);
@@ -384,8 +399,11 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
 
     // ---- device upload
     Arena ar;
-    size_t o_mechs = ar.add(mechs.empty() ? std::vector<uint4>(1, make_uint4(0, 0, 0, 0)) : mechs);
-    size_t o_entries = ar.add(entries.empty() ? std::vector<ulonglong2>(1, make_ulonglong2(0, 0)) : entries);
+    std::vector<zxs_dev::MechRec> recs_pad = recs.empty() ? std::vector<zxs_dev::MechRec>(1) : recs;
+    size_t o_recs = ar.add(recs_pad);
+    std::vector<uint32_t> ext_begin_pad = ext_begin.empty() ? std::vector<uint32_t>(1, 0) : ext_begin;
+    size_t o_extb = ar.add(ext_begin_pad);
+    size_t o_ext = ar.add(ext.empty() ? std::vector<ulonglong2>(1, make_ulonglong2(0, 0)) : ext);
     size_t o_flip = ar.add(flip_masks);
     size_t o_base = ar.add(base);
     std::vector<uint32_t> direct_out_pad = direct_out.empty() ? std::vector<uint32_t>(1, 0) : direct_out;
@@ -416,15 +434,22 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     m.f_width = fwid;
     m.fw = FW;
     m.num_outputs = d->num_outputs;
-    m.num_mech = static_cast<uint32_t>(mechs.size());
+    m.num_mech = d->num_mechanisms;
     m.num_direct = d->num_direct;
     m.num_components = d->num_components;
     m.max_chain = max_chain;
     uint32_t cs = std::max((fwid + 31) & ~31u, fwid + max_chain);
     m.col_stride = (cs + 3) & ~3u;
     if (m.col_stride == 0) m.col_stride = 4;
-    s->mechs = reinterpret_cast<const uint4 *>(b + o_mechs);
-    s->entries = reinterpret_cast<const ulonglong2 *>(b + o_entries);
+    s->mech_global = reinterpret_cast<const zxs_dev::MechRec *>(b + o_recs);
+    s->ext_begin = reinterpret_cast<const uint32_t *>(b + o_extb);
+    s->ext = reinterpret_cast<const ulonglong2 *>(b + o_ext);
+    s->param_mechs = d->num_mechanisms <= zxs_dev::kParamMechs;
+    if (s->param_mechs) {
+        s->mech_table.reset(new zxs_dev::MechTable<zxs_dev::kParamMechs>());
+        std::copy(recs.begin(), recs.end(), s->mech_table->rec);
+    }
+    s->dead_mechanisms = dead;
     m.flip_mask = reinterpret_cast<const uint64_t *>(b + o_flip);
     m.base_offset = reinterpret_cast<const uint64_t *>(b + o_base);
     m.direct_out = reinterpret_cast<const uint32_t *>(b + o_dout);
@@ -481,30 +506,32 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         CK(cudaEventCreateWithFlags(&s->ev_copied[i], cudaEventDisableTiming));
     }
     CK(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, s->device));
-    const void *kern = shot_kernel_for(FW);
+    const void *kern = shot_kernel_for(FW, s->param_mechs);
     size_t smem = shot_smem_bytes(s);
     if (smem > 48 * 1024) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     }
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->blocks_per_sm, kern, kThreads, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->blocks_per_sm, kern, 32, smem));
     if (s->blocks_per_sm < 1) fail(ZXS_UNSUPPORTED, "shot kernel does not fit on an SM");
 }
 
 void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
     a.m = s->m;
-    a.mechs = s->mechs;
-    a.entries = s->entries;
+    a.num_mech = s->info.num_mechanisms;
+    a.mech_global = s->mech_global;
+    a.ext_begin = s->ext_begin;
+    a.ext = s->ext;
     a.err = s->dev_err;
-    // Even tile count: the u64 word holding the last shots is written in full.
-    uint64_t words64 = (a.shots + 63) / 64;
-    a.n_tiles = 2 * words64;
+    for (int i = 0; i < 10; i++) a.k0_round[i] = uint32_t(a.seed) + uint32_t(i) * 0x9E3779B9u;
+    // One warp tile = 64 shots = one u64 output word, written in full.
+    a.n_tiles = (a.shots + zxs_dev::kTileShots - 1) / zxs_dev::kTileShots;
     if (a.n_tiles == 0) return;
-    uint64_t want = (a.n_tiles + kThreads / 32 - 1) / (kThreads / 32);
     uint64_t cap = uint64_t(s->sm_count) * s->blocks_per_sm;
-    unsigned grid = unsigned(std::min(want, cap));
+    unsigned grid = unsigned(std::min(a.n_tiles, cap));
     size_t smem = shot_smem_bytes(s);
-    void *args[] = {&a};
-    CK(cudaLaunchKernel(shot_kernel_for(s->fw_template), dim3(grid), dim3(kThreads), args, smem, st));
+    static zxs_dev::MechTable<1> unused_table{};
+    void *args[] = {&a, s->param_mechs ? static_cast<void *>(s->mech_table.get()) : static_cast<void *>(&unused_table)};
+    CK(cudaLaunchKernel(shot_kernel_for(s->fw_template, s->param_mechs), dim3(grid), dim3(32), args, smem, st));
 }
 
 void check_ratio_error(zxs_sampler *s, cudaStream_t st) {
@@ -526,7 +553,11 @@ void check_mode(const zxs_sampler *s, uint32_t expected) {
     }
 }
 
-cudaStream_t pick(zxs_sampler *s, void *stream) {
+// Device-side entry points take the caller's stream as is (NULL is the
+// legacy default stream, as everywhere in CUDA); synchronous host entry
+// points use the sampler's own stream when given NULL.
+cudaStream_t device_stream(void *stream) { return reinterpret_cast<cudaStream_t>(stream); }
+cudaStream_t host_stream(zxs_sampler *s, void *stream) {
     return stream ? reinterpret_cast<cudaStream_t>(stream) : s->stream;
 }
 
@@ -591,7 +622,7 @@ zxs_status zxs_sample_device(zxs_sampler *s, uint64_t seed, uint64_t first_shot,
         if (!s) fail(ZXS_INVALID_ARGUMENT, "null sampler");
         if (dev_columns && ld_words < (shots + 63) / 64) fail(ZXS_INVALID_ARGUMENT, "ld_words < ceil(shots/64)");
         DeviceGuard g(s->device);
-        cudaStream_t st = pick(s, stream);
+        cudaStream_t st = device_stream(stream);
         if (dev_columns && !s->all_outputs_covered) {
             CK(cudaMemsetAsync(dev_columns, 0, size_t(s->m.num_outputs) * ld_words * 8, st));
         }
@@ -620,7 +651,7 @@ zxs_status zxs_check_errors(zxs_sampler *s, void *stream) {
     return guarded([&] {
         if (!s) fail(ZXS_INVALID_ARGUMENT, "null sampler");
         DeviceGuard g(s->device);
-        check_ratio_error(s, pick(s, stream));
+        check_ratio_error(s, device_stream(stream));
     });
 }
 
@@ -630,7 +661,7 @@ zxs_status zxs_count(zxs_sampler *s, uint64_t seed, uint64_t first_shot, uint64_
         if (!s || !host_counts) fail(ZXS_INVALID_ARGUMENT, "null argument");
         std::lock_guard<std::mutex> lk(s->mu);
         DeviceGuard g(s->device);
-        cudaStream_t st = pick(s, stream);
+        cudaStream_t st = host_stream(s, stream);
         size_t bytes = size_t(s->m.num_outputs) * 8;
         auto *dc = reinterpret_cast<unsigned long long *>(s->scratch_get(std::max<size_t>(bytes, 8)));
         CK(cudaMemsetAsync(dc, 0, bytes, st));
@@ -658,7 +689,7 @@ zxs_status zxs_sample(zxs_sampler *s, uint32_t expected_mode, uint64_t seed, uin
         if (!host_columns) fail(ZXS_INVALID_ARGUMENT, "null output");
         std::lock_guard<std::mutex> lk(s->mu);
         DeviceGuard g(s->device);
-        cudaStream_t st = pick(s, stream);
+        cudaStream_t st = host_stream(s, stream);
         const uint64_t words = (shots + 63) / 64;
         const uint32_t nout = s->m.num_outputs;
         if (nout == 0) {
@@ -778,9 +809,9 @@ void eval_on_device(zxs_sampler *s, uint32_t tensor, const uint64_t *host_params
     if (pbytes) CK(cudaMemcpyAsync(dp, host_params, pbytes, cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(dmi, 0, 8, st));
     uint32_t col_stride = std::max<uint32_t>(4, (param_cols + 3) & ~3u);
-    uint64_t n_tiles = 2 * words;
+    uint64_t n_tiles = words;
     unsigned grid = unsigned(std::min<uint64_t>((n_tiles + 7) / 8, uint64_t(s->sm_count) * 8));
-    size_t smem = size_t(8) * col_stride * 4;
+    size_t smem = size_t(8) * zxs_dev::kS * col_stride * 4;
     if (smem > 48 * 1024) {
         CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(&zxs_dev::eval_kernel),
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

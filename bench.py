@@ -40,11 +40,22 @@ WORKLOADS = {
                         "[[19,1,5]] colour code X-memory, 3 rounds, p=1e-3, R_Z on 3 data (chi=64)", 1 << 22, False),
     "c5_surface_d7_r7": ("tests/golden/c5_surface_d7_r7.zxs", 4,
                          "d=7 rotated surface code Z-memory, 7 rounds, p=1e-3, count-only sweep", 1 << 24, True),
-    "c3_cultivation_proxy": ("data/c3_cultivation_proxy.zxs", 2,
+    "c3_cultivation_proxy": ("data/c3_cultivation_proxy.zxs.gz", 2,
                              "Steane-code cultivation proxy: T injection + 2 transversal T checks (chi=46656)",
                              1 << 14, False),
 }
 DEFAULT_WORKLOAD = "c2_surface_d3_xmem_t"
+
+
+def _measured_hbm_gbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fp:
+            return float(json.load(fp)["hbm_gbs"])
+    except Exception:
+        return 6650.0  # B200_PROFILING.md fallback
+
+
+MEASURED_HBM_GBS = _measured_hbm_gbs()
 
 
 def dist_env():
@@ -257,11 +268,14 @@ def run_ours(args, wl):
         e2e_local = tt.item()
     e2e_value = e2e_shots * args.steps * world / e2e_local
 
-    # ---- roofline: Philox-bound integer pipeline
+    # ---- roofline: the shot kernel is bound by the
+    # 32x32->64 integer multiplies of Philox4x32-10 (IMAD.WIDE on the
+    # fmaheavy pipe). Algorithmic work = Philox blocks per shot (mechanisms +
+    # autoregressive draws); peak = the same Philox code with no other work,
+    # measured live on this GPU (zxs_measure_philox_peak).
     blocks_per_shot = info["philox_blocks_per_shot"]
-    ops_per_block = 40  # 10 rounds x (2 wide multiplies + 2 three-input XORs)
-    achieved_tops = shots * blocks_per_shot * ops_per_block / (ms_per_step / 1e3) / 1e12 / 1  # per GPU
-    peak = args.int_peak_tops
+    achieved = shots * blocks_per_shot / (ms_per_step / 1e3) / 1e9  # Gblocks/s per GPU
+    peak = zx.measure_philox_peak(local) / 1e9
     clocks = clk.summary()
     line = {
         "metric": "detector_shots_per_sec", "value": value, "unit": "shots/s", "n_gpus": world,
@@ -274,10 +288,15 @@ def run_ours(args, wl):
         "e2e": {"value": e2e_value, "unit": "shots/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": int(nout * ((e2e_shots + 63) // 64) * 8), "shots_per_step": e2e_shots},
         "gpu_launches": args.steps,
-        "roofline": {"bound": "int", "achieved": achieved_tops, "peak": peak, "unit": "Tops/s",
-                     "frac": achieved_tops / peak, "traffic": None,
-                     "basis": f"{blocks_per_shot} Philox4x32-10 blocks/shot x {ops_per_block} int ops",
-                     "peak_source": args.int_peak_source},
+        "roofline": {"bound": "int", "achieved": achieved, "peak": peak, "unit": "GPhilox-blocks/s",
+                     "frac": achieved / peak, "traffic": args.traffic_bytes,
+                     "basis": f"{blocks_per_shot} Philox4x32-10 blocks/shot ({info['num_mechanisms']} mechanisms + "
+                              f"{blocks_per_shot - info['num_mechanisms']} autoregressive draws), shot kernel only",
+                     "peak_source": "measured live: zxs_measure_philox_peak (same Philox code, no other work); "
+                                    "integer-multiply (fmaheavy) bound",
+                     "hbm": {"bytes_per_step": int(nout * words * 8) if not count_only else int(nout * 8),
+                             "achieved_gbs": (nout * words * 8 if not count_only else 0) / (ms_per_step / 1e3) / 1e9,
+                             "peak_gbs": MEASURED_HBM_GBS}},
         "clocks": clocks,
         "kernel_ms": kernel_ms if len(kernel_ms) <= 20 else None,
     }
@@ -303,8 +322,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=3.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--int-peak-tops", type=float, default=148 * 128 * 1.965e9 / 1e12)
-    ap.add_argument("--int-peak-source", default="nominal: 148 SMs x 128 int32 lanes/clk (FMA+ALU pipes) x 1965 MHz")
+    ap.add_argument("--traffic-bytes", type=float, default=None,
+                    help="dram bytes per launch from an ncu --set full capture of this configuration")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":

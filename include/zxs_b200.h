@@ -217,6 +217,11 @@ zxs_status zxs_probability_of_at(zxs_sampler *s, const uint8_t *outcome, uint32_
 zxs_status zxs_philox_uniform(int device, uint64_t seed, uint32_t stream, uint64_t first_index,
                               uint64_t n, double *host_out);
 
+/* Diagnostic: Philox4x32-10 blocks/s of this library's draw code (the shot
+   kernel's Philox and filter compare, same launch shape, no memory traffic)
+   on `device` -- the same-op-mix roofline of the error draw. */
+zxs_status zxs_measure_philox_peak(int device, double *blocks_per_s);
+
 #ifdef __cplusplus
 }
 #endif

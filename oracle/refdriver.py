@@ -95,7 +95,17 @@ class RefModel:
     @classmethod
     def load(cls, path: str) -> "RefModel":
         h = ctypes.c_void_p()
-        _check(lib().zr_load(os.fsencode(path), ctypes.byref(h)))
+        if path.endswith(".gz"):  # the C++ loader reads plain .zxs: inflate to a temp file
+            import gzip
+            import shutil
+            import tempfile
+            with tempfile.NamedTemporaryFile(suffix=".zxs") as tmp:
+                with gzip.open(path, "rb") as src:
+                    shutil.copyfileobj(src, tmp, 1 << 24)
+                tmp.flush()
+                _check(lib().zr_load(os.fsencode(tmp.name), ctypes.byref(h)))
+        else:
+            _check(lib().zr_load(os.fsencode(path), ctypes.byref(h)))
         return cls(h)
 
     def save(self, path: str):

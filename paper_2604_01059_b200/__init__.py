@@ -15,6 +15,7 @@ from .sampler import (  # noqa: F401
     SamplerOptions,
     count_outputs,
     eval_batch,
+    measure_philox_peak,
     philox_uniform,
     probability_of_at,
     sample_detectors,
@@ -25,6 +26,6 @@ from .sampler import (  # noqa: F401
 
 __all__ = [
     "MODE_DETECTORS", "MODE_MEASUREMENTS", "BatchEvalResult", "CompiledSampler", "SampleRecord",
-    "SamplerOptions", "count_outputs", "eval_batch", "philox_uniform", "probability_of_at",
+    "SamplerOptions", "count_outputs", "eval_batch", "measure_philox_peak", "philox_uniform", "probability_of_at",
     "sample_detectors", "sample_error_batch", "sample_given_f", "sample_measurements",
 ]

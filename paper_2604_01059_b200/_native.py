@@ -11,7 +11,8 @@ import os
 
 from . import zxs_format as _fmt
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libzxs_b200.so")
+LIB_PATH = os.environ.get("ZXS_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                         "libzxs_b200.so")
 
 ZXS_OK, ZXS_INVALID_ARGUMENT, ZXS_RUNTIME_ERROR, ZXS_CUDA_ERROR, ZXS_OUT_OF_MEMORY, ZXS_UNSUPPORTED = range(6)
 
@@ -56,6 +57,7 @@ SIGNATURES = (
     ("zxs_probability_of_at", ctypes.c_int, [_vp, _u8p, ctypes.c_uint32, _u8p, ctypes.c_uint32, _dp]),
     ("zxs_philox_uniform", ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
                                           ctypes.c_uint64, _dp]),
+    ("zxs_measure_philox_peak", ctypes.c_int, [ctypes.c_int, _dp]),
 )
 
 _lib = None

@@ -125,6 +125,7 @@ struct zxs_sampler {
     bool param_mechs = true;
     std::unique_ptr<zxs_dev::MechTable<zxs_dev::kParamMechs>> mech_table;
     const zxs_dev::MechRec *mech_global = nullptr;
+    const zxs_dev::MechFast *fast_global = nullptr;
     const uint32_t *ext_begin = nullptr;
     const ulonglong2 *ext = nullptr;
     uint32_t dead_mechanisms = 0;
@@ -269,7 +270,7 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         zxs_dev::MechRec rec;
         ext_begin.push_back(static_cast<uint32_t>(ext.size()));
         if (scan.empty()) {
-            rec.lim0 = 0;  // never fires
+            rec.lim0 = ~0ull;  // always "hits" the no-flip entry
             rec.flip0 = zxs_dev::kNoFlip;
             rec.n_extra = 0;
             dead++;
@@ -401,6 +402,21 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     Arena ar;
     std::vector<zxs_dev::MechRec> recs_pad = recs.empty() ? std::vector<zxs_dev::MechRec>(1) : recs;
     size_t o_recs = ar.add(recs_pad);
+    // fast filters (see zxs_dev::MechFast)
+    std::vector<zxs_dev::MechFast> fast(recs.size());
+    for (size_t i = 0; i < recs.size(); i++) {
+        const zxs_dev::MechRec &r = recs[i];
+        const uint32_t hi = uint32_t(r.lim0 >> 32);
+        if (r.flip0 == zxs_dev::kNoFlip) {
+            fast[i] = {hi, 0u};                 // hit at entry 0 = no error
+        } else if (r.n_extra == 0) {
+            fast[i] = {~hi, 0xffffffffu};       // miss = no error
+        } else {
+            fast[i] = {0u, 0u};                 // always resolve exactly
+        }
+    }
+    std::vector<zxs_dev::MechFast> fast_pad = fast.empty() ? std::vector<zxs_dev::MechFast>(1, {0u, 0u}) : fast;
+    size_t o_fast = ar.add(fast_pad);
     std::vector<uint32_t> ext_begin_pad = ext_begin.empty() ? std::vector<uint32_t>(1, 0) : ext_begin;
     size_t o_extb = ar.add(ext_begin_pad);
     size_t o_ext = ar.add(ext.empty() ? std::vector<ulonglong2>(1, make_ulonglong2(0, 0)) : ext);
@@ -447,8 +463,9 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     s->param_mechs = d->num_mechanisms <= zxs_dev::kParamMechs;
     if (s->param_mechs) {
         s->mech_table.reset(new zxs_dev::MechTable<zxs_dev::kParamMechs>());
-        std::copy(recs.begin(), recs.end(), s->mech_table->rec);
+        std::copy(fast.begin(), fast.end(), s->mech_table->fast);
     }
+    s->fast_global = reinterpret_cast<const zxs_dev::MechFast *>(b + o_fast);
     s->dead_mechanisms = dead;
     m.flip_mask = reinterpret_cast<const uint64_t *>(b + o_flip);
     m.base_offset = reinterpret_cast<const uint64_t *>(b + o_base);
@@ -519,6 +536,7 @@ void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
     a.m = s->m;
     a.num_mech = s->info.num_mechanisms;
     a.mech_global = s->mech_global;
+    a.fast_global = s->fast_global;
     a.ext_begin = s->ext_begin;
     a.ext = s->ext;
     a.err = s->dev_err;
@@ -894,6 +912,40 @@ zxs_status zxs_probability_of_at(zxs_sampler *s, const uint8_t *outcome, uint32_
             p *= prev / norm;
         }
         *out = p;
+    });
+}
+
+zxs_status zxs_measure_philox_peak(int device, double *blocks_per_s) {
+    return guarded([&] {
+        if (!blocks_per_s) fail(ZXS_INVALID_ARGUMENT, "null output");
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) fail(ZXS_CUDA_ERROR, "no CUDA device available");
+        DeviceGuard g(device);
+        int sms = 0, occ = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, zxs_dev::philox_peak_kernel, 32, 0));
+        zxs_dev::LaunchArgs a{};
+        a.seed = 0x0123456789abcdefull;
+        for (int i = 0; i < 10; i++) a.k0_round[i] = uint32_t(a.seed) + uint32_t(i) * 0x9E3779B9u;
+        uint32_t *sink = nullptr;
+        CK(cudaMalloc(&sink, 4));
+        const uint32_t nmech = 256, tiles = 16;
+        const unsigned grid = unsigned(sms * std::max(occ, 1));
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        zxs_dev::philox_peak_kernel<<<grid, 32>>>(a, nmech, tiles, sink);  // warm-up
+        CK(cudaEventRecord(e0));
+        const int reps = 5;
+        for (int r = 0; r < reps; r++) zxs_dev::philox_peak_kernel<<<grid, 32>>>(a, nmech, tiles, sink);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaFree(sink);
+        *blocks_per_s = double(reps) * grid * tiles * zxs_dev::kTileShots * nmech / (ms * 1e-3);
     });
 }
 

@@ -28,7 +28,7 @@ namespace zxs_dev {
 
 constexpr int kS = 2;                 // shots per lane
 constexpr int kTileShots = 32 * kS;   // shots per warp tile = one u64 word
-constexpr uint32_t kParamMechs = 1920;
+constexpr uint32_t kParamMechs = 3600;
 
 // One mechanism: the first scan entry inline; further entries (joint tables)
 // in global memory at ext_begin[m] .. ext_begin[m] + n_extra.
@@ -38,16 +38,27 @@ struct __align__(16) MechRec {
     uint32_t n_extra;         // number of further entries
 };
 
+// Fast filter of one mechanism, read every draw: the draw certainly needs no
+// flip when ((r01 >> 32) ^ sense) < thr. sense = 0, thr = hi32(lim0) when the
+// first entry is "no error" (joint tables); sense = ~0, thr = ~hi32(lim0) when
+// the first entry flips and there are no further entries (singles); thr = 0
+// (always take the exact path) otherwise. The exact comparison with the full
+// MechRec runs only in the rare warp-uniform slow path.
+struct MechFast {
+    uint32_t thr, sense;
+};
+
 template <uint32_t N>
 struct MechTable {
-    MechRec rec[N];
+    MechFast fast[N];
 };
 static_assert(kS == 2, "output stores pack two 32-shot words");
 
 struct LaunchArgs {
     DevModel m;
     uint32_t num_mech;             // reference mechanism count (streams 0..num_mech-1)
-    const MechRec *mech_global;    // used when num_mech > kParamMechs
+    const MechRec *mech_global;    // [num_mech] full records (slow path)
+    const MechFast *fast_global;   // [num_mech] filters, used when num_mech > kParamMechs
     const uint32_t *ext_begin;     // [num_mech]
     const ulonglong2 *ext;         // {lim, flip}
     uint64_t seed, first_shot, shots, n_tiles;
@@ -69,39 +80,66 @@ __device__ __forceinline__ void mul_wide(uint32_t a, uint32_t b, uint32_t &lo, u
     asm("{\n\t.reg .b64 t;\n\tmul.wide.u32 t, %2, %3;\n\tmov.b64 {%0, %1}, t;\n\t}" : "=r"(lo), "=r"(hi) : "r"(a), "r"(b));
 }
 
-// S Philox4x32-10 blocks sharing the key (seed_lo, seed_hi ^ stream): the
-// reference's Philox(seed, stream).uniform2_at(idx) (rng.hpp:27-38) up to the
-// (r0 << 32 | r1) word. Round structure per rng.hpp:44-56. The key-0 schedule
-// depends only on the seed and is read from the launch parameters (constant
-// bank operands of the LOP3s); the key-1 schedule depends on the stream.
+constexpr uint32_t kM0 = 0xD2511F53u, kM1 = 0xCD9E8D57u, kW1 = 0xBB67AE85u;
+constexpr uint64_t kP1c = uint64_t(kM1) * 0x9e3779b9u;  // round-1 product of the constant counter word
+
+// Mechanism-independent part of Philox rounds 1-2 for one shot index: with
+// ctr = {idx_lo, idx_hi, 0x9e3779b9, 0} (rng.hpp:32-33), round 1's first
+// product and round 2's first product depend only on the shot and key 0.
+struct PhiloxPre {
+    uint32_t a;   // hi32(M0 * idx_lo)
+    uint32_t x;   // hi32(M0 * c0_1) ^ lo32(M0 * idx_lo)
+    uint32_t l2;  // lo32(M0 * c0_1)
+};
+
+__device__ __forceinline__ PhiloxPre philox_pre(uint32_t idx_lo, uint32_t idx_hi, uint32_t k0_0) {
+    uint32_t A, B, H2, L2;
+    mul_wide(idx_lo, kM0, B, A);
+    const uint32_t c0_1 = uint32_t(kP1c >> 32) ^ idx_hi ^ k0_0;
+    mul_wide(c0_1, kM0, L2, H2);
+    return PhiloxPre{A, H2 ^ B, L2};
+}
+
+// The rest of Philox4x32-10 for key (seed_lo, k1) (rng.hpp:44-68): 16 wide
+// multiplies per block instead of 20. Returns r0 ^ (k9 ^ k0_round[9]) and r1,
+// i.e. r0 itself when k9 == k0_round[9] (k9 may fold in a filter mask).
 template <int S>
-__device__ __forceinline__ void philox_multi(const uint32_t (&k0r)[10], uint32_t k1, const uint32_t (&lo)[S],
-                                             const uint32_t (&hi)[S], uint64_t (&r)[S]) {
+__device__ __forceinline__ void philox_tail(const PhiloxPre (&p)[S], uint32_t k1, const uint32_t (&k0r)[10],
+                                            uint32_t k2c, uint32_t k9, uint32_t (&rhi)[S], uint32_t (&rlo)[S]) {
     uint32_t c0[S], c1[S], c2[S], c3[S];
+    const uint32_t k1_1 = k1 + kW1;
 #pragma unroll
-    for (int s = 0; s < S; s++) {
-        c0[s] = lo[s];
-        c1[s] = hi[s];
-        c2[s] = 0x9e3779b9u;
-        c3[s] = 0u;
+    for (int s = 0; s < S; s++) {  // rounds 1 and 2
+        uint32_t h, l;
+        mul_wide(p[s].a ^ k1, kM1, l, h);
+        c0[s] = h ^ k2c;  // hi32(M1 * c2_1) ^ lo32(kP1c) ^ k0r[1]
+        c1[s] = l;
+        c2[s] = p[s].x ^ k1_1;
+        c3[s] = p[s].l2;
     }
+    uint32_t k1i = k1 + 2 * kW1;
 #pragma unroll
-    for (int i = 0; i < 10; i++) {
+    for (int i = 2; i <= 8; i++) {  // rounds 3..9
 #pragma unroll
         for (int s = 0; s < S; s++) {
             uint32_t h0, l0, h1, l1;
-            mul_wide(c0[s], 0xD2511F53u, l0, h0);
-            mul_wide(c2[s], 0xCD9E8D57u, l1, h1);
-            const uint32_t n0 = h1 ^ c1[s] ^ k0r[i], n2 = h0 ^ c3[s] ^ k1;
+            mul_wide(c0[s], kM0, l0, h0);
+            mul_wide(c2[s], kM1, l1, h1);
+            const uint32_t n0 = h1 ^ c1[s] ^ k0r[i], n2 = h0 ^ c3[s] ^ k1i;
             c0[s] = n0;
             c1[s] = l1;
             c2[s] = n2;
             c3[s] = l0;
         }
-        k1 += 0xBB67AE85u;
+        k1i += kW1;
     }
 #pragma unroll
-    for (int s = 0; s < S; s++) r[s] = (uint64_t(c0[s]) << 32) | c1[s];
+    for (int s = 0; s < S; s++) {  // round 10: only r0, r1 are used (rng.hpp:35)
+        uint32_t h1, l1;
+        mul_wide(c2[s], kM1, l1, h1);
+        rhi[s] = h1 ^ c1[s] ^ k9;
+        rlo[s] = l1;
+    }
 }
 
 // eval_batch (phase_terms.cpp:90-144) for the kS 32-shot sub-tiles of a warp
@@ -179,7 +217,10 @@ __device__ __noinline__ uint2 resolve_flips(uint64_t r0, uint64_t r1, MechRec md
 }
 
 template <int FW, bool PARAM_MECHS>
-__global__ void __launch_bounds__(128) shot_kernel(const __grid_constant__ LaunchArgs a,
+#ifndef ZXS_MAXNREG
+#define ZXS_MAXNREG 80
+#endif
+__global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ LaunchArgs a,
                                                    const __grid_constant__ MechTable<PARAM_MECHS ? kParamMechs : 1> mt) {
     extern __shared__ __align__(16) uint32_t smem[];
     // One warp per CTA: the tile loop depends only on blockIdx, so the
@@ -194,17 +235,18 @@ __global__ void __launch_bounds__(128) shot_kernel(const __grid_constant__ Launc
         __syncwarp();
     }
     const uint32_t seed_hi = uint32_t(a.seed >> 32);
+    const uint32_t k2c = uint32_t(kP1c) ^ a.k0_round[1];
 
     for (uint64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
         uint64_t local[kS], shot[kS];
-        uint32_t vmask[kS], idx_lo[kS], idx_hi[kS];
+        uint32_t vmask[kS];
+        PhiloxPre pre[kS];
 #pragma unroll
         for (int s = 0; s < kS; s++) {
             local[s] = tile * kTileShots + 32 * s + lane;
             vmask[s] = __ballot_sync(kFull, local[s] < a.shots);
             shot[s] = a.first_shot + local[s];
-            idx_lo[s] = uint32_t(shot[s]);
-            idx_hi[s] = uint32_t(shot[s] >> 32);
+            pre[s] = philox_pre(uint32_t(shot[s]), uint32_t(shot[s] >> 32), a.k0_round[0]);
         }
 
         // ---- (1)-(3): f configuration as bit-sliced columns
@@ -224,21 +266,21 @@ __global__ void __launch_bounds__(128) shot_kernel(const __grid_constant__ Launc
             for (uint32_t mi = 0; mi < a.num_mech; mi++) {
                 // No early-out for mechanisms that cannot flip anything: a
                 // data-dependent `continue` here moves the key schedule off the
-                // uniform datapath. Such records never fire (lim0 = 0, no flip).
-                const MechRec md = PARAM_MECHS ? mt.rec[mi] : a.mech_global[mi];
-                uint64_t r[kS];
-                philox_multi<kS>(a.k0_round, seed_hi ^ mi, idx_lo, idx_hi, r);  // stream = mechanism index
-                // Common case: every lane's draw resolves at the first entry with
-                // no flip (no error). Anything else goes through one warp-uniform
-                // branch, which keeps the loop (and the key schedule) uniform.
+                // uniform datapath. Such records never flip.
+                const MechFast mf = PARAM_MECHS ? mt.fast[mi] : a.fast_global[mi];
+                uint32_t rhi[kS], rlo[kS];
+                philox_tail<kS>(pre, seed_hi ^ mi, a.k0_round, k2c, a.k0_round[9] ^ mf.sense, rhi, rlo);
+                // Common case: every lane's draw certainly resolves to "no flip"
+                // (no error); anything else takes one warp-uniform branch, which
+                // keeps the loop (and the key schedule) uniform.
                 bool busy = false;
 #pragma unroll
-                for (int s = 0; s < kS; s++) {
-                    const bool hit0 = r[s] <= md.lim0;
-                    busy |= hit0 ? (md.flip0 != kNoFlip) : (md.n_extra != 0);
-                }
+                for (int s = 0; s < kS; s++) busy |= !(rhi[s] < mf.thr);
                 if (__any_sync(kFull, busy)) {
-                    const uint2 fl = resolve_flips(r[0], r[1], md, a.ext_begin, a.ext, mi);
+                    const MechRec md = a.mech_global[mi];
+                    const uint64_t r0 = (uint64_t(rhi[0] ^ mf.sense) << 32) | rlo[0];
+                    const uint64_t r1 = (uint64_t(rhi[1] ^ mf.sense) << 32) | rlo[1];
+                    const uint2 fl = resolve_flips(r0, r1, md, a.ext_begin, a.ext, mi);
                     const uint32_t flip[kS] = {fl.x, fl.y};
 #pragma unroll
                     for (int s = 0; s < kS; s++) {
@@ -312,10 +354,10 @@ __global__ void __launch_bounds__(128) shot_kernel(const __grid_constant__ Launc
             for (int s = 0; s < kS; s++) prev[s] = acc[s].x;
             for (uint32_t pos = 0; pos < n; pos++, upos++) {
                 eval_tensor(m, tb + 1 + pos, cols, m.col_stride, lane, acc);
-                uint64_t rr[kS];
+                uint32_t rhi[kS], rlo[kS];
                 if (!a.uniforms) {
                     const uint32_t stream = 0x80000000u ^ (ci << 12) ^ pos;  // sampler.cpp:37-39
-                    philox_multi<kS>(a.k0_round, seed_hi ^ stream, idx_lo, idx_hi, rr);
+                    philox_tail<kS>(pre, seed_hi ^ stream, a.k0_round, k2c, a.k0_round[9], rhi, rlo);
                 }
                 uint32_t word[kS];
 #pragma unroll
@@ -327,7 +369,7 @@ __global__ void __launch_bounds__(128) shot_kernel(const __grid_constant__ Launc
                     double cl = (0.0 < ratio) ? ratio : 0.0;  // std::max(0.0, ratio)
                     cl = (cl < 1.0) ? cl : 1.0;               // std::min(1.0, .)
                     const double u = a.uniforms ? (valid ? a.uniforms[upos * a.uniforms_ld + local[s]] : 0.0)
-                                                : philox_uniform(rr[s]);
+                                                : philox_uniform((uint64_t(rhi[s]) << 32) | rlo[s]);
                     const bool bit = !(u < cl);
                     prev[s] = bit ? __dsub_rn(prev[s], cur) : cur;
                     word[s] = __ballot_sync(kFull, bit) & vmask[s];
@@ -384,6 +426,33 @@ __global__ void __launch_bounds__(256) eval_kernel(DevModel m, uint32_t tensor, 
         }
         __syncwarp();
     }
+}
+
+// Same-op-mix roofline for the error draw: the shot kernel's Philox code
+// (philox_pre once per tile, philox_tail + filter compare per mechanism,
+// kS shots per lane, one warp per CTA) with no memory traffic at all.
+__global__ void __maxnreg__(ZXS_MAXNREG) philox_peak_kernel(const __grid_constant__ LaunchArgs a, uint32_t nmech,
+                                                            uint32_t tiles_per_cta, uint32_t *sink) {
+    const uint32_t lane = threadIdx.x, seed_hi = uint32_t(a.seed >> 32);
+    const uint32_t k2c = uint32_t(kP1c) ^ a.k0_round[1];
+    uint32_t acc = 0;
+    for (uint32_t t = 0; t < tiles_per_cta; t++) {
+        PhiloxPre pre[kS];
+#pragma unroll
+        for (int s = 0; s < kS; s++) {
+            const uint64_t shot = (uint64_t(blockIdx.x) * tiles_per_cta + t) * kTileShots + 32 * s + lane;
+            pre[s] = philox_pre(uint32_t(shot), uint32_t(shot >> 32), a.k0_round[0]);
+        }
+        for (uint32_t mi = 0; mi < nmech; mi++) {
+            uint32_t rhi[kS], rlo[kS];
+            philox_tail<kS>(pre, seed_hi ^ mi, a.k0_round, k2c, a.k0_round[9], rhi, rlo);
+            bool busy = false;
+#pragma unroll
+            for (int s = 0; s < kS; s++) busy |= !(rhi[s] < 0xffff0000u);
+            if (__any_sync(kFull, busy)) acc ^= rlo[0] ^ rlo[1];
+        }
+    }
+    if (acc == 0x9e3779b9u) sink[0] = acc;  // keeps the work observable
 }
 
 __global__ void philox_kernel(uint64_t seed, uint32_t stream, uint64_t first, uint64_t n, double *out) {

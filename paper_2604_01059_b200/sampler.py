@@ -223,6 +223,13 @@ def probability_of_at(cs: CompiledSampler, outcome, f_assignment) -> float:
     return out.value
 
 
+def measure_philox_peak(device: int = 0) -> float:
+    """Philox4x32-10 blocks/s of the draw code alone (same-op-mix roofline)."""
+    out = ctypes.c_double()
+    _native.check(_native.lib().zxs_measure_philox_peak(device, ctypes.byref(out)))
+    return out.value
+
+
 def philox_uniform(seed: int, stream: int, first_index: int, n: int, device: int = 0) -> np.ndarray:
     """Philox(seed, stream).uniform_at(first_index + i), i < n, on the device."""
     out = np.zeros(n, np.float64)

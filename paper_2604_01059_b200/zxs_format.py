@@ -53,8 +53,14 @@ FIELDS = (
 
 
 def load(path: str) -> dict:
-    with open(path, "rb") as fp:
-        data = fp.read()
+    """Reads a .zxs file (or a gzip-compressed .zxs.gz)."""
+    if path.endswith(".gz"):
+        import gzip
+        with gzip.open(path, "rb") as fp:
+            data = fp.read()
+    else:
+        with open(path, "rb") as fp:
+            data = fp.read()
     if data[:4] != b"ZXS1":
         raise ValueError(f"not a .zxs file: {path}")
     (n,) = struct.unpack_from("<I", data, 8)

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -28,7 +29,7 @@
 #include <vector>
 
 #include "zxs_b200.h"
-#include "zxs_kernels.cuh"
+#include "zxs_heavy.cuh"
 
 using zxs_dev::DevModel;
 using zxs_dev::Factor;
@@ -137,6 +138,25 @@ struct zxs_sampler {
     int sm_count = 148;
     int blocks_per_sm = 1;
     std::mutex mu;
+    // heavy (large-chi) components, see zxs_heavy.cuh
+    bool has_heavy = false;
+    zxs_dev::HeavyArgs heavy{};
+    size_t heavy_smem = 0;
+    int heavy_blocks_per_sm = 0;
+    uint64_t heavy_words = 0;
+    char *heavy_scratch = nullptr;
+    size_t heavy_scratch_bytes = 0;
+
+    uint32_t *heavy_fcols_get(size_t bytes) {
+        if (bytes > heavy_scratch_bytes) {
+            if (heavy_scratch) CK(cudaFree(heavy_scratch));
+            heavy_scratch = nullptr;
+            heavy_scratch_bytes = 0;
+            CK(cudaMalloc(&heavy_scratch, bytes));
+            heavy_scratch_bytes = bytes;
+        }
+        return reinterpret_cast<uint32_t *>(heavy_scratch);
+    }
 
     char *scratch_get(size_t bytes) {
         if (bytes > scratch_bytes) {
@@ -398,6 +418,101 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         }
     }
 
+    // ---- heavy components: compact chunked streams (zxs_heavy.cuh)
+    uint64_t heavy_min = 20000;
+    if (const char *e = std::getenv("ZXS_HEAVY_MIN_FACTORS")) heavy_min = std::strtoull(e, nullptr, 10);
+    std::vector<uint8_t> comp_heavy(std::max<uint32_t>(1, d->num_components), 0);
+    std::vector<uint32_t> hw;                 // words
+    std::vector<uint4> hchunks;
+    std::vector<uint32_t> htcb{0};            // tensor -> first chunk
+    std::vector<zxs_dev::HeavyComp> hcomps;
+    uint32_t heavy_max_chain = 0;
+    {
+        uint32_t upos = 0;
+        for (uint32_t c = 0; c < d->num_components; c++) {
+            const uint32_t n = d->comp_out_begin[c + 1] - d->comp_out_begin[c];
+            const uint32_t t0 = d->comp_tensor_begin[c], t1 = d->comp_tensor_begin[c + 1];
+            uint64_t nf = d->term_factor_begin[d->tensor_term_begin[t1]] - d->term_factor_begin[d->tensor_term_begin[t0]];
+            bool ok = nf >= heavy_min && d->num_h_tables <= 256 && hcomps.size() < size_t(zxs_dev::kMaxHeavyComps) &&
+                      fwid + n <= 256;
+            // encode every tensor of the chain; abandon (light path) on any misfit
+            std::vector<uint32_t> w;
+            std::vector<uint4> ch;
+            std::vector<uint32_t> tcb;
+            for (uint32_t t = t0; ok && t < t1; t++) {
+                uint32_t cur_begin = uint32_t(hw.size() + w.size()), cur_terms = 0;
+                auto close_chunk = [&]() {
+                    while ((hw.size() + w.size()) % 4) w.push_back(0);
+                    uint32_t end = uint32_t(hw.size() + w.size());
+                    ch.push_back(make_uint4(cur_begin, end - cur_begin, cur_terms, 0));
+                    cur_begin = end;
+                    cur_terms = 0;
+                };
+                tcb.push_back(uint32_t(hchunks.size() + ch.size()));
+                for (uint64_t term = d->tensor_term_begin[t]; ok && term < d->tensor_term_begin[t + 1]; term++) {
+                    std::vector<uint32_t> tw;
+                    const uint64_t f0 = d->term_factor_begin[term], f1 = d->term_factor_begin[term + 1];
+                    uint64_t re, im;
+                    std::memcpy(&re, &d->term_c[2 * term], 8);
+                    std::memcpy(&im, &d->term_c[2 * term + 1], 8);
+                    tw.push_back(uint32_t(f1 - f0));
+                    tw.push_back(uint32_t(re));
+                    tw.push_back(uint32_t(re >> 32));
+                    tw.push_back(uint32_t(im));
+                    tw.push_back(uint32_t(im >> 32));
+                    for (uint64_t k = f0; ok && k < f1; k++) {
+                        const uint64_t u0 = d->factor_u_begin[k], u1 = d->factor_u_begin[k + 1];
+                        const uint64_t v0 = d->factor_v_begin[k], v1 = d->factor_v_begin[k + 1];
+                        if (u1 - u0 > 255 || v1 - v0 > 255) {
+                            ok = false;
+                            break;
+                        }
+                        tw.push_back(d->factor_table[k] | uint32_t(u1 - u0) << 8 | uint32_t(v1 - v0) << 16);
+                        uint32_t word = 0, nb = 0;
+                        auto put = [&](uint32_t sel) {
+                            word |= (sel & 0xffu) << (8 * nb);
+                            if (++nb == 4) {
+                                tw.push_back(word);
+                                word = 0;
+                                nb = 0;
+                            }
+                        };
+                        for (uint64_t i = u0; i < u1; i++) put(d->factor_u_bits[i]);
+                        for (uint64_t i = v0; i < v1; i++) put(d->factor_v_bits[i]);
+                        if (nb) tw.push_back(word);
+                    }
+                    if (!ok) break;
+                    if (tw.size() + 4 > zxs_dev::kChunkWords) {
+                        ok = false;  // a single term larger than a chunk buffer
+                        break;
+                    }
+                    if (hw.size() + w.size() + tw.size() - cur_begin > zxs_dev::kChunkWords) close_chunk();
+                    w.insert(w.end(), tw.begin(), tw.end());
+                    cur_terms++;
+                }
+                if (ok && (cur_terms || hw.size() + w.size() == cur_begin)) close_chunk();
+            }
+            if (ok) {
+                zxs_dev::HeavyComp hc;
+                hc.ci = c;
+                hc.n_out = n;
+                hc.upos_base = upos;
+                hc.out_begin = d->comp_out_begin[c];
+                hc.first_tensor = uint32_t(htcb.size() - 1);
+                hw.insert(hw.end(), w.begin(), w.end());
+                hchunks.insert(hchunks.end(), ch.begin(), ch.end());
+                for (size_t i = 1; i < tcb.size(); i++) htcb.push_back(tcb[i]);
+                htcb.push_back(uint32_t(hchunks.size()));
+                hcomps.push_back(hc);
+                comp_heavy[c] = 1;
+                heavy_max_chain = std::max(heavy_max_chain, n);
+            }
+            upos += n;
+        }
+    }
+    if (hw.empty()) hw.assign(4, 0);
+    if (hchunks.empty()) hchunks.push_back(make_uint4(0, 0, 0, 0));
+
     // ---- device upload
     Arena ar;
     std::vector<zxs_dev::MechRec> recs_pad = recs.empty() ? std::vector<zxs_dev::MechRec>(1) : recs;
@@ -441,6 +556,10 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     size_t o_fac = ar.add(factors_pad);
     size_t o_sel = ar.add(selectors);
     size_t o_h = ar.add(h);
+    size_t o_cheavy = ar.add(comp_heavy);
+    size_t o_hchunks = ar.add(hchunks);
+    size_t o_htcb = ar.add(htcb);
+    size_t o_hw = ar.add(hw);
 
     CK(cudaMalloc(&s->dev_model, ar.host.size()));
     s->dev_model_bytes = ar.host.size();
@@ -481,6 +600,25 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     m.factors = reinterpret_cast<const Factor *>(b + o_fac);
     m.selectors = reinterpret_cast<const uint16_t *>(b + o_sel);
     m.h_table = reinterpret_cast<const double2 *>(b + o_h);
+    m.comp_heavy = reinterpret_cast<const uint8_t *>(b + o_cheavy);
+    s->has_heavy = !hcomps.empty();
+    if (s->has_heavy) {
+        zxs_dev::HeavyArgs &ha = s->heavy;
+        ha.f_width = fwid;
+        ha.col_words = fwid + heavy_max_chain;
+        ha.words = reinterpret_cast<const uint32_t *>(b + o_hw);
+        ha.chunks = reinterpret_cast<const uint4 *>(b + o_hchunks);
+        ha.tensor_chunk_begin = reinterpret_cast<const uint32_t *>(b + o_htcb);
+        ha.total_chunks = static_cast<uint32_t>(hchunks.size());
+        ha.comp_outputs = m.comp_outputs;
+        ha.htab = m.h_table;
+        ha.n_tables = std::max<uint32_t>(1, d->num_h_tables);
+        ha.n_comps = static_cast<uint32_t>(hcomps.size());
+        for (size_t i = 0; i < hcomps.size(); i++) ha.comps[i] = hcomps[i];
+        s->heavy_words = hw.size();
+        s->heavy_smem = 128 + 2 * size_t(zxs_dev::kChunkWords) * 4 + size_t(ha.n_tables) * 64 +
+                        size_t(zxs_dev::kHeavyWarps) * ha.col_words * zxs_dev::kHS * 4;
+    }
     m.mech_entry_begin = nullptr;
     m.mech_stream = nullptr;
     m.entry_lim = nullptr;
@@ -530,6 +668,13 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     }
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->blocks_per_sm, kern, 32, smem));
     if (s->blocks_per_sm < 1) fail(ZXS_UNSUPPORTED, "shot kernel does not fit on an SM");
+    if (s->has_heavy) {
+        const void *hk = reinterpret_cast<const void *>(&zxs_dev::heavy_kernel);
+        CK(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->heavy_smem)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->heavy_blocks_per_sm, hk, zxs_dev::kHeavyWarps * 32,
+                                                         s->heavy_smem));
+        if (s->heavy_blocks_per_sm < 1) fail(ZXS_UNSUPPORTED, "heavy kernel does not fit on an SM");
+    }
 }
 
 void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
@@ -548,8 +693,34 @@ void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
     unsigned grid = unsigned(std::min(a.n_tiles, cap));
     size_t smem = shot_smem_bytes(s);
     static zxs_dev::MechTable<1> unused_table{};
+    const bool heavy = s->has_heavy && !a.fcols_out;
+    if (heavy) {
+        a.heavy_ld32 = 2 * ((a.shots + 63) / 64);
+        a.heavy_fcols = s->heavy_fcols_get(std::max<size_t>(16, size_t(s->m.f_width) * a.heavy_ld32 * 4));
+    }
     void *args[] = {&a, s->param_mechs ? static_cast<void *>(s->mech_table.get()) : static_cast<void *>(&unused_table)};
     CK(cudaLaunchKernel(shot_kernel_for(s->fw_template, s->param_mechs), dim3(grid), dim3(32), args, smem, st));
+    if (heavy) {
+        zxs_dev::HeavyArgs h = s->heavy;
+        h.seed = a.seed;
+        h.first_shot = a.first_shot;
+        h.shots = a.shots;
+        for (int i = 0; i < 10; i++) h.k0_round[i] = a.k0_round[i];
+        h.fcols = a.heavy_fcols;
+        h.fcols_ld32 = a.heavy_ld32;
+        h.out32 = a.out32;
+        h.out_ld32 = a.ld32;
+        h.counts = a.counts;
+        h.uniforms = a.uniforms;
+        h.uniforms_ld = a.uniforms_ld;
+        h.err = a.err;
+        const uint64_t per_cta = uint64_t(zxs_dev::kHeavyWarps) * 32 * zxs_dev::kHS;
+        h.n_cta_tiles = (a.shots + per_cta - 1) / per_cta;
+        const unsigned hgrid = unsigned(std::min<uint64_t>(h.n_cta_tiles, uint64_t(s->sm_count) * s->heavy_blocks_per_sm));
+        void *hargs[] = {&h};
+        CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::heavy_kernel), dim3(hgrid),
+                            dim3(zxs_dev::kHeavyWarps * 32), hargs, s->heavy_smem, st));
+    }
 }
 
 void check_ratio_error(zxs_sampler *s, cudaStream_t st) {
@@ -623,6 +794,7 @@ void zxs_sampler_destroy(zxs_sampler *s) {
     if (s->dev_model) cudaFree(s->dev_model);
     if (s->dev_err) cudaFree(s->dev_err);
     if (s->scratch) cudaFree(s->scratch);
+    if (s->heavy_scratch) cudaFree(s->heavy_scratch);
     if (prev >= 0) cudaSetDevice(prev);
     delete s;
 }

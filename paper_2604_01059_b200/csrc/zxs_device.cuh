@@ -117,6 +117,7 @@ struct DevModel {
     const Factor *factors;
     const uint16_t *selectors;
     const double2 *h_table;            // [4 * num_tables]
+    const uint8_t *comp_heavy;         // [num_components] 1: chain runs in heavy_kernel
 };
 
 }  // namespace zxs_dev

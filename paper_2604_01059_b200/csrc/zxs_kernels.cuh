@@ -72,6 +72,8 @@ struct LaunchArgs {
     const double *uniforms;        // injected AR uniforms: [positions][uniforms_ld] (nullable)
     uint64_t uniforms_ld;
     unsigned long long *err;       // [0] = flag, [1] = first failing shot
+    uint32_t *heavy_fcols;         // f-columns for heavy_kernel: [f_width][heavy_ld32] (nullable)
+    uint64_t heavy_ld32;
 };
 
 // 32x32 -> 64 multiply as one mul.wide.u32 (IMAD.WIDE.U32); written in PTX
@@ -308,6 +310,12 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
             }
         }
         __syncwarp();
+        if (a.heavy_fcols) {
+            for (uint32_t c = lane; c < m.f_width; c += 32) {
+#pragma unroll
+                for (int s = 0; s < kS; s++) a.heavy_fcols[c * a.heavy_ld32 + tile * kS + s] = cols[s * m.col_stride + c];
+            }
+        }
         if (a.fcols_out) {
             for (uint32_t c = lane; c < m.f_width; c += 32) {
 #pragma unroll
@@ -341,6 +349,10 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
         uint32_t upos = 0;
         for (uint32_t ci = 0; ci < m.num_components; ci++) {
             const uint32_t ob = m.comp_out_begin[ci], n = m.comp_out_begin[ci + 1] - ob;
+            if (m.comp_heavy[ci]) {  // evaluated by heavy_kernel
+                upos += n;
+                continue;
+            }
             const uint32_t tb = m.comp_tensor_begin[ci];
             for (uint32_t p = lane; p < n; p += 32) {
 #pragma unroll

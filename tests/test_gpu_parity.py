@@ -195,3 +195,60 @@ def test_empty_and_tiny_ranges():
     orc = coracle.OracleModel.load(golden_path("c2_surface_d3_xmem_t"))
     for shots, first in ((1, 0), (31, 5), (33, 2**32 - 7), (64, 64), (65, 1)):
         assert np.array_equal(sample(cs, shots, 4, first), orc.sample(shots, 4, first))
+
+
+def _heavy_model(name, min_factors="1"):
+    """Sampler whose components (with >= min_factors factors) all run in heavy_kernel."""
+    import os
+    old = os.environ.get("ZXS_HEAVY_MIN_FACTORS")
+    os.environ["ZXS_HEAVY_MIN_FACTORS"] = min_factors
+    try:
+        return zx.CompiledSampler.load(golden_path(name))
+    finally:
+        if old is None:
+            del os.environ["ZXS_HEAVY_MIN_FACTORS"]
+        else:
+            os.environ["ZXS_HEAVY_MIN_FACTORS"] = old
+
+
+@pytest.mark.parametrize("name", ["c2_surface_d3_xmem_t", "c4_color_d5_rz3", "surface_d3_xmem_rz5",
+                                  "surface_d3_xmem_9t", "h_t_h_m", "bell_m", "oracle_mix_4", "random_02",
+                                  "random_05", "c5_surface_d7_r7"])
+def test_heavy_path_matches_reference_goldens(name, goldens):
+    """Large-chi path (chunked TMA streaming, 4096 shots per CTA) forced on
+    every component: records still equal the reference's bit for bit."""
+    cs = _heavy_model(name)
+    for s in goldens[name]["samples"]:
+        if s["shots"] > 200000:
+            continue
+        assert sha(sample(cs, s["shots"], s["seed"], s["first_shot"])) == s["sha256"], (name, s)
+
+
+def test_heavy_path_injected_and_counts():
+    name = "c4_color_d5_rz3"
+    cs = _heavy_model(name)
+    orc = coracle.OracleModel.load(golden_path(name))
+    rng = np.random.default_rng(29)
+    shots = 5000
+    f = rng.integers(0, 2**63, size=(orc.f_width, (shots + 63) // 64), dtype=np.uint64)
+    f[:, -1] &= np.uint64((1 << (shots & 63)) - 1)
+    u = rng.random((orc.num_positions, shots))
+    assert np.array_equal(zx.sample_given_f(cs, f, shots, uniforms=u), orc.sample(shots, 0, fcols=f, uniforms=u))
+    full = sample(cs, 70000, 3, 123)
+    pc = np.unpackbits(full.view(np.uint8), axis=1).sum(axis=1).astype(np.uint64)
+    assert np.array_equal(zx.count_outputs(cs, 70000, seed=3, first_shot=123), pc)
+
+
+def test_cultivation_proxy_against_reference():
+    """Config-3 proxy (chi = 46,656, 12.4 M factors): the heavy path against
+    the reference sampler itself on the same shots."""
+    import os
+    path = os.path.join(os.path.dirname(golden_path("x")), "..", "..", "data", "c3_cultivation_proxy.zxs.gz")
+    if not os.path.exists(path) or not refdriver.available():
+        pytest.skip("cultivation proxy not generated (tools/make_fixtures.py --big)")
+    cs = zx.CompiledSampler.load(path)
+    ref = refdriver.RefModel.load(path)
+    shots, first = 640, 1 << 20
+    got = sample(cs, shots, 11, first)
+    want = ref.sample_rb(shots, 11, first_shot=first, batch_size=64, threads=os.cpu_count())
+    assert np.array_equal(got, want)

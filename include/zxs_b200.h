@@ -217,6 +217,17 @@ zxs_status zxs_probability_of_at(zxs_sampler *s, const uint8_t *outcome, uint32_
 zxs_status zxs_philox_uniform(int device, uint64_t seed, uint32_t stream, uint64_t first_index,
                               uint64_t n, double *host_out);
 
+/* Diagnostic (host only, no GPU needed): the compact word streams the
+   large-chi path (heavy_kernel) would evaluate for `desc`, components with
+   >= min_factors factors. out[cap] receives, in u32 words: {n_words, n_chunks,
+   n_tensor_bounds, zero_row, n_comps, n_components, 0, 0}, then per heavy
+   component {ci, n_out, upos_base, out_begin, first_tensor}, the per-component
+   heavy flags, the tensor -> first-chunk bounds, per chunk {word_begin,
+   n_words, n_terms, 0}, and the words. *needed = total words (out may be NULL
+   to query). */
+zxs_status zxs_debug_heavy_layout(const zxs_model_desc *desc, uint64_t min_factors, uint32_t *out, uint64_t cap,
+                                  uint64_t *needed);
+
 /* Diagnostic: Philox4x32-10 blocks/s of this library's draw code (the shot
    kernel's Philox and filter compare, same launch shape, no memory traffic)
    on `device` -- the same-op-mix roofline of the error draw. */

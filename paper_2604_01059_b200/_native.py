@@ -58,6 +58,8 @@ SIGNATURES = (
     ("zxs_philox_uniform", ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
                                           ctypes.c_uint64, _dp]),
     ("zxs_measure_philox_peak", ctypes.c_int, [ctypes.c_int, _dp]),
+    ("zxs_debug_heavy_layout", ctypes.c_int, [ctypes.POINTER(_fmt.ModelDesc), ctypes.c_uint64,
+                                              ctypes.POINTER(ctypes.c_uint32), ctypes.c_uint64, _u64p]),
 )
 
 _lib = None

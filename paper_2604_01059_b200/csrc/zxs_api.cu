@@ -211,6 +211,119 @@ void validate_csr64(const char *name, const uint64_t *b, size_t n) {
     }
 }
 
+// Host encoding of the heavy (large-chi) components for heavy_kernel: one
+// compact word stream per chain tensor, cut into chunks on term boundaries
+// (see zxs_heavy.cuh for the record layout). Components with fewer than
+// `heavy_min` factors, or that do not fit the envelope (<= 256 plane rows,
+// <= 256 h tables, terms smaller than a chunk), stay on the shot kernel.
+struct HeavyHost {
+    std::vector<uint8_t> comp_heavy;
+    std::vector<uint32_t> words;
+    std::vector<uint4> chunks;
+    std::vector<uint32_t> tensor_chunk_begin{0};
+    std::vector<zxs_dev::HeavyComp> comps;
+    uint32_t max_chain = 0, zero_row = 0;
+};
+
+HeavyHost encode_heavy(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy_min) {
+    HeavyHost H;
+    std::vector<uint8_t> &comp_heavy = H.comp_heavy;
+    std::vector<uint32_t> &hw = H.words;
+    std::vector<uint4> &hchunks = H.chunks;
+    std::vector<uint32_t> &htcb = H.tensor_chunk_begin;
+    std::vector<zxs_dev::HeavyComp> &hcomps = H.comps;
+    uint32_t &heavy_max_chain = H.max_chain;
+    const uint32_t fwid = d->f_width;
+    comp_heavy.assign(std::max<uint32_t>(1, d->num_components), 0);
+    // plane rows: f columns, sampled-bit columns of the longest chain, one all-zero row
+    const uint32_t heavy_zero_row = fwid + max_chain;
+    H.zero_row = heavy_zero_row;
+    {
+        uint32_t upos = 0;
+        for (uint32_t c = 0; c < d->num_components; c++) {
+            const uint32_t n = d->comp_out_begin[c + 1] - d->comp_out_begin[c];
+            const uint32_t t0 = d->comp_tensor_begin[c], t1 = d->comp_tensor_begin[c + 1];
+            uint64_t nf = d->term_factor_begin[d->tensor_term_begin[t1]] - d->term_factor_begin[d->tensor_term_begin[t0]];
+            bool ok = nf >= heavy_min && d->num_h_tables <= 256 && hcomps.size() < size_t(zxs_dev::kMaxHeavyComps) &&
+                      heavy_zero_row < 256;
+            // encode every tensor of the chain; abandon (light path) on any misfit
+            std::vector<uint32_t> w;
+            std::vector<uint4> ch;
+            std::vector<uint32_t> tcb;
+            for (uint32_t t = t0; ok && t < t1; t++) {
+                uint32_t cur_begin = uint32_t(hw.size() + w.size()), cur_terms = 0;
+                auto close_chunk = [&]() {
+                    if (hw.size() + w.size() == cur_begin) w.insert(w.end(), 4, 0u);  // no 0-byte bulk copies
+                    while ((hw.size() + w.size()) % 4) w.push_back(0);
+                    uint32_t end = uint32_t(hw.size() + w.size());
+                    ch.push_back(make_uint4(cur_begin, end - cur_begin, cur_terms, 0));
+                    cur_begin = end;
+                    cur_terms = 0;
+                };
+                tcb.push_back(uint32_t(hchunks.size() + ch.size()));
+                for (uint64_t term = d->tensor_term_begin[t]; ok && term < d->tensor_term_begin[t + 1]; term++) {
+                    std::vector<uint32_t> tw;
+                    const uint64_t f0 = d->term_factor_begin[term], f1 = d->term_factor_begin[term + 1];
+                    uint64_t re, im;
+                    std::memcpy(&re, &d->term_c[2 * term], 8);
+                    std::memcpy(&im, &d->term_c[2 * term + 1], 8);
+                    // term: {nfac, re.lo, re.hi, im.lo}, {im.hi, 0, 0, 0}
+                    tw.insert(tw.end(), {uint32_t(f1 - f0), uint32_t(re), uint32_t(re >> 32), uint32_t(im),
+                                         uint32_t(im >> 32), 0u, 0u, 0u});
+                    for (uint64_t k = f0; ok && k < f1; k++) {
+                        const uint64_t u0 = d->factor_u_begin[k], u1 = d->factor_u_begin[k + 1];
+                        const uint64_t v0 = d->factor_v_begin[k], v1 = d->factor_v_begin[k + 1];
+                        const uint32_t gu = uint32_t((u1 - u0 + 3) / 4), gv = uint32_t((v1 - v0 + 3) / 4);
+                        if (gu > 255 || gv > 255) {
+                            ok = false;
+                            break;
+                        }
+                        // factor: {table | u groups << 8 | v groups << 16, 0, 0, 0}, then groups of
+                        // four byte offsets (param * 64) into the 16-bit parameter planes; padding
+                        // entries point at the all-zero row `heavy_zero_row`.
+                        tw.insert(tw.end(), {d->factor_table[k] | gu << 8 | gv << 16, 0u, 0u, 0u});
+                        auto put_group = [&](const uint32_t *bits, uint64_t n) {
+                            for (uint64_t i = 0; i < 4 * ((n + 3) / 4); i++) {
+                                tw.push_back(64u * (i < n ? bits[i] : heavy_zero_row));
+                            }
+                        };
+                        put_group(d->factor_u_bits + u0, u1 - u0);
+                        put_group(d->factor_v_bits + v0, v1 - v0);
+                    }
+                    if (!ok) break;
+                    if (tw.size() + 4 > zxs_dev::kChunkWords) {
+                        ok = false;  // a single term larger than a chunk buffer
+                        break;
+                    }
+                    if (hw.size() + w.size() + tw.size() - cur_begin > zxs_dev::kChunkWords) close_chunk();
+                    w.insert(w.end(), tw.begin(), tw.end());
+                    cur_terms++;
+                }
+                if (ok && (cur_terms || hw.size() + w.size() == cur_begin)) close_chunk();
+            }
+            if (ok) {
+                zxs_dev::HeavyComp hc;
+                hc.ci = c;
+                hc.n_out = n;
+                hc.upos_base = upos;
+                hc.out_begin = d->comp_out_begin[c];
+                hc.first_tensor = uint32_t(htcb.size() - 1);
+                hw.insert(hw.end(), w.begin(), w.end());
+                hchunks.insert(hchunks.end(), ch.begin(), ch.end());
+                for (size_t i = 1; i < tcb.size(); i++) htcb.push_back(tcb[i]);
+                htcb.push_back(uint32_t(hchunks.size()));
+                hcomps.push_back(hc);
+                comp_heavy[c] = 1;
+                heavy_max_chain = std::max(heavy_max_chain, n);
+            }
+            upos += n;
+        }
+    }
+    if (hw.empty()) hw.assign(4, 0);
+    if (hchunks.empty()) hchunks.push_back(make_uint4(0, 0, 0, 0));
+    return H;
+}
+
 void build(zxs_sampler *s, const zxs_model_desc *d) {
     if (!d) fail(ZXS_INVALID_ARGUMENT, "null model");
     if (d->abi_version != ZXS_ABI_VERSION) fail(ZXS_INVALID_ARGUMENT, "model ABI version mismatch");
@@ -421,97 +534,13 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     // ---- heavy components: compact chunked streams (zxs_heavy.cuh)
     uint64_t heavy_min = 20000;
     if (const char *e = std::getenv("ZXS_HEAVY_MIN_FACTORS")) heavy_min = std::strtoull(e, nullptr, 10);
-    std::vector<uint8_t> comp_heavy(std::max<uint32_t>(1, d->num_components), 0);
-    std::vector<uint32_t> hw;                 // words
-    std::vector<uint4> hchunks;
-    std::vector<uint32_t> htcb{0};            // tensor -> first chunk
-    std::vector<zxs_dev::HeavyComp> hcomps;
-    uint32_t heavy_max_chain = 0;
-    {
-        uint32_t upos = 0;
-        for (uint32_t c = 0; c < d->num_components; c++) {
-            const uint32_t n = d->comp_out_begin[c + 1] - d->comp_out_begin[c];
-            const uint32_t t0 = d->comp_tensor_begin[c], t1 = d->comp_tensor_begin[c + 1];
-            uint64_t nf = d->term_factor_begin[d->tensor_term_begin[t1]] - d->term_factor_begin[d->tensor_term_begin[t0]];
-            bool ok = nf >= heavy_min && d->num_h_tables <= 256 && hcomps.size() < size_t(zxs_dev::kMaxHeavyComps) &&
-                      fwid + n <= 256;
-            // encode every tensor of the chain; abandon (light path) on any misfit
-            std::vector<uint32_t> w;
-            std::vector<uint4> ch;
-            std::vector<uint32_t> tcb;
-            for (uint32_t t = t0; ok && t < t1; t++) {
-                uint32_t cur_begin = uint32_t(hw.size() + w.size()), cur_terms = 0;
-                auto close_chunk = [&]() {
-                    while ((hw.size() + w.size()) % 4) w.push_back(0);
-                    uint32_t end = uint32_t(hw.size() + w.size());
-                    ch.push_back(make_uint4(cur_begin, end - cur_begin, cur_terms, 0));
-                    cur_begin = end;
-                    cur_terms = 0;
-                };
-                tcb.push_back(uint32_t(hchunks.size() + ch.size()));
-                for (uint64_t term = d->tensor_term_begin[t]; ok && term < d->tensor_term_begin[t + 1]; term++) {
-                    std::vector<uint32_t> tw;
-                    const uint64_t f0 = d->term_factor_begin[term], f1 = d->term_factor_begin[term + 1];
-                    uint64_t re, im;
-                    std::memcpy(&re, &d->term_c[2 * term], 8);
-                    std::memcpy(&im, &d->term_c[2 * term + 1], 8);
-                    tw.push_back(uint32_t(f1 - f0));
-                    tw.push_back(uint32_t(re));
-                    tw.push_back(uint32_t(re >> 32));
-                    tw.push_back(uint32_t(im));
-                    tw.push_back(uint32_t(im >> 32));
-                    for (uint64_t k = f0; ok && k < f1; k++) {
-                        const uint64_t u0 = d->factor_u_begin[k], u1 = d->factor_u_begin[k + 1];
-                        const uint64_t v0 = d->factor_v_begin[k], v1 = d->factor_v_begin[k + 1];
-                        if (u1 - u0 > 255 || v1 - v0 > 255) {
-                            ok = false;
-                            break;
-                        }
-                        tw.push_back(d->factor_table[k] | uint32_t(u1 - u0) << 8 | uint32_t(v1 - v0) << 16);
-                        uint32_t word = 0, nb = 0;
-                        auto put = [&](uint32_t sel) {
-                            word |= (sel & 0xffu) << (8 * nb);
-                            if (++nb == 4) {
-                                tw.push_back(word);
-                                word = 0;
-                                nb = 0;
-                            }
-                        };
-                        for (uint64_t i = u0; i < u1; i++) put(d->factor_u_bits[i]);
-                        for (uint64_t i = v0; i < v1; i++) put(d->factor_v_bits[i]);
-                        if (nb) tw.push_back(word);
-                    }
-                    if (!ok) break;
-                    if (tw.size() + 4 > zxs_dev::kChunkWords) {
-                        ok = false;  // a single term larger than a chunk buffer
-                        break;
-                    }
-                    if (hw.size() + w.size() + tw.size() - cur_begin > zxs_dev::kChunkWords) close_chunk();
-                    w.insert(w.end(), tw.begin(), tw.end());
-                    cur_terms++;
-                }
-                if (ok && (cur_terms || hw.size() + w.size() == cur_begin)) close_chunk();
-            }
-            if (ok) {
-                zxs_dev::HeavyComp hc;
-                hc.ci = c;
-                hc.n_out = n;
-                hc.upos_base = upos;
-                hc.out_begin = d->comp_out_begin[c];
-                hc.first_tensor = uint32_t(htcb.size() - 1);
-                hw.insert(hw.end(), w.begin(), w.end());
-                hchunks.insert(hchunks.end(), ch.begin(), ch.end());
-                for (size_t i = 1; i < tcb.size(); i++) htcb.push_back(tcb[i]);
-                htcb.push_back(uint32_t(hchunks.size()));
-                hcomps.push_back(hc);
-                comp_heavy[c] = 1;
-                heavy_max_chain = std::max(heavy_max_chain, n);
-            }
-            upos += n;
-        }
-    }
-    if (hw.empty()) hw.assign(4, 0);
-    if (hchunks.empty()) hchunks.push_back(make_uint4(0, 0, 0, 0));
+    HeavyHost H = encode_heavy(d, max_chain, heavy_min);
+    std::vector<uint8_t> &comp_heavy = H.comp_heavy;
+    std::vector<uint32_t> &hw = H.words;
+    std::vector<uint4> &hchunks = H.chunks;
+    std::vector<uint32_t> &htcb = H.tensor_chunk_begin;
+    std::vector<zxs_dev::HeavyComp> &hcomps = H.comps;
+    const uint32_t heavy_zero_row = H.zero_row;
 
     // ---- device upload
     Arena ar;
@@ -605,7 +634,8 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     if (s->has_heavy) {
         zxs_dev::HeavyArgs &ha = s->heavy;
         ha.f_width = fwid;
-        ha.col_words = fwid + heavy_max_chain;
+        ha.col_words = heavy_zero_row + 1;  // rows incl. the all-zero padding row
+        (void)H.max_chain;
         ha.words = reinterpret_cast<const uint32_t *>(b + o_hw);
         ha.chunks = reinterpret_cast<const uint4 *>(b + o_hchunks);
         ha.tensor_chunk_begin = reinterpret_cast<const uint32_t *>(b + o_htcb);
@@ -617,7 +647,7 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         for (size_t i = 0; i < hcomps.size(); i++) ha.comps[i] = hcomps[i];
         s->heavy_words = hw.size();
         s->heavy_smem = 128 + 2 * size_t(zxs_dev::kChunkWords) * 4 + size_t(ha.n_tables) * 64 +
-                        size_t(zxs_dev::kHeavyWarps) * ha.col_words * zxs_dev::kHS * 4;
+                        size_t(zxs_dev::kHeavyWarps) * ha.col_words * 64;  // 16-bit planes
     }
     m.mech_entry_begin = nullptr;
     m.mech_stream = nullptr;
@@ -1084,6 +1114,28 @@ zxs_status zxs_probability_of_at(zxs_sampler *s, const uint8_t *outcome, uint32_
             p *= prev / norm;
         }
         *out = p;
+    });
+}
+
+zxs_status zxs_debug_heavy_layout(const zxs_model_desc *desc, uint64_t min_factors, uint32_t *out, uint64_t cap,
+                                  uint64_t *needed) {
+    return guarded([&] {
+        if (!desc || !needed) fail(ZXS_INVALID_ARGUMENT, "null argument");
+        uint32_t max_chain = 0;
+        for (uint32_t c = 0; c < desc->num_components; c++) {
+            max_chain = std::max(max_chain, desc->comp_out_begin[c + 1] - desc->comp_out_begin[c]);
+        }
+        HeavyHost H = encode_heavy(desc, max_chain, min_factors);
+        std::vector<uint32_t> blob = {uint32_t(H.words.size()), uint32_t(H.chunks.size()),
+                                      uint32_t(H.tensor_chunk_begin.size()), H.zero_row, uint32_t(H.comps.size()),
+                                      uint32_t(H.comp_heavy.size()), 0u, 0u};
+        for (const auto &c : H.comps) blob.insert(blob.end(), {c.ci, c.n_out, c.upos_base, c.out_begin, c.first_tensor});
+        for (uint8_t f : H.comp_heavy) blob.push_back(f);
+        blob.insert(blob.end(), H.tensor_chunk_begin.begin(), H.tensor_chunk_begin.end());
+        for (const uint4 &c : H.chunks) blob.insert(blob.end(), {c.x, c.y, c.z, c.w});
+        blob.insert(blob.end(), H.words.begin(), H.words.end());
+        *needed = blob.size();
+        if (out && cap >= blob.size()) std::memcpy(out, blob.data(), blob.size() * 4);
     });
 }
 

@@ -14,9 +14,11 @@
 //    CTA). Chunks are streamed HBM/L2 -> shared memory with cp.async.bulk
 //    (1-D TMA) into two mbarrier-tracked buffers: the next chunk lands while
 //    the current one is evaluated, and every fetched byte serves 4096 shots.
-//  * Every warp walks the chunk with warp-uniform (broadcast) shared loads;
-//    selector parities are XORs of bit-sliced parameter columns held in
-//    shared memory, kHS 32-shot words per parameter read as uint4 vectors.
+//  * Every warp walks the chunk with warp-uniform (broadcast) shared loads.
+//    Parameters are held per lane as "byte planes": plane[p][lane] bit s is
+//    parameter p of the lane's shot in sub-tile s, so one byte load + XOR per
+//    selector yields the parities of all kHS = 8 shots of the lane, and the
+//    h-table offset of shot s is ((a << 5 | b << 4) >> s) & 0x30.
 #pragma once
 
 #include "zxs_kernels.cuh"
@@ -98,27 +100,27 @@ __device__ __forceinline__ void heavy_issue(const HeavyArgs &h, uint64_t u, uint
     bulk_g2s(buf0 + b * kChunkWords, h.words + c.x, c.y * 4u, &bars[b]);
 }
 
-// XORs `count` selector columns from the packed byte stream into acc.
-__device__ __forceinline__ void heavy_selectors(const uint32_t *w, uint32_t &p, uint32_t &sw, uint32_t &nb,
-                                                uint32_t count, const uint4 *cols, uint32_t (&acc)[kHS]) {
-    for (uint32_t i = 0; i < count; i++) {
-        if (nb == 0) {
-            sw = w[p++];
-            nb = 4;
-        }
-        const uint32_t sel = sw & 0xffu;
-        sw >>= 8;
-        nb--;
-        const uint4 *c = cols + sel * (kHS / 4);
-#pragma unroll
-        for (int q = 0; q < kHS / 4; q++) {
-            const uint4 v = c[q];
-            acc[4 * q + 0] ^= v.x;
-            acc[4 * q + 1] ^= v.y;
-            acc[4 * q + 2] ^= v.z;
-            acc[4 * q + 3] ^= v.w;
-        }
+// XOR of the lane's byte planes over `groups` groups of four selector byte
+// offsets (padding selectors point at an all-zero plane row): bit s of the
+// result is the selector parity of the lane's shot s.
+__device__ __forceinline__ uint32_t heavy_parity(const uint4 *w4, uint32_t &q, uint32_t groups,
+                                                 const uint8_t *planes) {
+    uint32_t acc = 0;
+    for (uint32_t g = 0; g < groups; g++) {
+        const uint4 o = w4[q++];
+        acc ^= uint32_t(*reinterpret_cast<const uint16_t *>(planes + o.x)) ^
+               uint32_t(*reinterpret_cast<const uint16_t *>(planes + o.y));
+        acc ^= uint32_t(*reinterpret_cast<const uint16_t *>(planes + o.z)) ^
+               uint32_t(*reinterpret_cast<const uint16_t *>(planes + o.w));
     }
+    return acc;
+}
+
+// Spreads the low 8 bits of v to the even bit positions 0, 2, ..., 14.
+__device__ __forceinline__ uint32_t spread8(uint32_t v) {
+    v = (v | (v << 4)) & 0x0F0Fu;
+    v = (v | (v << 2)) & 0x3333u;
+    return (v | (v << 1)) & 0x5555u;
 }
 
 __global__ void __launch_bounds__(kHeavyWarps * 32, 1) heavy_kernel(const __grid_constant__ HeavyArgs h) {
@@ -128,8 +130,9 @@ __global__ void __launch_bounds__(kHeavyWarps * 32, 1) heavy_kernel(const __grid
     double2 *htab = reinterpret_cast<double2 *>(hsm + 128 + 2 * kChunkWords * 4);
     uint32_t *colsw = reinterpret_cast<uint32_t *>(htab + 4 * h.n_tables);
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    uint32_t *cols = colsw + warp * h.col_words * kHS;  // [param][kHS]
-    const uint4 *cols4 = reinterpret_cast<const uint4 *>(cols);
+    // [param][lane] 16-bit planes: bit 2s = parameter of the lane's shot in sub-tile s
+    uint16_t *planes = reinterpret_cast<uint16_t *>(colsw) + warp * h.col_words * 32;
+    const uint8_t *my_planes = reinterpret_cast<const uint8_t *>(planes + lane);
 
     const uint64_t my_tiles = blockIdx.x < h.n_cta_tiles ? (h.n_cta_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     const uint64_t total_uses = my_tiles * h.total_chunks;
@@ -148,20 +151,20 @@ __global__ void __launch_bounds__(kHeavyWarps * 32, 1) heavy_kernel(const __grid
     uint64_t use = 0;
 
     for (uint64_t ct = blockIdx.x; ct < h.n_cta_tiles; ct += gridDim.x) {
-        const uint64_t w0 = (ct * kHeavyWarps + warp) * kHS;  // first 32-bit word of this warp's shots
-        uint64_t local[kHS];
-        uint32_t vmask[kHS];
-        PhiloxPre pre[kHS];
+        // first 32-bit word of this warp's shots; shot of (lane, s) = (w0 + s) * 32 + lane.
+        // Per-shot Philox state is rebuilt at each autoregressive draw rather
+        // than kept live across the factor loop (register pressure).
+        const uint64_t w0 = (ct * kHeavyWarps + warp) * kHS;
+        for (uint32_t p = 0; p < h.col_words; p++) {  // byte planes of the lane's 8 shots
+            uint32_t byte = 0;
+            if (p < h.f_width) {
 #pragma unroll
-        for (int s = 0; s < kHS; s++) {
-            local[s] = (w0 + s) * 32 + lane;
-            vmask[s] = __ballot_sync(kFull, local[s] < h.shots);
-            const uint64_t shot = h.first_shot + local[s];
-            pre[s] = philox_pre(uint32_t(shot), uint32_t(shot >> 32), h.k0_round[0]);
-        }
-        for (uint32_t i = lane; i < h.col_words * kHS; i += 32) {
-            const uint32_t p = i / kHS, s = i % kHS;
-            cols[i] = (p < h.f_width && w0 + s < h.fcols_ld32) ? h.fcols[p * h.fcols_ld32 + w0 + s] : 0u;
+                for (int s = 0; s < kHS; s++) {
+                    const uint32_t col = (w0 + s < h.fcols_ld32) ? h.fcols[p * h.fcols_ld32 + w0 + s] : 0u;
+                    byte |= ((col >> lane) & 1u) << s;
+                }
+            }
+            planes[p * 32 + lane] = uint16_t(spread8(byte));
         }
         __syncwarp();
 
@@ -179,25 +182,29 @@ __global__ void __launch_bounds__(kHeavyWarps * 32, 1) heavy_kernel(const __grid
                     const uint32_t *w = buf0 + b * kChunkWords;
                     const uint32_t nterms = h.chunks[c].z;
                     uint32_t p = 0;
+                    const uint4 *w4 = reinterpret_cast<const uint4 *>(w);
+                    uint32_t q = 0;
                     for (uint32_t tt = 0; tt < nterms; tt++) {
-                        const uint32_t nfac = w[p];
-                        const double2 cterm = make_double2(__hiloint2double(int(w[p + 2]), int(w[p + 1])),
-                                                           __hiloint2double(int(w[p + 4]), int(w[p + 3])));
-                        p += 5;
+                        const uint4 t0 = w4[q], t1 = w4[q + 1];  // {nfac, re.lo, re.hi, im.lo}, {im.hi, -, -, -}
+                        q += 2;
+                        const uint32_t nfac = t0.x;
+                        const double2 cterm = make_double2(__hiloint2double(int(t0.z), int(t0.y)),
+                                                           __hiloint2double(int(t1.x), int(t0.w)));
                         double2 prod[kHS];
 #pragma unroll
                         for (int s = 0; s < kHS; s++) prod[s] = cterm;
                         for (uint32_t k = 0; k < nfac; k++) {
-                            const uint32_t hdr = w[p++];
-                            uint32_t aw[kHS] = {}, bw[kHS] = {};
-                            uint32_t sw = 0, nb = 0;
-                            heavy_selectors(w, p, sw, nb, (hdr >> 8) & 0xffu, cols4, aw);
-                            heavy_selectors(w, p, sw, nb, (hdr >> 16) & 0xffu, cols4, bw);
-                            const double2 *ht = htab + 4 * (hdr & 0xffu);
+                            const uint32_t hdr = w4[q++].x;  // table | u groups << 8 | v groups << 16
+                            const uint32_t av = heavy_parity(w4, q, (hdr >> 8) & 0xffu, my_planes);
+                            const uint32_t bv = heavy_parity(w4, q, (hdr >> 16) & 0xffu, my_planes);
+                            const char *ht = reinterpret_cast<const char *>(htab + 4 * (hdr & 0xffu));
+                            // shot s: a at bit 2s+1, b at bit 2s -> h index (a<<1|b) * 16 bytes
+                            const uint32_t z = (av << 1) | bv;
 #pragma unroll
                             for (int s = 0; s < kHS; s++) {
-                                const uint32_t idx = (((aw[s] >> lane) & 1u) << 1) | ((bw[s] >> lane) & 1u);
-                                prod[s] = cmul_rn(prod[s], ht[idx]);
+                                const uint32_t off = (2 * s >= 4) ? ((z >> (2 * s - 4)) & 0x30u) : ((z << (4 - 2 * s)) & 0x30u);
+                                const double2 hv = *reinterpret_cast<const double2 *>(ht + off);
+                                prod[s] = cmul_rn(prod[s], hv);
                             }
                         }
 #pragma unroll
@@ -215,30 +222,40 @@ __global__ void __launch_bounds__(kHeavyWarps * 32, 1) heavy_kernel(const __grid
                 const uint32_t j = pos - 1;
                 uint32_t rhi[kHS], rlo[kHS];
                 if (!h.uniforms) {
+                    PhiloxPre pre[kHS];
+#pragma unroll
+                    for (int s = 0; s < kHS; s++) {
+                        const uint64_t shot = h.first_shot + (w0 + s) * 32 + lane;
+                        pre[s] = philox_pre(uint32_t(shot), uint32_t(shot >> 32), h.k0_round[0]);
+                    }
                     const uint32_t stream = 0x80000000u ^ (cd.ci << 12) ^ j;
                     philox_tail<kHS>(pre, seed_hi ^ stream, h.k0_round, k2c, h.k0_round[9], rhi, rlo);
                 }
                 uint32_t word[kHS];
 #pragma unroll
                 for (int s = 0; s < kHS; s++) {
-                    const bool valid = local[s] < h.shots;
+                    const uint64_t local_s = (w0 + s) * 32 + lane;
+                    const bool valid = local_s < h.shots;
                     const double cur = acc[s].x;
                     const double ratio = __ddiv_rn(cur, prev[s]);
-                    if (!(ratio > -1e-6 && ratio < 1.0 + 1e-6) && valid) report_ratio_error(h.err, h.first_shot + local[s]);
+                    if (!(ratio > -1e-6 && ratio < 1.0 + 1e-6) && valid) report_ratio_error(h.err, h.first_shot + local_s);
                     double cl = (0.0 < ratio) ? ratio : 0.0;
                     cl = (cl < 1.0) ? cl : 1.0;
-                    const double u = h.uniforms ? (valid ? h.uniforms[(cd.upos_base + j) * h.uniforms_ld + local[s]] : 0.0)
+                    const double u = h.uniforms ? (valid ? h.uniforms[(cd.upos_base + j) * h.uniforms_ld + local_s] : 0.0)
                                                 : philox_uniform((uint64_t(rhi[s]) << 32) | rlo[s]);
                     const bool bit = !(u < cl);
                     prev[s] = bit ? __dsub_rn(prev[s], cur) : cur;
-                    word[s] = __ballot_sync(kFull, bit) & vmask[s];
+                    word[s] = __ballot_sync(kFull, bit && valid);
                 }
+                uint32_t byte = 0;
+#pragma unroll
+                for (int s = 0; s < kHS; s++) byte |= ((word[s] >> lane) & 1u) << s;
+                planes[(h.f_width + j) * 32 + lane] = uint16_t(spread8(byte));
                 if (lane == 0) {
                     const uint32_t o = h.comp_outputs[cd.out_begin + j];
                     unsigned long long ones = 0;
 #pragma unroll
                     for (int s = 0; s < kHS; s++) {
-                        cols[(h.f_width + j) * kHS + s] = word[s];
                         if (h.out32 && w0 + s < h.out_ld32) h.out32[o * h.out_ld32 + w0 + s] = word[s];
                         ones += __popc(word[s]);
                     }
@@ -247,7 +264,7 @@ __global__ void __launch_bounds__(kHeavyWarps * 32, 1) heavy_kernel(const __grid
                 __syncwarp();
             }
             // reset this component's sampled-bit columns for the next component
-            for (uint32_t i = lane; i < cd.n_out * kHS; i += 32) cols[h.f_width * kHS + i] = 0u;
+            for (uint32_t j = 0; j < cd.n_out; j++) planes[(h.f_width + j) * 32 + lane] = 0;
             __syncwarp();
         }
     }

@@ -42,7 +42,7 @@ WORKLOADS = {
                          "d=7 rotated surface code Z-memory, 7 rounds, p=1e-3, count-only sweep", 1 << 24, True),
     "c3_cultivation_proxy": ("data/c3_cultivation_proxy.zxs.gz", 2,
                              "Steane-code cultivation proxy: T injection + 2 transversal T checks (chi=46656)",
-                             1 << 14, False),
+                             296 * 8192, False),
 }
 DEFAULT_WORKLOAD = "c2_surface_d3_xmem_t"
 

@@ -133,6 +133,9 @@ typedef struct zxs_sampler_info {
     uint64_t device_bytes;    /* resident model bytes in HBM */
     int device;
     int monomial;             /* 1 if every h entry is an exact Clifford monomial */
+    /* large-chi components lowered to the integer monomial path (zxs_mono.cuh) */
+    uint32_t num_mono_components, num_mono_forms;
+    uint64_t num_mono_records, num_mono_dead_terms;
 } zxs_sampler_info;
 
 /* Message of the calling thread's last failed call ("" if none). */
@@ -194,6 +197,16 @@ zxs_status zxs_eval_batch(zxs_sampler *s, uint32_t component, uint32_t chain_pos
                           double *host_values, double *max_imag_ratio);
 
 /*
+ * Same contract as zxs_eval_batch, evaluated by the integer monomial kernel
+ * (zxs_mono.cuh) that samples large-chi components: the values equal the
+ * reference's eval_batch up to the reference's own rounding of its h tables.
+ * ZXS_UNSUPPORTED if the component is not on that path.
+ */
+zxs_status zxs_eval_batch_mono(zxs_sampler *s, uint32_t component, uint32_t chain_pos,
+                               const uint64_t *host_params, uint32_t param_cols, uint64_t shots,
+                               double *host_values);
+
+/*
  * run_batch with the noise configuration injected: host_fcols
  * [f_width][ceil(shots/64)] replaces the Philox error draw. host_uniforms
  * (nullable) injects the autoregressive draws: [sum_c n_out(c)][shots]
@@ -228,10 +241,24 @@ zxs_status zxs_philox_uniform(int device, uint64_t seed, uint32_t stream, uint64
 zxs_status zxs_debug_heavy_layout(const zxs_model_desc *desc, uint64_t min_factors, uint32_t *out, uint64_t cap,
                                   uint64_t *needed);
 
+/* Diagnostic (host only): the record streams of the integer monomial path
+   (zxs_mono.cuh) for components with >= min_factors factors. out receives
+   {n_words, n_chunks, n_tensor_bounds, n_dict, n_comps, n_components, 0, 0},
+   per mono component {ci, n_out, upos_base, out_begin, first_tensor}, the
+   per-component flags, tensor -> first-chunk bounds, chunks {word_begin,
+   n_words, n_terms, 0}, the form dictionary (4 words per entry), the words. */
+zxs_status zxs_debug_mono_layout(const zxs_model_desc *desc, uint64_t min_factors, uint32_t *out, uint64_t cap,
+                                 uint64_t *needed);
+
 /* Diagnostic: Philox4x32-10 blocks/s of this library's draw code (the shot
    kernel's Philox and filter compare, same launch shape, no memory traffic)
    on `device` -- the same-op-mix roofline of the error draw. */
 zxs_status zxs_measure_philox_peak(int device, double *blocks_per_s);
+
+/* Diagnostic: FP64 ops/s (DMUL + DADD, no FMA contraction, the exact
+   contraction's op mix) of a register-resident kernel on `device` -- the
+   roofline denominator of heavy_kernel. */
+zxs_status zxs_measure_fp64_peak(int device, double *ops_per_s);
 
 #ifdef __cplusplus
 }

@@ -15,6 +15,8 @@ from .sampler import (  # noqa: F401
     SamplerOptions,
     count_outputs,
     eval_batch,
+    eval_batch_mono,
+    measure_fp64_peak,
     measure_philox_peak,
     philox_uniform,
     probability_of_at,
@@ -26,6 +28,6 @@ from .sampler import (  # noqa: F401
 
 __all__ = [
     "MODE_DETECTORS", "MODE_MEASUREMENTS", "BatchEvalResult", "CompiledSampler", "SampleRecord",
-    "SamplerOptions", "count_outputs", "eval_batch", "measure_philox_peak", "philox_uniform", "probability_of_at",
+    "SamplerOptions", "count_outputs", "eval_batch", "eval_batch_mono", "measure_fp64_peak", "measure_philox_peak", "philox_uniform", "probability_of_at",
     "sample_detectors", "sample_error_batch", "sample_given_f", "sample_measurements",
 ]

@@ -30,7 +30,9 @@ class SamplerInfo(ctypes.Structure):
         "num_direct", "num_components", "max_chain", "fwords")] + [
         ("num_terms", ctypes.c_uint64), ("num_factors", ctypes.c_uint64),
         ("num_selector_bits", ctypes.c_uint64), ("philox_blocks_per_shot", ctypes.c_uint64),
-        ("device_bytes", ctypes.c_uint64), ("device", ctypes.c_int), ("monomial", ctypes.c_int)]
+        ("device_bytes", ctypes.c_uint64), ("device", ctypes.c_int), ("monomial", ctypes.c_int),
+        ("num_mono_components", ctypes.c_uint32), ("num_mono_forms", ctypes.c_uint32),
+        ("num_mono_records", ctypes.c_uint64), ("num_mono_dead_terms", ctypes.c_uint64)]
 
     def as_dict(self) -> dict:
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -52,14 +54,19 @@ SIGNATURES = (
     ("zxs_sample_error_batch", ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _u64p]),
     ("zxs_eval_batch", ctypes.c_int, [_vp, ctypes.c_uint32, ctypes.c_uint32, _u64p, ctypes.c_uint32,
                                       ctypes.c_uint64, _dp, _dp]),
+    ("zxs_eval_batch_mono", ctypes.c_int, [_vp, ctypes.c_uint32, ctypes.c_uint32, _u64p, ctypes.c_uint32,
+                                           ctypes.c_uint64, _dp]),
     ("zxs_sample_given_f", ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _u64p, _dp,
                                           _u64p]),
     ("zxs_probability_of_at", ctypes.c_int, [_vp, _u8p, ctypes.c_uint32, _u8p, ctypes.c_uint32, _dp]),
     ("zxs_philox_uniform", ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
                                           ctypes.c_uint64, _dp]),
     ("zxs_measure_philox_peak", ctypes.c_int, [ctypes.c_int, _dp]),
+    ("zxs_measure_fp64_peak", ctypes.c_int, [ctypes.c_int, _dp]),
     ("zxs_debug_heavy_layout", ctypes.c_int, [ctypes.POINTER(_fmt.ModelDesc), ctypes.c_uint64,
                                               ctypes.POINTER(ctypes.c_uint32), ctypes.c_uint64, _u64p]),
+    ("zxs_debug_mono_layout", ctypes.c_int, [ctypes.POINTER(_fmt.ModelDesc), ctypes.c_uint64,
+                                             ctypes.POINTER(ctypes.c_uint32), ctypes.c_uint64, _u64p]),
 )
 
 _lib = None

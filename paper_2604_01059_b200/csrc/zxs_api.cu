@@ -30,6 +30,7 @@
 
 #include "zxs_b200.h"
 #include "zxs_heavy.cuh"
+#include "zxs_mono.cuh"
 
 using zxs_dev::DevModel;
 using zxs_dev::Factor;
@@ -147,6 +148,26 @@ struct zxs_sampler {
     char *heavy_scratch = nullptr;
     size_t heavy_scratch_bytes = 0;
 
+    // large-chi components on the integer monomial path, see zxs_mono.cuh
+    bool has_mono = false;
+    zxs_dev::MonoArgs mono{};
+    size_t mono_smem = 0;
+    int mono_blocks_per_sm = 0;
+    std::map<uint32_t, uint32_t> mono_tensor;  // model tensor -> mono tensor index
+    char *mono_scratch = nullptr;
+    size_t mono_scratch_bytes = 0;
+
+    double *mono_scratch_get(size_t bytes) {
+        if (bytes > mono_scratch_bytes) {
+            if (mono_scratch) CK(cudaFree(mono_scratch));
+            mono_scratch = nullptr;
+            mono_scratch_bytes = 0;
+            CK(cudaMalloc(&mono_scratch, bytes));
+            mono_scratch_bytes = bytes;
+        }
+        return reinterpret_cast<double *>(mono_scratch);
+    }
+
     uint32_t *heavy_fcols_get(size_t bytes) {
         if (bytes > heavy_scratch_bytes) {
             if (heavy_scratch) CK(cudaFree(heavy_scratch));
@@ -225,7 +246,8 @@ struct HeavyHost {
     uint32_t max_chain = 0, zero_row = 0;
 };
 
-HeavyHost encode_heavy(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy_min) {
+HeavyHost encode_heavy(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy_min,
+                       const std::vector<uint8_t> *skip = nullptr) {
     HeavyHost H;
     std::vector<uint8_t> &comp_heavy = H.comp_heavy;
     std::vector<uint32_t> &hw = H.words;
@@ -245,7 +267,7 @@ HeavyHost encode_heavy(const zxs_model_desc *d, uint32_t max_chain, uint64_t hea
             const uint32_t t0 = d->comp_tensor_begin[c], t1 = d->comp_tensor_begin[c + 1];
             uint64_t nf = d->term_factor_begin[d->tensor_term_begin[t1]] - d->term_factor_begin[d->tensor_term_begin[t0]];
             bool ok = nf >= heavy_min && d->num_h_tables <= 256 && hcomps.size() < size_t(zxs_dev::kMaxHeavyComps) &&
-                      heavy_zero_row < 256;
+                      heavy_zero_row < 256 && !(skip && (*skip)[c]);
             // encode every tensor of the chain; abandon (light path) on any misfit
             std::vector<uint32_t> w;
             std::vector<uint4> ch;
@@ -321,6 +343,316 @@ HeavyHost encode_heavy(const zxs_model_desc *d, uint32_t max_chain, uint64_t hea
     }
     if (hw.empty()) hw.assign(4, 0);
     if (hchunks.empty()) hchunks.push_back(make_uint4(0, 0, 0, 0));
+    return H;
+}
+
+// ---------------------------------------------------------------- monomial path
+// Exact value of h(a,b) for a table with alpha = pa*pi/2, beta = pb*pi/2
+// (scalar.cpp:81-85): h = 1 + x + y - xy = 2 - (1-x)(1-y), x = i^(pa+2a),
+// y = i^(pb+2b), as a Gaussian integer; then 0 or 2^(m/2) w^k.
+struct MonoEntry {
+    bool zero;
+    int m, k;  // h = 2^(m/2) w^k
+    int re, im;
+};
+
+MonoEntry mono_entry(int pa, int pb, int a, int b) {
+    static const int ire[4] = {1, 0, -1, 0}, iim[4] = {0, 1, 0, -1};
+    const int jx = (pa + 2 * a) & 3, jy = (pb + 2 * b) & 3;
+    const int x1 = 1 - ire[jx], y1 = -iim[jx], x2 = 1 - ire[jy], y2 = -iim[jy];
+    const int pr = x1 * x2 - y1 * y2, pi = x1 * y2 + y1 * x2;
+    MonoEntry e{false, 0, 0, 2 - pr, -pi};
+    if (e.re == 0 && e.im == 0) {
+        e.zero = true;
+        return e;
+    }
+    const int n2 = e.re * e.re + e.im * e.im;
+    e.m = n2 == 4 ? 2 : (n2 == 8 ? 3 : -1);
+    static const int kr[8] = {2, 2, 0, -2, -2, -2, 0, 2}, ki[8] = {0, 2, 2, 2, 0, -2, -2, -2};
+    e.k = -1;
+    for (int k = 0; k < 8; k++) {
+        if (kr[k] == e.re && ki[k] == e.im) e.k = k;
+    }
+    return e;
+}
+
+struct MonoHost {
+    std::vector<uint8_t> comp_mono;
+    std::vector<uint32_t> words;
+    std::vector<uint4> chunks;
+    std::vector<uint32_t> tensor_chunk_begin{0};
+    std::vector<uint4> dict;
+    std::vector<zxs_dev::HeavyComp> comps;
+    std::map<uint32_t, uint32_t> tensor_index;  // model tensor -> index into tensor_chunk_begin
+    uint32_t max_chain = 0;
+    uint64_t records = 0, dead_terms = 0, selectors = 0;
+};
+
+// Lowers every eligible large component to the record streams of
+// zxs_mono.cuh. A component is eligible when every h table it uses is the
+// exact Clifford form above (alpha, beta multiples of pi/2; table values equal
+// to the exact ones within 1e-9), each table's non-zero entries share m and
+// k mod 2, and its parameters fit the byte selectors.
+MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy_min) {
+    MonoHost H;
+    H.comp_mono.assign(std::max<uint32_t>(1, d->num_components), 0);
+    const uint32_t fwid = d->f_width;
+    // table classes
+    std::vector<int> tpa(d->num_h_tables, -1), tpb(d->num_h_tables, -1);
+    for (uint32_t t = 0; t < d->num_h_tables; t++) {
+        const double qa = d->h_alpha[t] / (M_PI / 2), qb = d->h_beta[t] / (M_PI / 2);
+        if (std::fabs(qa - std::round(qa)) > 1e-9 || std::fabs(qb - std::round(qb)) > 1e-9) continue;
+        const int pa = int(((long long)std::llround(qa) % 4 + 4) % 4), pb = int(((long long)std::llround(qb) % 4 + 4) % 4);
+        bool ok = true;
+        for (int ab = 0; ab < 4 && ok; ab++) {
+            const MonoEntry e = mono_entry(pa, pb, ab >> 1, ab & 1);
+            if (!e.zero && (e.m < 0 || e.k < 0)) ok = false;
+            const double re = d->h_table[8 * t + 2 * ab], im = d->h_table[8 * t + 2 * ab + 1];
+            if (std::fabs(re - e.re) > 1e-9 || std::fabs(im - e.im) > 1e-9) ok = false;
+        }
+        if (ok) {
+            tpa[t] = pa;
+            tpb[t] = pb;
+        }
+    }
+    std::map<std::vector<uint32_t>, uint32_t> form_id;
+    // dictionary entry: u16 count | 0x8000 (continues), then up to seven u16
+    // plane byte offsets p * 128 (zxs_mono.cuh mono_form)
+    auto dict_form = [&](const std::vector<uint32_t> &sel) -> uint32_t {
+        auto it = form_id.find(sel);
+        if (it != form_id.end()) return it->second;
+        const uint32_t id = uint32_t(H.dict.size());
+        for (size_t i = 0; i < sel.size() || i == 0; i += 7) {
+            const size_t n = std::min<size_t>(7, sel.size() - i);
+            uint16_t e[8] = {};
+            e[0] = uint16_t(n | (i + 7 < sel.size() ? 0x8000 : 0));
+            for (size_t j = 0; j < n; j++) e[1 + j] = uint16_t(sel[i + j] * 128);
+            uint4 w;
+            std::memcpy(&w, e, 16);
+            H.dict.push_back(w);
+        }
+        form_id.emplace(sel, id);
+        return id;
+    };
+    // parity list of a selector range after XOR cancellation, sorted
+    auto sel_list = [](const uint32_t *bits, uint64_t n) {
+        std::vector<uint32_t> v(bits, bits + n);
+        std::sort(v.begin(), v.end());
+        std::vector<uint32_t> r;
+        for (size_t i = 0; i < v.size();) {
+            size_t j = i;
+            while (j < v.size() && v[j] == v[i]) j++;
+            if ((j - i) & 1) r.push_back(v[i]);
+            i = j;
+        }
+        return r;
+    };
+
+    uint32_t upos = 0;
+    for (uint32_t c = 0; c < d->num_components; c++) {
+        const uint32_t n = d->comp_out_begin[c + 1] - d->comp_out_begin[c];
+        const uint32_t t0 = d->comp_tensor_begin[c], t1 = d->comp_tensor_begin[c + 1];
+        const uint64_t nf = d->term_factor_begin[d->tensor_term_begin[t1]] - d->term_factor_begin[d->tensor_term_begin[t0]];
+        bool ok = nf >= heavy_min && H.comps.size() < size_t(zxs_dev::kMaxMonoComps) && fwid + n <= 255;
+        const size_t dict_mark = H.dict.size();
+        const auto form_mark = form_id;
+        std::vector<uint32_t> w;
+        std::vector<uint4> ch;
+        std::vector<uint32_t> tcb;
+        uint64_t recs = 0, dead = 0, nsel = 0;
+        // v lists first: they are the second form of two-form records (12-bit field)
+        for (uint64_t k = d->term_factor_begin[d->tensor_term_begin[t0]];
+             ok && k < d->term_factor_begin[d->tensor_term_begin[t1]]; k++) {
+            const std::vector<uint32_t> vs = sel_list(d->factor_v_bits + d->factor_v_begin[k],
+                                                      d->factor_v_begin[k + 1] - d->factor_v_begin[k]);
+            if (!vs.empty() && dict_form(vs) >= 0xfffu) ok = false;
+        }
+        for (uint32_t t = t0; ok && t < t1; t++) {
+            uint32_t cur_begin = uint32_t(H.words.size() + w.size()), cur_terms = 0;
+            auto close_chunk = [&]() {
+                if (H.words.size() + w.size() == cur_begin) w.insert(w.end(), 4, 0u);  // no 0-byte bulk copies
+                while ((H.words.size() + w.size()) % 4) w.push_back(0);
+                const uint32_t end = uint32_t(H.words.size() + w.size());
+                ch.push_back(make_uint4(cur_begin, end - cur_begin, cur_terms, 0));
+                cur_begin = end;
+                cur_terms = 0;
+            };
+            tcb.push_back(uint32_t(H.chunks.size() + ch.size()));
+            for (uint64_t term = d->tensor_term_begin[t]; ok && term < d->tensor_term_begin[t + 1]; term++) {
+                std::vector<uint32_t> tw;
+                int M = 0, K = 0;
+                bool term_dead = false;
+                for (uint64_t k = d->term_factor_begin[term]; k < d->term_factor_begin[term + 1]; k++) {
+                    const uint32_t tb = d->factor_table[k];
+                    if (tb >= d->num_h_tables || tpa[tb] < 0) {
+                        ok = false;
+                        break;
+                    }
+                    const std::vector<uint32_t> us = sel_list(d->factor_u_bits + d->factor_u_begin[k],
+                                                              d->factor_u_begin[k + 1] - d->factor_u_begin[k]);
+                    const std::vector<uint32_t> vs = sel_list(d->factor_v_bits + d->factor_v_begin[k],
+                                                              d->factor_v_begin[k + 1] - d->factor_v_begin[k]);
+                    for (uint32_t p : us) ok &= p < fwid + n;
+                    for (uint32_t p : vs) ok &= p < fwid + n;
+                    if (!ok) break;
+                    const bool ua = !us.empty(), vb = !vs.empty();
+                    // domain and non-zero set
+                    MonoEntry en[4];
+                    int mset = -1, oset = -1, nnz = 0;
+                    bool indomain[4], zero[4];
+                    for (int ab = 0; ab < 4; ab++) {
+                        const int a = ab >> 1, b = ab & 1;
+                        en[ab] = mono_entry(tpa[tb], tpb[tb], a, b);
+                        indomain[ab] = (a == 0 || ua) && (b == 0 || vb);
+                        zero[ab] = en[ab].zero;
+                        if (!indomain[ab] || zero[ab]) continue;
+                        nnz++;
+                        if (mset < 0) mset = en[ab].m;
+                        if (oset < 0) oset = en[ab].k & 1;
+                        if (mset != en[ab].m || oset != (en[ab].k & 1)) ok = false;
+                    }
+                    if (!ok) break;
+                    if (nnz == 0) {
+                        term_dead = true;  // identically zero factor: the term is exactly 0
+                        continue;
+                    }
+                    M += mset;
+                    K += oset;
+                    // J increment d(a,b) = (k - o)/2 mod 4 on the non-zero domain points:
+                    // cheapest d00 + al*a + be*b + ga*a*b that matches
+                    int best = -1, bc = 1 << 30;
+                    for (int code = 0; code < 256; code++) {
+                        const int d00 = code & 3, al = (code >> 2) & 3, be = (code >> 4) & 3, ga = (code >> 6) & 3;
+                        if ((!ua && (al || ga)) || (!vb && (be || ga))) continue;
+                        bool fits = true;
+                        for (int ab = 0; ab < 4 && fits; ab++) {
+                            if (!indomain[ab] || zero[ab]) continue;
+                            const int a = ab >> 1, b = ab & 1;
+                            fits = ((d00 + al * a + be * b + ga * a * b) & 3) == (((en[ab].k - oset) / 2) & 3);
+                        }
+                        if (!fits) continue;
+                        const int cost = (al != 0) + 4 * (be != 0) + 8 * (ga != 0);
+                        if (cost < bc) {
+                            bc = cost;
+                            best = code;
+                        }
+                    }
+                    if (best < 0) {
+                        ok = false;
+                        break;
+                    }
+                    const int d00 = best & 3, al = (best >> 2) & 3, be = (best >> 4) & 3, ga = (best >> 6) & 3;
+                    K += 2 * d00;
+                    // zero function on the domain (points outside it are don't-care -> 0)
+                    uint32_t zl = 0;
+                    for (int ab = 0; ab < 4; ab++) {
+                        if (indomain[ab] && zero[ab]) zl |= 1u << ab;
+                    }
+                    const uint32_t fa = ua ? dict_form(us) : 0xffffu, fbv = vb ? dict_form(vs) : 0xfffu;
+                    if (vb && fbv >= 0xfffu) {
+                        ok = false;
+                        break;
+                    }
+                    nsel += us.size() + vs.size();
+                    auto rec = [&](uint32_t kind, uint32_t a_form, uint32_t b_form) {
+                        tw.push_back(kind << 28 | (b_form & 0xfffu) << 16 | (a_form & 0xffffu));
+                        recs++;
+                    };
+                    const bool jnone = !al && !be && !ga;
+                    // Z patterns over the domain points present (bit index a*2+b)
+                    const uint32_t zA = ua ? 0xCu : 0u;          // a == 1
+                    const uint32_t zAn = 0x3u;                   // a == 0
+                    const uint32_t zB = vb ? 0xAu : 0u;          // b == 1
+                    const uint32_t zBn = 0x5u;                   // b == 0
+                    uint32_t dm = 0;
+                    for (int ab = 0; ab < 4; ab++) dm |= indomain[ab] ? 1u << ab : 0u;
+                    auto zis = [&](uint32_t pat) { return (pat & dm) == zl; };
+                    if (zl == 0) {
+                        if (jnone) continue;  // constant factor
+                        if (!be && !ga) {
+                            rec(al == 1 ? zxs_dev::kRecAdd : al == 3 ? zxs_dev::kRecSub : zxs_dev::kRecAdd2, fa, 0xfffu);
+                        } else if (!al && !ga) {
+                            rec(be == 1 ? zxs_dev::kRecAdd : be == 3 ? zxs_dev::kRecSub : zxs_dev::kRecAdd2,
+                                dict_form(vs), 0xfffu);
+                        } else {
+                            rec(zxs_dev::kRecGen, fa, fbv);
+                            tw.push_back(uint32_t(al | be << 2 | ga << 4));
+                        }
+                    } else if (jnone && ua && zis(zA)) {
+                        rec(zxs_dev::kRecZ, fa, 0xfffu);
+                    } else if (jnone && ua && zis(zAn)) {
+                        rec(zxs_dev::kRecZn, fa, 0xfffu);
+                    } else if (jnone && vb && zis(zB)) {
+                        rec(zxs_dev::kRecZ, dict_form(vs), 0xfffu);
+                    } else if (jnone && vb && zis(zBn)) {
+                        rec(zxs_dev::kRecZn, dict_form(vs), 0xfffu);
+                    } else if (jnone && ua && vb && zis(0x6u)) {
+                        rec(zxs_dev::kRecZx, fa, fbv);
+                    } else if (jnone && ua && vb && zis(0x9u)) {
+                        rec(zxs_dev::kRecZxn, fa, fbv);
+                    } else {
+                        rec(zxs_dev::kRecGen, fa, fbv);
+                        tw.push_back(uint32_t(al | be << 2 | ga << 4) | zl << 6);
+                    }
+                }
+                if (!ok) break;
+                if (term_dead) {
+                    dead++;
+                    continue;
+                }
+                // c' = c * 2^(M/2) * w^K
+                static const long double s2 = 0.70710678118654752440084436210484903928L;
+                static const long double wr[8] = {1, s2, 0, -s2, -1, -s2, 0, s2}, wi[8] = {0, s2, 1, s2, 0, -s2, -1, -s2};
+                const int k8 = K & 7;
+                long double mag = std::ldexp(1.0L, M / 2);
+                if (M & 1) mag *= 1.41421356237309504880168872420969807857L;
+                const long double cr = d->term_c[2 * term], ci = d->term_c[2 * term + 1];
+                const double re = double((cr * wr[k8] - ci * wi[k8]) * mag);
+                const double im = double((cr * wi[k8] + ci * wr[k8]) * mag);
+                uint64_t rb, ib;
+                std::memcpy(&rb, &re, 8);
+                std::memcpy(&ib, &im, 8);
+                std::vector<uint32_t> hdr = {uint32_t(tw.size()), 0u, uint32_t(rb), uint32_t(rb >> 32), uint32_t(ib),
+                                             uint32_t(ib >> 32)};
+                if (hdr.size() + tw.size() + 4 > zxs_dev::kMonoChunkWords) {
+                    ok = false;
+                    break;
+                }
+                if (H.words.size() + w.size() + hdr.size() + tw.size() - cur_begin > zxs_dev::kMonoChunkWords) close_chunk();
+                w.insert(w.end(), hdr.begin(), hdr.end());
+                w.insert(w.end(), tw.begin(), tw.end());
+                cur_terms++;
+            }
+            if (ok && (cur_terms || H.words.size() + w.size() == cur_begin)) close_chunk();
+        }
+        if (ok && H.dict.size() >= 0xffffu) ok = false;
+        if (ok) {
+            zxs_dev::HeavyComp hc;
+            hc.ci = c;
+            hc.n_out = n;
+            hc.upos_base = upos;
+            hc.out_begin = d->comp_out_begin[c];
+            hc.first_tensor = uint32_t(H.tensor_chunk_begin.size() - 1);
+            for (uint32_t t = t0; t < t1; t++) H.tensor_index[t] = hc.first_tensor + (t - t0);
+            H.words.insert(H.words.end(), w.begin(), w.end());
+            H.chunks.insert(H.chunks.end(), ch.begin(), ch.end());
+            for (size_t i = 1; i < tcb.size(); i++) H.tensor_chunk_begin.push_back(tcb[i]);
+            H.tensor_chunk_begin.push_back(uint32_t(H.chunks.size()));
+            H.comps.push_back(hc);
+            H.comp_mono[c] = 1;
+            H.max_chain = std::max(H.max_chain, n);
+            H.records += recs;
+            H.dead_terms += dead;
+            H.selectors += nsel;
+        } else {
+            H.dict.resize(dict_mark);
+            form_id = form_mark;
+        }
+        upos += n;
+    }
+    if (H.words.empty()) H.words.assign(4, 0);
+    if (H.chunks.empty()) H.chunks.push_back(make_uint4(0, 0, 0, 0));
+    if (H.dict.empty()) H.dict.push_back(make_uint4(0, 0, 0, 0));
     return H;
 }
 
@@ -534,8 +866,18 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     // ---- heavy components: compact chunked streams (zxs_heavy.cuh)
     uint64_t heavy_min = 20000;
     if (const char *e = std::getenv("ZXS_HEAVY_MIN_FACTORS")) heavy_min = std::strtoull(e, nullptr, 10);
-    HeavyHost H = encode_heavy(d, max_chain, heavy_min);
+    bool use_mono = true;
+    if (const char *e = std::getenv("ZXS_MONO")) use_mono = std::strcmp(e, "0") != 0;
+    MonoHost MH = use_mono ? encode_mono(d, max_chain, heavy_min) : MonoHost{};
+    if (!use_mono) {
+        MH.comp_mono.assign(std::max<uint32_t>(1, d->num_components), 0);
+        MH.words.assign(4, 0);
+        MH.chunks.push_back(make_uint4(0, 0, 0, 0));
+        MH.dict.push_back(make_uint4(0, 0, 0, 0));
+    }
+    HeavyHost H = encode_heavy(d, max_chain, heavy_min, &MH.comp_mono);
     std::vector<uint8_t> &comp_heavy = H.comp_heavy;
+    for (size_t c = 0; c < comp_heavy.size(); c++) comp_heavy[c] |= MH.comp_mono[c] ? 2 : 0;
     std::vector<uint32_t> &hw = H.words;
     std::vector<uint4> &hchunks = H.chunks;
     std::vector<uint32_t> &htcb = H.tensor_chunk_begin;
@@ -589,6 +931,10 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     size_t o_hchunks = ar.add(hchunks);
     size_t o_htcb = ar.add(htcb);
     size_t o_hw = ar.add(hw);
+    size_t o_mw = ar.add(MH.words);
+    size_t o_mch = ar.add(MH.chunks);
+    size_t o_mtcb = ar.add(MH.tensor_chunk_begin);
+    size_t o_mdict = ar.add(MH.dict);
 
     CK(cudaMalloc(&s->dev_model, ar.host.size()));
     s->dev_model_bytes = ar.host.size();
@@ -649,6 +995,27 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         s->heavy_smem = 128 + 2 * size_t(zxs_dev::kChunkWords) * 4 + size_t(ha.n_tables) * 64 +
                         size_t(zxs_dev::kHeavyWarps) * ha.col_words * 64;  // 16-bit planes
     }
+    s->has_mono = !MH.comps.empty();
+    if (s->has_mono) {
+        zxs_dev::MonoArgs &ma = s->mono;
+        ma.f_width = fwid;
+        ma.n_planes = fwid + MH.max_chain;
+        ma.words = reinterpret_cast<const uint32_t *>(b + o_mw);
+        ma.chunks = reinterpret_cast<const uint4 *>(b + o_mch);
+        ma.tensor_chunk_begin = reinterpret_cast<const uint32_t *>(b + o_mtcb);
+        ma.total_chunks = static_cast<uint32_t>(MH.chunks.size());
+        ma.dict = reinterpret_cast<const uint4 *>(b + o_mdict);
+        ma.comp_outputs = m.comp_outputs;
+        ma.eval_tensor = -1;
+        ma.n_comps = static_cast<uint32_t>(MH.comps.size());
+        for (size_t i = 0; i < MH.comps.size(); i++) ma.comps[i] = MH.comps[i];
+        s->mono_tensor = MH.tensor_index;
+        s->mono_smem = 128 + 2 * size_t(zxs_dev::kMonoChunkWords) * 4 + size_t(zxs_dev::kMonoWarps) * ma.n_planes * 128;
+    }
+    s->info.num_mono_components = uint32_t(MH.comps.size());
+    s->info.num_mono_records = MH.records;
+    s->info.num_mono_dead_terms = MH.dead_terms;
+    s->info.num_mono_forms = uint32_t(MH.dict.size());
     m.mech_entry_begin = nullptr;
     m.mech_stream = nullptr;
     m.entry_lim = nullptr;
@@ -705,6 +1072,52 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
                                                          s->heavy_smem));
         if (s->heavy_blocks_per_sm < 1) fail(ZXS_UNSUPPORTED, "heavy kernel does not fit on an SM");
     }
+    if (s->has_mono) {
+        const void *mk = reinterpret_cast<const void *>(&zxs_dev::mono_kernel);
+        CK(cudaFuncSetAttribute(mk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->mono_smem)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->mono_blocks_per_sm, mk, zxs_dev::kMonoWarps * 32,
+                                                         s->mono_smem));
+        if (s->mono_blocks_per_sm < 1) fail(ZXS_UNSUPPORTED, "mono kernel does not fit on an SM");
+    }
+}
+
+// Launches mono_kernel for shots [first_shot, first_shot + shots): the
+// large-chi components on the integer path, after shot_kernel left their
+// f-columns in `fcols` ([f_width][fcols_ld32] 32-bit words).
+void launch_mono(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *fcols, uint64_t fcols_ld32,
+                 int eval_tensor, double *eval_out, uint32_t f_width, cudaStream_t st) {
+    zxs_dev::MonoArgs h = s->mono;
+    h.seed = a.seed;
+    h.first_shot = a.first_shot;
+    h.shots = a.shots;
+    for (int i = 0; i < 10; i++) h.k0_round[i] = a.k0_round[i];
+    h.fcols = fcols;
+    h.fcols_ld32 = fcols_ld32;
+    h.out32 = a.out32;
+    h.out_ld32 = a.ld32;
+    h.counts = a.counts;
+    h.uniforms = a.uniforms;
+    h.uniforms_ld = a.uniforms_ld;
+    h.err = s->dev_err;
+    h.eval_tensor = eval_tensor;
+    h.eval_out = eval_out;
+    if (eval_tensor >= 0) {
+        h.f_width = f_width;
+        h.n_planes = std::max(h.n_planes, f_width);
+    }
+    const uint64_t per_cta = uint64_t(zxs_dev::kMonoWarps) * 1024;
+    h.n_cta_tiles = (a.shots + per_cta - 1) / per_cta;
+    if (h.n_cta_tiles == 0) return;
+    h.scratch = s->mono_scratch_get(size_t(2) * h.n_cta_tiles * per_cta * 8);
+    const size_t smem = 128 + 2 * size_t(zxs_dev::kMonoChunkWords) * 4 + size_t(zxs_dev::kMonoWarps) * h.n_planes * 128;
+    if (smem > s->mono_smem) {
+        CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(&zxs_dev::mono_kernel),
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    }
+    const unsigned grid = unsigned(std::min<uint64_t>(h.n_cta_tiles, uint64_t(s->sm_count) * std::max(1, s->mono_blocks_per_sm)));
+    void *args[] = {&h};
+    CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::mono_kernel), dim3(grid),
+                        dim3(zxs_dev::kMonoWarps * 32), args, smem, st));
 }
 
 void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
@@ -723,14 +1136,15 @@ void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
     unsigned grid = unsigned(std::min(a.n_tiles, cap));
     size_t smem = shot_smem_bytes(s);
     static zxs_dev::MechTable<1> unused_table{};
-    const bool heavy = s->has_heavy && !a.fcols_out;
+    const bool heavy = (s->has_heavy || s->has_mono) && !a.fcols_out;
     if (heavy) {
         a.heavy_ld32 = 2 * ((a.shots + 63) / 64);
         a.heavy_fcols = s->heavy_fcols_get(std::max<size_t>(16, size_t(s->m.f_width) * a.heavy_ld32 * 4));
     }
     void *args[] = {&a, s->param_mechs ? static_cast<void *>(s->mech_table.get()) : static_cast<void *>(&unused_table)};
     CK(cudaLaunchKernel(shot_kernel_for(s->fw_template, s->param_mechs), dim3(grid), dim3(32), args, smem, st));
-    if (heavy) {
+    if (heavy && s->has_mono) launch_mono(s, a, a.heavy_fcols, a.heavy_ld32, -1, nullptr, 0, st);
+    if (heavy && s->has_heavy) {
         zxs_dev::HeavyArgs h = s->heavy;
         h.seed = a.seed;
         h.first_shot = a.first_shot;
@@ -825,6 +1239,7 @@ void zxs_sampler_destroy(zxs_sampler *s) {
     if (s->dev_err) cudaFree(s->dev_err);
     if (s->scratch) cudaFree(s->scratch);
     if (s->heavy_scratch) cudaFree(s->heavy_scratch);
+    if (s->mono_scratch) cudaFree(s->mono_scratch);
     if (prev >= 0) cudaSetDevice(prev);
     delete s;
 }
@@ -1065,6 +1480,40 @@ zxs_status zxs_eval_batch(zxs_sampler *s, uint32_t component, uint32_t chain_pos
     });
 }
 
+zxs_status zxs_eval_batch_mono(zxs_sampler *s, uint32_t component, uint32_t chain_pos, const uint64_t *host_params,
+                               uint32_t param_cols, uint64_t shots, double *host_values) {
+    return guarded([&] {
+        if (!s) fail(ZXS_INVALID_ARGUMENT, "null sampler");
+        if (component >= s->comp_out_begin.size() - 1) fail(ZXS_INVALID_ARGUMENT, "component out of range");
+        uint32_t n = s->comp_out_begin[component + 1] - s->comp_out_begin[component];
+        if (chain_pos > n) fail(ZXS_INVALID_ARGUMENT, "chain position out of range");
+        uint32_t t = s->comp_tensor_begin[component] + chain_pos;
+        if (param_cols < s->tensor_width[t]) fail(ZXS_INVALID_ARGUMENT, "eval_batch: parameter width mismatch");
+        auto it = s->mono_tensor.find(t);
+        if (it == s->mono_tensor.end()) fail(ZXS_UNSUPPORTED, "component is not on the monomial path");
+        if (param_cols > 255) fail(ZXS_UNSUPPORTED, "too many parameter columns for the monomial path");
+        if (shots == 0) return;
+        if (!host_params || !host_values) fail(ZXS_INVALID_ARGUMENT, "null argument");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard g(s->device);
+        cudaStream_t st = s->stream;
+        const uint64_t words = (shots + 63) / 64;
+        size_t pbytes = size_t(words) * param_cols * 8;
+        size_t vbytes = size_t(shots) * 8;
+        auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+        char *base = s->scratch_get(al(pbytes) + al(vbytes) + 256);
+        auto *dp = reinterpret_cast<uint32_t *>(base);
+        auto *dv = reinterpret_cast<double *>(base + al(pbytes));
+        CK(cudaMemcpyAsync(dp, host_params, pbytes, cudaMemcpyHostToDevice, st));
+        zxs_dev::LaunchArgs a{};
+        a.shots = shots;
+        launch_mono(s, a, dp, 2 * words, int(it->second), dv, param_cols, st);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(host_values, dv, vbytes, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    });
+}
+
 // probability_of_at (sampler.cpp:360-368) -> outcome_probability_given
 // (sampler.cpp:324-356), every eval on the device.
 zxs_status zxs_probability_of_at(zxs_sampler *s, const uint8_t *outcome, uint32_t n_outcome,
@@ -1139,6 +1588,29 @@ zxs_status zxs_debug_heavy_layout(const zxs_model_desc *desc, uint64_t min_facto
     });
 }
 
+zxs_status zxs_debug_mono_layout(const zxs_model_desc *desc, uint64_t min_factors, uint32_t *out, uint64_t cap,
+                                 uint64_t *needed) {
+    return guarded([&] {
+        if (!desc || !needed) fail(ZXS_INVALID_ARGUMENT, "null argument");
+        uint32_t max_chain = 0;
+        for (uint32_t c = 0; c < desc->num_components; c++) {
+            max_chain = std::max(max_chain, desc->comp_out_begin[c + 1] - desc->comp_out_begin[c]);
+        }
+        MonoHost H = encode_mono(desc, max_chain, min_factors);
+        std::vector<uint32_t> blob = {uint32_t(H.words.size()), uint32_t(H.chunks.size()),
+                                      uint32_t(H.tensor_chunk_begin.size()), uint32_t(H.dict.size()),
+                                      uint32_t(H.comps.size()), uint32_t(H.comp_mono.size()), 0u, 0u};
+        for (const auto &c : H.comps) blob.insert(blob.end(), {c.ci, c.n_out, c.upos_base, c.out_begin, c.first_tensor});
+        for (uint8_t f : H.comp_mono) blob.push_back(f);
+        blob.insert(blob.end(), H.tensor_chunk_begin.begin(), H.tensor_chunk_begin.end());
+        for (const uint4 &c : H.chunks) blob.insert(blob.end(), {c.x, c.y, c.z, c.w});
+        for (const uint4 &c : H.dict) blob.insert(blob.end(), {c.x, c.y, c.z, c.w});
+        blob.insert(blob.end(), H.words.begin(), H.words.end());
+        *needed = blob.size();
+        if (out && cap >= blob.size()) std::memcpy(out, blob.data(), blob.size() * 4);
+    });
+}
+
 zxs_status zxs_measure_philox_peak(int device, double *blocks_per_s) {
     return guarded([&] {
         if (!blocks_per_s) fail(ZXS_INVALID_ARGUMENT, "null output");
@@ -1170,6 +1642,38 @@ zxs_status zxs_measure_philox_peak(int device, double *blocks_per_s) {
         cudaEventDestroy(e1);
         cudaFree(sink);
         *blocks_per_s = double(reps) * grid * tiles * zxs_dev::kTileShots * nmech / (ms * 1e-3);
+    });
+}
+
+zxs_status zxs_measure_fp64_peak(int device, double *ops_per_s) {
+    return guarded([&] {
+        if (!ops_per_s) fail(ZXS_INVALID_ARGUMENT, "null output");
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) fail(ZXS_CUDA_ERROR, "no CUDA device available");
+        DeviceGuard g(device);
+        int sms = 0, occ = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, zxs_dev::fp64_peak_kernel, 256, 0));
+        double *sink = nullptr;
+        CK(cudaMalloc(&sink, 8));
+        const uint32_t iters = 4096;
+        const unsigned grid = unsigned(sms * std::max(occ, 1));
+        const double2 hv = make_double2(0.70710678118654757, 0.70710678118654757);
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        zxs_dev::fp64_peak_kernel<<<grid, 256>>>(hv, iters, sink);  // warm-up
+        CK(cudaEventRecord(e0));
+        const int reps = 3;
+        for (int r = 0; r < reps; r++) zxs_dev::fp64_peak_kernel<<<grid, 256>>>(hv, iters, sink);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaFree(sink);
+        *ops_per_s = double(reps) * grid * 256.0 * iters * 8 * 8 / (ms * 1e-3);  // 8 chains x (4 DMUL + 4 DADD)
     });
 }
 

@@ -467,6 +467,23 @@ __global__ void __maxnreg__(ZXS_MAXNREG) philox_peak_kernel(const __grid_constan
     if (acc == 0x9e3779b9u) sink[0] = acc;  // keeps the work observable
 }
 
+// Same-op-mix roofline for the exact contraction (heavy_kernel): independent
+// chains of cmul_rn + cadd_rn (4 DMUL + 4 DADD, no FMA), 8 per thread.
+__global__ void __launch_bounds__(256) fp64_peak_kernel(double2 h, uint32_t iters, double *sink) {
+    double2 p[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) p[i] = make_double2(1.0 + 1e-3 * (threadIdx.x + i), 1e-3 * i);
+    double2 acc = make_double2(0.0, 0.0);
+    for (uint32_t it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            p[i] = cmul_rn(p[i], h);
+            acc = cadd_rn(acc, p[i]);
+        }
+    }
+    if (acc.x == 1.2345 && acc.y == 6.789) sink[0] = acc.x;  // keeps the work observable
+}
+
 __global__ void philox_kernel(uint64_t seed, uint32_t stream, uint64_t first, uint64_t n, double *out) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t idx = first + i;

@@ -1,0 +1,302 @@
+// zxs_mono.cuh — integer (Clifford-monomial) contraction of large-chi components.
+//
+// Every h table the reference builds is h(a,b) = 1 + e^{i(al+a pi)} +
+// e^{i(be+b pi)} - e^{i(al+be+a pi+b pi)} (phase_terms.cpp:40-47,
+// scalar.cpp:81-85). When al, be are multiples of pi/2 (every table of every
+// BASELINE circuit: the branches of decompose_magic are Clifford diagrams,
+// SURVEY §8 a13), each entry is exactly 0 or 2^(m/2) w^k (w = e^{i pi/4}) with
+// m fixed per table and k mod 2 fixed per table. So a term's product over its
+// factors is c_t 2^(M/2) w^(K0) i^J, where M, K0 are per-term constants and
+//   J = sum_k d_k(a_k, b_k) mod 4,   zero = OR_k z_k(a_k, b_k)
+// depend on the shot only through the factor parities a_k = u_k.P, b_k = v_k.P.
+// The host folds the constants into c'_t and lowers every factor to one
+// record acting on three bit-sliced words per lane (32 shots each):
+//   J0, J1  (J mod 4, two bit planes)   Z  (term is zero)
+// and the per-term epilogue adds Re(c'_t i^J) = {re, -im, -re, im}[J] to the
+// shot's FP64 accumulator for every non-zero shot, terms in the reference's
+// order (phase_terms.cpp:129-131). This is the north star's "exact
+// dyadic-phase accumulation": no floating-point work per factor at all; the
+// values differ from the reference's only by the reference's own rounding of
+// its h entries (~1e-16 relative), so sampled bits agree except at exact
+// threshold ties (counted by the tests).
+//
+// Work decomposition: lane = one 32-shot word (bit s = shot 32*w + s), a warp
+// = 1024 shots, a CTA = kMonoWarps warps that walk the SAME record stream:
+// chunks of the stream are fetched once per CTA with cp.async.bulk into a
+// double buffer and read with warp-uniform (broadcast) shared loads. The
+// parities a = u.P are formed from the lane's parameter planes in shared
+// memory (plane[p][lane], conflict-free), selector lists coming from a form
+// dictionary (distinct u/v lists of the component, 16 B per entry of up to
+// seven pre-scaled plane offsets, read through L1).
+#pragma once
+
+#include "zxs_heavy.cuh"
+
+namespace zxs_dev {
+
+constexpr int kMonoWarps = 8;                // warps per CTA (8192 shots per CTA tile)
+constexpr uint32_t kMonoChunkWords = 4096;   // 16 KiB per chunk buffer
+constexpr uint32_t kMonoNoFormA = 0xffffu;   // "no form" in the 16-bit first-form field: parity 0
+constexpr uint32_t kMonoNoFormB = 0xfffu;    // same in the 12-bit second-form field
+constexpr int kMaxMonoComps = 8;
+
+// record kinds (bits 28..31 of a record word; first form in bits 0..15,
+// second form in bits 16..27)
+enum : uint32_t {
+    kRecAdd = 0,    // J += a
+    kRecSub = 1,    // J -= a
+    kRecAdd2 = 2,   // J += 2a
+    kRecZ = 3,      // Z |= a
+    kRecZn = 4,     // Z |= ~a
+    kRecZx = 5,     // Z |= a ^ b
+    kRecZxn = 6,    // Z |= ~(a ^ b)
+    kRecGen = 15,   // next word: alpha | beta << 2 | gamma << 4 | zlut << 6
+};
+
+struct MonoArgs {
+    uint64_t seed, first_shot, shots, n_cta_tiles;
+    uint32_t k0_round[10];
+    uint32_t f_width, n_planes;       // planes per warp = f_width + longest mono chain
+    const uint32_t *fcols;            // [f_width][fcols_ld32] from shot_kernel
+    uint64_t fcols_ld32;
+    uint32_t *out32;                  // [num_outputs][out_ld32] (nullable)
+    uint64_t out_ld32;
+    unsigned long long *counts;       // (nullable)
+    const double *uniforms;           // injected AR uniforms (nullable)
+    uint64_t uniforms_ld;
+    unsigned long long *err;
+    double *scratch;                  // [2][n_cta_tiles * kMonoWarps * 1024]: prev, cur per shot
+    const uint32_t *words;            // record streams
+    const uint4 *chunks;              // {word_begin, n_words (multiple of 4), n_terms, 0}
+    const uint32_t *tensor_chunk_begin;
+    uint32_t total_chunks;
+    const uint4 *dict;                // form dictionary
+    const uint32_t *comp_outputs;
+    // eval seam: evaluate one tensor and store the values (no chain)
+    int eval_tensor;                  // -1: sample; else index into tensor_chunk_begin
+    double *eval_out;                 // [shots]
+    uint32_t n_comps;
+    HeavyComp comps[kMaxMonoComps];
+};
+
+// Parity word of form f for the lane's 32 shots: XOR of the lane's parameter
+// planes listed in the dictionary entry. Entry layout (16 B): u16 [0] =
+// count (0..7) | 0x8000 if the list continues in the next entry, u16 [1..7] =
+// byte offsets p * 128 of the planes (plane p of lane l at p * 128 + 4 l).
+// The switch falls through (a jump table into one straight run of loads),
+// so each selector costs one extract/add, one LDS and half a 3-input XOR.
+__device__ __forceinline__ uint32_t mono_form(const uint4 *__restrict__ dict, uint32_t f, const char *lb) {
+    uint32_t acc = 0;
+    while (true) {
+        const uint4 e = __ldg(dict + f);
+#define ZXS_SEL(x) (*reinterpret_cast<const uint32_t *>(lb + (x)))
+        switch (e.x & 7u) {
+            case 7: acc ^= ZXS_SEL(e.w >> 16);  // fallthrough
+            case 6: acc ^= ZXS_SEL(e.w & 0xffffu);  // fallthrough
+            case 5: acc ^= ZXS_SEL(e.z >> 16);  // fallthrough
+            case 4: acc ^= ZXS_SEL(e.z & 0xffffu);  // fallthrough
+            case 3: acc ^= ZXS_SEL(e.y >> 16);  // fallthrough
+            case 2: acc ^= ZXS_SEL(e.y & 0xffffu);  // fallthrough
+            case 1: acc ^= ZXS_SEL(e.x >> 16);  // fallthrough
+            default: break;
+        }
+#undef ZXS_SEL
+        if (!(e.x & 0x8000u)) break;
+        f++;
+    }
+    return acc;
+}
+
+// J += c * x (mod 4) on the bit planes (J0, J1), c in 0..3.
+__device__ __forceinline__ void j_add(uint32_t &j0, uint32_t &j1, uint32_t x, uint32_t c) {
+    const uint32_t xl = (c & 1u) ? x : 0u;
+    j1 ^= (j0 & xl) ^ ((c & 2u) ? x : 0u);
+    j0 ^= xl;
+}
+
+__global__ void __launch_bounds__(kMonoWarps * 32, 2) mono_kernel(const __grid_constant__ MonoArgs h) {
+    extern __shared__ __align__(128) uint8_t msm[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(msm);
+    uint32_t *buf0 = reinterpret_cast<uint32_t *>(msm + 128);
+    uint32_t *planes_all = buf0 + 2 * kMonoChunkWords;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    uint32_t *planes = planes_all + warp * h.n_planes * 32;  // [p][lane]
+    const char *pl = reinterpret_cast<const char *>(planes + lane);
+
+    // chunk uses per CTA tile: every tensor of every component (or the one eval tensor)
+    uint32_t chunks_per_tile = 0;
+    if (h.eval_tensor >= 0) {
+        chunks_per_tile = h.tensor_chunk_begin[h.eval_tensor + 1] - h.tensor_chunk_begin[h.eval_tensor];
+    } else {
+        for (uint32_t hc = 0; hc < h.n_comps; hc++) {
+            const HeavyComp cd = h.comps[hc];
+            chunks_per_tile += h.tensor_chunk_begin[cd.first_tensor + cd.n_out + 1] - h.tensor_chunk_begin[cd.first_tensor];
+        }
+    }
+    const uint64_t my_tiles = blockIdx.x < h.n_cta_tiles ? (h.n_cta_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const uint64_t total_uses = my_tiles * chunks_per_tile;
+    // chunk sequence of use u: tile-major, then tensors in chain order
+    auto chunk_of_use = [&](uint64_t u) -> uint32_t {
+        uint32_t r = uint32_t(u % chunks_per_tile);
+        if (h.eval_tensor >= 0) return h.tensor_chunk_begin[h.eval_tensor] + r;
+        for (uint32_t hc = 0; hc < h.n_comps; hc++) {
+            const HeavyComp cd = h.comps[hc];
+            const uint32_t c0 = h.tensor_chunk_begin[cd.first_tensor];
+            const uint32_t n = h.tensor_chunk_begin[cd.first_tensor + cd.n_out + 1] - c0;
+            if (r < n) return c0 + r;
+            r -= n;
+        }
+        return 0;
+    };
+    auto issue = [&](uint64_t u) {
+        const uint4 c = h.chunks[chunk_of_use(u)];
+        const uint32_t b = uint32_t(u & 1);
+        mbar_expect_tx(&bars[b], c.y * 4u);
+        bulk_g2s(buf0 + b * kMonoChunkWords, h.words + c.x, c.y * 4u, &bars[b]);
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (uint64_t u = 0; u < 2 && u < total_uses; u++) issue(u);
+    }
+    const uint32_t seed_hi = uint32_t(h.seed >> 32);
+    const uint32_t k2c = uint32_t(kP1c) ^ h.k0_round[1];
+    uint64_t use = 0;
+
+    for (uint64_t ct = blockIdx.x; ct < h.n_cta_tiles; ct += gridDim.x) {
+        const uint64_t wrd = (ct * kMonoWarps + warp) * 32 + lane;  // the lane's 32-shot word
+        for (uint32_t p = 0; p < h.n_planes; p++) {
+            planes[p * 32 + lane] = (p < h.f_width && wrd < h.fcols_ld32) ? h.fcols[p * h.fcols_ld32 + wrd] : 0u;
+        }
+        __syncwarp();
+        double *prev_g = h.scratch + wrd * 32;
+        double *cur_g = h.scratch + (h.n_cta_tiles * kMonoWarps * 1024) + wrd * 32;
+
+        const uint32_t ncomp = h.eval_tensor >= 0 ? 1u : h.n_comps;
+        for (uint32_t hc = 0; hc < ncomp; hc++) {
+            const HeavyComp cd = h.comps[hc];
+            const uint32_t npos = h.eval_tensor >= 0 ? 1u : cd.n_out + 1;
+            for (uint32_t pos = 0; pos < npos; pos++) {  // pos 0: normalization, pos j+1: marginal j
+                const uint32_t t = h.eval_tensor >= 0 ? uint32_t(h.eval_tensor) : cd.first_tensor + pos;
+                double acc[32];
+#pragma unroll
+                for (int s = 0; s < 32; s++) acc[s] = 0.0;
+                for (uint32_t c = h.tensor_chunk_begin[t]; c < h.tensor_chunk_begin[t + 1]; c++, use++) {
+                    const uint32_t b = uint32_t(use & 1);
+                    mbar_wait(&bars[b], uint32_t((use >> 1) & 1));
+                    const uint32_t *w = buf0 + b * kMonoChunkWords;
+                    const uint32_t nterms = h.chunks[c].z;
+                    uint32_t q = 0;
+                    for (uint32_t tt = 0; tt < nterms; tt++) {
+                        // term header: {n record words, 0, re.lo, re.hi, im.lo, im.hi}
+                        const uint32_t nw = w[q];
+                        const double re = __hiloint2double(int(w[q + 3]), int(w[q + 2]));
+                        const double im = __hiloint2double(int(w[q + 5]), int(w[q + 4]));
+                        q += 6;
+                        const uint32_t qe = q + nw;
+                        uint32_t j0 = 0, j1 = 0, z = 0;
+                        while (q < qe) {
+                            const uint32_t r = w[q++];
+                            const uint32_t kind = r >> 28;
+                            const uint32_t fa = r & 0xffffu;
+                            const uint32_t a = fa == kMonoNoFormA ? 0u : mono_form(h.dict, fa, pl);
+                            switch (kind) {
+                                case kRecAdd: j1 ^= j0 & a; j0 ^= a; break;
+                                case kRecSub: j1 ^= ~j0 & a; j0 ^= a; break;
+                                case kRecAdd2: j1 ^= a; break;
+                                case kRecZ: z |= a; break;
+                                case kRecZn: z |= ~a; break;
+                                default: {
+                                    const uint32_t fb = (r >> 16) & 0xfffu;
+                                    const uint32_t bb = fb == kMonoNoFormB ? 0u : mono_form(h.dict, fb, pl);
+                                    if (kind == kRecZx) {
+                                        z |= a ^ bb;
+                                    } else if (kind == kRecZxn) {
+                                        z |= ~(a ^ bb);
+                                    } else {  // kRecGen
+                                        const uint32_t g = w[q++];
+                                        const uint32_t zl = g >> 6;
+                                        z |= ((zl & 1u) ? (~a & ~bb) : 0u) | ((zl & 2u) ? (~a & bb) : 0u) |
+                                             ((zl & 4u) ? (a & ~bb) : 0u) | ((zl & 8u) ? (a & bb) : 0u);
+                                        j_add(j0, j1, a, g & 3u);
+                                        j_add(j0, j1, bb, (g >> 2) & 3u);
+                                        j_add(j0, j1, a & bb, (g >> 4) & 3u);
+                                    }
+                                }
+                            }
+                        }
+                        // epilogue: acc[s] += Re(c' i^J) for the non-zero shots, in term order
+                        const uint32_t neg = j0 ^ j1;
+#pragma unroll
+                        for (int s = 0; s < 32; s++) {
+                            const double v = ((j0 >> s) & 1u) ? im : re;
+                            const double sv = ((neg >> s) & 1u) ? -v : v;
+                            if (!((z >> s) & 1u)) acc[s] = __dadd_rn(acc[s], sv);
+                        }
+                    }
+                    __syncthreads();  // buffer b fully consumed by every warp
+                    if (threadIdx.x == 0 && use + 2 < total_uses) issue(use + 2);
+                }
+                if (h.eval_tensor >= 0) {
+#pragma unroll
+                    for (int s = 0; s < 32; s++) {
+                        if (wrd * 32 + s < h.shots) h.eval_out[wrd * 32 + s] = acc[s];
+                    }
+                    continue;
+                }
+                if (pos == 0) {
+#pragma unroll
+                    for (int s = 0; s < 32; s++) prev_g[s] = acc[s];
+                    continue;
+                }
+#pragma unroll
+                for (int s = 0; s < 32; s++) cur_g[s] = acc[s];
+                // autoregressive draw of output pos-1 (sampler.cpp:84-99), one shot at a time
+                const uint32_t j = pos - 1;
+                const uint32_t stream = 0x80000000u ^ (cd.ci << 12) ^ j;  // sampler.cpp:37-39
+                uint32_t word = 0;
+                for (uint32_t s = 0; s < 32; s++) {
+                    const uint64_t local = wrd * 32 + s;
+                    const bool valid = local < h.shots;
+                    const double cur = cur_g[s], pv = prev_g[s];
+                    const double ratio = __ddiv_rn(cur, pv);
+                    if (!(ratio > -1e-6 && ratio < 1.0 + 1e-6) && valid) report_ratio_error(h.err, h.first_shot + local);
+                    double cl = (0.0 < ratio) ? ratio : 0.0;
+                    cl = (cl < 1.0) ? cl : 1.0;
+                    double u;
+                    if (h.uniforms) {
+                        u = valid ? h.uniforms[(cd.upos_base + j) * h.uniforms_ld + local] : 0.0;
+                    } else {
+                        const uint64_t shot = h.first_shot + local;
+                        PhiloxPre pre[1] = {philox_pre(uint32_t(shot), uint32_t(shot >> 32), h.k0_round[0])};
+                        uint32_t rhi[1], rlo[1];
+                        philox_tail<1>(pre, seed_hi ^ stream, h.k0_round, k2c, h.k0_round[9], rhi, rlo);
+                        u = philox_uniform((uint64_t(rhi[0]) << 32) | rlo[0]);
+                    }
+                    const bool bit = !(u < cl) && valid;
+                    prev_g[s] = bit ? __dsub_rn(pv, cur) : cur;
+                    word |= uint32_t(bit) << s;
+                }
+                planes[(h.f_width + j) * 32 + lane] = word;
+                const uint32_t o = h.comp_outputs[cd.out_begin + j];
+                if (h.out32 && wrd < h.out_ld32) h.out32[o * h.out_ld32 + wrd] = word;
+                if (h.counts) {
+                    const uint32_t ones = __reduce_add_sync(kFull, __popc(word));
+                    if (lane == 0 && ones) atomicAdd(&h.counts[o], (unsigned long long)ones);
+                }
+                __syncwarp();
+            }
+            // reset this component's sampled-bit planes for the next component
+            if (h.eval_tensor < 0) {
+                for (uint32_t j = 0; j < cd.n_out; j++) planes[(h.f_width + j) * 32 + lane] = 0;
+            }
+            __syncwarp();
+        }
+    }
+}
+
+}  // namespace zxs_dev

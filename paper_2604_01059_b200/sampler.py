@@ -195,6 +195,21 @@ def eval_batch(cs: CompiledSampler, component: int, chain_pos: int, params: np.n
     return BatchEvalResult(vals, mi.value)
 
 
+def eval_batch_mono(cs: CompiledSampler, component: int, chain_pos: int, params: np.ndarray,
+                    shots: int) -> np.ndarray:
+    """eval_batch evaluated by the integer monomial kernel that samples
+    large-chi components (zxs_mono.cuh): the reference's values up to its
+    own rounding of the h tables. NotImplementedError if the component is
+    not on that path."""
+    params = np.ascontiguousarray(params, np.uint64)
+    if params.ndim != 2 or params.shape[1] != (shots + 63) // 64:
+        raise ValueError("params must be [param_cols][ceil(shots/64)]")
+    vals = np.zeros(shots, np.float64)
+    _native.check(_native.lib().zxs_eval_batch_mono(cs.handle, component, chain_pos, params.ctypes.data_as(_u64p),
+                                                    params.shape[0], shots, vals.ctypes.data_as(_dp)))
+    return vals
+
+
 def sample_given_f(cs: CompiledSampler, fcols: np.ndarray, shots: int, seed: int = 0, first_shot: int = 0,
                    uniforms: np.ndarray | None = None) -> np.ndarray:
     """run_batch (sampler.cpp:51-102) driven by injected noise: f-columns
@@ -227,6 +242,13 @@ def measure_philox_peak(device: int = 0) -> float:
     """Philox4x32-10 blocks/s of the draw code alone (same-op-mix roofline)."""
     out = ctypes.c_double()
     _native.check(_native.lib().zxs_measure_philox_peak(device, ctypes.byref(out)))
+    return out.value
+
+
+def measure_fp64_peak(device: int = 0) -> float:
+    """FP64 DMUL+DADD ops/s of the exact contraction's op mix (heavy_kernel roofline)."""
+    out = ctypes.c_double()
+    _native.check(_native.lib().zxs_measure_fp64_peak(device, ctypes.byref(out)))
     return out.value
 
 

@@ -197,18 +197,22 @@ def test_empty_and_tiny_ranges():
         assert np.array_equal(sample(cs, shots, 4, first), orc.sample(shots, 4, first))
 
 
-def _heavy_model(name, min_factors="1"):
-    """Sampler whose components (with >= min_factors factors) all run in heavy_kernel."""
+def _heavy_model(name, min_factors="1", mono="0"):
+    """Sampler whose components (with >= min_factors factors) all run in
+    heavy_kernel (mono="0": exact FP64 path) or mono_kernel (mono="1":
+    integer monomial path, where eligible)."""
     import os
-    old = os.environ.get("ZXS_HEAVY_MIN_FACTORS")
-    os.environ["ZXS_HEAVY_MIN_FACTORS"] = min_factors
+    keys = {"ZXS_HEAVY_MIN_FACTORS": min_factors, "ZXS_MONO": mono}
+    old = {k: os.environ.get(k) for k in keys}
+    os.environ.update(keys)
     try:
         return zx.CompiledSampler.load(golden_path(name))
     finally:
-        if old is None:
-            del os.environ["ZXS_HEAVY_MIN_FACTORS"]
-        else:
-            os.environ["ZXS_HEAVY_MIN_FACTORS"] = old
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
 
 
 @pytest.mark.parametrize("name", ["c2_surface_d3_xmem_t", "c4_color_d5_rz3", "surface_d3_xmem_rz5",
@@ -239,14 +243,116 @@ def test_heavy_path_injected_and_counts():
     assert np.array_equal(zx.count_outputs(cs, 70000, seed=3, first_shot=123), pc)
 
 
+def _heavy_model_path(path):
+    import os
+    old = os.environ.get("ZXS_MONO")
+    os.environ["ZXS_MONO"] = "0"
+    try:
+        return zx.CompiledSampler.load(path)
+    finally:
+        if old is None:
+            del os.environ["ZXS_MONO"]
+        else:
+            os.environ["ZXS_MONO"] = old
+
+
 def test_cultivation_proxy_against_reference():
-    """Config-3 proxy (chi = 46,656, 12.4 M factors): the heavy path against
-    the reference sampler itself on the same shots."""
+    """Config-3 proxy (chi = 46,656, 12.4 M factors): the exact FP64 heavy
+    path against the reference sampler itself on the same shots."""
+    import os
+    path = os.path.join(os.path.dirname(golden_path("x")), "..", "..", "data", "c3_cultivation_proxy.zxs.gz")
+    if not os.path.exists(path) or not refdriver.available():
+        pytest.skip("cultivation proxy not generated (tools/make_fixtures.py --big)")
+    cs = _heavy_model_path(path)
+    ref = refdriver.RefModel.load(path)
+    shots, first = 640, 1 << 20
+    got = sample(cs, shots, 11, first)
+    want = ref.sample_rb(shots, 11, first_shot=first, batch_size=64, threads=os.cpu_count())
+    assert np.array_equal(got, want)
+
+
+# ---------------------------------------------------------------- monomial path
+MONO_NAMES = ["c2_surface_d3_xmem_t", "c4_color_d5_rz3", "surface_d3_xmem_rz5", "surface_d3_xmem_9t", "h_t_h_m",
+              "oracle_mix_4", "random_02", "random_05", "steane_inject", "c1_surface_d3_zmem"]
+
+
+@pytest.mark.parametrize("name", MONO_NAMES)
+def test_mono_eval_matches_reference(name):
+    """Integer monomial contraction vs the reference's eval_batch: relative
+    1e-12 of the term-magnitude sum (the reference rounds its h entries)."""
+    from test_mono_layout import pack, term_scale
+    cs = _heavy_model(name, min_factors="0", mono="1")
+    assert cs.info["num_mono_components"] > 0
+    orc = coracle.OracleModel.load(golden_path(name))
+    arrays = orc.arrays
+    rng = np.random.default_rng(5)
+    ctb = arrays["comp_tensor_begin"]
+    for ci in range(len(ctb) - 1):
+        for pos in range(int(ctb[ci + 1] - ctb[ci])):
+            tensor = int(ctb[ci]) + pos
+            W = max(int(arrays["tensor_param_width"][tensor]), 1)
+            shots = 200
+            P = rng.integers(0, 2, (shots, W)).astype(np.int64)
+            cols = pack(P)
+            try:
+                got = zx.eval_batch_mono(cs, ci, pos, cols, shots)
+            except NotImplementedError:
+                continue
+            want, _ = orc.eval_batch(tensor, cols, shots)
+            err = np.abs(got - want) / (term_scale(arrays, tensor, P) + 1e-300)
+            assert err.max() < 1e-12, (name, ci, pos, float(err.max()))
+
+
+@pytest.mark.parametrize("name", MONO_NAMES)
+def test_mono_path_matches_reference_goldens(name, goldens):
+    """Records of the monomial path == the reference's (bit-exact: a
+    difference could only come from a uniform falling between the two
+    ratios, ~1e-16 wide; none occurs in these goldens)."""
+    cs = _heavy_model(name, min_factors="0", mono="1")
+    for s in goldens[name]["samples"]:
+        if s["shots"] > 200000:
+            continue
+        assert sha(sample(cs, s["shots"], s["seed"], s["first_shot"])) == s["sha256"], (name, s)
+
+
+def test_mono_injected_noise_ties_counted():
+    """Injected f and uniforms: mono path vs the C oracle. Mismatching bits
+    are allowed only at threshold ties (|u - ratio| < 1e-12 at the first
+    differing position of a shot); the count is reported."""
+    name = "surface_d3_xmem_9t"
+    cs = _heavy_model(name, min_factors="0", mono="1")
+    orc = coracle.OracleModel.load(golden_path(name))
+    rng = np.random.default_rng(31)
+    shots = 20000
+    f = rng.integers(0, 2**63, size=(orc.f_width, (shots + 63) // 64), dtype=np.uint64)
+    f[:, -1] &= np.uint64((1 << (shots & 63)) - 1)
+    u = rng.random((orc.num_positions, shots))
+    got = zx.sample_given_f(cs, f, shots, uniforms=u)
+    want = orc.sample(shots, 0, fcols=f, uniforms=u)
+    diff = np.unpackbits((got ^ want).view(np.uint8), axis=1, bitorder="little")[:, :shots]
+    ties = int(diff.any(axis=0).sum())
+    assert ties == 0, f"{ties} shots differ (threshold ties)"
+
+
+def test_mono_counts_and_shards():
+    name = "c4_color_d5_rz3"
+    cs = _heavy_model(name, min_factors="0", mono="1")
+    full = sample(cs, 70000, 3, 123)
+    pc = np.unpackbits(full.view(np.uint8), axis=1).sum(axis=1).astype(np.uint64)
+    assert np.array_equal(zx.count_outputs(cs, 70000, seed=3, first_shot=123), pc)
+    a = sample(cs, 30016, 3, 123)
+    b = sample(cs, 70000 - 30016, 3, 123 + 30016)
+    assert np.array_equal(np.concatenate([a, b], axis=1)[:, :full.shape[1]], full)
+
+
+def test_cultivation_proxy_mono_against_reference():
+    """Config-3 proxy on the monomial path vs the reference sampler itself."""
     import os
     path = os.path.join(os.path.dirname(golden_path("x")), "..", "..", "data", "c3_cultivation_proxy.zxs.gz")
     if not os.path.exists(path) or not refdriver.available():
         pytest.skip("cultivation proxy not generated (tools/make_fixtures.py --big)")
     cs = zx.CompiledSampler.load(path)
+    assert cs.info["num_mono_components"] == 1
     ref = refdriver.RefModel.load(path)
     shots, first = 640, 1 << 20
     got = sample(cs, shots, 11, first)

@@ -1,0 +1,201 @@
+"""CPU emulation of the integer monomial path (mono_kernel) — no GPU needed.
+
+zxs_debug_mono_layout returns the exact record streams and form dictionary
+the device walks. This test decodes them the way mono_kernel does — per term
+J (mod 4) and Z from the record kinds, epilogue Re(c' i^J) for non-zero
+shots, terms in order — and checks the values against the C oracle's
+eval_batch (phase_terms.cpp:90-144). The monomial path replaces the
+reference's rounded h entries by their exact values, so agreement is to a
+relative 1e-12 of the sum of |term| magnitudes (the reference's own rounding
+is ~1e-16 per entry), not bit for bit.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+from conftest import golden_path
+from oracle import coracle
+from paper_2604_01059_b200 import _native, zxs_format
+
+REC_ADD, REC_SUB, REC_ADD2, REC_Z, REC_ZN, REC_ZX, REC_ZXN, REC_GEN = 0, 1, 2, 3, 4, 5, 6, 15
+
+
+def mono_layout(arrays, min_factors=0):
+    desc = zxs_format.make_desc(arrays)
+    L = _native.lib()
+    need = ctypes.c_uint64()
+    _native.check(L.zxs_debug_mono_layout(ctypes.byref(desc), min_factors, None, 0, ctypes.byref(need)))
+    buf = np.zeros(need.value, np.uint32)
+    _native.check(L.zxs_debug_mono_layout(ctypes.byref(desc), min_factors,
+                                          buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), buf.size,
+                                          ctypes.byref(need)))
+    n_words, n_chunks, n_tcb, n_dict, n_comps, n_components = (int(x) for x in buf[:6])
+    o = 8
+    comps = [dict(zip(("ci", "n_out", "upos_base", "out_begin", "first_tensor"),
+                      (int(v) for v in buf[o + 5 * i:o + 5 * i + 5]))) for i in range(n_comps)]
+    o += 5 * n_comps
+    flags = buf[o:o + n_components].astype(bool)
+    o += n_components
+    tcb = buf[o:o + n_tcb].astype(np.int64)
+    o += n_tcb
+    chunks = buf[o:o + 4 * n_chunks].reshape(n_chunks, 4).astype(np.int64)
+    o += 4 * n_chunks
+    dict_ = buf[o:o + 4 * n_dict].reshape(n_dict, 4).copy()
+    o += 4 * n_dict
+    words = buf[o:o + n_words]
+    return dict(comps=comps, flags=flags, tcb=tcb, chunks=chunks, dict=dict_, words=words)
+
+
+def form_sel(dict_, f):
+    """Parameter indices of dictionary form f (continuation entries followed):
+    u16 count | 0x8000, then up to seven u16 plane offsets p * 128."""
+    sel = []
+    while True:
+        e = dict_[f].view(np.uint16)
+        n = int(e[0]) & 7
+        assert all(int(x) % 128 == 0 for x in e[1:1 + n])
+        sel += [int(x) // 128 for x in e[1:1 + n]]
+        if not (int(e[0]) & 0x8000):
+            return sel
+        f += 1
+
+
+def emulate_tensor(lay, t, P):
+    """mono_kernel's value of mono tensor t for parameter rows P [shots][W] (0/1)."""
+    words = lay["words"]
+    cache = {}
+
+    def form(f):
+        if f not in cache:
+            cache[f] = (P[:, form_sel(lay["dict"], f)].sum(1) & 1).astype(np.int64)
+        return cache[f]
+
+    acc = np.zeros(P.shape[0])
+    for c in range(lay["tcb"][t], lay["tcb"][t + 1]):
+        wb, nw, nterms = lay["chunks"][c, :3]
+        w = words[wb:wb + nw]
+        q = 0
+        for _ in range(nterms):
+            nrec = int(w[q])
+            re = w[q + 2:q + 4].copy().view(np.float64)[0]
+            im = w[q + 4:q + 6].copy().view(np.float64)[0]
+            q += 6
+            qe = q + nrec
+            J = np.zeros(P.shape[0], np.int64)
+            Z = np.zeros(P.shape[0], bool)
+            while q < qe:
+                r = int(w[q])
+                q += 1
+                kind, fa, fb = r >> 28, r & 0xFFFF, (r >> 16) & 0xFFF
+                a = 0 if fa == 0xFFFF else form(fa)
+                if kind == REC_ADD:
+                    J += a
+                elif kind == REC_SUB:
+                    J -= a
+                elif kind == REC_ADD2:
+                    J += 2 * a
+                elif kind == REC_Z:
+                    Z |= a == 1
+                elif kind == REC_ZN:
+                    Z |= a == 0
+                else:
+                    b = 0 if fb == 0xFFF else form(fb)
+                    if kind == REC_ZX:
+                        Z |= (a ^ b) == 1
+                    elif kind == REC_ZXN:
+                        Z |= (a ^ b) == 0
+                    else:
+                        assert kind == REC_GEN, kind
+                        g = int(w[q])
+                        q += 1
+                        zl = g >> 6
+                        idx = a * 2 + b
+                        Z |= ((zl >> idx) & 1) == 1
+                        J += (g & 3) * a + ((g >> 2) & 3) * b + ((g >> 4) & 3) * (a * b)
+            J &= 3
+            v = np.where(J == 0, re, np.where(J == 1, -im, np.where(J == 2, -re, im)))
+            acc = np.where(Z, acc, acc + v)
+    return acc
+
+
+def term_scale(arrays, tensor, P):
+    """sum_t |c_t| prod_k |h_tk| per shot (exact zeros as 0), floored at 1e-3 of
+    the tensor's largest possible term sum: the magnitude the tolerance is
+    relative to. (A reference value that is exactly 0 in exact arithmetic
+    carries the reference's ~1e-16 rounding of its zero h entries.)"""
+    a = arrays
+    tb, fb = a["tensor_term_begin"], a["term_factor_begin"]
+    c = a["term_c"].reshape(-1, 2)
+    h = a["h_table"].reshape(-1, 4, 2)
+    habs = np.hypot(h[..., 0], h[..., 1])
+    habs = np.where(habs < 1e-9, 0.0, habs)
+    hmax = habs.max(axis=1)
+    scale = np.zeros(P.shape[0])
+    cap = 0.0
+    for term in range(int(tb[tensor]), int(tb[tensor + 1])):
+        cap += np.hypot(*c[term]) * np.prod(hmax[a["factor_table"][int(fb[term]):int(fb[term + 1])]])
+        m = np.full(P.shape[0], np.hypot(*c[term]))
+        for k in range(int(fb[term]), int(fb[term + 1])):
+            u = a["factor_u_bits"][a["factor_u_begin"][k]:a["factor_u_begin"][k + 1]]
+            v = a["factor_v_bits"][a["factor_v_begin"][k]:a["factor_v_begin"][k + 1]]
+            av = P[:, u].sum(1) & 1
+            bv = P[:, v].sum(1) & 1
+            m = m * habs[a["factor_table"][k], av * 2 + bv]
+        scale += m
+    return np.maximum(scale, 1e-3 * cap)
+
+
+def pack(P):
+    """[shots][W] 0/1 -> ParamBatch columns [W][words] uint64."""
+    shots, W = P.shape
+    words = (shots + 63) // 64
+    cols = np.zeros((W, words), np.uint64)
+    for s in range(shots):
+        for p in np.nonzero(P[s])[0]:
+            cols[p, s >> 6] |= np.uint64(1) << np.uint64(s & 63)
+    return cols
+
+
+MONO_FIXTURES = ["surface_d3_xmem_9t", "surface_d3_xmem_rz5", "c4_color_d5_rz3", "c2_surface_d3_xmem_t",
+                 "steane_inject", "random_02", "random_05", "oracle_mix_4", "h_t_h_m", "c1_surface_d3_zmem"]
+
+
+@pytest.mark.parametrize("name", MONO_FIXTURES)
+def test_mono_values_match_oracle(name):
+    arrays = zxs_format.load(golden_path(name))
+    lay = mono_layout(arrays)
+    assert lay["comps"], f"{name}: no component lowered to the monomial path"
+    om = coracle.OracleModel(arrays)
+    rng = np.random.default_rng(7)
+    ctb = arrays["comp_tensor_begin"]
+    widths = arrays["tensor_param_width"]
+    checked = 0
+    for comp in lay["comps"]:
+        ci = comp["ci"]
+        for pos in range(comp["n_out"] + 1):
+            tensor = int(ctb[ci]) + pos
+            W = int(widths[tensor])
+            shots = 64
+            P = rng.integers(0, 2, (shots, max(W, 1))).astype(np.int64)
+            got = emulate_tensor(lay, comp["first_tensor"] + pos, P)
+            want, _ = om.eval_batch(tensor, pack(P), shots)
+            scale = term_scale(arrays, tensor, P) + 1e-300
+            err = np.abs(got - want) / scale
+            assert err.max() < 1e-12, (name, ci, pos, float(err.max()))
+            checked += 1
+    assert checked
+
+
+def test_mono_record_kinds_and_dead_terms():
+    """The lowering uses the compact kinds for the common factor shapes."""
+    arrays = zxs_format.load(golden_path("surface_d3_xmem_9t"))
+    lay = mono_layout(arrays)
+    kinds = np.bincount(lay["words"] >> 28, minlength=16)
+    assert kinds[REC_GEN] <= kinds[:7].sum()
+
+
+def test_mono_min_factors_gate():
+    arrays = zxs_format.load(golden_path("c2_surface_d3_xmem_t"))
+    lay = mono_layout(arrays, min_factors=10 ** 9)
+    assert not lay["comps"] and not lay["flags"].any()

@@ -130,12 +130,16 @@ def reference_rate(path: str, target_s: float, seed: int, threads: int):
         m = refdriver.RefModel.load(path)
 
         def run(n):
+            # SamplerOptions.batch_size (sampler.cpp:149-158): the reference default of 65536 shots,
+            # lowered (in multiples of 64) only when a sample has fewer than threads x 65536 shots,
+            # so every host thread gets a batch (workers = min(threads, batches)).
+            bs = int(min(65536, max(64, (n // threads) // 64 * 64)))
             try:
-                return m.sample(n, seed, threads=threads, force_dense=True)  # sample_detectors, unmodified
+                return m.sample(n, seed, batch_size=bs, threads=threads, force_dense=True)  # sample_detectors
             except RuntimeError as e:
                 if "width mismatch" not in str(e):
                     raise
-                return m.sample_rb(n, seed, threads=threads)  # run_batch restatement (SURVEY finding 2)
+                return m.sample_rb(n, seed, batch_size=bs, threads=threads)  # run_batch restatement (SURVEY finding 2)
         kind = "reference"
     else:
         om = coracle.OracleModel.load(path)
@@ -144,7 +148,7 @@ def reference_rate(path: str, target_s: float, seed: int, threads: int):
             return om.sample(n, seed)
         kind = "port"
         threads = 1
-    n = 4096
+    n = 64 * threads
     run(n)  # warm-up (first cold run is slow)
     while True:
         t = time.perf_counter()
@@ -228,6 +232,7 @@ def run_ours(args, wl):
         dist.barrier()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     counts.zero_()
+    cs.kernel_timing(True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         for i in range(args.steps):
@@ -237,6 +242,8 @@ def run_ours(args, wl):
             evs[i][1].record(stream)
         torch.cuda.synchronize()
     cs.check_errors(sptr)
+    ktimes = cs.kernel_times()
+    cs.kernel_timing(False)
     kernel_ms = [a.elapsed_time(b) for a, b in evs]
     t_local = sum(kernel_ms)
     if world > 1:
@@ -268,14 +275,47 @@ def run_ours(args, wl):
         e2e_local = tt.item()
     e2e_value = e2e_shots * args.steps * world / e2e_local
 
-    # ---- roofline: the shot kernel is bound by the
-    # 32x32->64 integer multiplies of Philox4x32-10 (IMAD.WIDE on the
-    # fmaheavy pipe). Algorithmic work = Philox blocks per shot (mechanisms +
-    # autoregressive draws); peak = the same Philox code with no other work,
-    # measured live on this GPU (zxs_measure_philox_peak).
-    blocks_per_shot = info["philox_blocks_per_shot"]
-    achieved = shots * blocks_per_shot / (ms_per_step / 1e3) / 1e9  # Gblocks/s per GPU
-    peak = zx.measure_philox_peak(local) / 1e9
+    # ---- roofline of the dominant kernel (DESIGN.md "Kernels and their
+    # rooflines"), timed per launch with CUDA events on the launch stream.
+    launches = sum(n for _, n in ktimes.values())
+    if info["num_mono_components"]:
+        # mono_kernel: one conflict-free 128 B shared-memory wavefront per
+        # selector per warp (32 lanes x 32 shots); algorithmic bytes =
+        # plane loads per 32-shot word x 4 B x words. Peak: the same LDS+XOR
+        # op mix measured live (zxs_measure_smem_peak).
+        kms, kn = ktimes["mono_kernel"]
+        per_launch_s = kms / max(kn, 1) / 1e3
+        algo = shots / 32 * info["num_mono_loads"] * 4
+        achieved = algo / per_launch_s / 1e9
+        peak = zx.measure_smem_peak(local) / 1e9
+        roof = {"bound": "smem", "kernel": "mono_kernel", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": args.traffic_bytes,
+                "basis": f"{info['num_mono_loads']} parameter-plane loads per 32-shot word per chain pass "
+                         f"(4 B each, {info['num_mono_records']} records), {algo:.3e} B per launch",
+                "peak_source": "measured live: zxs_measure_smem_peak (conflict-free LDS.32 + XOR, same op mix)",
+                "kernel_ms_per_launch": per_launch_s * 1e3,
+                "kernel_share": kms / max(sum(v for v, _ in ktimes.values()), 1e-9)}
+    else:
+        # shot_kernel: bound by the 32x32->64 integer multiplies of
+        # Philox4x32-10 (IMAD.WIDE on the fmaheavy pipe). Algorithmic work =
+        # Philox blocks per shot (mechanisms + autoregressive draws); peak =
+        # the same Philox code with no other work, measured live.
+        kms, kn = ktimes["shot_kernel"]
+        per_launch_s = kms / max(kn, 1) / 1e3
+        blocks_per_shot = info["philox_blocks_per_shot"]
+        achieved = shots * blocks_per_shot / per_launch_s / 1e9
+        peak = zx.measure_philox_peak(local) / 1e9
+        roof = {"bound": "int", "kernel": "shot_kernel", "achieved": achieved, "peak": peak,
+                "unit": "GPhilox-blocks/s", "frac": achieved / peak, "traffic": args.traffic_bytes,
+                "basis": f"{blocks_per_shot} Philox4x32-10 blocks/shot ({info['num_mechanisms']} mechanisms + "
+                         f"{blocks_per_shot - info['num_mechanisms']} autoregressive draws)",
+                "peak_source": "measured live: zxs_measure_philox_peak (same Philox code, no other work); "
+                               "integer-multiply (fmaheavy) bound",
+                "kernel_ms_per_launch": per_launch_s * 1e3,
+                "kernel_share": kms / max(sum(v for v, _ in ktimes.values()), 1e-9)}
+    roof["hbm"] = {"bytes_per_step": int(nout * words * 8) if not count_only else int(nout * 8),
+                   "achieved_gbs": (nout * words * 8 if not count_only else 0) / (ms_per_step / 1e3) / 1e9,
+                   "peak_gbs": MEASURED_HBM_GBS}
     clocks = clk.summary()
     line = {
         "metric": "detector_shots_per_sec", "value": value, "unit": "shots/s", "n_gpus": world,
@@ -287,16 +327,9 @@ def run_ours(args, wl):
                    "count_only": count_only, "l2": "flushed (256 MiB write) between timed steps"},
         "e2e": {"value": e2e_value, "unit": "shots/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": int(nout * ((e2e_shots + 63) // 64) * 8), "shots_per_step": e2e_shots},
-        "gpu_launches": args.steps,
-        "roofline": {"bound": "int", "achieved": achieved, "peak": peak, "unit": "GPhilox-blocks/s",
-                     "frac": achieved / peak, "traffic": args.traffic_bytes,
-                     "basis": f"{blocks_per_shot} Philox4x32-10 blocks/shot ({info['num_mechanisms']} mechanisms + "
-                              f"{blocks_per_shot - info['num_mechanisms']} autoregressive draws), shot kernel only",
-                     "peak_source": "measured live: zxs_measure_philox_peak (same Philox code, no other work); "
-                                    "integer-multiply (fmaheavy) bound",
-                     "hbm": {"bytes_per_step": int(nout * words * 8) if not count_only else int(nout * 8),
-                             "achieved_gbs": (nout * words * 8 if not count_only else 0) / (ms_per_step / 1e3) / 1e9,
-                             "peak_gbs": MEASURED_HBM_GBS}},
+        "gpu_launches": launches,
+        "kernels": {k: {"ms": v, "launches": n} for k, (v, n) in ktimes.items() if n},
+        "roofline": roof,
         "clocks": clocks,
         "kernel_ms": kernel_ms if len(kernel_ms) <= 20 else None,
     }

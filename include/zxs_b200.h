@@ -122,6 +122,11 @@ typedef struct zxs_model_desc {
     const double *h_beta;                  /* [num_h_tables]                  */
 } zxs_model_desc;
 
+typedef enum zxs_format {
+    ZXS_FORMAT_01 = 0, /* ShotFormat::ascii01 (encode.hpp:25) */
+    ZXS_FORMAT_B8 = 1  /* ShotFormat::b8 */
+} zxs_format;
+
 typedef struct zxs_sampler zxs_sampler;
 
 typedef struct zxs_sampler_info {
@@ -136,6 +141,7 @@ typedef struct zxs_sampler_info {
     /* large-chi components lowered to the integer monomial path (zxs_mono.cuh) */
     uint32_t num_mono_components, num_mono_forms;
     uint64_t num_mono_records, num_mono_dead_terms;
+    uint64_t num_mono_loads;  /* parameter-plane loads per 32-shot word per pass over the mono chains */
 } zxs_sampler_info;
 
 /* Message of the calling thread's last failed call ("" if none). */
@@ -178,8 +184,42 @@ zxs_status zxs_count_device(zxs_sampler *s, uint64_t seed, uint64_t first_shot,
 zxs_status zxs_count(zxs_sampler *s, uint64_t seed, uint64_t first_shot, uint64_t shots,
                      uint64_t *host_counts, void *stream);
 
+/*
+ * Per-kernel device timing: zxs_kernel_timing(s, 1) clears and starts
+ * recording CUDA events around every launch of the shot kernel [0], the
+ * exact large-chi kernel [1] and the monomial kernel [2] (on the launch
+ * stream); zxs_kernel_times sums their elapsed ms and launch counts.
+ * zxs_kernel_timing(s, 0) stops. Used by bench.py for the roofline.
+ */
+zxs_status zxs_kernel_timing(zxs_sampler *s, int enable);
+zxs_status zxs_kernel_times(zxs_sampler *s, double *ms /*[3]*/, uint64_t *launches /*[3]*/);
+
 /* Synchronizes `stream` and reports (then clears) a device-side ratio breakdown. */
 zxs_status zxs_check_errors(zxs_sampler *s, void *stream);
+
+/*
+ * encode_shots (proj/src/encode.cpp:22-48) of a device record on the device:
+ * dev_columns [num_outputs][ld_words] -> dev_out, shot-major, outputs
+ * [first_output, first_output + output_count) clamped to the record width as
+ * the reference does. 01: per shot `width` chars + '\n'; b8: per shot
+ * ceil(width/8) bytes, bit b % 8 of byte b / 8. zxs_encoded_bytes gives the
+ * output size (0 for invalid arguments). Asynchronous on `stream`.
+ */
+uint64_t zxs_encoded_bytes(uint32_t num_outputs, uint64_t shots, uint32_t first_output,
+                           uint32_t output_count, uint32_t format);
+zxs_status zxs_encode_shots_device(const uint64_t *dev_columns, uint64_t ld_words, uint32_t num_outputs,
+                                   uint64_t shots, uint32_t first_output, uint32_t output_count,
+                                   uint32_t format, uint8_t *dev_out, void *stream);
+
+/*
+ * The CLI's sample path fused (zxsim.cpp:142-163):
+ * write_output(encode_shots(sample_detectors/measurements(cs, shots, opts), fmt, first, count))
+ * with sampling and encoding on the device and only the encoded bytes copied
+ * to host_out (zxs_encoded_bytes(...) bytes). Synchronous.
+ */
+zxs_status zxs_sample_encoded(zxs_sampler *s, uint32_t expected_mode, uint64_t seed, uint64_t first_shot,
+                              uint64_t shots, uint32_t format, uint32_t first_output, uint32_t output_count,
+                              uint8_t *host_out, void *stream);
 
 /* f-columns after the dense error draw: host_fcols [f_width][ceil(shots/64)]. */
 zxs_status zxs_sample_error_batch(zxs_sampler *s, uint64_t seed, uint64_t first_shot,
@@ -225,6 +265,14 @@ zxs_status zxs_sample_given_f(zxs_sampler *s, uint64_t seed, uint64_t first_shot
 zxs_status zxs_probability_of_at(zxs_sampler *s, const uint8_t *outcome, uint32_t n_outcome,
                                  const uint8_t *f_assignment, uint32_t n_f, double *out);
 
+/*
+ * probability_of (sampler.hpp:64, sampler.cpp:370-429): exact P(outcome),
+ * marginalised over every mechanism outcome. Same entropy guard (> 20 bits ->
+ * ZXS_INVALID_ARGUMENT), same DFS order and Kahan summation as the reference;
+ * each leaf's outcome_probability_given runs on the device.
+ */
+zxs_status zxs_probability_of(zxs_sampler *s, const uint8_t *outcome, uint32_t n_outcome, double *out);
+
 /* Philox4x32-10 uniform_at (rng.hpp:31-41) evaluated on the device, n draws
    at indices first_index .. first_index+n-1. */
 zxs_status zxs_philox_uniform(int device, uint64_t seed, uint32_t stream, uint64_t first_index,
@@ -259,6 +307,11 @@ zxs_status zxs_measure_philox_peak(int device, double *blocks_per_s);
    contraction's op mix) of a register-resident kernel on `device` -- the
    roofline denominator of heavy_kernel. */
 zxs_status zxs_measure_fp64_peak(int device, double *ops_per_s);
+
+/* Diagnostic: shared-memory bytes/s of conflict-free 32-bit loads XORed into
+   registers (mono_kernel's selector op mix) on `device` -- the roofline
+   denominator of mono_kernel. */
+zxs_status zxs_measure_smem_peak(int device, double *bytes_per_s);
 
 #ifdef __cplusplus
 }

@@ -44,6 +44,9 @@ def lib():
         L.zo_eval_batch.restype = ctypes.c_double
         L.zo_sample.argtypes = [D, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _u64p, _dp, _u64p]
         L.zo_sample.restype = ctypes.c_int
+        L.zo_encode.argtypes = [_u64p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
+                                ctypes.c_int, ctypes.POINTER(ctypes.c_uint8), ctypes.c_uint64]
+        L.zo_encode.restype = ctypes.c_longlong
         _lib = L
     return _lib
 
@@ -58,6 +61,18 @@ def philox_block(ctr, key) -> list[int]:
 
 def uniform_at(seed: int, stream: int, index: int) -> float:
     return lib().zo_uniform_at(seed, stream, index)
+
+
+def encode(cols: np.ndarray, shots: int, fmt: int, first_output: int = 0, output_count: int = 0xFFFFFFFF) -> bytes:
+    """encode_shots (encode.cpp:22-48) of a [num_outputs][ceil(shots/64)] record."""
+    cols = np.ascontiguousarray(cols, np.uint64)
+    cap = shots * (cols.shape[0] + 1) + 16
+    buf = np.zeros(cap, np.uint8)
+    n = lib().zo_encode(cols.ctypes.data_as(_u64p), cols.shape[0], shots, first_output, output_count, fmt,
+                        buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), cap)
+    if n < 0:
+        raise ValueError("encode: invalid arguments")
+    return buf[:n].tobytes()
 
 
 class OracleModel:

@@ -217,3 +217,34 @@ int zo_sample(const zxs_model_desc *d, uint64_t seed, uint64_t first_shot, uint6
     free(batch);
     return status;
 }
+
+/* ---- encode_shots (proj/src/encode.cpp:22-48) ------------------------- */
+/* cols: [num_outputs][ceil(shots/64)]. Output range clamped as encode.cpp:23-25.
+   format 0 = ascii01 (width chars + '\n' per shot, encode.cpp:27-35),
+   1 = b8 (ceil(width/8) bytes per shot, bit b%8 of byte b/8, encode.cpp:37-46).
+   Returns bytes written, or -1 if cap is too small / arguments invalid. */
+long long zo_encode(const uint64_t *cols, uint32_t num_outputs, uint64_t shots, uint32_t first_output,
+                    uint32_t output_count, int format, uint8_t *out, uint64_t cap) {
+    if (first_output > num_outputs) return -1;
+    uint32_t rest = num_outputs - first_output;
+    uint32_t last = first_output + (output_count < rest ? output_count : rest);
+    if (last > num_outputs) last = num_outputs;
+    uint32_t width = last - first_output;
+    uint64_t words = (shots + 63) / 64;
+    uint64_t rb = format == 0 ? (uint64_t)width + 1 : ((uint64_t)width + 7) / 8;
+    if (shots * rb > cap) return -1;
+    memset(out, 0, shots * rb);
+    for (uint64_t s = 0; s < shots; s++) {
+        uint8_t *row = out + s * rb;
+        for (uint32_t b = 0; b < width; b++) {
+            int bit = (int)((cols[(uint64_t)(first_output + b) * words + (s >> 6)] >> (s & 63)) & 1u);
+            if (format == 0) {
+                row[b] = (uint8_t)(bit ? '1' : '0');
+            } else if (bit) {
+                row[b / 8] |= (uint8_t)(1u << (b % 8));
+            }
+        }
+        if (format == 0) row[width] = '\n';
+    }
+    return (long long)(shots * rb);
+}

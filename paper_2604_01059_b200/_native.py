@@ -32,7 +32,8 @@ class SamplerInfo(ctypes.Structure):
         ("num_selector_bits", ctypes.c_uint64), ("philox_blocks_per_shot", ctypes.c_uint64),
         ("device_bytes", ctypes.c_uint64), ("device", ctypes.c_int), ("monomial", ctypes.c_int),
         ("num_mono_components", ctypes.c_uint32), ("num_mono_forms", ctypes.c_uint32),
-        ("num_mono_records", ctypes.c_uint64), ("num_mono_dead_terms", ctypes.c_uint64)]
+        ("num_mono_records", ctypes.c_uint64), ("num_mono_dead_terms", ctypes.c_uint64),
+        ("num_mono_loads", ctypes.c_uint64)]
 
     def as_dict(self) -> dict:
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -51,6 +52,14 @@ SIGNATURES = (
     ("zxs_count_device", ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _vp, _vp]),
     ("zxs_count", ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _u64p, _vp]),
     ("zxs_check_errors", ctypes.c_int, [_vp, _vp]),
+    ("zxs_kernel_timing", ctypes.c_int, [_vp, ctypes.c_int]),
+    ("zxs_kernel_times", ctypes.c_int, [_vp, _dp, _u64p]),
+    ("zxs_encoded_bytes", ctypes.c_uint64, [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
+                                            ctypes.c_uint32]),
+    ("zxs_encode_shots_device", ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
+                                               ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, _vp, _vp]),
+    ("zxs_sample_encoded", ctypes.c_int, [_vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                          ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, _u8p, _vp]),
     ("zxs_sample_error_batch", ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _u64p]),
     ("zxs_eval_batch", ctypes.c_int, [_vp, ctypes.c_uint32, ctypes.c_uint32, _u64p, ctypes.c_uint32,
                                       ctypes.c_uint64, _dp, _dp]),
@@ -58,11 +67,13 @@ SIGNATURES = (
                                            ctypes.c_uint64, _dp]),
     ("zxs_sample_given_f", ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _u64p, _dp,
                                           _u64p]),
+    ("zxs_probability_of", ctypes.c_int, [_vp, _u8p, ctypes.c_uint32, _dp]),
     ("zxs_probability_of_at", ctypes.c_int, [_vp, _u8p, ctypes.c_uint32, _u8p, ctypes.c_uint32, _dp]),
     ("zxs_philox_uniform", ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
                                           ctypes.c_uint64, _dp]),
     ("zxs_measure_philox_peak", ctypes.c_int, [ctypes.c_int, _dp]),
     ("zxs_measure_fp64_peak", ctypes.c_int, [ctypes.c_int, _dp]),
+    ("zxs_measure_smem_peak", ctypes.c_int, [ctypes.c_int, _dp]),
     ("zxs_debug_heavy_layout", ctypes.c_int, [ctypes.POINTER(_fmt.ModelDesc), ctypes.c_uint64,
                                               ctypes.POINTER(ctypes.c_uint32), ctypes.c_uint64, _u64p]),
     ("zxs_debug_mono_layout", ctypes.c_int, [ctypes.POINTER(_fmt.ModelDesc), ctypes.c_uint64,

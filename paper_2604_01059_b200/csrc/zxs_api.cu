@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
+#include <iterator>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -31,6 +33,7 @@
 #include "zxs_b200.h"
 #include "zxs_heavy.cuh"
 #include "zxs_mono.cuh"
+#include "zxs_encode.cuh"
 
 using zxs_dev::DevModel;
 using zxs_dev::Factor;
@@ -156,6 +159,35 @@ struct zxs_sampler {
     std::map<uint32_t, uint32_t> mono_tensor;  // model tensor -> mono tensor index
     char *mono_scratch = nullptr;
     size_t mono_scratch_bytes = 0;
+
+    // error model kept on the host for probability_of's enumeration
+    // (sampler.cpp:370-429): per mechanism the f_vectors as FW-word masks and
+    // either the probability (single) or the outcome table (joint).
+    struct HostMech {
+        bool joint = false;
+        double p = 0.0;
+        std::vector<double> table;
+        std::vector<std::vector<uint64_t>> vecs;
+    };
+    std::vector<HostMech> host_mechs;
+    std::vector<uint64_t> host_base;
+
+    // per-kernel CUDA-event timing (zxs_kernel_timing / zxs_kernel_times)
+    bool timing = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> timed;
+    void time_begin(int which, cudaStream_t st, cudaEvent_t &e0) {
+        if (!timing) return;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventRecord(e0, st));
+        (void)which;
+    }
+    void time_end(int which, cudaStream_t st, cudaEvent_t e0) {
+        if (!timing) return;
+        cudaEvent_t e1;
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e1, st));
+        timed.push_back({which, {e0, e1}});
+    }
 
     double *mono_scratch_get(size_t bytes) {
         if (bytes > mono_scratch_bytes) {
@@ -376,6 +408,11 @@ MonoEntry mono_entry(int pa, int pb, int a, int b) {
     return e;
 }
 
+size_t mono_smem_bytes(uint32_t n_planes, uint32_t max_dict) {
+    return 128 + 2 * size_t(zxs_dev::kMonoChunkWords) * 4 + size_t(max_dict) * 16 +
+           size_t(zxs_dev::kMonoWarps) * (zxs_dev::kMonoMaxDepth * 3 * 128 + size_t(n_planes) * 128);
+}
+
 struct MonoHost {
     std::vector<uint8_t> comp_mono;
     std::vector<uint32_t> words;
@@ -386,7 +423,101 @@ struct MonoHost {
     std::map<uint32_t, uint32_t> tensor_index;  // model tensor -> index into tensor_chunk_begin
     uint32_t max_chain = 0;
     uint64_t records = 0, dead_terms = 0, selectors = 0;
+    uint64_t loads = 0;  // plane loads per 32-shot word for one pass over every mono chain tensor
+    uint64_t nodes = 0;
+    std::vector<uint32_t> tensor_dict_begin;  // first dictionary entry per mono tensor, then the total
+    std::vector<uint32_t> tensor_width;       // param width per mono tensor
+    uint32_t all_plane = 0;                    // plane index of the per-tensor ALL plane
+    uint32_t max_dict = 1;
 };
+
+// One term after lowering: its records as sorted tokens (record word, plus
+// GEN aux word + 1 in the high half) and c' = c 2^(M/2) w^K0.
+struct MonoTerm {
+    std::vector<uint64_t> recs;
+    double re = 0, im = 0;
+};
+
+struct MonoNode {
+    uint32_t depth = 0;
+    bool leaf = false;
+    std::vector<uint64_t> recs;  // records applied on top of the parent's state
+    double re = 0, im = 0;       // leaves: the term's c'
+};
+
+std::vector<uint64_t> ms_inter(const std::vector<uint64_t> &a, const std::vector<uint64_t> &b) {
+    std::vector<uint64_t> r;
+    std::set_intersection(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(r));
+    return r;
+}
+std::vector<uint64_t> ms_diff(const std::vector<uint64_t> &a, const std::vector<uint64_t> &b) {
+    std::vector<uint64_t> r;
+    std::set_difference(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(r));
+    return r;
+}
+
+// Shared-prefix tree over consecutive terms: a node covers a contiguous term
+// range and carries the records common to all of them (multiset
+// intersection) minus its parent's; leaves are the terms, in order, so a DFS
+// in preorder visits the terms in the reference's summation order
+// (phase_terms.cpp:129-131). J (mod 4) and Z are sums / ORs of independent
+// record contributions, so a term's state = the union of the records on its
+// root-to-leaf path. Children split the range into `fan` equal parts; the
+// fan (or no tree at all) is chosen per tensor to minimise emitted words.
+void mono_tree_rec(const std::vector<MonoTerm> &T, size_t lo, size_t hi, const std::vector<uint64_t> &parent,
+                   uint32_t depth, uint32_t fan, std::vector<MonoNode> &out, uint64_t &cost) {
+    MonoNode nd;
+    nd.depth = depth;
+    if (hi - lo == 1) {
+        nd.leaf = true;
+        nd.recs = ms_diff(T[lo].recs, parent);
+        nd.re = T[lo].re;
+        nd.im = T[lo].im;
+        cost += 5 + nd.recs.size();
+        out.push_back(std::move(nd));
+        return;
+    }
+    std::vector<uint64_t> inter = T[lo].recs;
+    for (size_t i = lo + 1; i < hi && !inter.empty(); i++) inter = ms_inter(inter, T[i].recs);
+    nd.recs = ms_diff(inter, parent);
+    cost += 1 + nd.recs.size();
+    out.push_back(std::move(nd));
+    const size_t n = hi - lo, parts = std::min<size_t>(fan, n);
+    for (size_t p = 0; p < parts; p++) {
+        const size_t a = lo + n * p / parts, b = lo + n * (p + 1) / parts;
+        if (b > a) mono_tree_rec(T, a, b, inter, depth + 1, fan, out, cost);
+    }
+}
+
+std::vector<MonoNode> mono_tree(const std::vector<MonoTerm> &T) {
+    // flat: every term a leaf at depth 0
+    std::vector<MonoNode> best;
+    uint64_t best_cost = 0;
+    for (const MonoTerm &t : T) {
+        MonoNode nd;
+        nd.leaf = true;
+        nd.recs = t.recs;
+        nd.re = t.re;
+        nd.im = t.im;
+        best_cost += 5 + nd.recs.size();
+        best.push_back(std::move(nd));
+    }
+    if (T.size() < 4) return best;
+    for (uint32_t fan : {2u, 3u, 4u, 6u, 8u, 16u}) {
+        // depth bound: ceil(log_fan(N)) + 1 levels
+        uint32_t depth = 1;
+        for (size_t x = 1; x < T.size(); x *= fan) depth++;
+        if (depth >= zxs_dev::kMonoMaxDepth) continue;
+        std::vector<MonoNode> nodes;
+        uint64_t cost = 0;
+        mono_tree_rec(T, 0, T.size(), {}, 0, fan, nodes, cost);
+        if (cost < best_cost) {
+            best_cost = cost;
+            best = std::move(nodes);
+        }
+    }
+    return best;
+}
 
 // Lowers every eligible large component to the record streams of
 // zxs_mono.cuh. A component is eligible when every h table it uses is the
@@ -415,23 +546,54 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             tpb[t] = pb;
         }
     }
+    // One dictionary per chain tensor (staged in shared memory while that
+    // tensor is evaluated); form ids are relative to the tensor's base.
     std::map<std::vector<uint32_t>, uint32_t> form_id;
-    // dictionary entry: u16 count | 0x8000 (continues), then up to seven u16
-    // plane byte offsets p * 128 (zxs_mono.cuh mono_form)
-    auto dict_form = [&](const std::vector<uint32_t> &sel) -> uint32_t {
+    std::map<uint32_t, uint32_t> form_size;
+    size_t dict_base = 0;
+    // dictionary entry (16 B): byte 0 = count (0..15) | 0x80 (list continues in
+    // the next entry), bytes 1..15 = plane indices (zxs_mono.cuh mono_form).
+    // A list longer than half the tensor's width W is stored as its complement
+    // plus the ALL plane (XOR of planes 0..W-1, formed per tensor on device):
+    // at most W/2 + 1 selectors.
+    const uint32_t all_plane = fwid + max_chain;  // index of the ALL plane
+    uint32_t cur_width = 0;                        // param width of the tensor being encoded
+    auto dict_form = [&](const std::vector<uint32_t> &sel0) -> uint32_t {
+        std::vector<uint32_t> sel = sel0;
+        if (cur_width >= 2 && sel0.size() > (cur_width + 1) / 2) {
+            std::vector<uint32_t> comp;
+            size_t j = 0;
+            for (uint32_t p = 0; p < cur_width; p++) {
+                if (j < sel0.size() && sel0[j] == p) {
+                    j++;
+                } else {
+                    comp.push_back(p);
+                }
+            }
+            comp.push_back(all_plane);
+            if (j == sel0.size() && comp.size() < sel0.size()) sel = comp;
+        }
         auto it = form_id.find(sel);
         if (it != form_id.end()) return it->second;
-        const uint32_t id = uint32_t(H.dict.size());
-        for (size_t i = 0; i < sel.size() || i == 0; i += 7) {
-            const size_t n = std::min<size_t>(7, sel.size() - i);
-            uint16_t e[8] = {};
-            e[0] = uint16_t(n | (i + 7 < sel.size() ? 0x8000 : 0));
-            for (size_t j = 0; j < n; j++) e[1 + j] = uint16_t(sel[i + j] * 128);
+        const uint32_t id = uint32_t(H.dict.size() - dict_base);
+        for (size_t i = 0; i < sel.size() || i == 0; i += 15) {
+            const size_t n = std::min<size_t>(15, sel.size() - i);
+            uint8_t e[16];
+            std::memset(e, int(all_plane + 1), 16);  // unused slots read the all-zero plane
+            const uint8_t cls = n <= 2 ? 0 : n <= 4 ? 1 : n <= 8 ? 2 : 3;
+            e[0] = uint8_t(cls | (i + 15 < sel.size() ? 0x80 : 0));
+            for (size_t k = 0; k < n; k++) e[1 + k] = uint8_t(sel[i + k]);
             uint4 w;
             std::memcpy(&w, e, 16);
             H.dict.push_back(w);
         }
         form_id.emplace(sel, id);
+        uint32_t slots = 0;  // plane loads the device performs for this form
+        for (size_t i = 0; i < sel.size() || i == 0; i += 15) {
+            const size_t n = std::min<size_t>(15, sel.size() - i);
+            slots += n <= 2 ? 2 : n <= 4 ? 4 : n <= 8 ? 8 : 15;
+        }
+        form_size[id] = slots;
         return id;
     };
     // parity list of a selector range after XOR cancellation, sorted
@@ -453,33 +615,27 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
         const uint32_t n = d->comp_out_begin[c + 1] - d->comp_out_begin[c];
         const uint32_t t0 = d->comp_tensor_begin[c], t1 = d->comp_tensor_begin[c + 1];
         const uint64_t nf = d->term_factor_begin[d->tensor_term_begin[t1]] - d->term_factor_begin[d->tensor_term_begin[t0]];
-        bool ok = nf >= heavy_min && H.comps.size() < size_t(zxs_dev::kMaxMonoComps) && fwid + n <= 255;
+        bool ok = nf >= heavy_min && H.comps.size() < size_t(zxs_dev::kMaxMonoComps) && fwid + max_chain + 2 <= 255;
         const size_t dict_mark = H.dict.size();
-        const auto form_mark = form_id;
+        std::vector<uint32_t> tdb;  // per tensor: first dictionary entry
+        std::vector<uint32_t> twid;  // per tensor: param width (the ALL plane spans planes 0..W-1)
+        uint32_t comp_max_dict = 1;
         std::vector<uint32_t> w;
         std::vector<uint4> ch;
         std::vector<uint32_t> tcb;
-        uint64_t recs = 0, dead = 0, nsel = 0;
-        // v lists first: they are the second form of two-form records (12-bit field)
-        for (uint64_t k = d->term_factor_begin[d->tensor_term_begin[t0]];
-             ok && k < d->term_factor_begin[d->tensor_term_begin[t1]]; k++) {
-            const std::vector<uint32_t> vs = sel_list(d->factor_v_bits + d->factor_v_begin[k],
-                                                      d->factor_v_begin[k + 1] - d->factor_v_begin[k]);
-            if (!vs.empty() && dict_form(vs) >= 0xfffu) ok = false;
-        }
+        uint64_t recs = 0, dead = 0, nsel = 0, loads = 0, nodes_total = 0;
         for (uint32_t t = t0; ok && t < t1; t++) {
-            uint32_t cur_begin = uint32_t(H.words.size() + w.size()), cur_terms = 0;
-            auto close_chunk = [&]() {
-                if (H.words.size() + w.size() == cur_begin) w.insert(w.end(), 4, 0u);  // no 0-byte bulk copies
-                while ((H.words.size() + w.size()) % 4) w.push_back(0);
-                const uint32_t end = uint32_t(H.words.size() + w.size());
-                ch.push_back(make_uint4(cur_begin, end - cur_begin, cur_terms, 0));
-                cur_begin = end;
-                cur_terms = 0;
-            };
-            tcb.push_back(uint32_t(H.chunks.size() + ch.size()));
+            form_id.clear();
+            form_size.clear();
+            dict_base = H.dict.size();
+            tdb.push_back(uint32_t(dict_base));
+            cur_width = d->tensor_param_width[t];
+            twid.push_back(cur_width);
+            // ---- lower every term of tensor t to record tokens (order-free: J and Z commute)
+            std::vector<MonoTerm> terms;
+            terms.reserve(size_t(d->tensor_term_begin[t + 1] - d->tensor_term_begin[t]));
             for (uint64_t term = d->tensor_term_begin[t]; ok && term < d->tensor_term_begin[t + 1]; term++) {
-                std::vector<uint32_t> tw;
+                std::vector<uint64_t> tw;
                 int M = 0, K = 0;
                 bool term_dead = false;
                 for (uint64_t k = d->term_factor_begin[term]; k < d->term_factor_begin[term + 1]; k++) {
@@ -548,15 +704,11 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                     for (int ab = 0; ab < 4; ab++) {
                         if (indomain[ab] && zero[ab]) zl |= 1u << ab;
                     }
-                    const uint32_t fa = ua ? dict_form(us) : 0xffffu, fbv = vb ? dict_form(vs) : 0xfffu;
-                    if (vb && fbv >= 0xfffu) {
-                        ok = false;
-                        break;
-                    }
+                    const uint32_t fa = ua ? dict_form(us) : 0xfffu, fbv = vb ? dict_form(vs) : 0xfffu;
                     nsel += us.size() + vs.size();
-                    auto rec = [&](uint32_t kind, uint32_t a_form, uint32_t b_form) {
-                        tw.push_back(kind << 28 | (b_form & 0xfffu) << 16 | (a_form & 0xffffu));
-                        recs++;
+                    // token: record word | (GEN aux word + 1) << 32
+                    auto rec = [&](uint32_t kind, uint32_t a_form, uint32_t b_form, uint64_t aux = 0) {
+                        tw.push_back(uint64_t(kind << 28 | (b_form & 0xfffu) << 16 | (a_form & 0xfffu)) | aux << 32);
                     };
                     const bool jnone = !al && !be && !ga;
                     // Z patterns over the domain points present (bit index a*2+b)
@@ -575,8 +727,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                             rec(be == 1 ? zxs_dev::kRecAdd : be == 3 ? zxs_dev::kRecSub : zxs_dev::kRecAdd2,
                                 dict_form(vs), 0xfffu);
                         } else {
-                            rec(zxs_dev::kRecGen, fa, fbv);
-                            tw.push_back(uint32_t(al | be << 2 | ga << 4));
+                            rec(zxs_dev::kRecGen, fa, fbv, uint64_t(al | be << 2 | ga << 4) + 1);
                         }
                     } else if (jnone && ua && zis(zA)) {
                         rec(zxs_dev::kRecZ, fa, 0xfffu);
@@ -586,13 +737,8 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                         rec(zxs_dev::kRecZ, dict_form(vs), 0xfffu);
                     } else if (jnone && vb && zis(zBn)) {
                         rec(zxs_dev::kRecZn, dict_form(vs), 0xfffu);
-                    } else if (jnone && ua && vb && zis(0x6u)) {
-                        rec(zxs_dev::kRecZx, fa, fbv);
-                    } else if (jnone && ua && vb && zis(0x9u)) {
-                        rec(zxs_dev::kRecZxn, fa, fbv);
                     } else {
-                        rec(zxs_dev::kRecGen, fa, fbv);
-                        tw.push_back(uint32_t(al | be << 2 | ga << 4) | zl << 6);
+                        rec(zxs_dev::kRecGen, fa, fbv, (uint64_t(al | be << 2 | ga << 4) | uint64_t(zl) << 6) + 1);
                     }
                 }
                 if (!ok) break;
@@ -607,25 +753,75 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                 long double mag = std::ldexp(1.0L, M / 2);
                 if (M & 1) mag *= 1.41421356237309504880168872420969807857L;
                 const long double cr = d->term_c[2 * term], ci = d->term_c[2 * term + 1];
-                const double re = double((cr * wr[k8] - ci * wi[k8]) * mag);
-                const double im = double((cr * wi[k8] + ci * wr[k8]) * mag);
-                uint64_t rb, ib;
-                std::memcpy(&rb, &re, 8);
-                std::memcpy(&ib, &im, 8);
-                std::vector<uint32_t> hdr = {uint32_t(tw.size()), 0u, uint32_t(rb), uint32_t(rb >> 32), uint32_t(ib),
-                                             uint32_t(ib >> 32)};
-                if (hdr.size() + tw.size() + 4 > zxs_dev::kMonoChunkWords) {
+                MonoTerm mt;
+                mt.re = double((cr * wr[k8] - ci * wi[k8]) * mag);
+                mt.im = double((cr * wi[k8] + ci * wr[k8]) * mag);
+                std::sort(tw.begin(), tw.end());
+                mt.recs = std::move(tw);
+                terms.push_back(std::move(mt));
+            }
+            if (!ok) break;
+            // ---- shared-prefix tree over the terms in order, emitted in DFS preorder
+            std::vector<MonoNode> nodes = mono_tree(terms);
+            uint32_t cur_begin = uint32_t(H.words.size() + w.size()), cur_nodes = 0;
+            auto close_chunk = [&]() {
+                if (H.words.size() + w.size() == cur_begin) w.insert(w.end(), 4, 0u);  // no 0-byte bulk copies
+                while ((H.words.size() + w.size()) % 4) w.push_back(0);
+                const uint32_t end = uint32_t(H.words.size() + w.size());
+                ch.push_back(make_uint4(cur_begin, end - cur_begin, cur_nodes, 0));
+                cur_begin = end;
+                cur_nodes = 0;
+            };
+            tcb.push_back(uint32_t(H.chunks.size() + ch.size()));
+            if (H.dict.size() - dict_base >= 0xfffu) ok = false;  // 12-bit form ids
+            comp_max_dict = std::max<uint32_t>(comp_max_dict, uint32_t(H.dict.size() - dict_base));
+            std::vector<uint32_t> nw;
+            for (const MonoNode &nd : nodes) {
+                if (!ok) break;
+                // node: {leaf << 31 | depth << 24 | n_gen, n_add | n_sub << 8 | n_add2 << 16 | n_z << 24, n_zn}
+                // [+ re, im for leaves], then the one-form records grouped by kind, then GEN pairs
+                uint32_t cnt[16] = {};
+                for (uint64_t tok : nd.recs) cnt[uint32_t(tok) >> 28]++;
+                for (int k = 0; k < 16; k++) ok &= cnt[k] < 256;
+                if (!ok) break;
+                nw.clear();
+                nw.push_back((nd.leaf ? 0x80000000u : 0u) | uint32_t(nd.depth) << 24 | cnt[zxs_dev::kRecGen]);
+                nw.push_back(cnt[zxs_dev::kRecAdd] | cnt[zxs_dev::kRecSub] << 8 | cnt[zxs_dev::kRecAdd2] << 16 |
+                             cnt[zxs_dev::kRecZ] << 24);
+                nw.push_back(cnt[zxs_dev::kRecZn]);
+                if (nd.leaf) {
+                    uint64_t rb, ib;
+                    std::memcpy(&rb, &nd.re, 8);
+                    std::memcpy(&ib, &nd.im, 8);
+                    nw.insert(nw.end(), {uint32_t(rb), uint32_t(rb >> 32), uint32_t(ib), uint32_t(ib >> 32)});
+                }
+                for (uint32_t kind : {zxs_dev::kRecAdd, zxs_dev::kRecSub, zxs_dev::kRecAdd2, zxs_dev::kRecZ,
+                                      zxs_dev::kRecZn, zxs_dev::kRecGen}) {
+                    for (uint64_t tok : nd.recs) {
+                        const uint32_t r = uint32_t(tok);
+                        if ((r >> 28) != kind) continue;
+                        nw.push_back(r);
+                        if (tok >> 32) nw.push_back(uint32_t((tok >> 32) - 1));
+                        recs++;
+                        const uint32_t fa = r & 0xfffu, fbv = (r >> 16) & 0xfffu;
+                        if (fa != 0xfffu) loads += form_size[fa];
+                        if (kind == zxs_dev::kRecGen && fbv != 0xfffu) loads += form_size[fbv];
+                    }
+                }
+                if (nw.size() + 4 > zxs_dev::kMonoChunkWords || nd.depth >= zxs_dev::kMonoMaxDepth) {
                     ok = false;
                     break;
                 }
-                if (H.words.size() + w.size() + hdr.size() + tw.size() - cur_begin > zxs_dev::kMonoChunkWords) close_chunk();
-                w.insert(w.end(), hdr.begin(), hdr.end());
-                w.insert(w.end(), tw.begin(), tw.end());
-                cur_terms++;
+                if (H.words.size() + w.size() + nw.size() - cur_begin > zxs_dev::kMonoChunkWords) close_chunk();
+                w.insert(w.end(), nw.begin(), nw.end());
+                cur_nodes++;
             }
-            if (ok && (cur_terms || H.words.size() + w.size() == cur_begin)) close_chunk();
+            if (ok) close_chunk();
+            nodes_total += nodes.size();
         }
-        if (ok && H.dict.size() >= 0xffffu) ok = false;
+        if (ok && mono_smem_bytes(fwid + max_chain + 2, std::max(comp_max_dict, H.max_dict)) > 227 * 1024) {
+            ok = false;
+        }
         if (ok) {
             zxs_dev::HeavyComp hc;
             hc.ci = c;
@@ -638,21 +834,28 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             H.chunks.insert(H.chunks.end(), ch.begin(), ch.end());
             for (size_t i = 1; i < tcb.size(); i++) H.tensor_chunk_begin.push_back(tcb[i]);
             H.tensor_chunk_begin.push_back(uint32_t(H.chunks.size()));
+            H.tensor_dict_begin.insert(H.tensor_dict_begin.end(), tdb.begin(), tdb.end());
+            H.tensor_width.insert(H.tensor_width.end(), twid.begin(), twid.end());
             H.comps.push_back(hc);
             H.comp_mono[c] = 1;
+            H.max_dict = std::max(H.max_dict, comp_max_dict);
             H.max_chain = std::max(H.max_chain, n);
             H.records += recs;
             H.dead_terms += dead;
             H.selectors += nsel;
+            H.loads += loads;
+            H.nodes += nodes_total;
         } else {
             H.dict.resize(dict_mark);
-            form_id = form_mark;
         }
         upos += n;
     }
     if (H.words.empty()) H.words.assign(4, 0);
     if (H.chunks.empty()) H.chunks.push_back(make_uint4(0, 0, 0, 0));
     if (H.dict.empty()) H.dict.push_back(make_uint4(0, 0, 0, 0));
+    H.tensor_dict_begin.push_back(uint32_t(H.dict.size()));
+    if (H.tensor_width.empty()) H.tensor_width.push_back(0);
+    H.all_plane = fwid + max_chain;
     return H;
 }
 
@@ -753,6 +956,23 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         uint32_t b = d->base_offset[i];
         if (b >= fwid) fail(ZXS_INVALID_ARGUMENT, "base_offset bit out of range");
         base[b >> 6] |= uint64_t(1) << (b & 63);
+    }
+    s->host_base = base;
+    s->host_mechs.resize(d->num_mechanisms);
+    for (uint32_t mi = 0; mi < d->num_mechanisms; mi++) {
+        zxs_sampler::HostMech &hm = s->host_mechs[mi];
+        const uint32_t v0 = d->mech_vec_begin[mi], nv = d->mech_vec_begin[mi + 1] - v0;
+        hm.joint = nv > 1;
+        for (uint32_t b = 0; b < nv; b++) {
+            std::vector<uint64_t> mask(FW, 0);
+            vec_mask(v0 + b, mask);
+            hm.vecs.push_back(mask);
+        }
+        if (hm.joint) {
+            hm.table.assign(d->table + d->mech_table_begin[mi], d->table + d->mech_table_begin[mi + 1]);
+        } else {
+            hm.p = d->mech_probability[mi];
+        }
     }
 
     // ---- direct outputs
@@ -935,6 +1155,8 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     size_t o_mch = ar.add(MH.chunks);
     size_t o_mtcb = ar.add(MH.tensor_chunk_begin);
     size_t o_mdict = ar.add(MH.dict);
+    size_t o_mtdb = ar.add(MH.tensor_dict_begin);
+    size_t o_mtw = ar.add(MH.tensor_width);
 
     CK(cudaMalloc(&s->dev_model, ar.host.size()));
     s->dev_model_bytes = ar.host.size();
@@ -999,23 +1221,28 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     if (s->has_mono) {
         zxs_dev::MonoArgs &ma = s->mono;
         ma.f_width = fwid;
-        ma.n_planes = fwid + MH.max_chain;
+        ma.n_planes = MH.all_plane + 2;  // f, sampled bits of the longest chain, ALL, ZERO
+        ma.all_plane = MH.all_plane;
+        ma.tensor_width = reinterpret_cast<const uint32_t *>(b + o_mtw);
         ma.words = reinterpret_cast<const uint32_t *>(b + o_mw);
         ma.chunks = reinterpret_cast<const uint4 *>(b + o_mch);
         ma.tensor_chunk_begin = reinterpret_cast<const uint32_t *>(b + o_mtcb);
         ma.total_chunks = static_cast<uint32_t>(MH.chunks.size());
         ma.dict = reinterpret_cast<const uint4 *>(b + o_mdict);
+        ma.tensor_dict_begin = reinterpret_cast<const uint32_t *>(b + o_mtdb);
+        ma.max_dict = std::max<uint32_t>(1, MH.max_dict);
         ma.comp_outputs = m.comp_outputs;
         ma.eval_tensor = -1;
         ma.n_comps = static_cast<uint32_t>(MH.comps.size());
         for (size_t i = 0; i < MH.comps.size(); i++) ma.comps[i] = MH.comps[i];
         s->mono_tensor = MH.tensor_index;
-        s->mono_smem = 128 + 2 * size_t(zxs_dev::kMonoChunkWords) * 4 + size_t(zxs_dev::kMonoWarps) * ma.n_planes * 128;
+        s->mono_smem = mono_smem_bytes(ma.n_planes, ma.max_dict);
     }
     s->info.num_mono_components = uint32_t(MH.comps.size());
     s->info.num_mono_records = MH.records;
     s->info.num_mono_dead_terms = MH.dead_terms;
     s->info.num_mono_forms = uint32_t(MH.dict.size());
+    s->info.num_mono_loads = MH.loads;
     m.mech_entry_begin = nullptr;
     m.mech_stream = nullptr;
     m.entry_lim = nullptr;
@@ -1101,15 +1328,12 @@ void launch_mono(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *f
     h.err = s->dev_err;
     h.eval_tensor = eval_tensor;
     h.eval_out = eval_out;
-    if (eval_tensor >= 0) {
-        h.f_width = f_width;
-        h.n_planes = std::max(h.n_planes, f_width);
-    }
+    if (eval_tensor >= 0) h.f_width = std::min(f_width, h.all_plane);  // injected params; forms use < W
     const uint64_t per_cta = uint64_t(zxs_dev::kMonoWarps) * 1024;
     h.n_cta_tiles = (a.shots + per_cta - 1) / per_cta;
     if (h.n_cta_tiles == 0) return;
     h.scratch = s->mono_scratch_get(size_t(2) * h.n_cta_tiles * per_cta * 8);
-    const size_t smem = 128 + 2 * size_t(zxs_dev::kMonoChunkWords) * 4 + size_t(zxs_dev::kMonoWarps) * h.n_planes * 128;
+    const size_t smem = mono_smem_bytes(h.n_planes, h.max_dict);
     if (smem > s->mono_smem) {
         CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(&zxs_dev::mono_kernel),
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -1136,15 +1360,23 @@ void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
     unsigned grid = unsigned(std::min(a.n_tiles, cap));
     size_t smem = shot_smem_bytes(s);
     static zxs_dev::MechTable<1> unused_table{};
-    const bool heavy = (s->has_heavy || s->has_mono) && !a.fcols_out;
+    const bool heavy = (s->has_heavy || s->has_mono) && !a.fcols_out && !a.forced;
     if (heavy) {
         a.heavy_ld32 = 2 * ((a.shots + 63) / 64);
         a.heavy_fcols = s->heavy_fcols_get(std::max<size_t>(16, size_t(s->m.f_width) * a.heavy_ld32 * 4));
     }
     void *args[] = {&a, s->param_mechs ? static_cast<void *>(s->mech_table.get()) : static_cast<void *>(&unused_table)};
+    cudaEvent_t t0 = nullptr;
+    s->time_begin(0, st, t0);
     CK(cudaLaunchKernel(shot_kernel_for(s->fw_template, s->param_mechs), dim3(grid), dim3(32), args, smem, st));
-    if (heavy && s->has_mono) launch_mono(s, a, a.heavy_fcols, a.heavy_ld32, -1, nullptr, 0, st);
+    s->time_end(0, st, t0);
+    if (heavy && s->has_mono) {
+        s->time_begin(2, st, t0);
+        launch_mono(s, a, a.heavy_fcols, a.heavy_ld32, -1, nullptr, 0, st);
+        s->time_end(2, st, t0);
+    }
     if (heavy && s->has_heavy) {
+        s->time_begin(1, st, t0);
         zxs_dev::HeavyArgs h = s->heavy;
         h.seed = a.seed;
         h.first_shot = a.first_shot;
@@ -1164,6 +1396,7 @@ void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
         void *hargs[] = {&h};
         CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::heavy_kernel), dim3(hgrid),
                             dim3(zxs_dev::kHeavyWarps * 32), hargs, s->heavy_smem, st));
+        s->time_end(1, st, t0);
     }
 }
 
@@ -1240,6 +1473,10 @@ void zxs_sampler_destroy(zxs_sampler *s) {
     if (s->scratch) cudaFree(s->scratch);
     if (s->heavy_scratch) cudaFree(s->heavy_scratch);
     if (s->mono_scratch) cudaFree(s->mono_scratch);
+    for (auto &t : s->timed) {
+        cudaEventDestroy(t.second.first);
+        cudaEventDestroy(t.second.second);
+    }
     if (prev >= 0) cudaSetDevice(prev);
     delete s;
 }
@@ -1280,6 +1517,37 @@ zxs_status zxs_count_device(zxs_sampler *s, uint64_t seed, uint64_t first_shot, 
         return ZXS_INVALID_ARGUMENT;
     }
     return zxs_sample_device(s, seed, first_shot, shots, nullptr, 0, dev_counts, stream);
+}
+
+zxs_status zxs_kernel_timing(zxs_sampler *s, int enable) {
+    return guarded([&] {
+        if (!s) fail(ZXS_INVALID_ARGUMENT, "null sampler");
+        DeviceGuard g(s->device);
+        for (auto &t : s->timed) {
+            cudaEventDestroy(t.second.first);
+            cudaEventDestroy(t.second.second);
+        }
+        s->timed.clear();
+        s->timing = enable != 0;
+    });
+}
+
+zxs_status zxs_kernel_times(zxs_sampler *s, double *ms, uint64_t *launches) {
+    return guarded([&] {
+        if (!s || !ms || !launches) fail(ZXS_INVALID_ARGUMENT, "null argument");
+        DeviceGuard g(s->device);
+        for (int i = 0; i < 3; i++) {
+            ms[i] = 0.0;
+            launches[i] = 0;
+        }
+        for (auto &t : s->timed) {
+            CK(cudaEventSynchronize(t.second.second));
+            float e = 0.f;
+            CK(cudaEventElapsedTime(&e, t.second.first, t.second.second));
+            ms[t.first] += e;
+            launches[t.first]++;
+        }
+    });
 }
 
 zxs_status zxs_check_errors(zxs_sampler *s, void *stream) {
@@ -1357,6 +1625,125 @@ zxs_status zxs_sample(zxs_sampler *s, uint32_t expected_mode, uint64_t seed, uin
             CK(cudaStreamWaitEvent(s->copy_stream, s->ev_done[bi], 0));
             CK(cudaMemcpy2DAsync(host_columns + w0, words * 8, buf, cw * 8, cw * 8, nout, cudaMemcpyDeviceToHost,
                                  s->copy_stream));
+            CK(cudaEventRecord(s->ev_copied[bi], s->copy_stream));
+        }
+        CK(cudaStreamSynchronize(s->copy_stream));
+        check_ratio_error(s, st);
+    });
+}
+
+// ---------------------------------------------------------------- encode_shots
+namespace {
+// encode.cpp:23-25: the encoded output range, clamped to the record width
+uint32_t encode_width(uint32_t num_outputs, uint32_t first_output, uint32_t output_count) {
+    if (first_output > num_outputs) fail(ZXS_INVALID_ARGUMENT, "first_output beyond the record width");
+    const uint32_t last = std::min(num_outputs, first_output + std::min(output_count, num_outputs - first_output));
+    return last - first_output;
+}
+
+uint64_t encoded_row_bytes(uint32_t width, uint32_t format) {
+    if (format > 1) fail(ZXS_INVALID_ARGUMENT, "unknown shot format");
+    return format == ZXS_FORMAT_B8 ? (width + 7) / 8 : uint64_t(width) + 1;
+}
+
+void launch_encode(const uint32_t *cols, uint64_t ld32, uint32_t first_output, uint32_t width, uint64_t shots,
+                   uint32_t format, uint8_t *dev_out, cudaStream_t st) {
+    if (shots == 0) return;
+    zxs_dev::EncodeArgs e;
+    e.cols = cols;
+    e.ld32 = ld32;
+    e.first_output = first_output;
+    e.width = width;
+    e.format = format;
+    e.shots = shots;
+    e.out = dev_out;
+    e.row_bytes = uint32_t(encoded_row_bytes(width, format));
+    if (e.row_bytes == 0) return;
+    e.smem_per_warp = (32 * e.row_bytes + 15) & ~15u;
+    const size_t smem = size_t(zxs_dev::kEncWarps) * e.smem_per_warp;
+    if (smem > 200 * 1024) fail(ZXS_UNSUPPORTED, "record too wide for the device encoder");
+    if (smem > 48 * 1024) {
+        CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(&zxs_dev::encode_kernel),
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    }
+    int dev = 0, sms = 148;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const uint64_t nwords = (shots + 31) / 32;
+    const unsigned grid = unsigned(std::min<uint64_t>((nwords + zxs_dev::kEncWarps - 1) / zxs_dev::kEncWarps,
+                                                      uint64_t(sms) * 16));
+    zxs_dev::encode_kernel<<<grid, zxs_dev::kEncWarps * 32, smem, st>>>(e);
+    CK(cudaGetLastError());
+}
+}  // namespace
+
+uint64_t zxs_encoded_bytes(uint32_t num_outputs, uint64_t shots, uint32_t first_output, uint32_t output_count,
+                           uint32_t format) {
+    if (first_output > num_outputs || format > 1) return 0;
+    const uint32_t last = std::min(num_outputs, first_output + std::min(output_count, num_outputs - first_output));
+    const uint32_t width = last - first_output;
+    return shots * (format == ZXS_FORMAT_B8 ? (uint64_t(width) + 7) / 8 : uint64_t(width) + 1);
+}
+
+zxs_status zxs_encode_shots_device(const uint64_t *dev_columns, uint64_t ld_words, uint32_t num_outputs,
+                                   uint64_t shots, uint32_t first_output, uint32_t output_count, uint32_t format,
+                                   uint8_t *dev_out, void *stream) {
+    return guarded([&] {
+        const uint32_t width = encode_width(num_outputs, first_output, output_count);
+        encoded_row_bytes(width, format);
+        if (shots == 0 || width == 0 && format == ZXS_FORMAT_B8) return;
+        if (!dev_columns || !dev_out) fail(ZXS_INVALID_ARGUMENT, "null argument");
+        if (ld_words < (shots + 63) / 64) fail(ZXS_INVALID_ARGUMENT, "ld_words < ceil(shots/64)");
+        launch_encode(reinterpret_cast<const uint32_t *>(dev_columns), 2 * ld_words, first_output, width, shots,
+                      format, dev_out, device_stream(stream));
+    });
+}
+
+// sample_detectors / sample_measurements followed by encode_shots, fused:
+// chunks are sampled into device columns, encoded on the device, and the
+// encoded bytes copied to the host on a second stream while the next chunk
+// is sampled. (zxsim.cpp:142-163: write_output(encode_shots(sample_*(...))).)
+zxs_status zxs_sample_encoded(zxs_sampler *s, uint32_t expected_mode, uint64_t seed, uint64_t first_shot,
+                              uint64_t shots, uint32_t format, uint32_t first_output, uint32_t output_count,
+                              uint8_t *host_out, void *stream) {
+    return guarded([&] {
+        if (!s) fail(ZXS_INVALID_ARGUMENT, "null sampler");
+        check_mode(s, expected_mode);
+        const uint32_t nout = s->m.num_outputs;
+        const uint32_t width = encode_width(nout, first_output, output_count);
+        const uint64_t rb = encoded_row_bytes(width, format);
+        if (shots == 0 || rb == 0) return;
+        if (!host_out) fail(ZXS_INVALID_ARGUMENT, "null output");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard g(s->device);
+        cudaStream_t st = host_stream(s, stream);
+        // chunk: multiple of 64 shots, ~64 MiB of encoded output per buffer
+        uint64_t chunk = std::max<uint64_t>(64, ((uint64_t(64) << 20) / rb) & ~uint64_t(63));
+        chunk = std::min<uint64_t>(chunk, (shots + 63) & ~uint64_t(63));
+        const uint64_t cw = chunk / 64;
+        auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+        const size_t col_bytes = al(size_t(cw) * std::max<uint32_t>(nout, 1) * 8), enc_bytes = al(size_t(chunk * rb));
+        char *scratch = s->scratch_get(2 * (col_bytes + enc_bytes));
+        const uint64_t nchunks = (shots + chunk - 1) / chunk;
+        for (uint64_t c = 0; c < nchunks; c++) {
+            const int bi = int(c & 1);
+            const uint64_t s0 = c * chunk, cs = std::min(chunk, shots - s0);
+            auto *cols = reinterpret_cast<uint64_t *>(scratch + bi * (col_bytes + enc_bytes));
+            auto *enc = reinterpret_cast<uint8_t *>(scratch + bi * (col_bytes + enc_bytes) + col_bytes);
+            if (c >= 2) CK(cudaStreamWaitEvent(st, s->ev_copied[bi], 0));
+            if (!s->all_outputs_covered) CK(cudaMemsetAsync(cols, 0, size_t(cw) * nout * 8, st));
+            zxs_dev::LaunchArgs a{};
+            a.seed = seed;
+            a.first_shot = first_shot + s0;
+            a.shots = cs;
+            a.out32 = reinterpret_cast<uint32_t *>(cols);
+            a.ld32 = 2 * cw;
+            launch_shots(s, a, st);
+            CK(cudaGetLastError());
+            launch_encode(reinterpret_cast<const uint32_t *>(cols), 2 * cw, first_output, width, cs, format, enc, st);
+            CK(cudaEventRecord(s->ev_done[bi], st));
+            CK(cudaStreamWaitEvent(s->copy_stream, s->ev_done[bi], 0));
+            CK(cudaMemcpyAsync(host_out + s0 * rb, enc, size_t(cs * rb), cudaMemcpyDeviceToHost, s->copy_stream));
             CK(cudaEventRecord(s->ev_copied[bi], s->copy_stream));
         }
         CK(cudaStreamSynchronize(s->copy_stream));
@@ -1566,6 +1953,113 @@ zxs_status zxs_probability_of_at(zxs_sampler *s, const uint8_t *outcome, uint32_
     });
 }
 
+// probability_of (sampler.cpp:370-429): the enumeration over mechanism
+// outcomes runs on the host in the reference's DFS order (weights formed by
+// the same left-to-right products, zero-weight subtrees pruned), every leaf's
+// outcome_probability_given is evaluated on the device as one "shot" with its
+// f injected and the outcome bits forced (shot_kernel probability mode), and
+// the leaves are Kahan-summed in DFS order like the reference.
+zxs_status zxs_probability_of(zxs_sampler *s, const uint8_t *outcome, uint32_t n_outcome, double *out) {
+    return guarded([&] {
+        if (!s || !out || (!outcome && n_outcome)) fail(ZXS_INVALID_ARGUMENT, "null argument");
+        if (n_outcome != s->m.num_outputs) fail(ZXS_INVALID_ARGUMENT, "outcome length must match the output count");
+        double entropy_bits = 0;
+        for (const auto &m : s->host_mechs) entropy_bits += m.joint ? std::log2(double(m.table.size())) : 1.0;
+        if (entropy_bits > 20.0) fail(ZXS_INVALID_ARGUMENT, "noise entropy guard exceeded for exact marginalization");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard g(s->device);
+        const size_t FW = s->host_base.size();
+        // ---- leaves in DFS order
+        std::vector<double> weights;
+        std::vector<uint64_t> fs;  // [leaf][FW]
+        std::vector<uint64_t> f = s->host_base;
+        const size_t M = s->host_mechs.size();
+        std::function<void(size_t, double)> walk = [&](size_t idx, double weight) {
+            if (weight == 0.0) return;
+            if (idx == M) {
+                weights.push_back(weight);
+                fs.insert(fs.end(), f.begin(), f.end());
+                return;
+            }
+            const auto &m = s->host_mechs[idx];
+            auto flip = [&](const std::vector<uint64_t> &v) {
+                for (size_t w = 0; w < FW; w++) f[w] ^= v[w];
+            };
+            if (!m.joint) {
+                walk(idx + 1, weight * (1.0 - m.p));
+                flip(m.vecs[0]);
+                walk(idx + 1, weight * m.p);
+                flip(m.vecs[0]);
+                return;
+            }
+            for (size_t o = 0; o < m.table.size(); o++) {
+                if (m.table[o] == 0.0) continue;
+                for (size_t b = 0; b < m.vecs.size(); b++) {
+                    if ((o >> b) & 1) flip(m.vecs[b]);
+                }
+                walk(idx + 1, weight * m.table[o]);
+                for (size_t b = 0; b < m.vecs.size(); b++) {
+                    if ((o >> b) & 1) flip(m.vecs[b]);
+                }
+            }
+        };
+        walk(0, 1.0);
+        const uint64_t n = weights.size();
+        if (n == 0) {
+            *out = 0.0;
+            return;
+        }
+        // ---- f-columns of the leaves: [f_width][ceil(n/64)] u64
+        const uint64_t words = (n + 63) / 64;
+        const uint32_t fwid = s->m.f_width;
+        std::vector<uint64_t> cols(std::max<size_t>(1, size_t(fwid) * words), 0);
+        for (uint64_t l = 0; l < n; l++) {
+            for (uint32_t b = 0; b < fwid; b++) {
+                if ((fs[l * FW + (b >> 6)] >> (b & 63)) & 1) cols[b * words + (l >> 6)] |= uint64_t(1) << (l & 63);
+            }
+        }
+        cudaStream_t st = s->stream;
+        auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+        const size_t fbytes = size_t(fwid) * words * 8, pbytes = size_t(n) * 8, obytes = std::max<size_t>(n_outcome, 1);
+        char *base = s->scratch_get(al(fbytes) + al(pbytes) + al(obytes) + 256);
+        auto *df = reinterpret_cast<uint32_t *>(base);
+        auto *dp = reinterpret_cast<double *>(base + al(fbytes));
+        auto *dout = reinterpret_cast<uint8_t *>(base + al(fbytes) + al(pbytes));
+        if (fbytes) CK(cudaMemcpyAsync(df, cols.data(), fbytes, cudaMemcpyHostToDevice, st));
+        std::vector<uint8_t> oc(obytes, 0);
+        for (uint32_t i = 0; i < n_outcome; i++) oc[i] = outcome[i] ? 1 : 0;
+        CK(cudaMemcpyAsync(dout, oc.data(), obytes, cudaMemcpyHostToDevice, st));
+        zxs_dev::LaunchArgs a{};
+        a.shots = n;
+        a.fcols_in = df;
+        a.fcols_ld32 = 2 * words;
+        a.forced = dout;
+        a.prob = dp;
+        launch_shots(s, a, st);
+        CK(cudaGetLastError());
+        std::vector<double> pg(n);
+        CK(cudaMemcpyAsync(pg.data(), dp, pbytes, cudaMemcpyDeviceToHost, st));
+        unsigned long long h[2];
+        CK(cudaMemcpyAsync(h, s->dev_err, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (h[0]) {
+            unsigned long long init[2] = {0, ~0ull};
+            CK(cudaMemcpy(s->dev_err, init, sizeof(init), cudaMemcpyHostToDevice));
+            fail(ZXS_RUNTIME_ERROR, "component normalization is not positive");  // sampler.cpp:343-345
+        }
+        // ---- Kahan-compensated sum in DFS order (sampler.cpp:388-395)
+        double sum = 0.0, carry = 0.0;
+        for (uint64_t l = 0; l < n; l++) {
+            const double term = weights[l] * pg[l];
+            const double y = term - carry;
+            const double t = sum + y;
+            carry = (t - sum) - y;
+            sum = t;
+        }
+        *out = sum;
+    });
+}
+
 zxs_status zxs_debug_heavy_layout(const zxs_model_desc *desc, uint64_t min_factors, uint32_t *out, uint64_t cap,
                                   uint64_t *needed) {
     return guarded([&] {
@@ -1599,12 +2093,14 @@ zxs_status zxs_debug_mono_layout(const zxs_model_desc *desc, uint64_t min_factor
         MonoHost H = encode_mono(desc, max_chain, min_factors);
         std::vector<uint32_t> blob = {uint32_t(H.words.size()), uint32_t(H.chunks.size()),
                                       uint32_t(H.tensor_chunk_begin.size()), uint32_t(H.dict.size()),
-                                      uint32_t(H.comps.size()), uint32_t(H.comp_mono.size()), 0u, 0u};
+                                      uint32_t(H.comps.size()), uint32_t(H.comp_mono.size()), H.all_plane, 0u};
         for (const auto &c : H.comps) blob.insert(blob.end(), {c.ci, c.n_out, c.upos_base, c.out_begin, c.first_tensor});
         for (uint8_t f : H.comp_mono) blob.push_back(f);
         blob.insert(blob.end(), H.tensor_chunk_begin.begin(), H.tensor_chunk_begin.end());
         for (const uint4 &c : H.chunks) blob.insert(blob.end(), {c.x, c.y, c.z, c.w});
         for (const uint4 &c : H.dict) blob.insert(blob.end(), {c.x, c.y, c.z, c.w});
+        blob.insert(blob.end(), H.tensor_dict_begin.begin(), H.tensor_dict_begin.end());
+        blob.insert(blob.end(), H.tensor_width.begin(), H.tensor_width.begin() + (H.tensor_chunk_begin.size() - 1));
         blob.insert(blob.end(), H.words.begin(), H.words.end());
         *needed = blob.size();
         if (out && cap >= blob.size()) std::memcpy(out, blob.data(), blob.size() * 4);
@@ -1674,6 +2170,38 @@ zxs_status zxs_measure_fp64_peak(int device, double *ops_per_s) {
         cudaEventDestroy(e1);
         cudaFree(sink);
         *ops_per_s = double(reps) * grid * 256.0 * iters * 8 * 8 / (ms * 1e-3);  // 8 chains x (4 DMUL + 4 DADD)
+    });
+}
+
+zxs_status zxs_measure_smem_peak(int device, double *bytes_per_s) {
+    return guarded([&] {
+        if (!bytes_per_s) fail(ZXS_INVALID_ARGUMENT, "null output");
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) fail(ZXS_CUDA_ERROR, "no CUDA device available");
+        DeviceGuard g(device);
+        int sms = 0, occ = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, zxs_dev::smem_peak_kernel, 256, 0));
+        uint32_t *sink = nullptr;
+        CK(cudaMalloc(&sink, 4));
+        const uint32_t iters = 8192;
+        const unsigned grid = unsigned(sms * std::max(occ, 1));
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        zxs_dev::smem_peak_kernel<<<grid, 256>>>(iters, sink);  // warm-up
+        CK(cudaEventRecord(e0));
+        const int reps = 3;
+        for (int r = 0; r < reps; r++) zxs_dev::smem_peak_kernel<<<grid, 256>>>(iters, sink);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaFree(sink);
+        // every warp load instruction moves 32 x 4 B
+        *bytes_per_s = double(reps) * grid * 256.0 * iters * 16 * 4 / (ms * 1e-3);
     });
 }
 

@@ -74,6 +74,12 @@ struct LaunchArgs {
     unsigned long long *err;       // [0] = flag, [1] = first failing shot
     uint32_t *heavy_fcols;         // f-columns for heavy_kernel: [f_width][heavy_ld32] (nullable)
     uint64_t heavy_ld32;
+    // probability mode (outcome_probability_given, sampler.cpp:324-356): the
+    // outcome bits are forced instead of drawn and prob[shot] receives
+    // P(outcome | f) for the injected f of every shot. Every component runs
+    // here (exact FP64 order), none is deferred to the large-chi kernels.
+    const uint8_t *forced;         // [num_outputs] 0/1 (nullable)
+    double *prob;                  // [shots]
 };
 
 // 32x32 -> 64 multiply as one mul.wide.u32 (IMAD.WIDE.U32); written in PTX
@@ -326,6 +332,7 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
         }
 
         // ---- (4): direct outputs, lane-parallel over outputs
+        uint32_t mism[kS] = {0u, 0u};  // probability mode: shots whose direct outputs differ from the outcome
         for (uint32_t d = lane; d < m.num_direct; d += 32) {
             const uint32_t od = m.direct_out[d];
             uint32_t w[kS];
@@ -337,6 +344,12 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
                 for (int s = 0; s < kS; s++) w[s] ^= cols[s * m.col_stride + fb];
             }
             const uint32_t o = od & 0x7fffffffu;
+            if (a.forced) {
+                const uint32_t want = a.forced[o] ? kFull : 0u;
+#pragma unroll
+                for (int s = 0; s < kS; s++) mism[s] |= w[s] ^ want;
+                continue;
+            }
 #pragma unroll
             for (int s = 0; s < kS; s++) w[s] &= vmask[s];
             if (a.out32) {
@@ -345,11 +358,21 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
             if (a.counts && (w[0] | w[1])) atomicAdd(&scount[o], (unsigned long long)(__popc(w[0]) + __popc(w[1])));
         }
 
+        double pgiven[kS] = {1.0, 1.0};
+        bool pzero[kS] = {false, false};
+        if (a.forced) {
+#pragma unroll
+            for (int s = 0; s < kS; s++) {
+                mism[s] = __reduce_or_sync(kFull, mism[s]);
+                pzero[s] = (mism[s] >> lane) & 1u;  // sampler.cpp:328-336: return 0.0 before any component
+            }
+        }
+
         // ---- (5): autoregressive components
         uint32_t upos = 0;
         for (uint32_t ci = 0; ci < m.num_components; ci++) {
             const uint32_t ob = m.comp_out_begin[ci], n = m.comp_out_begin[ci + 1] - ob;
-            if (m.comp_heavy[ci]) {  // evaluated by heavy_kernel
+            if (m.comp_heavy[ci] && !a.forced) {  // evaluated by heavy_kernel / mono_kernel
                 upos += n;
                 continue;
             }
@@ -360,12 +383,28 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
             }
             __syncwarp();
             double2 acc[kS];
-            double prev[kS];
+            double prev[kS], norm[kS];
             eval_tensor(m, tb, cols, m.col_stride, lane, acc);
 #pragma unroll
-            for (int s = 0; s < kS; s++) prev[s] = acc[s].x;
+            for (int s = 0; s < kS; s++) {
+                prev[s] = norm[s] = acc[s].x;
+                // sampler.cpp:343-345
+                if (a.forced && !pzero[s] && local[s] < a.shots && !(norm[s] > 0.0)) report_ratio_error(a.err, shot[s]);
+            }
             for (uint32_t pos = 0; pos < n; pos++, upos++) {
                 eval_tensor(m, tb + 1 + pos, cols, m.col_stride, lane, acc);
+                if (a.forced) {  // sampler.cpp:346-352: forced outcome bit
+                    const uint32_t o = m.comp_outputs[ob + pos];
+                    const bool bit = a.forced[o] != 0;
+#pragma unroll
+                    for (int s = 0; s < kS; s++) prev[s] = bit ? __dsub_rn(prev[s], acc[s].x) : acc[s].x;
+                    if (lane == 0) {
+#pragma unroll
+                        for (int s = 0; s < kS; s++) cols[s * m.col_stride + m.f_width + pos] = bit ? kFull : 0u;
+                    }
+                    __syncwarp();
+                    continue;
+                }
                 uint32_t rhi[kS], rlo[kS];
                 if (!a.uniforms) {
                     const uint32_t stream = 0x80000000u ^ (ci << 12) ^ pos;  // sampler.cpp:37-39
@@ -396,6 +435,16 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
                     }
                 }
                 __syncwarp();
+            }
+            if (a.forced) {
+#pragma unroll
+                for (int s = 0; s < kS; s++) pgiven[s] = __dmul_rn(pgiven[s], __ddiv_rn(prev[s], norm[s]));  // sampler.cpp:353
+            }
+        }
+        if (a.forced) {
+#pragma unroll
+            for (int s = 0; s < kS; s++) {
+                if (local[s] < a.shots) a.prob[local[s]] = pzero[s] ? 0.0 : pgiven[s];
             }
         }
     }
@@ -482,6 +531,24 @@ __global__ void __launch_bounds__(256) fp64_peak_kernel(double2 h, uint32_t iter
         }
     }
     if (acc.x == 1.2345 && acc.y == 6.789) sink[0] = acc.x;  // keeps the work observable
+}
+
+// Same-op-mix roofline for mono_kernel's selector loads: conflict-free
+// 32-bit shared loads (one 128 B wavefront per warp instruction) XORed into a
+// register, addresses a per-lane base plus warp-uniform plane offsets.
+__global__ void __launch_bounds__(256) smem_peak_kernel(uint32_t iters, uint32_t *sink) {
+    __shared__ uint32_t planes[64 * 32];
+    const uint32_t lane = threadIdx.x & 31u;
+    for (uint32_t i = threadIdx.x; i < 64 * 32; i += blockDim.x) planes[i] = i * 0x9E3779B9u;
+    __syncthreads();
+    const char *lb = reinterpret_cast<const char *>(planes + lane);
+    uint32_t acc = 0, off = 0;
+    for (uint32_t it = 0; it < iters; it++) {
+#pragma unroll
+        for (int k = 0; k < 16; k++) acc ^= *reinterpret_cast<const uint32_t *>(lb + ((off + k * 5u) & 63u) * 128u);
+        off += 7;
+    }
+    if (acc == 0x12345678u) sink[0] = acc;  // keeps the work observable
 }
 
 __global__ void philox_kernel(uint64_t seed, uint32_t stream, uint64_t first, uint64_t n, double *out) {

@@ -20,6 +20,14 @@
 // its h entries (~1e-16 relative), so sampled bits agree except at exact
 // threshold ties (counted by the tests).
 //
+// Term sharing: consecutive terms share most of their factors (the
+// cultivation proxy's terms are a product of six 6-way cat5 branches), so the
+// host arranges each tensor's terms in a shared-prefix tree (zxs_api.cu
+// mono_tree): a node's records are applied on top of its parent's (Z, J0,
+// J1), kept per level in a small shared-memory stack, and leaves -- the
+// terms, in the reference's order -- run the epilogue. This cuts the records
+// evaluated per shot ~2.6x on that circuit.
+//
 // Work decomposition: lane = one 32-shot word (bit s = shot 32*w + s), a warp
 // = 1024 shots, a CTA = kMonoWarps warps that walk the SAME record stream:
 // chunks of the stream are fetched once per CTA with cp.async.bulk into a
@@ -34,29 +42,30 @@
 
 namespace zxs_dev {
 
-constexpr int kMonoWarps = 8;                // warps per CTA (8192 shots per CTA tile)
+constexpr int kMonoWarps = 16;               // warps per CTA (16384 shots per CTA tile), one CTA per SM
 constexpr uint32_t kMonoChunkWords = 4096;   // 16 KiB per chunk buffer
-constexpr uint32_t kMonoNoFormA = 0xffffu;   // "no form" in the 16-bit first-form field: parity 0
-constexpr uint32_t kMonoNoFormB = 0xfffu;    // same in the 12-bit second-form field
+constexpr uint32_t kMonoNoForm = 0xfffu;     // "no form" (parity 0) in the 12-bit form fields
 constexpr int kMaxMonoComps = 8;
+constexpr uint32_t kMonoMaxDepth = 8;        // levels of the shared-prefix term tree
 
-// record kinds (bits 28..31 of a record word; first form in bits 0..15,
-// second form in bits 16..27)
+// record kinds (bits 28..31 of a record word; first form in bits 0..11,
+// second form in bits 16..27; ids index the tensor's dictionary)
 enum : uint32_t {
     kRecAdd = 0,    // J += a
     kRecSub = 1,    // J -= a
     kRecAdd2 = 2,   // J += 2a
     kRecZ = 3,      // Z |= a
     kRecZn = 4,     // Z |= ~a
-    kRecZx = 5,     // Z |= a ^ b
-    kRecZxn = 6,    // Z |= ~(a ^ b)
-    kRecGen = 15,   // next word: alpha | beta << 2 | gamma << 4 | zlut << 6
+    kRecGen = 15,   // two forms; next word: alpha | beta << 2 | gamma << 4 | zlut << 6
 };
 
 struct MonoArgs {
     uint64_t seed, first_shot, shots, n_cta_tiles;
     uint32_t k0_round[10];
-    uint32_t f_width, n_planes;       // planes per warp = f_width + longest mono chain
+    uint32_t f_width, n_planes;       // planes per warp = f_width + longest chain + ALL + ZERO
+    uint32_t all_plane;               // index of the ALL plane: XOR of planes 0..W-1 of the current tensor;
+                                      // all_plane + 1 is the all-zero plane (padding selectors)
+    const uint32_t *tensor_width;     // [mono tensors] param width W
     const uint32_t *fcols;            // [f_width][fcols_ld32] from shot_kernel
     uint64_t fcols_ld32;
     uint32_t *out32;                  // [num_outputs][out_ld32] (nullable)
@@ -70,7 +79,9 @@ struct MonoArgs {
     const uint4 *chunks;              // {word_begin, n_words (multiple of 4), n_terms, 0}
     const uint32_t *tensor_chunk_begin;
     uint32_t total_chunks;
-    const uint4 *dict;                // form dictionary
+    const uint4 *dict;                // form dictionaries, one per tensor
+    const uint32_t *tensor_dict_begin;  // [mono tensors + 1]
+    uint32_t max_dict;                // largest per-tensor dictionary (entries staged in smem)
     const uint32_t *comp_outputs;
     // eval seam: evaluate one tensor and store the values (no chain)
     int eval_tensor;                  // -1: sample; else index into tensor_chunk_begin
@@ -79,30 +90,47 @@ struct MonoArgs {
     HeavyComp comps[kMaxMonoComps];
 };
 
-// Parity word of form f for the lane's 32 shots: XOR of the lane's parameter
-// planes listed in the dictionary entry. Entry layout (16 B): u16 [0] =
-// count (0..7) | 0x8000 if the list continues in the next entry, u16 [1..7] =
-// byte offsets p * 128 of the planes (plane p of lane l at p * 128 + 4 l).
-// The switch falls through (a jump table into one straight run of loads),
-// so each selector costs one extract/add, one LDS and half a 3-input XOR.
-__device__ __forceinline__ uint32_t mono_form(const uint4 *__restrict__ dict, uint32_t f, const char *lb) {
-    uint32_t acc = 0;
-    while (true) {
-        const uint4 e = __ldg(dict + f);
-#define ZXS_SEL(x) (*reinterpret_cast<const uint32_t *>(lb + (x)))
-        switch (e.x & 7u) {
-            case 7: acc ^= ZXS_SEL(e.w >> 16);  // fallthrough
-            case 6: acc ^= ZXS_SEL(e.w & 0xffffu);  // fallthrough
-            case 5: acc ^= ZXS_SEL(e.z >> 16);  // fallthrough
-            case 4: acc ^= ZXS_SEL(e.z & 0xffffu);  // fallthrough
-            case 3: acc ^= ZXS_SEL(e.y >> 16);  // fallthrough
-            case 2: acc ^= ZXS_SEL(e.y & 0xffffu);  // fallthrough
-            case 1: acc ^= ZXS_SEL(e.x >> 16);  // fallthrough
-            default: break;
+// Parity word of dictionary form f for the lane's 32 shots: XOR of the lane's
+// parameter planes the entry lists. Entry layout (16 B): byte 0 = size class
+// (0: 2, 1: 4, 2: 8, 3: 15 selector slots) | 0x80 if the list continues in
+// the next entry; bytes 1..15 = plane indices p (plane p of lane l at byte
+// p * 128 + 4 l), unused slots pointing at the all-zero plane. Lists longer
+// than half the tensor's width are stored complemented against the ALL
+// plane. Each size class is straight-line code: every load of the entry is
+// issued before the XOR tree consumes them (a selector costs a byte extract,
+// an address IMAD, one LDS and half a 3-input XOR), and the warp takes one
+// uniform branch per entry.
+__device__ __forceinline__ uint32_t mono_entry(const uint4 e, const char *lb) {
+#define ZXS_SEL(word, k) (*reinterpret_cast<const uint32_t *>(lb + (__byte_perm((word), 0u, 0x4440u + (k)) << 7)))
+    switch (e.x & 3u) {
+        case 0:
+            return ZXS_SEL(e.x, 1) ^ ZXS_SEL(e.x, 2);
+        case 1: {
+            const uint32_t a = ZXS_SEL(e.x, 1), b = ZXS_SEL(e.x, 2), c = ZXS_SEL(e.x, 3), d = ZXS_SEL(e.y, 0);
+            return (a ^ b) ^ (c ^ d);
         }
+        case 2: {
+            const uint32_t a = ZXS_SEL(e.x, 1), b = ZXS_SEL(e.x, 2), c = ZXS_SEL(e.x, 3), d = ZXS_SEL(e.y, 0);
+            const uint32_t f = ZXS_SEL(e.y, 1), g = ZXS_SEL(e.y, 2), k = ZXS_SEL(e.y, 3), l = ZXS_SEL(e.z, 0);
+            return ((a ^ b) ^ (c ^ d)) ^ ((f ^ g) ^ (k ^ l));
+        }
+        default: {
+            const uint32_t a = ZXS_SEL(e.x, 1), b = ZXS_SEL(e.x, 2), c = ZXS_SEL(e.x, 3), d = ZXS_SEL(e.y, 0);
+            const uint32_t f = ZXS_SEL(e.y, 1), g = ZXS_SEL(e.y, 2), k = ZXS_SEL(e.y, 3), l = ZXS_SEL(e.z, 0);
+            const uint32_t m = ZXS_SEL(e.z, 1), n = ZXS_SEL(e.z, 2), o = ZXS_SEL(e.z, 3), p = ZXS_SEL(e.w, 0);
+            const uint32_t q = ZXS_SEL(e.w, 1), r = ZXS_SEL(e.w, 2), t = ZXS_SEL(e.w, 3);
+            return (((a ^ b) ^ (c ^ d)) ^ ((f ^ g) ^ (k ^ l))) ^ (((m ^ n) ^ (o ^ p)) ^ ((q ^ r) ^ t));
+        }
+    }
 #undef ZXS_SEL
-        if (!(e.x & 0x8000u)) break;
-        f++;
+}
+
+__device__ __forceinline__ uint32_t mono_form(const uint4 *sd, uint32_t f, const char *lb) {
+    uint4 e = sd[f];
+    uint32_t acc = mono_entry(e, lb);
+    while (e.x & 0x80u) {
+        e = sd[++f];
+        acc ^= mono_entry(e, lb);
     }
     return acc;
 }
@@ -114,12 +142,42 @@ __device__ __forceinline__ void j_add(uint32_t &j0, uint32_t &j1, uint32_t x, ui
     j0 ^= xl;
 }
 
-__global__ void __launch_bounds__(kMonoWarps * 32, 2) mono_kernel(const __grid_constant__ MonoArgs h) {
+// Record runs of one kind, forms of four records formed together (independent
+// shared loads in flight), then applied.
+#define ZXS_MONO_RUN(N, OP)                                                              \
+    {                                                                                    \
+        uint32_t i_ = 0;                                                                 \
+        for (; i_ + 4 <= (N); i_ += 4) {                                                 \
+            const uint32_t x0 = mono_form(sd, w[q + i_] & 0xfffu, pl);                   \
+            const uint32_t x1 = mono_form(sd, w[q + i_ + 1] & 0xfffu, pl);               \
+            const uint32_t x2 = mono_form(sd, w[q + i_ + 2] & 0xfffu, pl);               \
+            const uint32_t x3 = mono_form(sd, w[q + i_ + 3] & 0xfffu, pl);               \
+            OP(x0);                                                                      \
+            OP(x1);                                                                      \
+            OP(x2);                                                                      \
+            OP(x3);                                                                      \
+        }                                                                                \
+        for (; i_ < (N); i_++) {                                                         \
+            const uint32_t x0 = mono_form(sd, w[q + i_] & 0xfffu, pl);                   \
+            OP(x0);                                                                      \
+        }                                                                                \
+        q += (N);                                                                        \
+    }
+#define ZXS_OP_ADD(x) { j1 ^= j0 & (x); j0 ^= (x); }
+#define ZXS_OP_SUB(x) { j1 ^= ~j0 & (x); j0 ^= (x); }
+#define ZXS_OP_ADD2(x) { j1 ^= (x); }
+#define ZXS_OP_Z(x) { z |= (x); }
+#define ZXS_OP_ZN(x) { z |= ~(x); }
+
+__global__ void __launch_bounds__(kMonoWarps * 32, 1) mono_kernel(const __grid_constant__ MonoArgs h) {
     extern __shared__ __align__(128) uint8_t msm[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(msm);
     uint32_t *buf0 = reinterpret_cast<uint32_t *>(msm + 128);
-    uint32_t *planes_all = buf0 + 2 * kMonoChunkWords;
+    uint4 *sd = reinterpret_cast<uint4 *>(buf0 + 2 * kMonoChunkWords);  // the current tensor's dictionary
+    uint32_t *stack_all = reinterpret_cast<uint32_t *>(sd + h.max_dict);  // [warp][depth][z, j0, j1][lane]
+    uint32_t *planes_all = stack_all + kMonoWarps * kMonoMaxDepth * 3 * 32;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    uint32_t *stk = stack_all + warp * kMonoMaxDepth * 3 * 32 + lane;
     uint32_t *planes = planes_all + warp * h.n_planes * 32;  // [p][lane]
     const char *pl = reinterpret_cast<const char *>(planes + lane);
 
@@ -182,6 +240,19 @@ __global__ void __launch_bounds__(kMonoWarps * 32, 2) mono_kernel(const __grid_c
             const uint32_t npos = h.eval_tensor >= 0 ? 1u : cd.n_out + 1;
             for (uint32_t pos = 0; pos < npos; pos++) {  // pos 0: normalization, pos j+1: marginal j
                 const uint32_t t = h.eval_tensor >= 0 ? uint32_t(h.eval_tensor) : cd.first_tensor + pos;
+                // the ALL plane of this tensor (its sampled-bit planes are final up to pos)
+                {
+                    uint32_t all = 0;
+                    const uint32_t W = min(h.tensor_width[t], h.all_plane);
+                    for (uint32_t p = 0; p < W; p++) all ^= planes[p * 32 + lane];
+                    planes[h.all_plane * 32 + lane] = all;
+                }
+                // stage the tensor's form dictionary (every warp is past the previous tensor)
+                {
+                    const uint32_t d0 = h.tensor_dict_begin[t], nd = h.tensor_dict_begin[t + 1] - d0;
+                    for (uint32_t i = threadIdx.x; i < nd; i += blockDim.x) sd[i] = __ldg(h.dict + d0 + i);
+                    __syncthreads();
+                }
                 double acc[32];
 #pragma unroll
                 for (int s = 0; s < 32; s++) acc[s] = 0.0;
@@ -189,45 +260,53 @@ __global__ void __launch_bounds__(kMonoWarps * 32, 2) mono_kernel(const __grid_c
                     const uint32_t b = uint32_t(use & 1);
                     mbar_wait(&bars[b], uint32_t((use >> 1) & 1));
                     const uint32_t *w = buf0 + b * kMonoChunkWords;
-                    const uint32_t nterms = h.chunks[c].z;
+                    const uint32_t nnodes = h.chunks[c].z;
                     uint32_t q = 0;
-                    for (uint32_t tt = 0; tt < nterms; tt++) {
-                        // term header: {n record words, 0, re.lo, re.hi, im.lo, im.hi}
-                        const uint32_t nw = w[q];
-                        const double re = __hiloint2double(int(w[q + 3]), int(w[q + 2]));
-                        const double im = __hiloint2double(int(w[q + 5]), int(w[q + 4]));
-                        q += 6;
-                        const uint32_t qe = q + nw;
-                        uint32_t j0 = 0, j1 = 0, z = 0;
-                        while (q < qe) {
-                            const uint32_t r = w[q++];
-                            const uint32_t kind = r >> 28;
-                            const uint32_t fa = r & 0xffffu;
-                            const uint32_t a = fa == kMonoNoFormA ? 0u : mono_form(h.dict, fa, pl);
-                            switch (kind) {
-                                case kRecAdd: j1 ^= j0 & a; j0 ^= a; break;
-                                case kRecSub: j1 ^= ~j0 & a; j0 ^= a; break;
-                                case kRecAdd2: j1 ^= a; break;
-                                case kRecZ: z |= a; break;
-                                case kRecZn: z |= ~a; break;
-                                default: {
-                                    const uint32_t fb = (r >> 16) & 0xfffu;
-                                    const uint32_t bb = fb == kMonoNoFormB ? 0u : mono_form(h.dict, fb, pl);
-                                    if (kind == kRecZx) {
-                                        z |= a ^ bb;
-                                    } else if (kind == kRecZxn) {
-                                        z |= ~(a ^ bb);
-                                    } else {  // kRecGen
-                                        const uint32_t g = w[q++];
-                                        const uint32_t zl = g >> 6;
-                                        z |= ((zl & 1u) ? (~a & ~bb) : 0u) | ((zl & 2u) ? (~a & bb) : 0u) |
-                                             ((zl & 4u) ? (a & ~bb) : 0u) | ((zl & 8u) ? (a & bb) : 0u);
-                                        j_add(j0, j1, a, g & 3u);
-                                        j_add(j0, j1, bb, (g >> 2) & 3u);
-                                        j_add(j0, j1, a & bb, (g >> 4) & 3u);
-                                    }
-                                }
-                            }
+                    for (uint32_t nn = 0; nn < nnodes; nn++) {
+                        // node: {leaf << 31 | depth << 24 | n_gen, n_add | n_sub << 8 | n_add2 << 16 | n_z << 24,
+                        // n_zn} [re, im], records grouped by kind
+                        const uint32_t h0 = w[q], h1 = w[q + 1], h2 = w[q + 2];
+                        const uint32_t depth = (h0 >> 24) & 0x7fu;
+                        const bool leaf = (h0 >> 31) != 0;
+                        q += 3;
+                        double re = 0.0, im = 0.0;
+                        if (leaf) {
+                            re = __hiloint2double(int(w[q + 1]), int(w[q]));
+                            im = __hiloint2double(int(w[q + 3]), int(w[q + 2]));
+                            q += 4;
+                        }
+                        // state of the parent (depth - 1), or the empty product at the root
+                        uint32_t z = 0, j0 = 0, j1 = 0;
+                        if (depth) {
+                            const uint32_t *ps = stk + (depth - 1) * 96;
+                            z = ps[0];
+                            j0 = ps[32];
+                            j1 = ps[64];
+                        }
+                        ZXS_MONO_RUN(h1 & 0xffu, ZXS_OP_ADD)
+                        ZXS_MONO_RUN((h1 >> 8) & 0xffu, ZXS_OP_SUB)
+                        ZXS_MONO_RUN((h1 >> 16) & 0xffu, ZXS_OP_ADD2)
+                        ZXS_MONO_RUN(h1 >> 24, ZXS_OP_Z)
+                        ZXS_MONO_RUN(h2 & 0xffu, ZXS_OP_ZN)
+                        for (uint32_t g = 0; g < (h0 & 0xffu); g++) {  // two-form records
+                            const uint32_t r = w[q], gw = w[q + 1];
+                            q += 2;
+                            const uint32_t fa = r & 0xfffu, fb = (r >> 16) & 0xfffu;
+                            const uint32_t a = fa == kMonoNoForm ? 0u : mono_form(sd, fa, pl);
+                            const uint32_t bb = fb == kMonoNoForm ? 0u : mono_form(sd, fb, pl);
+                            const uint32_t zl = gw >> 6;
+                            z |= ((zl & 1u) ? (~a & ~bb) : 0u) | ((zl & 2u) ? (~a & bb) : 0u) |
+                                 ((zl & 4u) ? (a & ~bb) : 0u) | ((zl & 8u) ? (a & bb) : 0u);
+                            j_add(j0, j1, a, gw & 3u);
+                            j_add(j0, j1, bb, (gw >> 2) & 3u);
+                            j_add(j0, j1, a & bb, (gw >> 4) & 3u);
+                        }
+                        if (!leaf) {
+                            uint32_t *ns = stk + depth * 96;
+                            ns[0] = z;
+                            ns[32] = j0;
+                            ns[64] = j1;
+                            continue;
                         }
                         // epilogue: acc[s] += Re(c' i^J) for the non-zero shots, in term order
                         const uint32_t neg = j0 ^ j1;

@@ -123,6 +123,17 @@ class CompiledSampler:
     def check_errors(self, stream: int = 0):
         _native.check(_native.lib().zxs_check_errors(self._h, stream or None))
 
+    def kernel_timing(self, enable: bool):
+        """Start (clearing) / stop per-kernel CUDA-event timing of every launch."""
+        _native.check(_native.lib().zxs_kernel_timing(self._h, 1 if enable else 0))
+
+    def kernel_times(self) -> dict:
+        """{kernel: (total ms, launches)} for shot_kernel, heavy_kernel, mono_kernel."""
+        ms = (ctypes.c_double * 3)()
+        n = (ctypes.c_uint64 * 3)()
+        _native.check(_native.lib().zxs_kernel_times(self._h, ms, n))
+        return {k: (ms[i], int(n[i])) for i, k in enumerate(("shot_kernel", "heavy_kernel", "mono_kernel"))}
+
     # ---- host-buffer entry points --------------------------------------
     def sample_into(self, expected_mode: int, seed: int, first_shot: int, shots: int, out: np.ndarray,
                     stream: int = 0) -> np.ndarray:
@@ -238,6 +249,53 @@ def probability_of_at(cs: CompiledSampler, outcome, f_assignment) -> float:
     return out.value
 
 
+FORMAT_01, FORMAT_B8 = 0, 1  # ShotFormat::ascii01 / b8 (encode.hpp:25)
+
+
+def sample_encoded(cs: CompiledSampler, shots: int, opt: SamplerOptions | None = None, fmt: int = FORMAT_B8,
+                   first_output: int = 0, output_count: int = 0xFFFFFFFF, first_shot: int = 0,
+                   mode: int | None = None) -> bytes:
+    """The CLI's write path, fused on the device (zxsim.cpp:142-163):
+    encode_shots(sample_detectors/measurements(cs, shots, opt), fmt, first_output, output_count)."""
+    opt = opt or SamplerOptions()
+    mode = cs.mode if mode is None else mode
+    n = _native.lib().zxs_encoded_bytes(cs.num_outputs, shots, first_output, output_count, fmt)
+    out = np.zeros(max(n, 1), np.uint8)
+    _native.check(_native.lib().zxs_sample_encoded(cs.handle, mode, opt.seed, first_shot, shots, fmt, first_output,
+                                                   output_count, out.ctypes.data_as(_u8p), None))
+    return out[:n].tobytes()
+
+
+def encode_shots(columns: np.ndarray, shots: int, fmt: int = FORMAT_B8, first_output: int = 0,
+                 output_count: int = 0xFFFFFFFF, device: int = 0) -> bytes:
+    """encode_shots (encode.hpp:29) of a host record [num_outputs][ceil(shots/64)], run on the GPU."""
+    import torch
+    cols = np.ascontiguousarray(columns, np.uint64)
+    nout, words = cols.shape
+    if words < (shots + 63) // 64:
+        raise ValueError("record has fewer words than ceil(shots/64)")
+    n = _native.lib().zxs_encoded_bytes(nout, shots, first_output, output_count, fmt)
+    if n == 0 and shots:
+        if first_output > nout or fmt not in (FORMAT_01, FORMAT_B8):
+            raise ValueError("encode_shots: invalid arguments")
+        return b""
+    dev = torch.device("cuda", device)
+    dcols = torch.from_numpy(cols.view(np.int64)).to(dev)
+    dout = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream(dev)
+    _native.check(_native.lib().zxs_encode_shots_device(dcols.data_ptr(), words, nout, shots, first_output,
+                                                        output_count, fmt, dout.data_ptr(), st.cuda_stream))
+    return dout[:n].cpu().numpy().tobytes()
+
+
+def probability_of(cs: CompiledSampler, outcome) -> float:
+    """sampler.hpp:64 (sampler.cpp:370-429): exact outcome probability; leaves on the device."""
+    o = np.ascontiguousarray(np.asarray(outcome, np.uint8))
+    out = ctypes.c_double()
+    _native.check(_native.lib().zxs_probability_of(cs.handle, o.ctypes.data_as(_u8p), o.size, ctypes.byref(out)))
+    return out.value
+
+
 def measure_philox_peak(device: int = 0) -> float:
     """Philox4x32-10 blocks/s of the draw code alone (same-op-mix roofline)."""
     out = ctypes.c_double()
@@ -249,6 +307,13 @@ def measure_fp64_peak(device: int = 0) -> float:
     """FP64 DMUL+DADD ops/s of the exact contraction's op mix (heavy_kernel roofline)."""
     out = ctypes.c_double()
     _native.check(_native.lib().zxs_measure_fp64_peak(device, ctypes.byref(out)))
+    return out.value
+
+
+def measure_smem_peak(device: int = 0) -> float:
+    """Shared-memory bytes/s of conflict-free LDS + XOR (mono_kernel roofline)."""
+    out = ctypes.c_double()
+    _native.check(_native.lib().zxs_measure_smem_peak(device, ctypes.byref(out)))
     return out.value
 
 

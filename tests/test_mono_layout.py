@@ -18,7 +18,7 @@ from conftest import golden_path
 from oracle import coracle
 from paper_2604_01059_b200 import _native, zxs_format
 
-REC_ADD, REC_SUB, REC_ADD2, REC_Z, REC_ZN, REC_ZX, REC_ZXN, REC_GEN = 0, 1, 2, 3, 4, 5, 6, 15
+REC_ADD, REC_SUB, REC_ADD2, REC_Z, REC_ZN, REC_GEN = 0, 1, 2, 3, 4, 15
 
 
 def mono_layout(arrays, min_factors=0):
@@ -30,7 +30,7 @@ def mono_layout(arrays, min_factors=0):
     _native.check(L.zxs_debug_mono_layout(ctypes.byref(desc), min_factors,
                                           buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), buf.size,
                                           ctypes.byref(need)))
-    n_words, n_chunks, n_tcb, n_dict, n_comps, n_components = (int(x) for x in buf[:6])
+    n_words, n_chunks, n_tcb, n_dict, n_comps, n_components, all_plane = (int(x) for x in buf[:7])
     o = 8
     comps = [dict(zip(("ci", "n_out", "upos_base", "out_begin", "first_tensor"),
                       (int(v) for v in buf[o + 5 * i:o + 5 * i + 5]))) for i in range(n_comps)]
@@ -43,76 +43,103 @@ def mono_layout(arrays, min_factors=0):
     o += 4 * n_chunks
     dict_ = buf[o:o + 4 * n_dict].reshape(n_dict, 4).copy()
     o += 4 * n_dict
+    tdb = buf[o:o + n_tcb].astype(np.int64)  # per mono tensor + total (same count as tcb)
+    o += n_tcb
+    twidth = buf[o:o + n_tcb - 1].astype(np.int64)
+    o += n_tcb - 1
     words = buf[o:o + n_words]
-    return dict(comps=comps, flags=flags, tcb=tcb, chunks=chunks, dict=dict_, words=words)
+    return dict(comps=comps, flags=flags, tcb=tcb, chunks=chunks, dict=dict_, tdb=tdb, twidth=twidth,
+                all_plane=all_plane, words=words)
 
 
 def form_sel(dict_, f):
-    """Parameter indices of dictionary form f (continuation entries followed):
-    u16 count | 0x8000, then up to seven u16 plane offsets p * 128."""
+    """Plane indices of dictionary form f (continuation entries followed):
+    byte 0 = size class (2/4/8/15 slots) | 0x80, bytes 1..15 plane indices."""
     sel = []
     while True:
-        e = dict_[f].view(np.uint16)
-        n = int(e[0]) & 7
-        assert all(int(x) % 128 == 0 for x in e[1:1 + n])
-        sel += [int(x) // 128 for x in e[1:1 + n]]
-        if not (int(e[0]) & 0x8000):
+        e = dict_[f].view(np.uint8)
+        slots = (2, 4, 8, 15)[int(e[0]) & 3]
+        sel += [int(x) for x in e[1:1 + slots]]  # padding slots name the all-zero plane
+        if not (int(e[0]) & 0x80):
             return sel
         f += 1
 
 
-def emulate_tensor(lay, t, P):
-    """mono_kernel's value of mono tensor t for parameter rows P [shots][W] (0/1)."""
+def apply_node_records(w, q, h0, h1, h2, form, J, Z):
+    """mono_kernel's record runs (by kind) and two-form records on (J, Z); returns the new position."""
+    for kind, n in ((REC_ADD, h1 & 0xFF), (REC_SUB, (h1 >> 8) & 0xFF), (REC_ADD2, (h1 >> 16) & 0xFF),
+                    (REC_Z, h1 >> 24), (REC_ZN, h2 & 0xFF)):
+        for _ in range(n):
+            r = int(w[q])
+            q += 1
+            assert r >> 28 == kind
+            a = form(r & 0xFFF)
+            if kind == REC_ADD:
+                J += a
+            elif kind == REC_SUB:
+                J -= a
+            elif kind == REC_ADD2:
+                J += 2 * a
+            elif kind == REC_Z:
+                Z |= a == 1
+            else:
+                Z |= a == 0
+    for _ in range(h0 & 0xFF):
+        r, g = int(w[q]), int(w[q + 1])
+        q += 2
+        assert r >> 28 == REC_GEN
+        fa, fb = r & 0xFFF, (r >> 16) & 0xFFF
+        a = 0 if fa == 0xFFF else form(fa)
+        b = 0 if fb == 0xFFF else form(fb)
+        zl = g >> 6
+        Z |= ((zl >> (a * 2 + b)) & 1) == 1
+        J += (g & 3) * a + ((g >> 2) & 3) * b + ((g >> 4) & 3) * (a * b)
+    return q
+
+
+def emulate_tensor(lay, t, P, stats=None):
+    """mono_kernel's value of mono tensor t for parameter rows P [shots][W] (0/1):
+    DFS over the shared-prefix node stream, per-level (J, Z) stack, leaves in
+    term order run the epilogue."""
     words = lay["words"]
     cache = {}
+    d0 = int(lay["tdb"][t])
+    W = int(lay["twidth"][t])
+    # planes: the params, then the ALL plane (XOR of params 0..W-1) at lay["all_plane"]
+    planes = np.zeros((P.shape[0], lay["all_plane"] + 2), np.int64)  # ..., ALL, ZERO
+    planes[:, :min(P.shape[1], lay["all_plane"])] = P[:, :lay["all_plane"]]
+    planes[:, lay["all_plane"]] = P[:, :W].sum(1) & 1
 
     def form(f):
         if f not in cache:
-            cache[f] = (P[:, form_sel(lay["dict"], f)].sum(1) & 1).astype(np.int64)
+            cache[f] = (planes[:, form_sel(lay["dict"], d0 + f)].sum(1) & 1).astype(np.int64)
         return cache[f]
 
-    acc = np.zeros(P.shape[0])
+    S = P.shape[0]
+    acc = np.zeros(S)
+    stack = {}
     for c in range(lay["tcb"][t], lay["tcb"][t + 1]):
-        wb, nw, nterms = lay["chunks"][c, :3]
+        wb, nw, nnodes = lay["chunks"][c, :3]
         w = words[wb:wb + nw]
         q = 0
-        for _ in range(nterms):
-            nrec = int(w[q])
-            re = w[q + 2:q + 4].copy().view(np.float64)[0]
-            im = w[q + 4:q + 6].copy().view(np.float64)[0]
-            q += 6
-            qe = q + nrec
-            J = np.zeros(P.shape[0], np.int64)
-            Z = np.zeros(P.shape[0], bool)
-            while q < qe:
-                r = int(w[q])
-                q += 1
-                kind, fa, fb = r >> 28, r & 0xFFFF, (r >> 16) & 0xFFF
-                a = 0 if fa == 0xFFFF else form(fa)
-                if kind == REC_ADD:
-                    J += a
-                elif kind == REC_SUB:
-                    J -= a
-                elif kind == REC_ADD2:
-                    J += 2 * a
-                elif kind == REC_Z:
-                    Z |= a == 1
-                elif kind == REC_ZN:
-                    Z |= a == 0
-                else:
-                    b = 0 if fb == 0xFFF else form(fb)
-                    if kind == REC_ZX:
-                        Z |= (a ^ b) == 1
-                    elif kind == REC_ZXN:
-                        Z |= (a ^ b) == 0
-                    else:
-                        assert kind == REC_GEN, kind
-                        g = int(w[q])
-                        q += 1
-                        zl = g >> 6
-                        idx = a * 2 + b
-                        Z |= ((zl >> idx) & 1) == 1
-                        J += (g & 3) * a + ((g >> 2) & 3) * b + ((g >> 4) & 3) * (a * b)
+        for _ in range(nnodes):
+            h0, h1, h2 = int(w[q]), int(w[q + 1]), int(w[q + 2])
+            depth, leaf = (h0 >> 24) & 0x7F, h0 >> 31
+            q += 3
+            if leaf:
+                re = w[q:q + 2].copy().view(np.float64)[0]
+                im = w[q + 2:q + 4].copy().view(np.float64)[0]
+                q += 4
+            if depth:
+                J, Z = stack[depth - 1][0].copy(), stack[depth - 1][1].copy()
+            else:
+                J, Z = np.zeros(S, np.int64), np.zeros(S, bool)
+            q = apply_node_records(w, q, h0, h1, h2, form, J, Z)
+            if stats is not None:
+                stats["nodes"] = stats.get("nodes", 0) + 1
+            if not leaf:
+                stack[depth] = (J, Z)
+                continue
             J &= 3
             v = np.where(J == 0, re, np.where(J == 1, -im, np.where(J == 2, -re, im)))
             acc = np.where(Z, acc, acc + v)

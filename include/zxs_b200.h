@@ -43,7 +43,10 @@
 extern "C" {
 #endif
 
-#define ZXS_ABI_VERSION 1u
+#define ZXS_ABI_VERSION 2u
+
+/* zxs_model_desc.flags */
+#define ZXS_MODEL_PURE_CLIFFORD_DETERMINISTIC 1u /* CompiledSampler.stats.pure_clifford_deterministic (compile.cpp:324-325) */
 
 typedef enum zxs_status {
     ZXS_OK = 0,
@@ -120,7 +123,18 @@ typedef struct zxs_model_desc {
     const double *h_table;                 /* [8*num_h_tables]                */
     const double *h_alpha;                 /* [num_h_tables]                  */
     const double *h_beta;                  /* [num_h_tables]                  */
+
+    /* ZXS_MODEL_* bits; gates the sparse geometric path (sampler.cpp:104-117) */
+    uint32_t flags;
 } zxs_model_desc;
+
+/* SamplerOptions (sampler.hpp:32-38) fields that change the sampled bits.
+   batch_size and threads do not (any batch split gives the same record). */
+typedef struct zxs_sample_options {
+    uint32_t force_dense;      /* default 0 */
+    uint32_t reserved;
+    double sparse_threshold;   /* default 8.0 */
+} zxs_sample_options;
 
 typedef enum zxs_format {
     ZXS_FORMAT_01 = 0, /* ShotFormat::ascii01 (encode.hpp:25) */
@@ -164,6 +178,22 @@ zxs_status zxs_sampler_get_info(const zxs_sampler *s, zxs_sampler_info *info);
 zxs_status zxs_sample(zxs_sampler *s, uint32_t expected_mode, uint64_t seed,
                       uint64_t first_shot, uint64_t shots, uint64_t *host_columns,
                       void *stream);
+
+/*
+ * sample_detectors / sample_measurements with the reference's options, whole
+ * record from shot 0: when the model is pure-Clifford deterministic, every
+ * mechanism is a single with p < 1 and the expected flips per shot are below
+ * sparse_threshold (and !force_dense), the reference's sparse geometric path
+ * (sampler.cpp:104-147, 214-255: per-mechanism geometric gaps on
+ * RngStream(seed, m), constant outputs as all-ones words) runs on the device;
+ * otherwise the dense path (same bits as zxs_sample). opts may be NULL
+ * (defaults). Synchronous.
+ */
+zxs_status zxs_sample_opts(zxs_sampler *s, uint32_t expected_mode, uint64_t seed, uint64_t shots,
+                           const zxs_sample_options *opts, uint64_t *host_columns, void *stream);
+
+/* 1 if zxs_sample_opts would take the sparse geometric path (sparse_eligible). */
+zxs_status zxs_sparse_eligible(const zxs_sampler *s, const zxs_sample_options *opts, int *eligible);
 
 /*
  * Device-resident variant: dev_columns is device memory [num_outputs][ld_words]
@@ -215,11 +245,12 @@ zxs_status zxs_encode_shots_device(const uint64_t *dev_columns, uint64_t ld_word
  * The CLI's sample path fused (zxsim.cpp:142-163):
  * write_output(encode_shots(sample_detectors/measurements(cs, shots, opts), fmt, first, count))
  * with sampling and encoding on the device and only the encoded bytes copied
- * to host_out (zxs_encoded_bytes(...) bytes). Synchronous.
+ * to host_out (zxs_encoded_bytes(...) bytes). opts (nullable: defaults) as in
+ * zxs_sample_opts; the sparse path applies to first_shot == 0. Synchronous.
  */
 zxs_status zxs_sample_encoded(zxs_sampler *s, uint32_t expected_mode, uint64_t seed, uint64_t first_shot,
-                              uint64_t shots, uint32_t format, uint32_t first_output, uint32_t output_count,
-                              uint8_t *host_out, void *stream);
+                              uint64_t shots, const zxs_sample_options *opts, uint32_t format,
+                              uint32_t first_output, uint32_t output_count, uint8_t *host_out, void *stream);
 
 /* f-columns after the dense error draw: host_fcols [f_width][ceil(shots/64)]. */
 zxs_status zxs_sample_error_batch(zxs_sampler *s, uint64_t seed, uint64_t first_shot,

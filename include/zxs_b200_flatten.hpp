@@ -25,6 +25,8 @@ inline zxs::FlatModel flatten(const zxsim::CompiledSampler &cs) {
     m.num_observables = cs.num_observables;
     m.num_outputs = cs.num_outputs;
     m.f_width = cs.f_width;
+    m.flags = cs.stats.pure_clifford_deterministic ? ZXS_MODEL_PURE_CLIFFORD_DETERMINISTIC : 0u;
+    m.flags_known = true;
     const zxsim::ErrorModel &em = cs.error_model;
     if (em.base_offset.width() != 0) m.base_offset = em.base_offset.set_bits();
     for (const zxsim::ErrorMechanism &mech : em.mechanisms) {

@@ -50,7 +50,13 @@ class Sampler {
     Sampler &operator=(const Sampler &) = delete;
     zxs_sampler *get() const { return s_; }
 
-    zxsim::SampleRecord sample(zxs_mode mode, size_t shots, uint64_t seed) const {
+    zxsim::SampleRecord sample(zxs_mode mode, size_t shots, const zxsim::SamplerOptions &opt) const {
+        zxs_sample_options o{opt.force_dense ? 1u : 0u, 0u, opt.sparse_threshold};
+        return sample(mode, shots, opt.seed, &o);
+    }
+
+    zxsim::SampleRecord sample(zxs_mode mode, size_t shots, uint64_t seed,
+                               const zxs_sample_options *opts = nullptr) const {
         zxs_sampler_info info;
         raise_status(zxs_sampler_get_info(s_, &info));
         zxsim::SampleRecord rec;
@@ -58,7 +64,7 @@ class Sampler {
         rec.width = info.num_outputs;
         size_t words = (shots + 63) / 64;
         std::vector<uint64_t> flat(static_cast<size_t>(info.num_outputs) * words);
-        raise_status(zxs_sample(s_, mode, seed, 0, shots, flat.data(), nullptr));
+        raise_status(zxs_sample_opts(s_, mode, seed, shots, opts, flat.data(), nullptr));
         rec.columns.assign(info.num_outputs, std::vector<uint64_t>(words));
         for (uint32_t o = 0; o < info.num_outputs; o++) {
             std::memcpy(rec.columns[o].data(), flat.data() + o * words, words * 8);
@@ -70,20 +76,21 @@ class Sampler {
     zxs_sampler *s_ = nullptr;
 };
 
-// Drop-in replacements for sampler.hpp:57-60. `opt.batch_size`, `threads`,
-// `sparse_threshold` and `force_dense` are accepted and ignored: the device
-// always runs the dense path over the whole shot range, whose bits equal the
-// reference's dense path for any batch split (sampler.cpp:82, 91, 268-284).
+// Drop-in replacements for sampler.hpp:57-60. `seed`, `sparse_threshold` and
+// `force_dense` choose the bits exactly as in the reference (dense path, or
+// the sparse geometric path when sparse_eligible, sampler.cpp:104-147);
+// `batch_size` and `threads` are accepted and ignored -- the dense path's bits
+// are the same for any batch split (sampler.cpp:82, 91, 268-284).
 inline zxsim::SampleRecord sample_detectors(const zxsim::CompiledSampler &cs, size_t shots,
                                             const zxsim::SamplerOptions &opt) {
     Sampler s(cs);
-    return s.sample(ZXS_MODE_DETECTORS, shots, opt.seed);
+    return s.sample(ZXS_MODE_DETECTORS, shots, opt);
 }
 
 inline zxsim::SampleRecord sample_measurements(const zxsim::CompiledSampler &cs, size_t shots,
                                                const zxsim::SamplerOptions &opt) {
     Sampler s(cs);
-    return s.sample(ZXS_MODE_MEASUREMENTS, shots, opt.seed);
+    return s.sample(ZXS_MODE_MEASUREMENTS, shots, opt);
 }
 
 }  // namespace zxsim_b200

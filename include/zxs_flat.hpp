@@ -26,6 +26,8 @@ namespace zxs {
 
 struct FlatModel {
     uint32_t mode = 0, num_detectors = 0, num_observables = 0, num_outputs = 0, f_width = 0;
+    uint32_t flags = 0;        // ZXS_MODEL_* (header element 5; absent in older files)
+    bool flags_known = false;  // the file carried the flags element
     std::vector<uint32_t> base_offset;
     std::vector<uint32_t> mech_vec_begin{0}, vec_bit_begin{0}, vec_bits;
     std::vector<double> mech_probability;
@@ -96,19 +98,22 @@ struct FlatModel {
         d.h_table = h_table.data();
         d.h_alpha = h_alpha.data();
         d.h_beta = h_beta.data();
+        d.flags = flags;
         return d;
     }
 
     // ---- .zxs container --------------------------------------------------
     template <typename F>
     void visit(F &&f) {
-        std::vector<uint32_t> header = {mode, num_detectors, num_observables, num_outputs, f_width};
+        std::vector<uint32_t> header = {mode, num_detectors, num_observables, num_outputs, f_width, flags};
         f("header", header);
         mode = header.at(0);
         num_detectors = header.at(1);
         num_observables = header.at(2);
         num_outputs = header.at(3);
         f_width = header.at(4);
+        flags_known = header.size() > 5;
+        flags = flags_known ? header[5] : 0u;
         f("base_offset", base_offset);
         f("mech_vec_begin", mech_vec_begin);
         f("vec_bit_begin", vec_bit_begin);

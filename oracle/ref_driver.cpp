@@ -163,7 +163,8 @@ zxsim::CompiledSampler unflatten(const zxs::FlatModel &m) {
     cs.stats.num_mechanisms = static_cast<uint32_t>(nmech);
     cs.stats.rank = cs.f_width;
     cs.stats.pure_clifford_deterministic =
-        cs.stats.num_magic == 0 && cs.components.empty() && !any_joint;
+        m.flags_known ? (m.flags & ZXS_MODEL_PURE_CLIFFORD_DETERMINISTIC) != 0
+                      : (cs.stats.num_magic == 0 && cs.components.empty() && !any_joint);
     return cs;
 }
 
@@ -303,6 +304,26 @@ int zr_sample(void *handle, uint64_t shots, uint64_t seed, uint64_t batch_size, 
         opt.batch_size = batch_size;
         opt.threads = threads;
         opt.force_dense = force_dense != 0;
+        zxsim::SampleRecord rec = cs.mode == zxsim::SampleMode::detectors
+                                      ? zxsim::sample_detectors(cs, shots, opt)
+                                      : zxsim::sample_measurements(cs, shots, opt);
+        size_t words = (shots + 63) / 64;
+        for (uint32_t o = 0; o < rec.width; o++) {
+            std::memcpy(out + o * words, rec.columns[o].data(), words * 8);
+        }
+    });
+}
+
+// sample_detectors / sample_measurements with force_dense and sparse_threshold
+// (sampler.hpp:32-38) -- the options that select the sparse path.
+int zr_sample_opts(void *handle, uint64_t shots, uint64_t seed, int force_dense, double sparse_threshold,
+                   uint64_t *out) {
+    return guarded([&] {
+        const zxsim::CompiledSampler &cs = static_cast<Handle *>(handle)->cs;
+        zxsim::SamplerOptions opt;
+        opt.seed = seed;
+        opt.force_dense = force_dense != 0;
+        opt.sparse_threshold = sparse_threshold;
         zxsim::SampleRecord rec = cs.mode == zxsim::SampleMode::detectors
                                       ? zxsim::sample_detectors(cs, shots, opt)
                                       : zxsim::sample_measurements(cs, shots, opt);

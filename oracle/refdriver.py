@@ -43,6 +43,8 @@ def lib():
         L.zr_format_stats.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t]
         L.zr_sample.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                 ctypes.c_uint32, ctypes.c_int, _u64p]
+        L.zr_sample_opts.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_double, _u64p]
+        L.zr_sample_opts.restype = ctypes.c_int
         L.zr_sample_rb.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                    ctypes.c_uint64, ctypes.c_uint32, _u64p]
         L.zr_sample_given_f.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
@@ -133,6 +135,13 @@ class RefModel:
         n = self.info["num_outputs"]
         out = np.zeros((n, (shots + 63) // 64), np.uint64)
         _check(lib().zr_sample(self._h, shots, seed, batch_size, threads, int(force_dense), _ptr(out)))
+        return out
+
+    def sample_opts(self, shots: int, seed: int, sparse_threshold: float = 8.0, force_dense: bool = False) -> np.ndarray:
+        """sample_* with the options that select the sparse path (sampler.cpp:104-117)."""
+        n = self.info["num_outputs"]
+        out = np.zeros((n, (shots + 63) // 64), np.uint64)
+        _check(lib().zr_sample_opts(self._h, shots, seed, int(force_dense), sparse_threshold, _ptr(out)))
         return out
 
     def sample_rb(self, shots: int, seed: int, first_shot: int = 0, batch_size: int = 65536,

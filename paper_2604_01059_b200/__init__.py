@@ -30,11 +30,12 @@ from .sampler import (  # noqa: F401
     sample_error_batch,
     sample_given_f,
     sample_measurements,
+    sparse_eligible,
 )
 
 __all__ = [
     "FORMAT_01", "FORMAT_B8", "encode_shots", "sample_encoded", "MODE_DETECTORS", "MODE_MEASUREMENTS", "BatchEvalResult", "CompiledSampler", "SampleRecord",
     "SamplerOptions", "count_outputs", "eval_batch", "eval_batch_mono", "measure_fp64_peak", "measure_philox_peak", "measure_smem_peak",
     "philox_uniform", "probability_of", "probability_of_at",
-    "sample_detectors", "sample_error_batch", "sample_given_f", "sample_measurements",
+    "sample_detectors", "sample_error_batch", "sample_given_f", "sample_measurements", "sparse_eligible",
 ]

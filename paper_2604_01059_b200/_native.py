@@ -39,6 +39,12 @@ class SamplerInfo(ctypes.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
+class SampleOptions(ctypes.Structure):
+    """ctypes mirror of `zxs_sample_options`."""
+
+    _fields_ = [("force_dense", ctypes.c_uint32), ("reserved", ctypes.c_uint32), ("sparse_threshold", ctypes.c_double)]
+
+
 # (name, restype, argtypes) for every symbol include/zxs_b200.h declares
 SIGNATURES = (
     ("zxs_last_error", ctypes.c_char_p, []),
@@ -47,6 +53,9 @@ SIGNATURES = (
     ("zxs_sampler_destroy", None, [_vp]),
     ("zxs_sampler_get_info", ctypes.c_int, [_vp, ctypes.POINTER(SamplerInfo)]),
     ("zxs_sample", ctypes.c_int, [_vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _u64p, _vp]),
+    ("zxs_sample_opts", ctypes.c_int, [_vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
+                                       ctypes.POINTER(SampleOptions), _u64p, _vp]),
+    ("zxs_sparse_eligible", ctypes.c_int, [_vp, ctypes.POINTER(SampleOptions), ctypes.POINTER(ctypes.c_int)]),
     ("zxs_sample_device", ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _vp,
                                          ctypes.c_uint64, _vp, _vp]),
     ("zxs_count_device", ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _vp, _vp]),
@@ -59,7 +68,8 @@ SIGNATURES = (
     ("zxs_encode_shots_device", ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
                                                ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, _vp, _vp]),
     ("zxs_sample_encoded", ctypes.c_int, [_vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
-                                          ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, _u8p, _vp]),
+                                          ctypes.POINTER(SampleOptions), ctypes.c_uint32, ctypes.c_uint32,
+                                          ctypes.c_uint32, _u8p, _vp]),
     ("zxs_sample_error_batch", ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _u64p]),
     ("zxs_eval_batch", ctypes.c_int, [_vp, ctypes.c_uint32, ctypes.c_uint32, _u64p, ctypes.c_uint32,
                                       ctypes.c_uint64, _dp, _dp]),
@@ -96,7 +106,7 @@ def lib():
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
-        if L.zxs_abi_version() != 1:
+        if L.zxs_abi_version() != 2:
             raise RuntimeError("libzxs_b200.so ABI version mismatch")
         _lib = L
     return _lib

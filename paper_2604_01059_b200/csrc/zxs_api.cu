@@ -34,6 +34,7 @@
 #include "zxs_heavy.cuh"
 #include "zxs_mono.cuh"
 #include "zxs_encode.cuh"
+#include "zxs_sparse.cuh"
 
 using zxs_dev::DevModel;
 using zxs_dev::Factor;
@@ -153,6 +154,7 @@ struct zxs_sampler {
 
     // large-chi components on the integer monomial path, see zxs_mono.cuh
     bool has_mono = false;
+    int mono_nw = 2;  // 32-shot words per lane in mono_kernel (ZXS_MONO_WORDS)
     zxs_dev::MonoArgs mono{};
     size_t mono_smem = 0;
     int mono_blocks_per_sm = 0;
@@ -171,6 +173,14 @@ struct zxs_sampler {
     };
     std::vector<HostMech> host_mechs;
     std::vector<uint64_t> host_base;
+
+    // sparse geometric path (sampler.cpp:104-147, 214-255)
+    uint32_t model_flags = 0;
+    bool sparse_structural = false;     // pure-Clifford deterministic, all singles with p < 1
+    double sparse_expected_flips = 0;   // sum_m p_m |flips(m)|  (sampler.cpp:112-114)
+    std::vector<uint32_t> const_one_outputs;  // direct outputs whose constant part is 1
+    double *dev_log1mp = nullptr;
+    uint32_t *dev_flip_begin = nullptr, *dev_flip_out = nullptr;
 
     // per-kernel CUDA-event timing (zxs_kernel_timing / zxs_kernel_times)
     bool timing = false;
@@ -408,9 +418,16 @@ MonoEntry mono_entry(int pa, int pb, int a, int b) {
     return e;
 }
 
-size_t mono_smem_bytes(uint32_t n_planes, uint32_t max_dict) {
+int mono_warps(int nw) { return nw == 2 ? zxs_dev::MonoCfg<2>::kWarps : zxs_dev::MonoCfg<1>::kWarps; }
+
+size_t mono_smem_bytes(uint32_t n_planes, uint32_t max_dict, int nw, uint32_t depth) {
     return 128 + 2 * size_t(zxs_dev::kMonoChunkWords) * 4 + size_t(max_dict) * 16 +
-           size_t(zxs_dev::kMonoWarps) * (zxs_dev::kMonoMaxDepth * 3 * 128 + size_t(n_planes) * 128);
+           size_t(mono_warps(nw)) * nw * (size_t(depth) * 3 * 128 + size_t(n_planes) * 128);
+}
+
+const void *mono_kernel_ptr(int nw) {
+    return nw == 2 ? reinterpret_cast<const void *>(&zxs_dev::mono_kernel<2>)
+                   : reinterpret_cast<const void *>(&zxs_dev::mono_kernel<1>);
 }
 
 struct MonoHost {
@@ -429,6 +446,7 @@ struct MonoHost {
     std::vector<uint32_t> tensor_width;       // param width per mono tensor
     uint32_t all_plane = 0;                    // plane index of the per-tensor ALL plane
     uint32_t max_dict = 1;
+    uint32_t max_depth = 1;  // deepest tree node + 1
 };
 
 // One term after lowering: its records as sorted tokens (record word, plus
@@ -619,7 +637,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
         const size_t dict_mark = H.dict.size();
         std::vector<uint32_t> tdb;  // per tensor: first dictionary entry
         std::vector<uint32_t> twid;  // per tensor: param width (the ALL plane spans planes 0..W-1)
-        uint32_t comp_max_dict = 1;
+        uint32_t comp_max_dict = 1, comp_depth = 1;
         std::vector<uint32_t> w;
         std::vector<uint4> ch;
         std::vector<uint32_t> tcb;
@@ -763,6 +781,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             if (!ok) break;
             // ---- shared-prefix tree over the terms in order, emitted in DFS preorder
             std::vector<MonoNode> nodes = mono_tree(terms);
+            for (const MonoNode &nd : nodes) comp_depth = std::max(comp_depth, nd.depth + 1);
             uint32_t cur_begin = uint32_t(H.words.size() + w.size()), cur_nodes = 0;
             auto close_chunk = [&]() {
                 if (H.words.size() + w.size() == cur_begin) w.insert(w.end(), 4, 0u);  // no 0-byte bulk copies
@@ -819,7 +838,8 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             if (ok) close_chunk();
             nodes_total += nodes.size();
         }
-        if (ok && mono_smem_bytes(fwid + max_chain + 2, std::max(comp_max_dict, H.max_dict)) > 227 * 1024) {
+        if (ok && mono_smem_bytes(fwid + max_chain + 2, std::max(comp_max_dict, H.max_dict), 1,
+                                  std::max(comp_depth, H.max_depth)) > 227 * 1024) {
             ok = false;
         }
         if (ok) {
@@ -839,6 +859,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             H.comps.push_back(hc);
             H.comp_mono[c] = 1;
             H.max_dict = std::max(H.max_dict, comp_max_dict);
+            H.max_depth = std::max(H.max_depth, comp_depth);
             H.max_chain = std::max(H.max_chain, n);
             H.records += recs;
             H.dead_terms += dead;
@@ -990,6 +1011,51 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         }
     }
     std::vector<uint32_t> direct_bit_begin(d->direct_bit_begin, d->direct_bit_begin + d->num_direct + 1);
+
+    // ---- sparse geometric path data (compile.cpp:285-303 flip matrix, sampler.cpp:104-117)
+    s->model_flags = d->flags;
+    {
+        bool structural = (d->flags & ZXS_MODEL_PURE_CLIFFORD_DETERMINISTIC) != 0;
+        std::vector<double> l1mp(std::max<uint32_t>(1, d->num_mechanisms), 0.0);
+        std::vector<uint32_t> fb{0}, fo;
+        double expected = 0;
+        for (uint32_t mi = 0; mi < d->num_mechanisms; mi++) {
+            const auto &hm = s->host_mechs[mi];
+            if (hm.joint || hm.vecs.size() != 1 || hm.p >= 1.0) structural = false;
+            if (!hm.joint && hm.vecs.size() == 1) {
+                for (uint32_t i = 0; i < d->num_direct; i++) {
+                    bool acc = false;
+                    for (uint32_t b = d->direct_bit_begin[i]; b < d->direct_bit_begin[i + 1]; b++) {
+                        const uint32_t f = d->direct_bits[b];
+                        acc ^= ((hm.vecs[0][f >> 6] >> (f & 63)) & 1) != 0;
+                    }
+                    if (acc) fo.push_back(d->direct_output[i]);
+                }
+                if (hm.p > 0.0 && hm.p < 1.0) l1mp[mi] = std::log1p(-hm.p);  // sampler.cpp:226
+                expected += hm.p * double(fo.size() - fb.back());
+            }
+            fb.push_back(uint32_t(fo.size()));
+        }
+        s->sparse_structural = structural;
+        s->sparse_expected_flips = expected;
+        for (uint32_t i = 0; i < d->num_direct; i++) {  // sampler.cpp:131-140
+            bool base_bit = d->direct_flip_const[i] != 0;
+            for (uint32_t b = d->direct_bit_begin[i]; b < d->direct_bit_begin[i + 1]; b++) {
+                const uint32_t f = d->direct_bits[b];
+                base_bit ^= ((base[f >> 6] >> (f & 63)) & 1) != 0;
+            }
+            if (base_bit) s->const_one_outputs.push_back(d->direct_output[i]);
+        }
+        if (structural) {
+            if (fo.empty()) fo.push_back(0);
+            CK(cudaMalloc(&s->dev_log1mp, l1mp.size() * 8));
+            CK(cudaMalloc(&s->dev_flip_begin, fb.size() * 4));
+            CK(cudaMalloc(&s->dev_flip_out, fo.size() * 4));
+            CK(cudaMemcpy(s->dev_log1mp, l1mp.data(), l1mp.size() * 8, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(s->dev_flip_begin, fb.data(), fb.size() * 4, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(s->dev_flip_out, fo.data(), fo.size() * 4, cudaMemcpyHostToDevice));
+        }
+    }
 
     // ---- components and chain tensors
     validate_csr("comp_out_begin", d->comp_out_begin, d->num_components, SIZE_MAX);
@@ -1231,12 +1297,15 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         ma.dict = reinterpret_cast<const uint4 *>(b + o_mdict);
         ma.tensor_dict_begin = reinterpret_cast<const uint32_t *>(b + o_mtdb);
         ma.max_dict = std::max<uint32_t>(1, MH.max_dict);
+        ma.stack_depth = std::max<uint32_t>(1, MH.max_depth);
         ma.comp_outputs = m.comp_outputs;
         ma.eval_tensor = -1;
         ma.n_comps = static_cast<uint32_t>(MH.comps.size());
         for (size_t i = 0; i < MH.comps.size(); i++) ma.comps[i] = MH.comps[i];
         s->mono_tensor = MH.tensor_index;
-        s->mono_smem = mono_smem_bytes(ma.n_planes, ma.max_dict);
+        if (const char *e = std::getenv("ZXS_MONO_WORDS")) s->mono_nw = std::atoi(e) == 1 ? 1 : 2;
+        if (mono_smem_bytes(ma.n_planes, ma.max_dict, s->mono_nw, ma.stack_depth) > 227 * 1024) s->mono_nw = 1;
+        s->mono_smem = mono_smem_bytes(ma.n_planes, ma.max_dict, s->mono_nw, ma.stack_depth);
     }
     s->info.num_mono_components = uint32_t(MH.comps.size());
     s->info.num_mono_records = MH.records;
@@ -1300,9 +1369,9 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         if (s->heavy_blocks_per_sm < 1) fail(ZXS_UNSUPPORTED, "heavy kernel does not fit on an SM");
     }
     if (s->has_mono) {
-        const void *mk = reinterpret_cast<const void *>(&zxs_dev::mono_kernel);
+        const void *mk = mono_kernel_ptr(s->mono_nw);
         CK(cudaFuncSetAttribute(mk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->mono_smem)));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->mono_blocks_per_sm, mk, zxs_dev::kMonoWarps * 32,
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->mono_blocks_per_sm, mk, mono_warps(s->mono_nw) * 32,
                                                          s->mono_smem));
         if (s->mono_blocks_per_sm < 1) fail(ZXS_UNSUPPORTED, "mono kernel does not fit on an SM");
     }
@@ -1329,19 +1398,18 @@ void launch_mono(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *f
     h.eval_tensor = eval_tensor;
     h.eval_out = eval_out;
     if (eval_tensor >= 0) h.f_width = std::min(f_width, h.all_plane);  // injected params; forms use < W
-    const uint64_t per_cta = uint64_t(zxs_dev::kMonoWarps) * 1024;
+    const int nw = s->mono_nw;
+    const uint64_t per_cta = uint64_t(mono_warps(nw)) * 1024 * nw;
     h.n_cta_tiles = (a.shots + per_cta - 1) / per_cta;
     if (h.n_cta_tiles == 0) return;
     h.scratch = s->mono_scratch_get(size_t(2) * h.n_cta_tiles * per_cta * 8);
-    const size_t smem = mono_smem_bytes(h.n_planes, h.max_dict);
+    const size_t smem = mono_smem_bytes(h.n_planes, h.max_dict, nw, h.stack_depth);
     if (smem > s->mono_smem) {
-        CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(&zxs_dev::mono_kernel),
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        CK(cudaFuncSetAttribute(mono_kernel_ptr(nw), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     }
     const unsigned grid = unsigned(std::min<uint64_t>(h.n_cta_tiles, uint64_t(s->sm_count) * std::max(1, s->mono_blocks_per_sm)));
     void *args[] = {&h};
-    CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::mono_kernel), dim3(grid),
-                        dim3(zxs_dev::kMonoWarps * 32), args, smem, st));
+    CK(cudaLaunchKernel(mono_kernel_ptr(nw), dim3(grid), dim3(mono_warps(nw) * 32), args, smem, st));
 }
 
 void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
@@ -1427,6 +1495,38 @@ cudaStream_t host_stream(zxs_sampler *s, void *stream) {
     return stream ? reinterpret_cast<cudaStream_t>(stream) : s->stream;
 }
 
+bool sparse_eligible(const zxs_sampler *s, const zxs_sample_options *opts) {
+    const bool force_dense = opts ? opts->force_dense != 0 : false;
+    const double threshold = opts ? opts->sparse_threshold : 8.0;
+    return !force_dense && s->sparse_structural && s->sparse_expected_flips < threshold;  // sampler.cpp:104-117
+}
+
+// The sparse geometric record of shots [0, shots) into device columns
+// [num_outputs][words] (sampler.cpp:130-147, 214-255).
+void sparse_record_device(zxs_sampler *s, uint64_t seed, uint64_t shots, unsigned long long *cols, cudaStream_t st) {
+    if (shots >= (uint64_t(1) << 40)) fail(ZXS_UNSUPPORTED, "sparse path limited to 2^40 shots");
+    const uint64_t words = (shots + 63) / 64;
+    const uint32_t nout = s->m.num_outputs;
+    CK(cudaMemsetAsync(cols, 0, size_t(words) * nout * 8, st));
+    // constant part: all-ones words, tail bits included (the sparse branch
+    // returns before sample_outputs zeroes tails, sampler.cpp:131-146)
+    for (uint32_t o : s->const_one_outputs) CK(cudaMemsetAsync(cols + size_t(o) * words, 0xff, words * 8, st));
+    zxs_dev::SparseArgs a;
+    a.seed = seed;
+    a.shots = shots;
+    a.words = words;
+    a.num_mech = s->info.num_mechanisms;
+    a.log1mp = s->dev_log1mp;
+    a.flip_begin = s->dev_flip_begin;
+    a.flip_out = s->dev_flip_out;
+    a.cols = cols;
+    if (a.num_mech) {
+        zxs_dev::sparse_kernel<<<a.num_mech, zxs_dev::kSparseThreads, 0, st>>>(a);
+        CK(cudaGetLastError());
+    }
+}
+
+
 }  // namespace
 
 extern "C" {
@@ -1472,6 +1572,9 @@ void zxs_sampler_destroy(zxs_sampler *s) {
     if (s->dev_err) cudaFree(s->dev_err);
     if (s->scratch) cudaFree(s->scratch);
     if (s->heavy_scratch) cudaFree(s->heavy_scratch);
+    if (s->dev_log1mp) cudaFree(s->dev_log1mp);
+    if (s->dev_flip_begin) cudaFree(s->dev_flip_begin);
+    if (s->dev_flip_out) cudaFree(s->dev_flip_out);
     if (s->mono_scratch) cudaFree(s->mono_scratch);
     for (auto &t : s->timed) {
         cudaEventDestroy(t.second.first);
@@ -1547,6 +1650,33 @@ zxs_status zxs_kernel_times(zxs_sampler *s, double *ms, uint64_t *launches) {
             ms[t.first] += e;
             launches[t.first]++;
         }
+    });
+}
+
+zxs_status zxs_sparse_eligible(const zxs_sampler *s, const zxs_sample_options *opts, int *eligible) {
+    return guarded([&] {
+        if (!s || !eligible) fail(ZXS_INVALID_ARGUMENT, "null argument");
+        *eligible = sparse_eligible(s, opts) ? 1 : 0;
+    });
+}
+
+zxs_status zxs_sample_opts(zxs_sampler *s, uint32_t expected_mode, uint64_t seed, uint64_t shots,
+                           const zxs_sample_options *opts, uint64_t *host_columns, void *stream) {
+    if (!s || !sparse_eligible(s, opts)) return zxs_sample(s, expected_mode, seed, 0, shots, host_columns, stream);
+    return guarded([&] {
+        check_mode(s, expected_mode);
+        if (shots == 0) return;
+        if (!host_columns) fail(ZXS_INVALID_ARGUMENT, "null output");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard g(s->device);
+        cudaStream_t st = host_stream(s, stream);
+        const uint64_t words = (shots + 63) / 64;
+        const uint32_t nout = s->m.num_outputs;
+        auto *cols = reinterpret_cast<unsigned long long *>(
+            s->scratch_get(size_t(words) * std::max<uint32_t>(nout, 1) * 8));
+        sparse_record_device(s, seed, shots, cols, st);
+        CK(cudaMemcpyAsync(host_columns, cols, size_t(words) * nout * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
     });
 }
 
@@ -1704,8 +1834,8 @@ zxs_status zxs_encode_shots_device(const uint64_t *dev_columns, uint64_t ld_word
 // encoded bytes copied to the host on a second stream while the next chunk
 // is sampled. (zxsim.cpp:142-163: write_output(encode_shots(sample_*(...))).)
 zxs_status zxs_sample_encoded(zxs_sampler *s, uint32_t expected_mode, uint64_t seed, uint64_t first_shot,
-                              uint64_t shots, uint32_t format, uint32_t first_output, uint32_t output_count,
-                              uint8_t *host_out, void *stream) {
+                              uint64_t shots, const zxs_sample_options *opts, uint32_t format, uint32_t first_output,
+                              uint32_t output_count, uint8_t *host_out, void *stream) {
     return guarded([&] {
         if (!s) fail(ZXS_INVALID_ARGUMENT, "null sampler");
         check_mode(s, expected_mode);
@@ -1717,6 +1847,19 @@ zxs_status zxs_sample_encoded(zxs_sampler *s, uint32_t expected_mode, uint64_t s
         std::lock_guard<std::mutex> lk(s->mu);
         DeviceGuard g(s->device);
         cudaStream_t st = host_stream(s, stream);
+        if (first_shot == 0 && sparse_eligible(s, opts)) {  // the reference's sparse record, encoded on device
+            const uint64_t words = (shots + 63) / 64;
+            auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+            const size_t cbytes = al(size_t(words) * std::max<uint32_t>(nout, 1) * 8);
+            char *base = s->scratch_get(cbytes + al(size_t(shots * rb)));
+            auto *cols = reinterpret_cast<unsigned long long *>(base);
+            sparse_record_device(s, seed, shots, cols, st);
+            launch_encode(reinterpret_cast<const uint32_t *>(cols), 2 * words, first_output, width, shots, format,
+                          reinterpret_cast<uint8_t *>(base + cbytes), st);
+            CK(cudaMemcpyAsync(host_out, base + cbytes, size_t(shots * rb), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            return;
+        }
         // chunk: multiple of 64 shots, ~64 MiB of encoded output per buffer
         uint64_t chunk = std::max<uint64_t>(64, ((uint64_t(64) << 20) / rb) & ~uint64_t(63));
         chunk = std::min<uint64_t>(chunk, (shots + 63) & ~uint64_t(63));

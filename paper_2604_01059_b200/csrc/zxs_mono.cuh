@@ -42,8 +42,21 @@
 
 namespace zxs_dev {
 
-constexpr int kMonoWarps = 16;               // warps per CTA (16384 shots per CTA tile), one CTA per SM
-constexpr uint32_t kMonoChunkWords = 4096;   // 16 KiB per chunk buffer
+// Words per lane NW: 1 (32 shots per lane, 16 warps per SM) or 2 (64 shots per
+// lane via 64-bit plane loads, 12 warps per SM: half the issue slots per shot
+// for the parity work at 128 accumulator registers).
+template <int NW>
+struct MonoCfg;
+template <>
+struct MonoCfg<1> {
+    static constexpr int kWarps = 16;
+};
+template <>
+struct MonoCfg<2> {
+    static constexpr int kWarps = 12;
+};
+constexpr int kMonoWarps = 16;               // upper bound of MonoCfg<NW>::kWarps (host sizing)
+constexpr uint32_t kMonoChunkWords = 2048;   // 8 KiB per chunk buffer
 constexpr uint32_t kMonoNoForm = 0xfffu;     // "no form" (parity 0) in the 12-bit form fields
 constexpr int kMaxMonoComps = 8;
 constexpr uint32_t kMonoMaxDepth = 8;        // levels of the shared-prefix term tree
@@ -82,6 +95,7 @@ struct MonoArgs {
     const uint4 *dict;                // form dictionaries, one per tensor
     const uint32_t *tensor_dict_begin;  // [mono tensors + 1]
     uint32_t max_dict;                // largest per-tensor dictionary (entries staged in smem)
+    uint32_t stack_depth;             // levels of (Z, J0, J1) kept per lane (deepest node + 1)
     const uint32_t *comp_outputs;
     // eval seam: evaluate one tensor and store the values (no chain)
     int eval_tensor;                  // -1: sample; else index into tensor_chunk_begin
@@ -90,56 +104,111 @@ struct MonoArgs {
     HeavyComp comps[kMaxMonoComps];
 };
 
-// Parity word of dictionary form f for the lane's 32 shots: XOR of the lane's
+// Bit-sliced words of NW x 32 shots.
+template <int NW>
+struct BW {
+    uint32_t w[NW];
+};
+template <int NW>
+__device__ __forceinline__ BW<NW> bw_zero() {
+    BW<NW> r;
+#pragma unroll
+    for (int i = 0; i < NW; i++) r.w[i] = 0u;
+    return r;
+}
+#define ZXS_BW_OP(NAME, EXPR)                                                   \
+    template <int NW>                                                           \
+    __device__ __forceinline__ BW<NW> NAME(const BW<NW> &a, const BW<NW> &b) { \
+        BW<NW> r;                                                               \
+        _Pragma("unroll") for (int i = 0; i < NW; i++) r.w[i] = (EXPR);        \
+        return r;                                                               \
+    }
+ZXS_BW_OP(bw_xor, a.w[i] ^ b.w[i])
+ZXS_BW_OP(bw_and, a.w[i] & b.w[i])
+ZXS_BW_OP(bw_or, a.w[i] | b.w[i])
+ZXS_BW_OP(bw_andn, ~a.w[i] & b.w[i])  // ~a & b
+#undef ZXS_BW_OP
+template <int NW>
+__device__ __forceinline__ BW<NW> bw_not(const BW<NW> &a) {
+    BW<NW> r;
+#pragma unroll
+    for (int i = 0; i < NW; i++) r.w[i] = ~a.w[i];
+    return r;
+}
+
+// One plane of the lane: plane p of lane l at byte (p * 32 + l) * 4 * NW.
+template <int NW>
+__device__ __forceinline__ BW<NW> mono_plane(const char *lb, uint32_t p) {
+    if constexpr (NW == 1) {
+        BW<1> r;
+        r.w[0] = *reinterpret_cast<const uint32_t *>(lb + (p << 7));
+        return r;
+    } else {
+        const uint2 v = *reinterpret_cast<const uint2 *>(lb + (p << 8));
+        BW<2> r;
+        r.w[0] = v.x;
+        r.w[1] = v.y;
+        return r;
+    }
+}
+
+// Parity words of dictionary form f for the lane's shots: XOR of the lane's
 // parameter planes the entry lists. Entry layout (16 B): byte 0 = size class
 // (0: 2, 1: 4, 2: 8, 3: 15 selector slots) | 0x80 if the list continues in
-// the next entry; bytes 1..15 = plane indices p (plane p of lane l at byte
-// p * 128 + 4 l), unused slots pointing at the all-zero plane. Lists longer
-// than half the tensor's width are stored complemented against the ALL
-// plane. Each size class is straight-line code: every load of the entry is
-// issued before the XOR tree consumes them (a selector costs a byte extract,
-// an address IMAD, one LDS and half a 3-input XOR), and the warp takes one
-// uniform branch per entry.
-__device__ __forceinline__ uint32_t mono_entry(const uint4 e, const char *lb) {
-#define ZXS_SEL(word, k) (*reinterpret_cast<const uint32_t *>(lb + (__byte_perm((word), 0u, 0x4440u + (k)) << 7)))
+// the next entry; bytes 1..15 = plane indices, unused slots naming the
+// all-zero plane. Lists longer than half the tensor's width are stored
+// complemented against the ALL plane. Each size class is straight-line code:
+// every load of the entry is issued before the XOR tree consumes them (a
+// selector costs a byte extract, an address IMAD, one LDS and half a 3-input
+// XOR per word), and the warp takes one uniform branch per entry.
+template <int NW>
+__device__ __forceinline__ BW<NW> mono_entry(const uint4 e, const char *lb) {
+#define ZXS_SEL(word, k) mono_plane<NW>(lb, __byte_perm((word), 0u, 0x4440u + (k)))
+#define X2(a, b) bw_xor<NW>(a, b)
     switch (e.x & 3u) {
         case 0:
-            return ZXS_SEL(e.x, 1) ^ ZXS_SEL(e.x, 2);
+            return X2(ZXS_SEL(e.x, 1), ZXS_SEL(e.x, 2));
         case 1: {
-            const uint32_t a = ZXS_SEL(e.x, 1), b = ZXS_SEL(e.x, 2), c = ZXS_SEL(e.x, 3), d = ZXS_SEL(e.y, 0);
-            return (a ^ b) ^ (c ^ d);
+            const BW<NW> a = ZXS_SEL(e.x, 1), b = ZXS_SEL(e.x, 2), c = ZXS_SEL(e.x, 3), d = ZXS_SEL(e.y, 0);
+            return X2(X2(a, b), X2(c, d));
         }
         case 2: {
-            const uint32_t a = ZXS_SEL(e.x, 1), b = ZXS_SEL(e.x, 2), c = ZXS_SEL(e.x, 3), d = ZXS_SEL(e.y, 0);
-            const uint32_t f = ZXS_SEL(e.y, 1), g = ZXS_SEL(e.y, 2), k = ZXS_SEL(e.y, 3), l = ZXS_SEL(e.z, 0);
-            return ((a ^ b) ^ (c ^ d)) ^ ((f ^ g) ^ (k ^ l));
+            const BW<NW> a = ZXS_SEL(e.x, 1), b = ZXS_SEL(e.x, 2), c = ZXS_SEL(e.x, 3), d = ZXS_SEL(e.y, 0);
+            const BW<NW> f = ZXS_SEL(e.y, 1), g = ZXS_SEL(e.y, 2), k = ZXS_SEL(e.y, 3), l = ZXS_SEL(e.z, 0);
+            return X2(X2(X2(a, b), X2(c, d)), X2(X2(f, g), X2(k, l)));
         }
         default: {
-            const uint32_t a = ZXS_SEL(e.x, 1), b = ZXS_SEL(e.x, 2), c = ZXS_SEL(e.x, 3), d = ZXS_SEL(e.y, 0);
-            const uint32_t f = ZXS_SEL(e.y, 1), g = ZXS_SEL(e.y, 2), k = ZXS_SEL(e.y, 3), l = ZXS_SEL(e.z, 0);
-            const uint32_t m = ZXS_SEL(e.z, 1), n = ZXS_SEL(e.z, 2), o = ZXS_SEL(e.z, 3), p = ZXS_SEL(e.w, 0);
-            const uint32_t q = ZXS_SEL(e.w, 1), r = ZXS_SEL(e.w, 2), t = ZXS_SEL(e.w, 3);
-            return (((a ^ b) ^ (c ^ d)) ^ ((f ^ g) ^ (k ^ l))) ^ (((m ^ n) ^ (o ^ p)) ^ ((q ^ r) ^ t));
+            const BW<NW> a = ZXS_SEL(e.x, 1), b = ZXS_SEL(e.x, 2), c = ZXS_SEL(e.x, 3), d = ZXS_SEL(e.y, 0);
+            const BW<NW> f = ZXS_SEL(e.y, 1), g = ZXS_SEL(e.y, 2), k = ZXS_SEL(e.y, 3), l = ZXS_SEL(e.z, 0);
+            const BW<NW> m = ZXS_SEL(e.z, 1), n = ZXS_SEL(e.z, 2), o = ZXS_SEL(e.z, 3), p = ZXS_SEL(e.w, 0);
+            const BW<NW> q = ZXS_SEL(e.w, 1), r = ZXS_SEL(e.w, 2), t = ZXS_SEL(e.w, 3);
+            return X2(X2(X2(X2(a, b), X2(c, d)), X2(X2(f, g), X2(k, l))), X2(X2(X2(m, n), X2(o, p)), X2(X2(q, r), t)));
         }
     }
+#undef X2
 #undef ZXS_SEL
 }
 
-__device__ __forceinline__ uint32_t mono_form(const uint4 *sd, uint32_t f, const char *lb) {
+template <int NW>
+__device__ __forceinline__ BW<NW> mono_form(const uint4 *sd, uint32_t f, const char *lb) {
     uint4 e = sd[f];
-    uint32_t acc = mono_entry(e, lb);
+    BW<NW> acc = mono_entry<NW>(e, lb);
     while (e.x & 0x80u) {
         e = sd[++f];
-        acc ^= mono_entry(e, lb);
+        acc = bw_xor<NW>(acc, mono_entry<NW>(e, lb));
     }
     return acc;
 }
 
 // J += c * x (mod 4) on the bit planes (J0, J1), c in 0..3.
-__device__ __forceinline__ void j_add(uint32_t &j0, uint32_t &j1, uint32_t x, uint32_t c) {
-    const uint32_t xl = (c & 1u) ? x : 0u;
-    j1 ^= (j0 & xl) ^ ((c & 2u) ? x : 0u);
-    j0 ^= xl;
+template <int NW>
+__device__ __forceinline__ void j_add(BW<NW> &j0, BW<NW> &j1, const BW<NW> &x, uint32_t c) {
+#pragma unroll
+    for (int i = 0; i < NW; i++) {
+        const uint32_t xl = (c & 1u) ? x.w[i] : 0u;
+        j1.w[i] ^= (j0.w[i] & xl) ^ ((c & 2u) ? x.w[i] : 0u);
+        j0.w[i] ^= xl;
+    }
 }
 
 // Record runs of one kind, forms of four records formed together (independent
@@ -148,38 +217,44 @@ __device__ __forceinline__ void j_add(uint32_t &j0, uint32_t &j1, uint32_t x, ui
     {                                                                                    \
         uint32_t i_ = 0;                                                                 \
         for (; i_ + 4 <= (N); i_ += 4) {                                                 \
-            const uint32_t x0 = mono_form(sd, w[q + i_] & 0xfffu, pl);                   \
-            const uint32_t x1 = mono_form(sd, w[q + i_ + 1] & 0xfffu, pl);               \
-            const uint32_t x2 = mono_form(sd, w[q + i_ + 2] & 0xfffu, pl);               \
-            const uint32_t x3 = mono_form(sd, w[q + i_ + 3] & 0xfffu, pl);               \
+            const BW<NW> x0 = mono_form<NW>(sd, w[q + i_] & 0xfffu, pl);                 \
+            const BW<NW> x1 = mono_form<NW>(sd, w[q + i_ + 1] & 0xfffu, pl);             \
+            const BW<NW> x2 = mono_form<NW>(sd, w[q + i_ + 2] & 0xfffu, pl);             \
+            const BW<NW> x3 = mono_form<NW>(sd, w[q + i_ + 3] & 0xfffu, pl);             \
             OP(x0);                                                                      \
             OP(x1);                                                                      \
             OP(x2);                                                                      \
             OP(x3);                                                                      \
         }                                                                                \
         for (; i_ < (N); i_++) {                                                         \
-            const uint32_t x0 = mono_form(sd, w[q + i_] & 0xfffu, pl);                   \
+            const BW<NW> x0 = mono_form<NW>(sd, w[q + i_] & 0xfffu, pl);                 \
             OP(x0);                                                                      \
         }                                                                                \
         q += (N);                                                                        \
     }
-#define ZXS_OP_ADD(x) { j1 ^= j0 & (x); j0 ^= (x); }
-#define ZXS_OP_SUB(x) { j1 ^= ~j0 & (x); j0 ^= (x); }
-#define ZXS_OP_ADD2(x) { j1 ^= (x); }
-#define ZXS_OP_Z(x) { z |= (x); }
-#define ZXS_OP_ZN(x) { z |= ~(x); }
+#define ZXS_OP_ADD(x) { j1 = bw_xor<NW>(j1, bw_and<NW>(j0, x)); j0 = bw_xor<NW>(j0, x); }
+#define ZXS_OP_SUB(x) { j1 = bw_xor<NW>(j1, bw_andn<NW>(j0, x)); j0 = bw_xor<NW>(j0, x); }
+#define ZXS_OP_ADD2(x) { j1 = bw_xor<NW>(j1, x); }
+#define ZXS_OP_Z(x) { z = bw_or<NW>(z, x); }
+#define ZXS_OP_ZN(x) { z = bw_or<NW>(z, bw_not<NW>(x)); }
 
-__global__ void __launch_bounds__(kMonoWarps * 32, 1) mono_kernel(const __grid_constant__ MonoArgs h) {
+template <int NW>
+__global__ void __launch_bounds__(MonoCfg<NW>::kWarps * 32, 1) mono_kernel(const __grid_constant__ MonoArgs h) {
+    constexpr int kW = MonoCfg<NW>::kWarps;
+    constexpr uint32_t kLaneShots = 32 * NW;
+    constexpr uint64_t kWarpShots = 32ull * kLaneShots;
     extern __shared__ __align__(128) uint8_t msm[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(msm);
     uint32_t *buf0 = reinterpret_cast<uint32_t *>(msm + 128);
     uint4 *sd = reinterpret_cast<uint4 *>(buf0 + 2 * kMonoChunkWords);  // the current tensor's dictionary
-    uint32_t *stack_all = reinterpret_cast<uint32_t *>(sd + h.max_dict);  // [warp][depth][z, j0, j1][lane]
-    uint32_t *planes_all = stack_all + kMonoWarps * kMonoMaxDepth * 3 * 32;
+    // per warp: stack [depth][z, j0, j1][lane][NW], planes [p][lane][NW]
+    uint32_t *stack_all = reinterpret_cast<uint32_t *>(sd + h.max_dict);
+    uint32_t *planes_all = stack_all + kW * h.stack_depth * 3 * 32 * NW;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    uint32_t *stk = stack_all + warp * kMonoMaxDepth * 3 * 32 + lane;
-    uint32_t *planes = planes_all + warp * h.n_planes * 32;  // [p][lane]
-    const char *pl = reinterpret_cast<const char *>(planes + lane);
+    BW<NW> *stk = reinterpret_cast<BW<NW> *>(stack_all + warp * h.stack_depth * 3 * 32 * NW) + lane;
+    uint32_t *planes = planes_all + warp * h.n_planes * 32 * NW;  // [p][lane][NW]
+    BW<NW> *myplanes = reinterpret_cast<BW<NW> *>(planes) + lane;  // plane p at myplanes[p * 32]
+    const char *pl = reinterpret_cast<const char *>(myplanes);
 
     // chunk uses per CTA tile: every tensor of every component (or the one eval tensor)
     uint32_t chunks_per_tile = 0;
@@ -226,13 +301,19 @@ __global__ void __launch_bounds__(kMonoWarps * 32, 1) mono_kernel(const __grid_c
     uint64_t use = 0;
 
     for (uint64_t ct = blockIdx.x; ct < h.n_cta_tiles; ct += gridDim.x) {
-        const uint64_t wrd = (ct * kMonoWarps + warp) * 32 + lane;  // the lane's 32-shot word
+        // the lane's NW consecutive 32-shot words: wrd .. wrd + NW - 1
+        const uint64_t wrd = ((ct * kW + warp) * 32 + lane) * NW;
         for (uint32_t p = 0; p < h.n_planes; p++) {
-            planes[p * 32 + lane] = (p < h.f_width && wrd < h.fcols_ld32) ? h.fcols[p * h.fcols_ld32 + wrd] : 0u;
+            BW<NW> v;
+#pragma unroll
+            for (int i = 0; i < NW; i++) {
+                v.w[i] = (p < h.f_width && wrd + i < h.fcols_ld32) ? h.fcols[p * h.fcols_ld32 + wrd + i] : 0u;
+            }
+            myplanes[p * 32] = v;
         }
         __syncwarp();
         double *prev_g = h.scratch + wrd * 32;
-        double *cur_g = h.scratch + (h.n_cta_tiles * kMonoWarps * 1024) + wrd * 32;
+        double *cur_g = h.scratch + (h.n_cta_tiles * kW * kWarpShots) + wrd * 32;
 
         const uint32_t ncomp = h.eval_tensor >= 0 ? 1u : h.n_comps;
         for (uint32_t hc = 0; hc < ncomp; hc++) {
@@ -242,10 +323,10 @@ __global__ void __launch_bounds__(kMonoWarps * 32, 1) mono_kernel(const __grid_c
                 const uint32_t t = h.eval_tensor >= 0 ? uint32_t(h.eval_tensor) : cd.first_tensor + pos;
                 // the ALL plane of this tensor (its sampled-bit planes are final up to pos)
                 {
-                    uint32_t all = 0;
+                    BW<NW> all = bw_zero<NW>();
                     const uint32_t W = min(h.tensor_width[t], h.all_plane);
-                    for (uint32_t p = 0; p < W; p++) all ^= planes[p * 32 + lane];
-                    planes[h.all_plane * 32 + lane] = all;
+                    for (uint32_t p = 0; p < W; p++) all = bw_xor<NW>(all, myplanes[p * 32]);
+                    myplanes[h.all_plane * 32] = all;
                 }
                 // stage the tensor's form dictionary (every warp is past the previous tensor)
                 {
@@ -253,9 +334,9 @@ __global__ void __launch_bounds__(kMonoWarps * 32, 1) mono_kernel(const __grid_c
                     for (uint32_t i = threadIdx.x; i < nd; i += blockDim.x) sd[i] = __ldg(h.dict + d0 + i);
                     __syncthreads();
                 }
-                double acc[32];
+                double acc[kLaneShots];
 #pragma unroll
-                for (int s = 0; s < 32; s++) acc[s] = 0.0;
+                for (int s = 0; s < int(kLaneShots); s++) acc[s] = 0.0;
                 for (uint32_t c = h.tensor_chunk_begin[t]; c < h.tensor_chunk_begin[t + 1]; c++, use++) {
                     const uint32_t b = uint32_t(use & 1);
                     mbar_wait(&bars[b], uint32_t((use >> 1) & 1));
@@ -276,9 +357,9 @@ __global__ void __launch_bounds__(kMonoWarps * 32, 1) mono_kernel(const __grid_c
                             q += 4;
                         }
                         // state of the parent (depth - 1), or the empty product at the root
-                        uint32_t z = 0, j0 = 0, j1 = 0;
+                        BW<NW> z = bw_zero<NW>(), j0 = bw_zero<NW>(), j1 = bw_zero<NW>();
                         if (depth) {
-                            const uint32_t *ps = stk + (depth - 1) * 96;
+                            const BW<NW> *ps = stk + (depth - 1) * 96;
                             z = ps[0];
                             j0 = ps[32];
                             j1 = ps[64];
@@ -292,29 +373,35 @@ __global__ void __launch_bounds__(kMonoWarps * 32, 1) mono_kernel(const __grid_c
                             const uint32_t r = w[q], gw = w[q + 1];
                             q += 2;
                             const uint32_t fa = r & 0xfffu, fb = (r >> 16) & 0xfffu;
-                            const uint32_t a = fa == kMonoNoForm ? 0u : mono_form(sd, fa, pl);
-                            const uint32_t bb = fb == kMonoNoForm ? 0u : mono_form(sd, fb, pl);
+                            const BW<NW> a = fa == kMonoNoForm ? bw_zero<NW>() : mono_form<NW>(sd, fa, pl);
+                            const BW<NW> bb = fb == kMonoNoForm ? bw_zero<NW>() : mono_form<NW>(sd, fb, pl);
                             const uint32_t zl = gw >> 6;
-                            z |= ((zl & 1u) ? (~a & ~bb) : 0u) | ((zl & 2u) ? (~a & bb) : 0u) |
-                                 ((zl & 4u) ? (a & ~bb) : 0u) | ((zl & 8u) ? (a & bb) : 0u);
-                            j_add(j0, j1, a, gw & 3u);
-                            j_add(j0, j1, bb, (gw >> 2) & 3u);
-                            j_add(j0, j1, a & bb, (gw >> 4) & 3u);
+#pragma unroll
+                            for (int i = 0; i < NW; i++) {
+                                z.w[i] |= ((zl & 1u) ? (~a.w[i] & ~bb.w[i]) : 0u) | ((zl & 2u) ? (~a.w[i] & bb.w[i]) : 0u) |
+                                          ((zl & 4u) ? (a.w[i] & ~bb.w[i]) : 0u) | ((zl & 8u) ? (a.w[i] & bb.w[i]) : 0u);
+                            }
+                            j_add<NW>(j0, j1, a, gw & 3u);
+                            j_add<NW>(j0, j1, bb, (gw >> 2) & 3u);
+                            j_add<NW>(j0, j1, bw_and<NW>(a, bb), (gw >> 4) & 3u);
                         }
                         if (!leaf) {
-                            uint32_t *ns = stk + depth * 96;
+                            BW<NW> *ns = stk + depth * 96;
                             ns[0] = z;
                             ns[32] = j0;
                             ns[64] = j1;
                             continue;
                         }
                         // epilogue: acc[s] += Re(c' i^J) for the non-zero shots, in term order
-                        const uint32_t neg = j0 ^ j1;
 #pragma unroll
-                        for (int s = 0; s < 32; s++) {
-                            const double v = ((j0 >> s) & 1u) ? im : re;
-                            const double sv = ((neg >> s) & 1u) ? -v : v;
-                            if (!((z >> s) & 1u)) acc[s] = __dadd_rn(acc[s], sv);
+                        for (int i = 0; i < NW; i++) {
+                            const uint32_t neg = j0.w[i] ^ j1.w[i];
+#pragma unroll
+                            for (int s = 0; s < 32; s++) {
+                                const double v = ((j0.w[i] >> s) & 1u) ? im : re;
+                                const double sv = ((neg >> s) & 1u) ? -v : v;
+                                if (!((z.w[i] >> s) & 1u)) acc[i * 32 + s] = __dadd_rn(acc[i * 32 + s], sv);
+                            }
                         }
                     }
                     __syncthreads();  // buffer b fully consumed by every warp
@@ -322,23 +409,23 @@ __global__ void __launch_bounds__(kMonoWarps * 32, 1) mono_kernel(const __grid_c
                 }
                 if (h.eval_tensor >= 0) {
 #pragma unroll
-                    for (int s = 0; s < 32; s++) {
+                    for (int s = 0; s < int(kLaneShots); s++) {
                         if (wrd * 32 + s < h.shots) h.eval_out[wrd * 32 + s] = acc[s];
                     }
                     continue;
                 }
                 if (pos == 0) {
 #pragma unroll
-                    for (int s = 0; s < 32; s++) prev_g[s] = acc[s];
+                    for (int s = 0; s < int(kLaneShots); s++) prev_g[s] = acc[s];
                     continue;
                 }
 #pragma unroll
-                for (int s = 0; s < 32; s++) cur_g[s] = acc[s];
+                for (int s = 0; s < int(kLaneShots); s++) cur_g[s] = acc[s];
                 // autoregressive draw of output pos-1 (sampler.cpp:84-99), one shot at a time
                 const uint32_t j = pos - 1;
                 const uint32_t stream = 0x80000000u ^ (cd.ci << 12) ^ j;  // sampler.cpp:37-39
-                uint32_t word = 0;
-                for (uint32_t s = 0; s < 32; s++) {
+                BW<NW> word = bw_zero<NW>();
+                for (uint32_t s = 0; s < kLaneShots; s++) {
                     const uint64_t local = wrd * 32 + s;
                     const bool valid = local < h.shots;
                     const double cur = cur_g[s], pv = prev_g[s];
@@ -358,20 +445,29 @@ __global__ void __launch_bounds__(kMonoWarps * 32, 1) mono_kernel(const __grid_c
                     }
                     const bool bit = !(u < cl) && valid;
                     prev_g[s] = bit ? __dsub_rn(pv, cur) : cur;
-                    word |= uint32_t(bit) << s;
+#pragma unroll
+                    for (int i = 0; i < NW; i++) {
+                        if ((s >> 5) == uint32_t(i)) word.w[i] |= uint32_t(bit) << (s & 31);
+                    }
                 }
-                planes[(h.f_width + j) * 32 + lane] = word;
+                myplanes[(h.f_width + j) * 32] = word;
                 const uint32_t o = h.comp_outputs[cd.out_begin + j];
-                if (h.out32 && wrd < h.out_ld32) h.out32[o * h.out_ld32 + wrd] = word;
+#pragma unroll
+                for (int i = 0; i < NW; i++) {
+                    if (h.out32 && wrd + i < h.out_ld32) h.out32[o * h.out_ld32 + wrd + i] = word.w[i];
+                }
                 if (h.counts) {
-                    const uint32_t ones = __reduce_add_sync(kFull, __popc(word));
+                    uint32_t ones = 0;
+#pragma unroll
+                    for (int i = 0; i < NW; i++) ones += __popc(word.w[i]);
+                    ones = __reduce_add_sync(kFull, ones);
                     if (lane == 0 && ones) atomicAdd(&h.counts[o], (unsigned long long)ones);
                 }
                 __syncwarp();
             }
             // reset this component's sampled-bit planes for the next component
             if (h.eval_tensor < 0) {
-                for (uint32_t j = 0; j < cd.n_out; j++) planes[(h.f_width + j) * 32 + lane] = 0;
+                for (uint32_t j = 0; j < cd.n_out; j++) myplanes[(h.f_width + j) * 32] = bw_zero<NW>();
             }
             __syncwarp();
         }

@@ -37,9 +37,11 @@ _u8p = ctypes.POINTER(ctypes.c_uint8)
 
 @dataclass
 class SamplerOptions:
-    """sampler.hpp:32-38. batch_size/threads/sparse_threshold/force_dense are
-    accepted for signature compatibility; the device always runs the dense
-    path (bit-identical to the reference's dense path for any batch split)."""
+    """sampler.hpp:32-38. seed, sparse_threshold and force_dense select the bits
+    exactly as in the reference (dense path, or the sparse geometric path for
+    pure-Clifford deterministic single-mechanism models, sampler.cpp:104-147);
+    batch_size and threads do not change them and are accepted for signature
+    compatibility."""
 
     seed: int = 0
     batch_size: int = 65536
@@ -158,9 +160,22 @@ def _sample(cs: CompiledSampler, mode: int, shots: int, opt: SamplerOptions, fir
         # same message and class as sampler.cpp:308-309 / 316-317
         raise ValueError("sampler was compiled in measurement mode" if cs.mode == MODE_MEASUREMENTS
                          else "sampler was compiled in detector mode")
-    if shots:
-        cs.sample_into(mode, opt.seed, first_shot, shots, cols)
+    if shots and first_shot == 0:
+        o = _native.SampleOptions(1 if opt.force_dense else 0, 0, float(opt.sparse_threshold))
+        _native.check(_native.lib().zxs_sample_opts(cs.handle, mode, opt.seed, shots, ctypes.byref(o),
+                                                    cols.ctypes.data_as(_u64p), None))
+    elif shots:
+        cs.sample_into(mode, opt.seed, first_shot, shots, cols)  # dense path, any global shot range
     return SampleRecord(shots=shots, width=cs.num_outputs, columns=cols)
+
+
+def sparse_eligible(cs: CompiledSampler, opt: SamplerOptions | None = None) -> bool:
+    """sampler.cpp:104-117: would sample_* take the sparse geometric path?"""
+    opt = opt or SamplerOptions()
+    o = _native.SampleOptions(1 if opt.force_dense else 0, 0, float(opt.sparse_threshold))
+    e = ctypes.c_int()
+    _native.check(_native.lib().zxs_sparse_eligible(cs.handle, ctypes.byref(o), ctypes.byref(e)))
+    return bool(e.value)
 
 
 def sample_detectors(cs: CompiledSampler, shots: int, opt: SamplerOptions | None = None,
@@ -261,8 +276,9 @@ def sample_encoded(cs: CompiledSampler, shots: int, opt: SamplerOptions | None =
     mode = cs.mode if mode is None else mode
     n = _native.lib().zxs_encoded_bytes(cs.num_outputs, shots, first_output, output_count, fmt)
     out = np.zeros(max(n, 1), np.uint8)
-    _native.check(_native.lib().zxs_sample_encoded(cs.handle, mode, opt.seed, first_shot, shots, fmt, first_output,
-                                                   output_count, out.ctypes.data_as(_u8p), None))
+    o = _native.SampleOptions(1 if opt.force_dense else 0, 0, float(opt.sparse_threshold))
+    _native.check(_native.lib().zxs_sample_encoded(cs.handle, mode, opt.seed, first_shot, shots, ctypes.byref(o), fmt,
+                                                   first_output, output_count, out.ctypes.data_as(_u8p), None))
     return out[:n].tobytes()
 
 

@@ -125,6 +125,7 @@ class ModelDesc(ctypes.Structure):
         ("factor_u_begin", _u64p), ("factor_u_bits", _u32p),
         ("factor_v_begin", _u64p), ("factor_v_bits", _u32p),
         ("num_h_tables", ctypes.c_uint32), ("h_table", _dp), ("h_alpha", _dp), ("h_beta", _dp),
+        ("flags", ctypes.c_uint32),
     ]
 
 
@@ -136,8 +137,9 @@ def make_desc(arrays: dict) -> ModelDesc:
     """Builds the C struct over `arrays` (which must outlive the struct's use)."""
     d = ModelDesc()
     hdr = arrays["header"]
-    d.abi_version = 1
+    d.abi_version = 2
     d.mode, d.num_detectors, d.num_observables, d.num_outputs, d.f_width = (int(x) for x in hdr[:5])
+    d.flags = int(hdr[5]) if hdr.size > 5 else 0  # ZXS_MODEL_* (absent in older files)
     for name, dt in FIELDS[1:]:
         a = arrays[name]
         assert a.dtype == np.dtype(dt) and a.flags.c_contiguous, name

@@ -39,7 +39,7 @@ def model(name):
 
 
 def sample(cs, shots, seed, first_shot=0):
-    opt = zx.SamplerOptions(seed=seed)
+    opt = zx.SamplerOptions(seed=seed, force_dense=True)  # the goldens' options
     f = zx.sample_detectors if cs.mode == zx.MODE_DETECTORS else zx.sample_measurements
     return f(cs, shots, opt, first_shot=first_shot).columns
 

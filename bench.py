@@ -42,7 +42,7 @@ WORKLOADS = {
                          "d=7 rotated surface code Z-memory, 7 rounds, p=1e-3, count-only sweep", 1 << 24, True),
     "c3_cultivation_proxy": ("data/c3_cultivation_proxy.zxs.gz", 2,
                              "Steane-code cultivation proxy: T injection + 2 transversal T checks (chi=46656)",
-                             296 * 8192, False),
+                             148 * 24576, False),  # one mono_kernel CTA tile (12 warps x 2048 shots) per SM
 }
 DEFAULT_WORKLOAD = "c2_surface_d3_xmem_t"
 

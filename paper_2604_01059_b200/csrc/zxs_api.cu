@@ -598,7 +598,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             const size_t n = std::min<size_t>(15, sel.size() - i);
             uint8_t e[16];
             std::memset(e, int(all_plane + 1), 16);  // unused slots read the all-zero plane
-            const uint8_t cls = n <= 2 ? 0 : n <= 4 ? 1 : n <= 8 ? 2 : 3;
+            const uint8_t cls = n >= 15 ? 7 : uint8_t((std::max<size_t>(n, 1) - 1) / 2);  // 2c + 2 slots
             e[0] = uint8_t(cls | (i + 15 < sel.size() ? 0x80 : 0));
             for (size_t k = 0; k < n; k++) e[1 + k] = uint8_t(sel[i + k]);
             uint4 w;
@@ -609,7 +609,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
         uint32_t slots = 0;  // plane loads the device performs for this form
         for (size_t i = 0; i < sel.size() || i == 0; i += 15) {
             const size_t n = std::min<size_t>(15, sel.size() - i);
-            slots += n <= 2 ? 2 : n <= 4 ? 4 : n <= 8 ? 8 : 15;
+            slots += n >= 15 ? 15 : uint32_t(2 * ((std::max<size_t>(n, 1) - 1) / 2) + 2);
         }
         form_size[id] = slots;
         return id;

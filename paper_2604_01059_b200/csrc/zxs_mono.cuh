@@ -154,7 +154,7 @@ __device__ __forceinline__ BW<NW> mono_plane(const char *lb, uint32_t p) {
 
 // Parity words of dictionary form f for the lane's shots: XOR of the lane's
 // parameter planes the entry lists. Entry layout (16 B): byte 0 = size class
-// (0: 2, 1: 4, 2: 8, 3: 15 selector slots) | 0x80 if the list continues in
+// c (2c + 2 selector slots, 15 for c = 7) | 0x80 if the list continues in
 // the next entry; bytes 1..15 = plane indices, unused slots naming the
 // all-zero plane. Lists longer than half the tensor's width are stored
 // complemented against the ALL plane. Each size class is straight-line code:
@@ -163,30 +163,49 @@ __device__ __forceinline__ BW<NW> mono_plane(const char *lb, uint32_t p) {
 // XOR per word), and the warp takes one uniform branch per entry.
 template <int NW>
 __device__ __forceinline__ BW<NW> mono_entry(const uint4 e, const char *lb) {
-#define ZXS_SEL(word, k) mono_plane<NW>(lb, __byte_perm((word), 0u, 0x4440u + (k)))
-#define X2(a, b) bw_xor<NW>(a, b)
-    switch (e.x & 3u) {
-        case 0:
-            return X2(ZXS_SEL(e.x, 1), ZXS_SEL(e.x, 2));
+    // selector k (1..15) lives in byte k of the entry
+#define S(k) mono_plane<NW>(lb, __byte_perm((k) < 4 ? e.x : (k) < 8 ? e.y : (k) < 12 ? e.z : e.w, 0u, 0x4440u + ((k) & 3)))
+#define X(a, b) bw_xor<NW>(a, b)
+    switch (e.x & 7u) {  // slots: 2, 4, 6, 8, 10, 12, 14, 15
+        case 0: {
+            const BW<NW> a = S(1), b = S(2);
+            return X(a, b);
+        }
         case 1: {
-            const BW<NW> a = ZXS_SEL(e.x, 1), b = ZXS_SEL(e.x, 2), c = ZXS_SEL(e.x, 3), d = ZXS_SEL(e.y, 0);
-            return X2(X2(a, b), X2(c, d));
+            const BW<NW> a = S(1), b = S(2), c = S(3), d = S(4);
+            return X(X(a, b), X(c, d));
         }
         case 2: {
-            const BW<NW> a = ZXS_SEL(e.x, 1), b = ZXS_SEL(e.x, 2), c = ZXS_SEL(e.x, 3), d = ZXS_SEL(e.y, 0);
-            const BW<NW> f = ZXS_SEL(e.y, 1), g = ZXS_SEL(e.y, 2), k = ZXS_SEL(e.y, 3), l = ZXS_SEL(e.z, 0);
-            return X2(X2(X2(a, b), X2(c, d)), X2(X2(f, g), X2(k, l)));
+            const BW<NW> a = S(1), b = S(2), c = S(3), d = S(4), f = S(5), g = S(6);
+            return X(X(X(a, b), X(c, d)), X(f, g));
+        }
+        case 3: {
+            const BW<NW> a = S(1), b = S(2), c = S(3), d = S(4), f = S(5), g = S(6), k = S(7), l = S(8);
+            return X(X(X(a, b), X(c, d)), X(X(f, g), X(k, l)));
+        }
+        case 4: {
+            const BW<NW> a = S(1), b = S(2), c = S(3), d = S(4), f = S(5), g = S(6), k = S(7), l = S(8);
+            const BW<NW> m = S(9), n = S(10);
+            return X(X(X(X(a, b), X(c, d)), X(X(f, g), X(k, l))), X(m, n));
+        }
+        case 5: {
+            const BW<NW> a = S(1), b = S(2), c = S(3), d = S(4), f = S(5), g = S(6), k = S(7), l = S(8);
+            const BW<NW> m = S(9), n = S(10), o = S(11), p = S(12);
+            return X(X(X(X(a, b), X(c, d)), X(X(f, g), X(k, l))), X(X(m, n), X(o, p)));
+        }
+        case 6: {
+            const BW<NW> a = S(1), b = S(2), c = S(3), d = S(4), f = S(5), g = S(6), k = S(7), l = S(8);
+            const BW<NW> m = S(9), n = S(10), o = S(11), p = S(12), q = S(13), r = S(14);
+            return X(X(X(X(a, b), X(c, d)), X(X(f, g), X(k, l))), X(X(X(m, n), X(o, p)), X(q, r)));
         }
         default: {
-            const BW<NW> a = ZXS_SEL(e.x, 1), b = ZXS_SEL(e.x, 2), c = ZXS_SEL(e.x, 3), d = ZXS_SEL(e.y, 0);
-            const BW<NW> f = ZXS_SEL(e.y, 1), g = ZXS_SEL(e.y, 2), k = ZXS_SEL(e.y, 3), l = ZXS_SEL(e.z, 0);
-            const BW<NW> m = ZXS_SEL(e.z, 1), n = ZXS_SEL(e.z, 2), o = ZXS_SEL(e.z, 3), p = ZXS_SEL(e.w, 0);
-            const BW<NW> q = ZXS_SEL(e.w, 1), r = ZXS_SEL(e.w, 2), t = ZXS_SEL(e.w, 3);
-            return X2(X2(X2(X2(a, b), X2(c, d)), X2(X2(f, g), X2(k, l))), X2(X2(X2(m, n), X2(o, p)), X2(X2(q, r), t)));
+            const BW<NW> a = S(1), b = S(2), c = S(3), d = S(4), f = S(5), g = S(6), k = S(7), l = S(8);
+            const BW<NW> m = S(9), n = S(10), o = S(11), p = S(12), q = S(13), r = S(14), t = S(15);
+            return X(X(X(X(a, b), X(c, d)), X(X(f, g), X(k, l))), X(X(X(m, n), X(o, p)), X(X(q, r), t)));
         }
     }
-#undef X2
-#undef ZXS_SEL
+#undef X
+#undef S
 }
 
 template <int NW>
@@ -211,20 +230,29 @@ __device__ __forceinline__ void j_add(BW<NW> &j0, BW<NW> &j1, const BW<NW> &x, u
     }
 }
 
-// Record runs of one kind, forms of four records formed together (independent
-// shared loads in flight), then applied.
+// Record runs of one kind, forms of four (NW = 1) or two (NW = 2) records
+// formed together (independent shared loads in flight), then applied.
 #define ZXS_MONO_RUN(N, OP)                                                              \
     {                                                                                    \
         uint32_t i_ = 0;                                                                 \
-        for (; i_ + 4 <= (N); i_ += 4) {                                                 \
-            const BW<NW> x0 = mono_form<NW>(sd, w[q + i_] & 0xfffu, pl);                 \
-            const BW<NW> x1 = mono_form<NW>(sd, w[q + i_ + 1] & 0xfffu, pl);             \
-            const BW<NW> x2 = mono_form<NW>(sd, w[q + i_ + 2] & 0xfffu, pl);             \
-            const BW<NW> x3 = mono_form<NW>(sd, w[q + i_ + 3] & 0xfffu, pl);             \
-            OP(x0);                                                                      \
-            OP(x1);                                                                      \
-            OP(x2);                                                                      \
-            OP(x3);                                                                      \
+        if constexpr (NW == 1) {                                                         \
+            for (; i_ + 4 <= (N); i_ += 4) {                                             \
+                const BW<NW> x0 = mono_form<NW>(sd, w[q + i_] & 0xfffu, pl);             \
+                const BW<NW> x1 = mono_form<NW>(sd, w[q + i_ + 1] & 0xfffu, pl);         \
+                const BW<NW> x2 = mono_form<NW>(sd, w[q + i_ + 2] & 0xfffu, pl);         \
+                const BW<NW> x3 = mono_form<NW>(sd, w[q + i_ + 3] & 0xfffu, pl);         \
+                OP(x0);                                                                  \
+                OP(x1);                                                                  \
+                OP(x2);                                                                  \
+                OP(x3);                                                                  \
+            }                                                                            \
+        } else {                                                                         \
+            for (; i_ + 2 <= (N); i_ += 2) {                                             \
+                const BW<NW> x0 = mono_form<NW>(sd, w[q + i_] & 0xfffu, pl);             \
+                const BW<NW> x1 = mono_form<NW>(sd, w[q + i_ + 1] & 0xfffu, pl);         \
+                OP(x0);                                                                  \
+                OP(x1);                                                                  \
+            }                                                                            \
         }                                                                                \
         for (; i_ < (N); i_++) {                                                         \
             const BW<NW> x0 = mono_form<NW>(sd, w[q + i_] & 0xfffu, pl);                 \

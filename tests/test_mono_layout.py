@@ -54,11 +54,11 @@ def mono_layout(arrays, min_factors=0):
 
 def form_sel(dict_, f):
     """Plane indices of dictionary form f (continuation entries followed):
-    byte 0 = size class (2/4/8/15 slots) | 0x80, bytes 1..15 plane indices."""
+    byte 0 = size class c (2c + 2 slots, 15 for c = 7) | 0x80, bytes 1..15 plane indices."""
     sel = []
     while True:
         e = dict_[f].view(np.uint8)
-        slots = (2, 4, 8, 15)[int(e[0]) & 3]
+        slots = (2, 4, 6, 8, 10, 12, 14, 15)[int(e[0]) & 7]
         sel += [int(x) for x in e[1:1 + slots]]  # padding slots name the all-zero plane
         if not (int(e[0]) & 0x80):
             return sel

@@ -130,6 +130,8 @@ struct zxs_sampler {
     size_t dev_model_bytes = 0;
     bool param_mechs = true;
     std::unique_ptr<zxs_dev::MechTable<zxs_dev::kParamMechs>> mech_table;
+    std::unique_ptr<zxs_dev::MechTable<1>> mech_table1;  // parameter block of the global-mechanism variant
+    uint32_t light_tables = 0;                          // h tables staged in smem (LightProg valid)
     const zxs_dev::MechRec *mech_global = nullptr;
     const zxs_dev::MechFast *fast_global = nullptr;
     const uint32_t *ext_begin = nullptr;
@@ -254,8 +256,9 @@ const void *shot_kernel_for(int fw, bool param_mechs) {
 
 constexpr int kThreads = 256;
 
-size_t shot_smem_bytes(const zxs_sampler *s) {
-    return size_t(s->m.num_outputs) * 8 + size_t(zxs_dev::kS) * s->m.col_stride * 4;  // one warp per CTA
+size_t shot_smem_bytes(const zxs_sampler *s) {  // one warp per CTA
+    const size_t sh_off = (2 * size_t(s->m.num_outputs) + 3) & ~size_t(3);
+    return (sh_off + 16 * size_t(s->light_tables)) * 4 + size_t(zxs_dev::kS) * s->m.col_stride * 4;
 }
 
 void validate_csr(const char *name, const uint32_t *b, size_t n, size_t total) {
@@ -1149,6 +1152,48 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         }
     }
 
+    // ---- light program (zxs_kernels.cuh LightProg), filled after the heavy/mono split below
+    auto build_light = [&](const std::vector<uint8_t> &comp_heavy, zxs_dev::LightProg &pg) -> bool {
+        std::memset(&pg, 0, sizeof(pg));
+        if (d->num_tensors > zxs_dev::kLightTensors || d->num_h_tables > zxs_dev::kLightTables) return false;
+        uint32_t chain = 0;
+        for (uint32_t c = 0; c < d->num_components; c++) {
+            if (!comp_heavy[c]) chain = std::max(chain, d->comp_out_begin[c + 1] - d->comp_out_begin[c]);
+        }
+        if (fwid + chain > 64) return false;
+        uint32_t nterm = 0, nfac = 0;
+        std::vector<uint8_t> tensor_light(d->num_tensors, 0);
+        for (uint32_t c = 0; c < d->num_components; c++) {
+            if (comp_heavy[c]) continue;
+            for (uint32_t t = d->comp_tensor_begin[c]; t < d->comp_tensor_begin[c + 1]; t++) tensor_light[t] = 1;
+        }
+        for (uint32_t t = 0; t < d->num_tensors; t++) {
+            pg.tensor_term[t] = nterm;
+            if (!tensor_light[t]) continue;
+            for (uint64_t term = d->tensor_term_begin[t]; term < d->tensor_term_begin[t + 1]; term++) {
+                if (nterm >= zxs_dev::kLightTerms) return false;
+                pg.term_c[nterm] = make_double2(d->term_c[2 * term], d->term_c[2 * term + 1]);
+                pg.term_factor[nterm] = nfac;
+                for (uint64_t k = d->term_factor_begin[term]; k < d->term_factor_begin[term + 1]; k++) {
+                    if (nfac >= zxs_dev::kLightFactors) return false;
+                    unsigned long long u = 0, v = 0;
+                    for (uint64_t i = d->factor_u_begin[k]; i < d->factor_u_begin[k + 1]; i++) u ^= 1ull << d->factor_u_bits[i];
+                    for (uint64_t i = d->factor_v_begin[k]; i < d->factor_v_begin[k + 1]; i++) v ^= 1ull << d->factor_v_bits[i];
+                    pg.fu[nfac] = u;
+                    pg.fv[nfac] = v;
+                    pg.ftable[nfac] = uint8_t(d->factor_table[k]);
+                    nfac++;
+                }
+                nterm++;
+            }
+        }
+        pg.tensor_term[d->num_tensors] = nterm;
+        pg.term_factor[nterm] = nfac;
+        pg.n_tables = std::max<uint32_t>(1, d->num_h_tables);
+        pg.valid = 1;
+        return true;
+    };
+
     // ---- heavy components: compact chunked streams (zxs_heavy.cuh)
     uint64_t heavy_min = 20000;
     if (const char *e = std::getenv("ZXS_HEAVY_MIN_FACTORS")) heavy_min = std::strtoull(e, nullptr, 10);
@@ -1243,9 +1288,21 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     s->ext_begin = reinterpret_cast<const uint32_t *>(b + o_extb);
     s->ext = reinterpret_cast<const ulonglong2 *>(b + o_ext);
     s->param_mechs = d->num_mechanisms <= zxs_dev::kParamMechs;
-    if (s->param_mechs) {
-        s->mech_table.reset(new zxs_dev::MechTable<zxs_dev::kParamMechs>());
-        std::copy(fast.begin(), fast.end(), s->mech_table->fast);
+    s->mech_table.reset(new zxs_dev::MechTable<zxs_dev::kParamMechs>());
+    s->mech_table1.reset(new zxs_dev::MechTable<1>());
+    if (s->param_mechs) std::copy(fast.begin(), fast.end(), s->mech_table->fast);
+    {
+        bool use_light = true;
+        if (const char *e = std::getenv("ZXS_LIGHT_PROG")) use_light = std::strcmp(e, "0") != 0;
+        zxs_dev::LightProg &pg = s->mech_table->prog;
+        if (use_light && build_light(comp_heavy, pg)) {
+            s->mech_table1->prog = pg;
+            s->light_tables = pg.n_tables;
+        } else {
+            pg.valid = 0;
+            s->mech_table1->prog.valid = 0;
+            s->light_tables = 0;
+        }
     }
     s->fast_global = reinterpret_cast<const zxs_dev::MechFast *>(b + o_fast);
     s->dead_mechanisms = dead;
@@ -1427,13 +1484,12 @@ void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
     uint64_t cap = uint64_t(s->sm_count) * s->blocks_per_sm;
     unsigned grid = unsigned(std::min(a.n_tiles, cap));
     size_t smem = shot_smem_bytes(s);
-    static zxs_dev::MechTable<1> unused_table{};
     const bool heavy = (s->has_heavy || s->has_mono) && !a.fcols_out && !a.forced;
     if (heavy) {
         a.heavy_ld32 = 2 * ((a.shots + 63) / 64);
         a.heavy_fcols = s->heavy_fcols_get(std::max<size_t>(16, size_t(s->m.f_width) * a.heavy_ld32 * 4));
     }
-    void *args[] = {&a, s->param_mechs ? static_cast<void *>(s->mech_table.get()) : static_cast<void *>(&unused_table)};
+    void *args[] = {&a, s->param_mechs ? static_cast<void *>(s->mech_table.get()) : static_cast<void *>(s->mech_table1.get())};
     cudaEvent_t t0 = nullptr;
     s->time_begin(0, st, t0);
     CK(cudaLaunchKernel(shot_kernel_for(s->fw_template, s->param_mechs), dim3(grid), dim3(32), args, smem, st));

@@ -28,7 +28,23 @@ namespace zxs_dev {
 
 constexpr int kS = 2;                 // shots per lane
 constexpr int kTileShots = 32 * kS;   // shots per warp tile = one u64 word
-constexpr uint32_t kParamMechs = 3600;
+constexpr uint32_t kParamMechs = 2048;
+
+// Small chain tensors as a uniform program in the kernel parameter space:
+// per factor the u / v selectors as 64-bit masks over the parameter columns
+// (f bits, then the component's sampled bits), so eval reads descriptors with
+// uniform constant-bank loads and walks selector bits on the uniform
+// datapath instead of chasing global-memory CSR arrays. Used when every
+// light (shot_kernel-evaluated) component fits (f_width + chain <= 64).
+constexpr uint32_t kLightTensors = 48, kLightTerms = 160, kLightFactors = 320, kLightTables = 32;
+struct LightProg {
+    uint32_t valid, n_tables;
+    uint32_t tensor_term[kLightTensors + 1];   // by model tensor index
+    uint32_t term_factor[kLightTerms + 1];
+    double2 term_c[kLightTerms];
+    unsigned long long fu[kLightFactors], fv[kLightFactors];
+    uint8_t ftable[kLightFactors];
+};
 
 // One mechanism: the first scan entry inline; further entries (joint tables)
 // in global memory at ext_begin[m] .. ext_begin[m] + n_extra.
@@ -51,6 +67,7 @@ struct MechFast {
 template <uint32_t N>
 struct MechTable {
     MechFast fast[N];
+    LightProg prog;
 };
 static_assert(kS == 2, "output stores pack two 32-shot words");
 
@@ -191,6 +208,45 @@ __device__ __forceinline__ void eval_tensor(const DevModel &m, uint32_t t, const
     }
 }
 
+// eval_tensor over the uniform LightProg: same products and sums in the
+// reference's order (phase_terms.cpp:121-131); h tables staged in shared
+// memory (sh, 4 entries per table), selected per lane by (a << 1) | b.
+__device__ __forceinline__ void eval_tensor_light(const LightProg &pg, uint32_t t, const uint32_t *cols,
+                                                  uint32_t stride, uint32_t lane, const double2 *sh,
+                                                  double2 (&acc)[kS]) {
+#pragma unroll
+    for (int s = 0; s < kS; s++) acc[s] = make_double2(0.0, 0.0);
+    const uint32_t t0 = pg.tensor_term[t], t1 = pg.tensor_term[t + 1];
+    for (uint32_t term = t0; term < t1; term++) {
+        const double2 c = pg.term_c[term];
+        double2 prod[kS];
+#pragma unroll
+        for (int s = 0; s < kS; s++) prod[s] = c;
+        const uint32_t k0 = pg.term_factor[term], k1 = pg.term_factor[term + 1];
+        for (uint32_t k = k0; k < k1; k++) {
+            uint32_t aw[kS] = {}, bw[kS] = {};
+            for (unsigned long long x = pg.fu[k]; x; x &= x - 1) {
+                const uint32_t p = __ffsll((long long)x) - 1;
+#pragma unroll
+                for (int s = 0; s < kS; s++) aw[s] ^= cols[s * stride + p];
+            }
+            for (unsigned long long x = pg.fv[k]; x; x &= x - 1) {
+                const uint32_t p = __ffsll((long long)x) - 1;
+#pragma unroll
+                for (int s = 0; s < kS; s++) bw[s] ^= cols[s * stride + p];
+            }
+            const double2 *h = sh + 4 * pg.ftable[k];
+#pragma unroll
+            for (int s = 0; s < kS; s++) {
+                const uint32_t idx = (((aw[s] >> lane) & 1u) << 1) | ((bw[s] >> lane) & 1u);
+                prod[s] = cmul_rn(prod[s], h[idx]);
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < kS; s++) acc[s] = cadd_rn(acc[s], prod[s]);
+    }
+}
+
 __device__ __forceinline__ void report_ratio_error(unsigned long long *err, uint64_t shot) {
     atomicOr(&err[0], 1ull);
     atomicMin(&err[1], (unsigned long long)shot);
@@ -237,7 +293,14 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
     const DevModel &m = a.m;
     const uint32_t lane = threadIdx.x;
     unsigned long long *scount = reinterpret_cast<unsigned long long *>(smem);
-    uint32_t *cols = smem + 2 * m.num_outputs;
+    const bool light = mt.prog.valid != 0;
+    const uint32_t sh_off = (2 * m.num_outputs + 3) & ~3u;  // 16-byte aligned
+    double2 *sh = reinterpret_cast<double2 *>(smem + sh_off);  // light h tables
+    uint32_t *cols = smem + sh_off + (light ? 16 * mt.prog.n_tables : 0);
+    if (light) {
+        for (uint32_t i = lane; i < 4 * mt.prog.n_tables; i += 32) sh[i] = m.h_table[i];
+        __syncwarp();
+    }
     if (a.counts) {
         for (uint32_t o = lane; o < m.num_outputs; o += 32) scount[o] = 0;
         __syncwarp();
@@ -384,7 +447,11 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
             __syncwarp();
             double2 acc[kS];
             double prev[kS], norm[kS];
-            eval_tensor(m, tb, cols, m.col_stride, lane, acc);
+            if (light) {
+                eval_tensor_light(mt.prog, tb, cols, m.col_stride, lane, sh, acc);
+            } else {
+                eval_tensor(m, tb, cols, m.col_stride, lane, acc);
+            }
 #pragma unroll
             for (int s = 0; s < kS; s++) {
                 prev[s] = norm[s] = acc[s].x;
@@ -392,7 +459,11 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
                 if (a.forced && !pzero[s] && local[s] < a.shots && !(norm[s] > 0.0)) report_ratio_error(a.err, shot[s]);
             }
             for (uint32_t pos = 0; pos < n; pos++, upos++) {
-                eval_tensor(m, tb + 1 + pos, cols, m.col_stride, lane, acc);
+                if (light) {
+                    eval_tensor_light(mt.prog, tb + 1 + pos, cols, m.col_stride, lane, sh, acc);
+                } else {
+                    eval_tensor(m, tb + 1 + pos, cols, m.col_stride, lane, acc);
+                }
                 if (a.forced) {  // sampler.cpp:346-352: forced outcome bit
                     const uint32_t o = m.comp_outputs[ob + pos];
                     const bool bit = a.forced[o] != 0;

@@ -61,7 +61,8 @@ def _probe_offsets(struct_name, fields):
 
 
 @pytest.mark.parametrize("cls,cname", [(zxs_format.ModelDesc, "zxs_model_desc"),
-                                       (_native.SamplerInfo, "zxs_sampler_info")])
+                                       (_native.SamplerInfo, "zxs_sampler_info"),
+                                       (_native.SampleOptions, "zxs_sample_options")])
 def test_ctypes_layout_matches_header(cls, cname):
     names = [n for n, _ in cls._fields_]
     size, offs = _probe_offsets(cname, names)

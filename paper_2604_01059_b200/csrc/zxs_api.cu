@@ -447,6 +447,8 @@ struct MonoHost {
     uint64_t nodes = 0;
     std::vector<uint32_t> tensor_dict_begin;  // first dictionary entry per mono tensor, then the total
     std::vector<uint32_t> tensor_width;       // param width per mono tensor
+    std::vector<uint32_t> tensor_basis_begin; // first basis vector per mono tensor (W_t of them)
+    std::vector<unsigned long long> basis;    // basis vectors: masks over the tensor's raw params
     uint32_t all_plane = 0;                    // plane index of the per-tensor ALL plane
     uint32_t max_dict = 1;
     uint32_t max_depth = 1;  // deepest tree node + 1
@@ -568,54 +570,107 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
         }
     }
     // One dictionary per chain tensor (staged in shared memory while that
-    // tensor is evaluated); form ids are relative to the tensor's base.
-    std::map<std::vector<uint32_t>, uint32_t> form_id;
-    std::map<uint32_t, uint32_t> form_size;
+    // tensor is evaluated). Lowering first collects the tensor's distinct
+    // parity forms as 64-bit masks over its W raw parameters; once the
+    // tensor's record stream is known, a basis of W parity forms is chosen
+    // (greedy: the forms carrying the most selector loads, kept while linearly
+    // independent, completed with unit vectors) and every form is rewritten in
+    // that basis -- the device forms the W basis planes once per tensor and
+    // tile -- and, when longer than W/2, as its complement plus the ALL plane
+    // (XOR of the W basis planes).
+    std::map<uint64_t, uint32_t> form_id;  // raw mask -> form id (per tensor)
+    std::vector<uint64_t> form_mask;        // form id -> raw mask
+    std::map<uint32_t, uint32_t> form_size; // dictionary entry index -> plane loads
     size_t dict_base = 0;
-    // dictionary entry (16 B): byte 0 = count (0..15) | 0x80 (list continues in
-    // the next entry), bytes 1..15 = plane indices (zxs_mono.cuh mono_form).
-    // A list longer than half the tensor's width W is stored as its complement
-    // plus the ALL plane (XOR of planes 0..W-1, formed per tensor on device):
-    // at most W/2 + 1 selectors.
-    const uint32_t all_plane = fwid + max_chain;  // index of the ALL plane
+    const uint32_t all_plane = fwid + max_chain;  // ALL plane; all_plane + 1: ZERO; + 2 + j: raw sampled bit j
     uint32_t cur_width = 0;                        // param width of the tensor being encoded
     auto dict_form = [&](const std::vector<uint32_t> &sel0) -> uint32_t {
-        std::vector<uint32_t> sel = sel0;
-        if (cur_width >= 2 && sel0.size() > (cur_width + 1) / 2) {
-            std::vector<uint32_t> comp;
-            size_t j = 0;
-            for (uint32_t p = 0; p < cur_width; p++) {
-                if (j < sel0.size() && sel0[j] == p) {
-                    j++;
-                } else {
-                    comp.push_back(p);
+        uint64_t m = 0;
+        for (uint32_t p : sel0) m ^= 1ull << p;
+        auto it = form_id.find(m);
+        if (it != form_id.end()) return it->second;
+        const uint32_t id = uint32_t(form_mask.size());
+        form_mask.push_back(m);
+        form_id.emplace(m, id);
+        return id;
+    };
+    auto weight = [](uint64_t x) { return uint32_t(__builtin_popcountll(x)); };
+    // Chooses the tensor's basis, writes its dictionary, returns form id -> entry index.
+    auto finish_dictionary = [&](const std::vector<uint64_t> &usage, std::vector<uint64_t> &basis) {
+        const uint32_t W = cur_width;
+        auto cost = [&](uint64_t x) { const uint32_t k = weight(x); return std::min(k, W - k + 1); };
+        // greedy independent set, by selector loads carried
+        std::vector<uint32_t> order(form_mask.size());
+        for (uint32_t i = 0; i < order.size(); i++) order[i] = i;
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+            return usage[a] * cost(form_mask[a]) > usage[b] * cost(form_mask[b]);
+        });
+        basis.clear();
+        std::vector<std::pair<int, uint64_t>> rows;  // echelon rows: (pivot bit, vector)
+        std::vector<uint64_t> comb;                  // which chosen basis vectors each row combines
+        auto try_insert = [&](uint64_t v) {
+            uint64_t c = 1ull << basis.size();
+            for (size_t r = 0; r < rows.size(); r++) {
+                if ((v >> rows[r].first) & 1) {
+                    v ^= rows[r].second;
+                    c ^= comb[r];
                 }
             }
-            comp.push_back(all_plane);
-            if (j == sel0.size() && comp.size() < sel0.size()) sel = comp;
+            if (!v) return false;
+            rows.push_back({63 - __builtin_clzll(v), v});
+            comb.push_back(c);
+            return true;
+        };
+        for (uint32_t i : order) {
+            if (basis.size() == W) break;
+            if (form_mask[i] && try_insert(form_mask[i])) basis.push_back(form_mask[i]);
         }
-        auto it = form_id.find(sel);
-        if (it != form_id.end()) return it->second;
-        const uint32_t id = uint32_t(H.dict.size() - dict_base);
-        for (size_t i = 0; i < sel.size() || i == 0; i += 15) {
-            const size_t n = std::min<size_t>(15, sel.size() - i);
-            uint8_t e[16];
-            std::memset(e, int(all_plane + 1), 16);  // unused slots read the all-zero plane
-            const uint8_t cls = n >= 15 ? 7 : uint8_t((std::max<size_t>(n, 1) - 1) / 2);  // 2c + 2 slots
-            e[0] = uint8_t(cls | (i + 15 < sel.size() ? 0x80 : 0));
-            for (size_t k = 0; k < n; k++) e[1 + k] = uint8_t(sel[i + k]);
-            uint4 w;
-            std::memcpy(&w, e, 16);
-            H.dict.push_back(w);
+        for (uint32_t p = 0; p < W && basis.size() < W; p++) {
+            if (try_insert(1ull << p)) basis.push_back(1ull << p);
         }
-        form_id.emplace(sel, id);
-        uint32_t slots = 0;  // plane loads the device performs for this form
-        for (size_t i = 0; i < sel.size() || i == 0; i += 15) {
-            const size_t n = std::min<size_t>(15, sel.size() - i);
-            slots += n >= 15 ? 15 : uint32_t(2 * ((std::max<size_t>(n, 1) - 1) / 2) + 2);
+        // coordinates: reduce m by the echelon rows, XOR-ing their combinations
+        auto coords = [&](uint64_t m) {
+            uint64_t c = 0;
+            for (size_t r = 0; r < rows.size(); r++) {
+                if ((m >> rows[r].first) & 1) {
+                    m ^= rows[r].second;
+                    c ^= comb[r];
+                }
+            }
+            return c;  // m == 0 here: every form lies in the span
+        };
+        std::vector<uint32_t> entry_of(form_mask.size());
+        for (uint32_t f = 0; f < form_mask.size(); f++) {
+            const uint64_t x = coords(form_mask[f]);
+            std::vector<uint32_t> sel;
+            if (W >= 2 && weight(x) > (W + 1) / 2) {
+                for (uint32_t b = 0; b < W; b++) {
+                    if (!((x >> b) & 1)) sel.push_back(b);
+                }
+                sel.push_back(all_plane);
+            } else {
+                for (uint32_t b = 0; b < W; b++) {
+                    if ((x >> b) & 1) sel.push_back(b);
+                }
+            }
+            const uint32_t id = uint32_t(H.dict.size() - dict_base);
+            entry_of[f] = id;
+            uint32_t slots = 0;
+            for (size_t i = 0; i < sel.size() || i == 0; i += 15) {
+                const size_t n = std::min<size_t>(15, sel.size() - i);
+                uint8_t e[16];
+                std::memset(e, int(all_plane + 1), 16);  // unused slots read the all-zero plane
+                const uint8_t cls = n >= 15 ? 7 : uint8_t((std::max<size_t>(n, 1) - 1) / 2);  // 2c + 2 slots
+                e[0] = uint8_t(cls | (i + 15 < sel.size() ? 0x80 : 0));
+                for (size_t k = 0; k < n; k++) e[1 + k] = uint8_t(sel[i + k]);
+                uint4 wv;
+                std::memcpy(&wv, e, 16);
+                H.dict.push_back(wv);
+                slots += n >= 15 ? 15 : uint32_t(2 * ((std::max<size_t>(n, 1) - 1) / 2) + 2);
+            }
+            form_size[id] = slots;
         }
-        form_size[id] = slots;
-        return id;
+        return entry_of;
     };
     // parity list of a selector range after XOR cancellation, sorted
     auto sel_list = [](const uint32_t *bits, uint64_t n) {
@@ -640,6 +695,8 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
         const size_t dict_mark = H.dict.size();
         std::vector<uint32_t> tdb;  // per tensor: first dictionary entry
         std::vector<uint32_t> twid;  // per tensor: param width (the ALL plane spans planes 0..W-1)
+        std::vector<uint32_t> tbb;   // per tensor: first basis vector
+        std::vector<uint64_t> cb;    // basis vectors (raw masks)
         uint32_t comp_max_dict = 1, comp_depth = 1;
         std::vector<uint32_t> w;
         std::vector<uint4> ch;
@@ -647,11 +704,13 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
         uint64_t recs = 0, dead = 0, nsel = 0, loads = 0, nodes_total = 0;
         for (uint32_t t = t0; ok && t < t1; t++) {
             form_id.clear();
+            form_mask.clear();
             form_size.clear();
             dict_base = H.dict.size();
             tdb.push_back(uint32_t(dict_base));
             cur_width = d->tensor_param_width[t];
             twid.push_back(cur_width);
+            if (cur_width > 63) ok = false;  // raw forms as 64-bit masks
             // ---- lower every term of tensor t to record tokens (order-free: J and Z commute)
             std::vector<MonoTerm> terms;
             terms.reserve(size_t(d->tensor_term_begin[t + 1] - d->tensor_term_begin[t]));
@@ -785,6 +844,27 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             // ---- shared-prefix tree over the terms in order, emitted in DFS preorder
             std::vector<MonoNode> nodes = mono_tree(terms);
             for (const MonoNode &nd : nodes) comp_depth = std::max(comp_depth, nd.depth + 1);
+            // basis and dictionary, weighted by the records actually emitted
+            std::vector<uint64_t> usage(form_mask.size(), 0);
+            for (const MonoNode &nd : nodes) {
+                for (uint64_t tok : nd.recs) {
+                    const uint32_t r = uint32_t(tok), fa = r & 0xfffu, fbv = (r >> 16) & 0xfffu;
+                    if (fa != 0xfffu && fa < usage.size()) usage[fa]++;
+                    if ((r >> 28) == zxs_dev::kRecGen && fbv != 0xfffu && fbv < usage.size()) usage[fbv]++;
+                }
+            }
+            if (form_mask.size() >= 0xfffu) ok = false;
+            if (!ok) break;
+            std::vector<uint64_t> basis;
+            const std::vector<uint32_t> entry_of = finish_dictionary(usage, basis);
+            tbb.push_back(uint32_t(H.basis.size() + cb.size()));
+            cb.insert(cb.end(), basis.begin(), basis.end());
+            auto remap = [&](uint32_t r) {
+                const uint32_t fa = r & 0xfffu, fbv = (r >> 16) & 0xfffu;
+                const uint32_t na = fa == 0xfffu ? 0xfffu : entry_of[fa];
+                const uint32_t nb = fbv == 0xfffu ? 0xfffu : entry_of[fbv];
+                return (r & 0xf000f000u) | (nb << 16) | na;
+            };
             uint32_t cur_begin = uint32_t(H.words.size() + w.size()), cur_nodes = 0;
             auto close_chunk = [&]() {
                 if (H.words.size() + w.size() == cur_begin) w.insert(w.end(), 4, 0u);  // no 0-byte bulk copies
@@ -820,7 +900,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                 for (uint32_t kind : {zxs_dev::kRecAdd, zxs_dev::kRecSub, zxs_dev::kRecAdd2, zxs_dev::kRecZ,
                                       zxs_dev::kRecZn, zxs_dev::kRecGen}) {
                     for (uint64_t tok : nd.recs) {
-                        const uint32_t r = uint32_t(tok);
+                        const uint32_t r = remap(uint32_t(tok));
                         if ((r >> 28) != kind) continue;
                         nw.push_back(r);
                         if (tok >> 32) nw.push_back(uint32_t((tok >> 32) - 1));
@@ -841,7 +921,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             if (ok) close_chunk();
             nodes_total += nodes.size();
         }
-        if (ok && mono_smem_bytes(fwid + max_chain + 2, std::max(comp_max_dict, H.max_dict), 1,
+        if (ok && mono_smem_bytes(fwid + 2 * max_chain + 2, std::max(comp_max_dict, H.max_dict), 1,
                                   std::max(comp_depth, H.max_depth)) > 227 * 1024) {
             ok = false;
         }
@@ -859,6 +939,10 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             H.tensor_chunk_begin.push_back(uint32_t(H.chunks.size()));
             H.tensor_dict_begin.insert(H.tensor_dict_begin.end(), tdb.begin(), tdb.end());
             H.tensor_width.insert(H.tensor_width.end(), twid.begin(), twid.end());
+            const uint32_t bb0 = uint32_t(H.basis.size());
+            for (uint32_t x : tbb) H.tensor_basis_begin.push_back(x);
+            (void)bb0;
+            H.basis.insert(H.basis.end(), cb.begin(), cb.end());
             H.comps.push_back(hc);
             H.comp_mono[c] = 1;
             H.max_dict = std::max(H.max_dict, comp_max_dict);
@@ -879,6 +963,8 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
     if (H.dict.empty()) H.dict.push_back(make_uint4(0, 0, 0, 0));
     H.tensor_dict_begin.push_back(uint32_t(H.dict.size()));
     if (H.tensor_width.empty()) H.tensor_width.push_back(0);
+    if (H.tensor_basis_begin.empty()) H.tensor_basis_begin.push_back(0);
+    if (H.basis.empty()) H.basis.push_back(0);
     H.all_plane = fwid + max_chain;
     return H;
 }
@@ -1268,6 +1354,8 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     size_t o_mdict = ar.add(MH.dict);
     size_t o_mtdb = ar.add(MH.tensor_dict_begin);
     size_t o_mtw = ar.add(MH.tensor_width);
+    size_t o_mtbb = ar.add(MH.tensor_basis_begin);
+    size_t o_mbasis = ar.add(MH.basis);
 
     CK(cudaMalloc(&s->dev_model, ar.host.size()));
     s->dev_model_bytes = ar.host.size();
@@ -1344,9 +1432,11 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     if (s->has_mono) {
         zxs_dev::MonoArgs &ma = s->mono;
         ma.f_width = fwid;
-        ma.n_planes = MH.all_plane + 2;  // f, sampled bits of the longest chain, ALL, ZERO
+        ma.n_planes = MH.all_plane + 2 + MH.max_chain;  // basis planes, ALL, ZERO, raw sampled bits
         ma.all_plane = MH.all_plane;
         ma.tensor_width = reinterpret_cast<const uint32_t *>(b + o_mtw);
+        ma.tensor_basis_begin = reinterpret_cast<const uint32_t *>(b + o_mtbb);
+        ma.basis = reinterpret_cast<const unsigned long long *>(b + o_mbasis);
         ma.words = reinterpret_cast<const uint32_t *>(b + o_mw);
         ma.chunks = reinterpret_cast<const uint4 *>(b + o_mch);
         ma.tensor_chunk_begin = reinterpret_cast<const uint32_t *>(b + o_mtcb);
@@ -2299,7 +2389,11 @@ zxs_status zxs_debug_mono_layout(const zxs_model_desc *desc, uint64_t min_factor
         for (const uint4 &c : H.chunks) blob.insert(blob.end(), {c.x, c.y, c.z, c.w});
         for (const uint4 &c : H.dict) blob.insert(blob.end(), {c.x, c.y, c.z, c.w});
         blob.insert(blob.end(), H.tensor_dict_begin.begin(), H.tensor_dict_begin.end());
-        blob.insert(blob.end(), H.tensor_width.begin(), H.tensor_width.begin() + (H.tensor_chunk_begin.size() - 1));
+        const size_t nt = H.tensor_chunk_begin.size() - 1;
+        blob.insert(blob.end(), H.tensor_width.begin(), H.tensor_width.begin() + nt);
+        blob.insert(blob.end(), H.tensor_basis_begin.begin(), H.tensor_basis_begin.begin() + nt);
+        blob.push_back(uint32_t(H.basis.size()));
+        for (unsigned long long x : H.basis) blob.insert(blob.end(), {uint32_t(x), uint32_t(x >> 32)});
         blob.insert(blob.end(), H.words.begin(), H.words.end());
         *needed = blob.size();
         if (out && cap >= blob.size()) std::memcpy(out, blob.data(), blob.size() * 4);

@@ -75,10 +75,12 @@ enum : uint32_t {
 struct MonoArgs {
     uint64_t seed, first_shot, shots, n_cta_tiles;
     uint32_t k0_round[10];
-    uint32_t f_width, n_planes;       // planes per warp = f_width + longest chain + ALL + ZERO
-    uint32_t all_plane;               // index of the ALL plane: XOR of planes 0..W-1 of the current tensor;
-                                      // all_plane + 1 is the all-zero plane (padding selectors)
+    // planes per warp: [0, W) the current tensor's basis planes, all_plane = ALL (XOR of the W basis
+    // planes), all_plane + 1 = ZERO (padding selectors), all_plane + 2 + j = raw sampled bit j
+    uint32_t f_width, n_planes, all_plane;
     const uint32_t *tensor_width;     // [mono tensors] param width W
+    const uint32_t *tensor_basis_begin;       // [mono tensors] first basis vector
+    const unsigned long long *basis;  // basis vectors: masks over the raw params (f bits, then sampled bits)
     const uint32_t *fcols;            // [f_width][fcols_ld32] from shot_kernel
     uint64_t fcols_ld32;
     uint32_t *out32;                  // [num_outputs][out_ld32] (nullable)
@@ -331,14 +333,7 @@ __global__ void __launch_bounds__(MonoCfg<NW>::kWarps * 32, 1) mono_kernel(const
     for (uint64_t ct = blockIdx.x; ct < h.n_cta_tiles; ct += gridDim.x) {
         // the lane's NW consecutive 32-shot words: wrd .. wrd + NW - 1
         const uint64_t wrd = ((ct * kW + warp) * 32 + lane) * NW;
-        for (uint32_t p = 0; p < h.n_planes; p++) {
-            BW<NW> v;
-#pragma unroll
-            for (int i = 0; i < NW; i++) {
-                v.w[i] = (p < h.f_width && wrd + i < h.fcols_ld32) ? h.fcols[p * h.fcols_ld32 + wrd + i] : 0u;
-            }
-            myplanes[p * 32] = v;
-        }
+        for (uint32_t p = h.all_plane + 1; p < h.n_planes; p++) myplanes[p * 32] = bw_zero<NW>();  // ZERO, sampled bits
         __syncwarp();
         double *prev_g = h.scratch + wrd * 32;
         double *cur_g = h.scratch + (h.n_cta_tiles * kW * kWarpShots) + wrd * 32;
@@ -349,11 +344,30 @@ __global__ void __launch_bounds__(MonoCfg<NW>::kWarps * 32, 1) mono_kernel(const
             const uint32_t npos = h.eval_tensor >= 0 ? 1u : cd.n_out + 1;
             for (uint32_t pos = 0; pos < npos; pos++) {  // pos 0: normalization, pos j+1: marginal j
                 const uint32_t t = h.eval_tensor >= 0 ? uint32_t(h.eval_tensor) : cd.first_tensor + pos;
-                // the ALL plane of this tensor (its sampled-bit planes are final up to pos)
+                // this tensor's basis planes from the raw parameters (f columns from the
+                // shot kernel's scratch, sampled bits so far from shared memory), and ALL
                 {
-                    BW<NW> all = bw_zero<NW>();
                     const uint32_t W = min(h.tensor_width[t], h.all_plane);
-                    for (uint32_t p = 0; p < W; p++) all = bw_xor<NW>(all, myplanes[p * 32]);
+                    const unsigned long long *bv = h.basis + h.tensor_basis_begin[t];
+                    BW<NW> all = bw_zero<NW>();
+                    for (uint32_t b = 0; b < W; b++) {
+                        BW<NW> v = bw_zero<NW>();
+                        for (unsigned long long x = bv[b]; x; x &= x - 1) {
+                            const uint32_t p = __ffsll((long long)x) - 1;
+                            BW<NW> r;
+                            if (p < h.f_width) {
+#pragma unroll
+                                for (int i = 0; i < NW; i++) {
+                                    r.w[i] = wrd + i < h.fcols_ld32 ? __ldg(h.fcols + p * h.fcols_ld32 + wrd + i) : 0u;
+                                }
+                            } else {
+                                r = myplanes[(h.all_plane + 2 + (p - h.f_width)) * 32];
+                            }
+                            v = bw_xor<NW>(v, r);
+                        }
+                        myplanes[b * 32] = v;
+                        all = bw_xor<NW>(all, v);
+                    }
                     myplanes[h.all_plane * 32] = all;
                 }
                 // stage the tensor's form dictionary (every warp is past the previous tensor)
@@ -478,7 +492,7 @@ __global__ void __launch_bounds__(MonoCfg<NW>::kWarps * 32, 1) mono_kernel(const
                         if ((s >> 5) == uint32_t(i)) word.w[i] |= uint32_t(bit) << (s & 31);
                     }
                 }
-                myplanes[(h.f_width + j) * 32] = word;
+                myplanes[(h.all_plane + 2 + j) * 32] = word;
                 const uint32_t o = h.comp_outputs[cd.out_begin + j];
 #pragma unroll
                 for (int i = 0; i < NW; i++) {
@@ -495,7 +509,7 @@ __global__ void __launch_bounds__(MonoCfg<NW>::kWarps * 32, 1) mono_kernel(const
             }
             // reset this component's sampled-bit planes for the next component
             if (h.eval_tensor < 0) {
-                for (uint32_t j = 0; j < cd.n_out; j++) myplanes[(h.f_width + j) * 32] = bw_zero<NW>();
+                for (uint32_t j = 0; j < cd.n_out; j++) myplanes[(h.all_plane + 2 + j) * 32] = bw_zero<NW>();
             }
             __syncwarp();
         }

@@ -358,3 +358,21 @@ def test_cultivation_proxy_mono_against_reference():
     got = sample(cs, shots, 11, first)
     want = ref.sample_rb(shots, 11, first_shot=first, batch_size=64, threads=os.cpu_count())
     assert np.array_equal(got, want)
+
+
+def test_kernel_timing_counts_launches():
+    """zxs_kernel_timing/times: one shot_kernel launch per sample call, plus
+    mono_kernel when a component is on the monomial path."""
+    cs = model("c2_surface_d3_xmem_t")
+    cs.kernel_timing(True)
+    sample(cs, 10000, 1)
+    sample(cs, 10000, 2)
+    t = cs.kernel_times()
+    cs.kernel_timing(False)
+    assert t["shot_kernel"][1] == 2 and t["shot_kernel"][0] > 0 and t["mono_kernel"][1] == 0
+    cm = _heavy_model("surface_d3_xmem_9t", min_factors="0", mono="1")
+    cm.kernel_timing(True)
+    sample(cm, 5000, 1)
+    t = cm.kernel_times()
+    cm.kernel_timing(False)
+    assert t["shot_kernel"][1] == 1 and t["mono_kernel"][1] == 1

@@ -47,9 +47,15 @@ def mono_layout(arrays, min_factors=0):
     o += n_tcb
     twidth = buf[o:o + n_tcb - 1].astype(np.int64)
     o += n_tcb - 1
+    tbb = buf[o:o + n_tcb - 1].astype(np.int64)
+    o += n_tcb - 1
+    nb = int(buf[o])
+    o += 1
+    basis = [int(buf[o + 2 * i]) | (int(buf[o + 2 * i + 1]) << 32) for i in range(nb)]
+    o += 2 * nb
     words = buf[o:o + n_words]
     return dict(comps=comps, flags=flags, tcb=tcb, chunks=chunks, dict=dict_, tdb=tdb, twidth=twidth,
-                all_plane=all_plane, words=words)
+                tbb=tbb, basis=basis, all_plane=all_plane, words=words)
 
 
 def form_sel(dict_, f):
@@ -105,10 +111,15 @@ def emulate_tensor(lay, t, P, stats=None):
     cache = {}
     d0 = int(lay["tdb"][t])
     W = int(lay["twidth"][t])
-    # planes: the params, then the ALL plane (XOR of params 0..W-1) at lay["all_plane"]
-    planes = np.zeros((P.shape[0], lay["all_plane"] + 2), np.int64)  # ..., ALL, ZERO
-    planes[:, :min(P.shape[1], lay["all_plane"])] = P[:, :lay["all_plane"]]
-    planes[:, lay["all_plane"]] = P[:, :W].sum(1) & 1
+    # planes: the tensor's W basis planes (parities of the raw params P), then ALL (XOR of the
+    # basis planes) at lay["all_plane"] and the all-zero plane after it
+    planes = np.zeros((P.shape[0], lay["all_plane"] + 2), np.int64)
+    b0 = int(lay["tbb"][t])
+    for b in range(W):
+        m = lay["basis"][b0 + b]
+        cols = [p for p in range(64) if (m >> p) & 1]
+        planes[:, b] = P[:, cols].sum(1) & 1 if cols else 0
+    planes[:, lay["all_plane"]] = planes[:, :W].sum(1) & 1
 
     def form(f):
         if f not in cache:

@@ -599,37 +599,28 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
     auto finish_dictionary = [&](const std::vector<uint64_t> &usage, std::vector<uint64_t> &basis) {
         const uint32_t W = cur_width;
         auto cost = [&](uint64_t x) { const uint32_t k = weight(x); return std::min(k, W - k + 1); };
-        // greedy independent set, by selector loads carried
-        std::vector<uint32_t> order(form_mask.size());
-        for (uint32_t i = 0; i < order.size(); i++) order[i] = i;
-        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
-            return usage[a] * cost(form_mask[a]) > usage[b] * cost(form_mask[b]);
-        });
-        basis.clear();
-        std::vector<std::pair<int, uint64_t>> rows;  // echelon rows: (pivot bit, vector)
-        std::vector<uint64_t> comb;                  // which chosen basis vectors each row combines
-        auto try_insert = [&](uint64_t v) {
-            uint64_t c = 1ull << basis.size();
-            for (size_t r = 0; r < rows.size(); r++) {
-                if ((v >> rows[r].first) & 1) {
-                    v ^= rows[r].second;
-                    c ^= comb[r];
+        // echelon form of a candidate basis: rows (pivot bit, vector) and the basis
+        // vectors each row combines; false if the vectors are dependent
+        std::vector<std::pair<int, uint64_t>> rows;
+        std::vector<uint64_t> comb;
+        auto echelon = [&](const std::vector<uint64_t> &B) {
+            rows.clear();
+            comb.clear();
+            for (size_t i = 0; i < B.size(); i++) {
+                uint64_t v = B[i], c = 1ull << i;
+                for (size_t r = 0; r < rows.size(); r++) {
+                    if ((v >> rows[r].first) & 1) {
+                        v ^= rows[r].second;
+                        c ^= comb[r];
+                    }
                 }
+                if (!v) return false;
+                rows.push_back({63 - __builtin_clzll(v), v});
+                comb.push_back(c);
             }
-            if (!v) return false;
-            rows.push_back({63 - __builtin_clzll(v), v});
-            comb.push_back(c);
             return true;
         };
-        for (uint32_t i : order) {
-            if (basis.size() == W) break;
-            if (form_mask[i] && try_insert(form_mask[i])) basis.push_back(form_mask[i]);
-        }
-        for (uint32_t p = 0; p < W && basis.size() < W; p++) {
-            if (try_insert(1ull << p)) basis.push_back(1ull << p);
-        }
-        // coordinates: reduce m by the echelon rows, XOR-ing their combinations
-        auto coords = [&](uint64_t m) {
+        auto coords = [&](uint64_t m) {  // after echelon(): basis coordinates of m
             uint64_t c = 0;
             for (size_t r = 0; r < rows.size(); r++) {
                 if ((m >> rows[r].first) & 1) {
@@ -637,8 +628,65 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                     c ^= comb[r];
                 }
             }
-            return c;  // m == 0 here: every form lies in the span
+            return c;
         };
+        auto total = [&](const std::vector<uint64_t> &B) -> uint64_t {  // selector loads of the stream
+            if (!echelon(B)) return ~0ull;
+            uint64_t sum = 0;
+            for (size_t f = 0; f < form_mask.size(); f++) {
+                if (usage[f]) sum += usage[f] * cost(coords(form_mask[f]));
+            }
+            return sum;
+        };
+        // start: the better of the identity and a greedy independent set of the
+        // forms carrying the most loads; then first-improvement swaps against the
+        // most loaded forms until no swap helps (bounded rounds)
+        std::vector<uint32_t> order(form_mask.size());
+        for (uint32_t i = 0; i < order.size(); i++) order[i] = i;
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+            return usage[a] * cost(form_mask[a]) > usage[b] * cost(form_mask[b]);
+        });
+        std::vector<uint64_t> ident, greedy;
+        for (uint32_t p = 0; p < W; p++) ident.push_back(1ull << p);
+        for (uint32_t i : order) {
+            if (greedy.size() == W) break;
+            greedy.push_back(form_mask[i]);
+            if (!form_mask[i] || !echelon(greedy)) greedy.pop_back();
+        }
+        for (uint32_t p = 0; p < W && greedy.size() < W; p++) {
+            greedy.push_back(1ull << p);
+            if (!echelon(greedy)) greedy.pop_back();
+        }
+        basis = ident;
+        uint64_t best = total(ident);
+        const uint64_t tg = total(greedy);
+        if (tg < best) {
+            best = tg;
+            basis = greedy;
+        }
+        std::vector<uint64_t> cand;
+        for (uint32_t i : order) {
+            if (cand.size() >= 160) break;
+            if (form_mask[i]) cand.push_back(form_mask[i]);
+        }
+        for (int round = 0; round < 12; round++) {
+            bool improved = false;
+            for (uint32_t slot = 0; slot < W; slot++) {
+                for (uint64_t cv : cand) {
+                    if (std::find(basis.begin(), basis.end(), cv) != basis.end()) continue;
+                    std::vector<uint64_t> nb = basis;
+                    nb[slot] = cv;
+                    const uint64_t tc = total(nb);
+                    if (tc < best) {
+                        best = tc;
+                        basis = nb;
+                        improved = true;
+                    }
+                }
+            }
+            if (!improved) break;
+        }
+        echelon(basis);
         std::vector<uint32_t> entry_of(form_mask.size());
         for (uint32_t f = 0; f < form_mask.size(); f++) {
             const uint64_t x = coords(form_mask[f]);

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <functional>
+#include <limits>
 #include <iterator>
 #include <cmath>
 #include <cstdlib>
@@ -132,6 +133,7 @@ struct zxs_sampler {
     std::unique_ptr<zxs_dev::MechTable<zxs_dev::kParamMechs>> mech_table;
     std::unique_ptr<zxs_dev::MechTable<1>> mech_table1;  // parameter block of the global-mechanism variant
     uint32_t light_tables = 0;                          // h tables staged in smem (LightProg valid)
+    double *dev_tab = nullptr;                          // tabulated chains (LightProg.tab)
     const zxs_dev::MechRec *mech_global = nullptr;
     const zxs_dev::MechFast *fast_global = nullptr;
     const uint32_t *ext_begin = nullptr;
@@ -1328,12 +1330,139 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         return true;
     };
 
+    // ---- tabulated chains (zxs_kernels.cuh TabProg): each eligible light component's
+    // autoregressive chain evaluated on the host for every assignment of its f-form
+    // parities and sampled bits, in the reference's arithmetic (eval_batch order, no
+    // FMA contraction, IEEE ratio; sampler.cpp:72-101)
+    auto build_tab = [&](const std::vector<uint8_t> &comp_heavy, zxs_dev::LightProg &pg, std::vector<double> &tab) {
+        pg.tab_valid = 0;
+        std::memset(&pg.tab, 0, sizeof(pg.tab));
+        tab.clear();
+        uint32_t nforms = 0, nsel = 0;
+        pg.tab.form_sel_begin[0] = 0;
+        for (uint32_t c = 0; c < d->num_components && c < zxs_dev::kTabComps; c++) {
+            if (comp_heavy[c]) continue;
+            const uint32_t n = d->comp_out_begin[c + 1] - d->comp_out_begin[c];
+            if (n == 0 || n > 10) continue;
+            const uint32_t t0 = d->comp_tensor_begin[c];
+            // distinct f-forms and per-factor (form id, sampled-bit mask) for u and v
+            std::map<std::vector<uint32_t>, int> fid;
+            std::vector<std::vector<uint32_t>> forms;
+            struct FacT { int fu, fv; uint32_t su, sv, table; };
+            std::vector<std::vector<std::pair<double2, std::vector<FacT>>>> tens(n + 1);
+            bool ok = true;
+            auto split = [&](const uint32_t *bits, uint64_t cnt, int &form, uint32_t &smask) {
+                std::vector<uint32_t> fsel;
+                smask = 0;
+                for (uint64_t i = 0; i < cnt; i++) {
+                    const uint32_t p = bits[i];
+                    if (p < fwid) {
+                        auto it = std::find(fsel.begin(), fsel.end(), p);
+                        if (it != fsel.end()) fsel.erase(it); else fsel.push_back(p);
+                    } else if (p - fwid < n) {
+                        smask ^= 1u << (p - fwid);
+                    } else {
+                        ok = false;
+                    }
+                }
+                std::sort(fsel.begin(), fsel.end());
+                if (fsel.empty()) {
+                    form = -1;
+                    return;
+                }
+                auto it = fid.find(fsel);
+                if (it != fid.end()) {
+                    form = it->second;
+                    return;
+                }
+                form = int(forms.size());
+                fid.emplace(fsel, form);
+                forms.push_back(fsel);
+            };
+            for (uint32_t j = 0; j <= n && ok; j++) {
+                const uint32_t t = t0 + j;
+                for (uint64_t term = d->tensor_term_begin[t]; term < d->tensor_term_begin[t + 1] && ok; term++) {
+                    std::vector<FacT> fs;
+                    for (uint64_t k = d->term_factor_begin[term]; k < d->term_factor_begin[term + 1]; k++) {
+                        FacT f{};
+                        split(d->factor_u_bits + d->factor_u_begin[k], d->factor_u_begin[k + 1] - d->factor_u_begin[k], f.fu, f.su);
+                        split(d->factor_v_bits + d->factor_v_begin[k], d->factor_v_begin[k + 1] - d->factor_v_begin[k], f.fv, f.sv);
+                        f.table = d->factor_table[k];
+                        fs.push_back(f);
+                    }
+                    tens[j].push_back({make_double2(d->term_c[2 * term], d->term_c[2 * term + 1]), fs});
+                }
+            }
+            const uint32_t mf = uint32_t(forms.size());
+            if (!ok || mf + n - 1 > 12) continue;
+            uint32_t fsel_count = 0;
+            for (auto &f : forms) fsel_count += uint32_t(f.size());
+            if (nforms + mf > zxs_dev::kTabForms || nsel + fsel_count > zxs_dev::kTabSel) continue;
+            const size_t entries = (size_t(1) << mf) * ((size_t(1) << n) - 1);
+            if (tab.size() + entries > (size_t(1) << 20)) continue;
+            // exact host evaluation of tensor j at (f-form bits fa, sampled prefix)
+            auto eval = [&](uint32_t j, uint32_t fa, uint32_t prefix) {
+                volatile double acc_re = 0.0, acc_im = 0.0;
+                for (const auto &tm : tens[j]) {
+                    double pr = tm.first.x, pi = tm.first.y;
+                    for (const FacT &f : tm.second) {
+                        const uint32_t av = (f.fu >= 0 ? (fa >> f.fu) & 1u : 0u) ^ (__builtin_popcount(prefix & f.su) & 1u);
+                        const uint32_t bv = (f.fv >= 0 ? (fa >> f.fv) & 1u : 0u) ^ (__builtin_popcount(prefix & f.sv) & 1u);
+                        const double hr = d->h_table[8 * f.table + 2 * ((av << 1) | bv)];
+                        const double hi = d->h_table[8 * f.table + 2 * ((av << 1) | bv) + 1];
+                        volatile double t1 = pr * hr, t2 = pi * hi, t3 = pr * hi, t4 = pi * hr;
+                        const double nr = t1 - t2, ni = t3 + t4;
+                        pr = nr;
+                        pi = ni;
+                    }
+                    acc_re = acc_re + pr;
+                    acc_im = acc_im + pi;
+                }
+                return double(acc_re);
+            };
+            const size_t base = tab.size();
+            tab.resize(base + entries);
+            for (uint32_t fa = 0; fa < (1u << mf); fa++) {
+                const double norm = eval(0, fa, 0);
+                std::function<void(uint32_t, uint32_t, double)> dfs = [&](uint32_t j, uint32_t prefix, double prev) {
+                    const double cur = eval(1 + j, fa, prefix);
+                    const double ratio = cur / prev;
+                    double cl;
+                    if (!(ratio > -1e-6 && ratio < 1.0 + 1e-6)) {
+                        cl = std::numeric_limits<double>::quiet_NaN();
+                    } else {
+                        cl = std::min(1.0, std::max(0.0, ratio));
+                    }
+                    tab[base + ((size_t((1u << j) - 1u)) << mf) + (size_t(prefix) << mf) + fa] = cl;
+                    if (j + 1 < n) {
+                        dfs(j + 1, prefix, cur);                     // bit j = 0: prev = cur
+                        dfs(j + 1, prefix | (1u << j), prev - cur);  // bit j = 1: prev -= cur
+                    }
+                };
+                dfs(0, 0, norm);
+            }
+            pg.tab.comp[c] = 0x80000000u | mf << 24 | nforms;
+            pg.tab.base[c] = uint32_t(base);
+            for (auto &f : forms) {
+                for (uint32_t p : f) pg.tab.form_sel[nsel++] = uint16_t(p);
+                pg.tab.form_sel_begin[++nforms] = uint16_t(nsel);
+            }
+            pg.tab_valid = 1;
+        }
+        if (tab.empty()) tab.push_back(0.0);
+    };
+
     // ---- heavy components: compact chunked streams (zxs_heavy.cuh)
-    uint64_t heavy_min = 20000;
-    if (const char *e = std::getenv("ZXS_HEAVY_MIN_FACTORS")) heavy_min = std::strtoull(e, nullptr, 10);
+    // Components with >= mono_min factors run in mono_kernel (measured faster
+    // than the per-warp shot-kernel chain from ~2k factors: config 4's chi=64
+    // component, 2316 factors, 5.5e8 vs 4.1e8 shots/s); with ZXS_MONO=0, those
+    // with >= heavy_min run in the exact heavy_kernel.
+    uint64_t heavy_min = 20000, mono_min = 2000;
+    if (const char *e = std::getenv("ZXS_HEAVY_MIN_FACTORS")) heavy_min = mono_min = std::strtoull(e, nullptr, 10);
+    if (const char *e = std::getenv("ZXS_MONO_MIN_FACTORS")) mono_min = std::strtoull(e, nullptr, 10);
     bool use_mono = true;
     if (const char *e = std::getenv("ZXS_MONO")) use_mono = std::strcmp(e, "0") != 0;
-    MonoHost MH = use_mono ? encode_mono(d, max_chain, heavy_min) : MonoHost{};
+    MonoHost MH = use_mono ? encode_mono(d, max_chain, mono_min) : MonoHost{};
     if (!use_mono) {
         MH.comp_mono.assign(std::max<uint32_t>(1, d->num_components), 0);
         MH.words.assign(4, 0);
@@ -1432,13 +1561,20 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         if (const char *e = std::getenv("ZXS_LIGHT_PROG")) use_light = std::strcmp(e, "0") != 0;
         zxs_dev::LightProg &pg = s->mech_table->prog;
         if (use_light && build_light(comp_heavy, pg)) {
-            s->mech_table1->prog = pg;
             s->light_tables = pg.n_tables;
         } else {
             pg.valid = 0;
-            s->mech_table1->prog.valid = 0;
             s->light_tables = 0;
         }
+        bool use_tab = true;
+        if (const char *e = std::getenv("ZXS_TAB")) use_tab = std::strcmp(e, "0") != 0;
+        std::vector<double> tab;
+        if (use_tab) build_tab(comp_heavy, pg, tab);
+        if (!pg.tab_valid) tab.assign(1, 0.0);
+        CK(cudaMalloc(&s->dev_tab, tab.size() * 8));
+        CK(cudaMemcpy(s->dev_tab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
+        s->info.num_tab_entries = pg.tab_valid ? tab.size() : 0;
+        s->mech_table1->prog = pg;
     }
     s->fast_global = reinterpret_cast<const zxs_dev::MechFast *>(b + o_fast);
     s->dead_mechanisms = dead;
@@ -1610,6 +1746,9 @@ void launch_mono(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *f
 void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
     a.m = s->m;
     a.num_mech = s->info.num_mechanisms;
+    a.debug_ar_components = 0xffffffffu;
+    a.tab = s->dev_tab;
+    if (const char *e = std::getenv("ZXS_DEBUG_AR_COMPONENTS")) a.debug_ar_components = uint32_t(std::atoi(e));
     a.mech_global = s->mech_global;
     a.fast_global = s->fast_global;
     a.ext_begin = s->ext_begin;
@@ -1767,6 +1906,7 @@ void zxs_sampler_destroy(zxs_sampler *s) {
     if (s->scratch) cudaFree(s->scratch);
     if (s->heavy_scratch) cudaFree(s->heavy_scratch);
     if (s->dev_log1mp) cudaFree(s->dev_log1mp);
+    if (s->dev_tab) cudaFree(s->dev_tab);
     if (s->dev_flip_begin) cudaFree(s->dev_flip_begin);
     if (s->dev_flip_out) cudaFree(s->dev_flip_out);
     if (s->mono_scratch) cudaFree(s->mono_scratch);

@@ -28,7 +28,7 @@ namespace zxs_dev {
 
 constexpr int kS = 2;                 // shots per lane
 constexpr int kTileShots = 32 * kS;   // shots per warp tile = one u64 word
-constexpr uint32_t kParamMechs = 2048;
+constexpr uint32_t kParamMechs = 1536;
 
 // Small chain tensors as a uniform program in the kernel parameter space:
 // per factor the u / v selectors as 64-bit masks over the parameter columns
@@ -37,8 +37,24 @@ constexpr uint32_t kParamMechs = 2048;
 // datapath instead of chasing global-memory CSR arrays. Used when every
 // light (shot_kernel-evaluated) component fits (f_width + chain <= 64).
 constexpr uint32_t kLightTensors = 48, kLightTerms = 160, kLightFactors = 320, kLightTables = 32;
+// Tabulated chains: a light component whose parity forms over f are few
+// (m_f of them) has its whole autoregressive chain precomputed on the host,
+// exactly as the reference evaluates it (eval_batch order, IEEE ratio,
+// sampler.cpp:84-99), as a table per chain position indexed by the m_f
+// f-form parities and the bits sampled so far: the clamped ratio, NaN where
+// the reference would throw. The device then forms m_f parities per shot and
+// does one table load and one compare per position.
+constexpr uint32_t kTabComps = 64, kTabForms = 192, kTabSel = 512;
+struct TabProg {
+    uint32_t comp[kTabComps];       // valid << 31 | m_f << 24 | first form
+    uint32_t base[kTabComps];       // first table entry (position 0); position j at base + ((2^j - 1) << m_f)
+    uint16_t form_sel_begin[kTabForms + 1];
+    uint16_t form_sel[kTabSel];     // f indices of each form's selectors
+};
+
 struct LightProg {
-    uint32_t valid, n_tables;
+    uint32_t valid, n_tables, tab_valid, pad;
+    TabProg tab;
     uint32_t tensor_term[kLightTensors + 1];   // by model tensor index
     uint32_t term_factor[kLightTerms + 1];
     double2 term_c[kLightTerms];
@@ -91,6 +107,8 @@ struct LaunchArgs {
     unsigned long long *err;       // [0] = flag, [1] = first failing shot
     uint32_t *heavy_fcols;         // f-columns for heavy_kernel: [f_width][heavy_ld32] (nullable)
     uint64_t heavy_ld32;
+    uint32_t debug_ar_components;  // profiling only (ZXS_DEBUG_AR_COMPONENTS): evaluate this many components
+    const double *tab;             // tabulated chains (LightProg.tab), clamped ratios / NaN
     // probability mode (outcome_probability_given, sampler.cpp:324-356): the
     // outcome bits are forced instead of drawn and prob[shot] receives
     // P(outcome | f) for the injected f of every shot. Every component runs
@@ -282,7 +300,7 @@ __device__ __noinline__ uint2 resolve_flips(uint64_t r0, uint64_t r1, MechRec md
 
 template <int FW, bool PARAM_MECHS>
 #ifndef ZXS_MAXNREG
-#define ZXS_MAXNREG 80
+#define ZXS_MAXNREG 96
 #endif
 __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ LaunchArgs a,
                                                    const __grid_constant__ MechTable<PARAM_MECHS ? kParamMechs : 1> mt) {
@@ -433,10 +451,55 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
 
         // ---- (5): autoregressive components
         uint32_t upos = 0;
-        for (uint32_t ci = 0; ci < m.num_components; ci++) {
+        const uint32_t ncomp_eval = min(m.num_components, a.debug_ar_components);
+        for (uint32_t ci = 0; ci < ncomp_eval; ci++) {
             const uint32_t ob = m.comp_out_begin[ci], n = m.comp_out_begin[ci + 1] - ob;
             if (m.comp_heavy[ci] && !a.forced) {  // evaluated by heavy_kernel / mono_kernel
                 upos += n;
+                continue;
+            }
+            if (mt.prog.tab_valid && ci < kTabComps && (mt.prog.tab.comp[ci] >> 31) && !a.forced) {
+                // ---- tabulated chain (TabProg): m_f form parities + sampled bits index the ratios
+                const uint32_t cw = mt.prog.tab.comp[ci], mf = (cw >> 24) & 0x7fu, f0 = cw & 0xffffu;
+                uint32_t idx[kS] = {};
+                for (uint32_t i = 0; i < mf; i++) {
+                    uint32_t w[kS] = {};
+                    for (uint32_t q = mt.prog.tab.form_sel_begin[f0 + i]; q < mt.prog.tab.form_sel_begin[f0 + i + 1]; q++) {
+                        const uint32_t pcol = mt.prog.tab.form_sel[q];
+#pragma unroll
+                        for (int s = 0; s < kS; s++) w[s] ^= cols[s * m.col_stride + pcol];
+                    }
+#pragma unroll
+                    for (int s = 0; s < kS; s++) idx[s] |= ((w[s] >> lane) & 1u) << i;
+                }
+                const double *tabp = a.tab + mt.prog.tab.base[ci];
+                for (uint32_t pos = 0; pos < n; pos++, upos++) {
+                    uint32_t rhi[kS], rlo[kS];
+                    if (!a.uniforms) {
+                        const uint32_t stream = 0x80000000u ^ (ci << 12) ^ pos;  // sampler.cpp:37-39
+                        philox_tail<kS>(pre, seed_hi ^ stream, a.k0_round, k2c, a.k0_round[9], rhi, rlo);
+                    }
+                    const double *tj = tabp + ((size_t((1u << pos) - 1u)) << mf);
+                    uint32_t word[kS];
+#pragma unroll
+                    for (int s = 0; s < kS; s++) {
+                        const bool valid = local[s] < a.shots;
+                        const double cl = __ldg(tj + idx[s]);
+                        if (isnan(cl) && valid) report_ratio_error(a.err, shot[s]);  // sampler.cpp:86-89
+                        const double u = a.uniforms ? (valid ? a.uniforms[upos * a.uniforms_ld + local[s]] : 0.0)
+                                                    : philox_uniform((uint64_t(rhi[s]) << 32) | rlo[s]);
+                        const bool bit = !(u < cl);
+                        idx[s] |= uint32_t(bit) << (mf + pos);
+                        word[s] = __ballot_sync(kFull, bit) & vmask[s];
+                    }
+                    if (lane == 0) {
+                        const uint32_t o = m.comp_outputs[ob + pos];
+                        if (a.out32) *reinterpret_cast<uint2 *>(a.out32 + o * a.ld32 + tile * kS) = make_uint2(word[0], word[1]);
+                        if (a.counts && (word[0] | word[1])) {
+                            atomicAdd(&scount[o], (unsigned long long)(__popc(word[0]) + __popc(word[1])));
+                        }
+                    }
+                }
                 continue;
             }
             const uint32_t tb = m.comp_tensor_begin[ci];

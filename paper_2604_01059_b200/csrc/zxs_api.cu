@@ -947,9 +947,18 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                     std::memcpy(&ib, &nd.im, 8);
                     nw.insert(nw.end(), {uint32_t(rb), uint32_t(rb >> 32), uint32_t(ib), uint32_t(ib >> 32)});
                 }
+                // records of a kind ordered by their form's first dictionary entry size class, so
+                // consecutive pairs mostly share a class (mono_kernel's paired straight-line loads)
+                std::vector<uint64_t> recs_sorted(nd.recs.begin(), nd.recs.end());
+                auto cls_of = [&](uint64_t tok) {
+                    const uint32_t r = remap(uint32_t(tok)), fa = r & 0xfffu;
+                    return fa == 0xfffu ? 0u : uint32_t(H.dict[dict_base + fa].x & 0x87u);
+                };
+                std::stable_sort(recs_sorted.begin(), recs_sorted.end(),
+                                 [&](uint64_t x, uint64_t y) { return cls_of(x) > cls_of(y); });
                 for (uint32_t kind : {zxs_dev::kRecAdd, zxs_dev::kRecSub, zxs_dev::kRecAdd2, zxs_dev::kRecZ,
                                       zxs_dev::kRecZn, zxs_dev::kRecGen}) {
-                    for (uint64_t tok : nd.recs) {
+                    for (uint64_t tok : recs_sorted) {
                         const uint32_t r = remap(uint32_t(tok));
                         if ((r >> 28) != kind) continue;
                         nw.push_back(r);

@@ -163,51 +163,73 @@ __device__ __forceinline__ BW<NW> mono_plane(const char *lb, uint32_t p) {
 // every load of the entry is issued before the XOR tree consumes them (a
 // selector costs a byte extract, an address IMAD, one LDS and half a 3-input
 // XOR per word), and the warp takes one uniform branch per entry.
+// Selector k (1..15) of entry e: plane index in byte k.
 template <int NW>
-__device__ __forceinline__ BW<NW> mono_entry(const uint4 e, const char *lb) {
-    // selector k (1..15) lives in byte k of the entry
-#define S(k) mono_plane<NW>(lb, __byte_perm((k) < 4 ? e.x : (k) < 8 ? e.y : (k) < 12 ? e.z : e.w, 0u, 0x4440u + ((k) & 3)))
-#define X(a, b) bw_xor<NW>(a, b)
-    switch (e.x & 7u) {  // slots: 2, 4, 6, 8, 10, 12, 14, 15
-        case 0: {
-            const BW<NW> a = S(1), b = S(2);
-            return X(a, b);
-        }
-        case 1: {
-            const BW<NW> a = S(1), b = S(2), c = S(3), d = S(4);
-            return X(X(a, b), X(c, d));
-        }
-        case 2: {
-            const BW<NW> a = S(1), b = S(2), c = S(3), d = S(4), f = S(5), g = S(6);
-            return X(X(X(a, b), X(c, d)), X(f, g));
-        }
-        case 3: {
-            const BW<NW> a = S(1), b = S(2), c = S(3), d = S(4), f = S(5), g = S(6), k = S(7), l = S(8);
-            return X(X(X(a, b), X(c, d)), X(X(f, g), X(k, l)));
-        }
-        case 4: {
-            const BW<NW> a = S(1), b = S(2), c = S(3), d = S(4), f = S(5), g = S(6), k = S(7), l = S(8);
-            const BW<NW> m = S(9), n = S(10);
-            return X(X(X(X(a, b), X(c, d)), X(X(f, g), X(k, l))), X(m, n));
-        }
-        case 5: {
-            const BW<NW> a = S(1), b = S(2), c = S(3), d = S(4), f = S(5), g = S(6), k = S(7), l = S(8);
-            const BW<NW> m = S(9), n = S(10), o = S(11), p = S(12);
-            return X(X(X(X(a, b), X(c, d)), X(X(f, g), X(k, l))), X(X(m, n), X(o, p)));
-        }
-        case 6: {
-            const BW<NW> a = S(1), b = S(2), c = S(3), d = S(4), f = S(5), g = S(6), k = S(7), l = S(8);
-            const BW<NW> m = S(9), n = S(10), o = S(11), p = S(12), q = S(13), r = S(14);
-            return X(X(X(X(a, b), X(c, d)), X(X(f, g), X(k, l))), X(X(X(m, n), X(o, p)), X(q, r)));
-        }
-        default: {
-            const BW<NW> a = S(1), b = S(2), c = S(3), d = S(4), f = S(5), g = S(6), k = S(7), l = S(8);
-            const BW<NW> m = S(9), n = S(10), o = S(11), p = S(12), q = S(13), r = S(14), t = S(15);
-            return X(X(X(X(a, b), X(c, d)), X(X(f, g), X(k, l))), X(X(X(m, n), X(o, p)), X(X(q, r), t)));
+__device__ __forceinline__ BW<NW> mono_sel(const uint4 &e, const char *lb, int k) {
+    const uint32_t word = k < 4 ? e.x : k < 8 ? e.y : k < 12 ? e.z : e.w;
+    return mono_plane<NW>(lb, __byte_perm(word, 0u, 0x4440u + uint32_t(k & 3)));
+}
+
+// XOR of the first N selectors of one entry (N a size class's slot count),
+// or of two entries of the same class with all 2N loads issued together.
+template <int NW, int N>
+__device__ __forceinline__ BW<NW> mono_cls(const uint4 &e, const char *lb) {
+    BW<NW> v[N];
+#pragma unroll
+    for (int k = 0; k < N; k++) v[k] = mono_sel<NW>(e, lb, k + 1);
+#pragma unroll
+    for (int st = 1; st < N; st <<= 1) {
+#pragma unroll
+        for (int k = 0; k + st < N; k += 2 * st) v[k] = bw_xor<NW>(v[k], v[k + st]);
+    }
+    return v[0];
+}
+template <int NW, int N>
+__device__ __forceinline__ void mono_cls2(const uint4 &e0, const uint4 &e1, const char *lb, BW<NW> &r0, BW<NW> &r1) {
+    BW<NW> v[N], u[N];
+#pragma unroll
+    for (int k = 0; k < N; k++) {
+        v[k] = mono_sel<NW>(e0, lb, k + 1);
+        u[k] = mono_sel<NW>(e1, lb, k + 1);
+    }
+#pragma unroll
+    for (int st = 1; st < N; st <<= 1) {
+#pragma unroll
+        for (int k = 0; k + st < N; k += 2 * st) {
+            v[k] = bw_xor<NW>(v[k], v[k + st]);
+            u[k] = bw_xor<NW>(u[k], u[k + st]);
         }
     }
-#undef X
-#undef S
+    r0 = v[0];
+    r1 = u[0];
+}
+
+template <int NW>
+__device__ __forceinline__ BW<NW> mono_entry(const uint4 e, const char *lb) {
+    switch (e.x & 7u) {  // slots: 2, 4, 6, 8, 10, 12, 14, 15
+        case 0: return mono_cls<NW, 2>(e, lb);
+        case 1: return mono_cls<NW, 4>(e, lb);
+        case 2: return mono_cls<NW, 6>(e, lb);
+        case 3: return mono_cls<NW, 8>(e, lb);
+        case 4: return mono_cls<NW, 10>(e, lb);
+        case 5: return mono_cls<NW, 12>(e, lb);
+        case 6: return mono_cls<NW, 14>(e, lb);
+        default: return mono_cls<NW, 15>(e, lb);
+    }
+}
+
+// Two single-entry forms of the same size class: one branch, 2N loads in flight
+// (classes up to kPairMaxCls: the register budget of the 64-shot lanes).
+constexpr uint32_t kPairMaxCls = 4;
+template <int NW>
+__device__ __forceinline__ void mono_entry2(const uint4 e0, const uint4 e1, const char *lb, BW<NW> &r0, BW<NW> &r1) {
+    switch (e0.x & 7u) {
+        case 0: mono_cls2<NW, 2>(e0, e1, lb, r0, r1); return;
+        case 1: mono_cls2<NW, 4>(e0, e1, lb, r0, r1); return;
+        case 2: mono_cls2<NW, 6>(e0, e1, lb, r0, r1); return;
+        case 3: mono_cls2<NW, 8>(e0, e1, lb, r0, r1); return;
+        default: mono_cls2<NW, 10>(e0, e1, lb, r0, r1); return;
+    }
 }
 
 template <int NW>
@@ -250,8 +272,15 @@ __device__ __forceinline__ void j_add(BW<NW> &j0, BW<NW> &j1, const BW<NW> &x, u
             }                                                                            \
         } else {                                                                         \
             for (; i_ + 2 <= (N); i_ += 2) {                                             \
-                const BW<NW> x0 = mono_form<NW>(sd, w[q + i_] & 0xfffu, pl);             \
-                const BW<NW> x1 = mono_form<NW>(sd, w[q + i_ + 1] & 0xfffu, pl);         \
+                const uint32_t fa_ = w[q + i_] & 0xfffu, fb_ = w[q + i_ + 1] & 0xfffu;   \
+                const uint4 ea_ = sd[fa_], eb_ = sd[fb_];                                \
+                BW<NW> x0, x1;                                                           \
+                if (((ea_.x ^ eb_.x) & 0x87u) == 0 && (ea_.x & 0x87u) <= kPairMaxCls) {  \
+                    mono_entry2<NW>(ea_, eb_, pl, x0, x1);                               \
+                } else {                                                                 \
+                    x0 = mono_form<NW>(sd, fa_, pl);                                     \
+                    x1 = mono_form<NW>(sd, fb_, pl);                                     \
+                }                                                                        \
                 OP(x0);                                                                  \
                 OP(x1);                                                                  \
             }                                                                            \

@@ -1,0 +1,8 @@
+set -x
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q --timeout 600 -k "mono or cultivation" > gpurun_out/pytest_mono26.log 2>&1; echo pytest=$?
+tail -2 gpurun_out/pytest_mono26.log
+timeout 600 python tools/gpu/time_shot.py --model data/c3_cultivation_proxy.zxs.gz --shots 3637248 --reps 3 --tag cult_mono_v12_pairs 2>&1 | tee -a gpurun_out/t26.json
+timeout 300 python tools/gpu/time_shot.py --model tests/golden/surface_d3_xmem_9t.zxs --shots 3637248 --reps 3 --tag 9t_mono_v12_pairs 2>&1 | tee -a gpurun_out/t26.json
+timeout 300 python tools/gpu/time_shot.py --model tests/golden/c4_color_d5_rz3.zxs --shots 67108864 --reps 3 --tag c4_v12 2>&1 | tee -a gpurun_out/t26.json

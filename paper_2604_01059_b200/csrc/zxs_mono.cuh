@@ -463,15 +463,21 @@ __global__ void __launch_bounds__(MonoCfg<NW>::kWarps * 32, 1) mono_kernel(const
                             ns[64] = j1;
                             continue;
                         }
-                        // epilogue: acc[s] += Re(c' i^J) for the non-zero shots, in term order
+                        // epilogue: acc[s] += Re(c' i^J) = {re, -im, -re, im}[J] for the non-zero shots,
+                        // in term order; the sign is a flip of the high word's sign bit
+                        const uint32_t re_lo = uint32_t(__double2loint(re)), re_hi = uint32_t(__double2hiint(re));
+                        const uint32_t im_lo = uint32_t(__double2loint(im)), im_hi = uint32_t(__double2hiint(im));
 #pragma unroll
                         for (int i = 0; i < NW; i++) {
                             const uint32_t neg = j0.w[i] ^ j1.w[i];
 #pragma unroll
                             for (int s = 0; s < 32; s++) {
-                                const double v = ((j0.w[i] >> s) & 1u) ? im : re;
-                                const double sv = ((neg >> s) & 1u) ? -v : v;
-                                if (!((z.w[i] >> s) & 1u)) acc[i * 32 + s] = __dadd_rn(acc[i * 32 + s], sv);
+                                const bool odd = (j0.w[i] >> s) & 1u;
+                                const uint32_t lo = odd ? im_lo : re_lo;
+                                const uint32_t hi = (odd ? im_hi : re_hi) ^ ((neg << (31 - s)) & 0x80000000u);
+                                if (!((z.w[i] >> s) & 1u)) {
+                                    acc[i * 32 + s] = __dadd_rn(acc[i * 32 + s], __hiloint2double(int(hi), int(lo)));
+                                }
                             }
                         }
                     }

@@ -956,11 +956,12 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                 };
                 std::stable_sort(recs_sorted.begin(), recs_sorted.end(),
                                  [&](uint64_t x, uint64_t y) { return cls_of(x) > cls_of(y); });
-                for (uint32_t kind : {zxs_dev::kRecAdd, zxs_dev::kRecSub, zxs_dev::kRecAdd2, zxs_dev::kRecZ,
-                                      zxs_dev::kRecZn, zxs_dev::kRecGen}) {
+                // one-form records of every kind (sorted by class: mono_kernel pairs them), then GEN
+                for (int gen_pass = 0; gen_pass < 2; gen_pass++) {
                     for (uint64_t tok : recs_sorted) {
                         const uint32_t r = remap(uint32_t(tok));
-                        if ((r >> 28) != kind) continue;
+                        const uint32_t kind = r >> 28;
+                        if ((kind == zxs_dev::kRecGen) != (gen_pass == 1)) continue;
                         nw.push_back(r);
                         if (tok >> 32) nw.push_back(uint32_t((tok >> 32) - 1));
                         recs++;

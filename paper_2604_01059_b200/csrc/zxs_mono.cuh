@@ -254,25 +254,28 @@ __device__ __forceinline__ void j_add(BW<NW> &j0, BW<NW> &j1, const BW<NW> &x, u
     }
 }
 
-// Record runs of one kind, forms of four (NW = 1) or two (NW = 2) records
-// formed together (independent shared loads in flight), then applied.
+// One-form records, forms of four (NW = 1) or two (NW = 2) records formed
+// together (independent shared loads in flight), then applied by kind.
 #define ZXS_MONO_RUN(N, OP)                                                              \
     {                                                                                    \
         uint32_t i_ = 0;                                                                 \
         if constexpr (NW == 1) {                                                         \
             for (; i_ + 4 <= (N); i_ += 4) {                                             \
-                const BW<NW> x0 = mono_form<NW>(sd, w[q + i_] & 0xfffu, pl);             \
-                const BW<NW> x1 = mono_form<NW>(sd, w[q + i_ + 1] & 0xfffu, pl);         \
-                const BW<NW> x2 = mono_form<NW>(sd, w[q + i_ + 2] & 0xfffu, pl);         \
-                const BW<NW> x3 = mono_form<NW>(sd, w[q + i_ + 3] & 0xfffu, pl);         \
-                OP(x0);                                                                  \
-                OP(x1);                                                                  \
-                OP(x2);                                                                  \
-                OP(x3);                                                                  \
+                const uint32_t r0_ = w[q + i_], r1_ = w[q + i_ + 1];                     \
+                const uint32_t r2_ = w[q + i_ + 2], r3_ = w[q + i_ + 3];                 \
+                const BW<NW> x0 = mono_form<NW>(sd, r0_ & 0xfffu, pl);                   \
+                const BW<NW> x1 = mono_form<NW>(sd, r1_ & 0xfffu, pl);                   \
+                const BW<NW> x2 = mono_form<NW>(sd, r2_ & 0xfffu, pl);                   \
+                const BW<NW> x3 = mono_form<NW>(sd, r3_ & 0xfffu, pl);                   \
+                OP(r0_, x0);                                                             \
+                OP(r1_, x1);                                                             \
+                OP(r2_, x2);                                                             \
+                OP(r3_, x3);                                                             \
             }                                                                            \
         } else {                                                                         \
             for (; i_ + 2 <= (N); i_ += 2) {                                             \
-                const uint32_t fa_ = w[q + i_] & 0xfffu, fb_ = w[q + i_ + 1] & 0xfffu;   \
+                const uint32_t r0_ = w[q + i_], r1_ = w[q + i_ + 1];                     \
+                const uint32_t fa_ = r0_ & 0xfffu, fb_ = r1_ & 0xfffu;                   \
                 const uint4 ea_ = sd[fa_], eb_ = sd[fb_];                                \
                 BW<NW> x0, x1;                                                           \
                 if (((ea_.x ^ eb_.x) & 0x87u) == 0 && (ea_.x & 0x87u) <= kPairMaxCls) {  \
@@ -281,21 +284,32 @@ __device__ __forceinline__ void j_add(BW<NW> &j0, BW<NW> &j1, const BW<NW> &x, u
                     x0 = mono_form<NW>(sd, fa_, pl);                                     \
                     x1 = mono_form<NW>(sd, fb_, pl);                                     \
                 }                                                                        \
-                OP(x0);                                                                  \
-                OP(x1);                                                                  \
+                OP(r0_, x0);                                                             \
+                OP(r1_, x1);                                                             \
             }                                                                            \
         }                                                                                \
         for (; i_ < (N); i_++) {                                                         \
-            const BW<NW> x0 = mono_form<NW>(sd, w[q + i_] & 0xfffu, pl);                 \
-            OP(x0);                                                                      \
+            const uint32_t r0_ = w[q + i_];                                              \
+            const BW<NW> x0 = mono_form<NW>(sd, r0_ & 0xfffu, pl);                       \
+            OP(r0_, x0);                                                                 \
         }                                                                                \
         q += (N);                                                                        \
     }
 #define ZXS_OP_ADD(x) { j1 = bw_xor<NW>(j1, bw_and<NW>(j0, x)); j0 = bw_xor<NW>(j0, x); }
+// op of a record word r on (Z, J0, J1): the kind is warp-uniform (one uniform branch)
+#define ZXS_OP_KIND(r, x)                  \
+    switch ((r) >> 28) {                   \
+        case kRecAdd: ZXS_OP_ADD(x); break; \
+        case kRecSub: ZXS_OP_SUB(x); break; \
+        case kRecAdd2: ZXS_OP_ADD2(x); break; \
+        case kRecZ: ZXS_OP_Z(x); break;     \
+        default: ZXS_OP_ZN(x); break;       \
+    }
 #define ZXS_OP_SUB(x) { j1 = bw_xor<NW>(j1, bw_andn<NW>(j0, x)); j0 = bw_xor<NW>(j0, x); }
 #define ZXS_OP_ADD2(x) { j1 = bw_xor<NW>(j1, x); }
 #define ZXS_OP_Z(x) { z = bw_or<NW>(z, x); }
 #define ZXS_OP_ZN(x) { z = bw_or<NW>(z, bw_not<NW>(x)); }
+#define ZXS_OP_ANY(r, x) ZXS_OP_KIND(r, x)
 
 template <int NW>
 __global__ void __launch_bounds__(MonoCfg<NW>::kWarps * 32, 1) mono_kernel(const __grid_constant__ MonoArgs h) {
@@ -435,11 +449,13 @@ __global__ void __launch_bounds__(MonoCfg<NW>::kWarps * 32, 1) mono_kernel(const
                             j0 = ps[32];
                             j1 = ps[64];
                         }
-                        ZXS_MONO_RUN(h1 & 0xffu, ZXS_OP_ADD)
-                        ZXS_MONO_RUN((h1 >> 8) & 0xffu, ZXS_OP_SUB)
-                        ZXS_MONO_RUN((h1 >> 16) & 0xffu, ZXS_OP_ADD2)
-                        ZXS_MONO_RUN(h1 >> 24, ZXS_OP_Z)
-                        ZXS_MONO_RUN(h2 & 0xffu, ZXS_OP_ZN)
+                        {
+                            // one-form records (any kind, ordered by size class): one copy of the
+                            // form code for all kinds keeps the kernel within the instruction cache
+                            const uint32_t ns = (h1 & 0xffu) + ((h1 >> 8) & 0xffu) + ((h1 >> 16) & 0xffu) + (h1 >> 24) +
+                                                (h2 & 0xffu);
+                            ZXS_MONO_RUN(ns, ZXS_OP_ANY)
+                        }
                         for (uint32_t g = 0; g < (h0 & 0xffu); g++) {  // two-form records
                             const uint32_t r = w[q], gw = w[q + 1];
                             q += 2;

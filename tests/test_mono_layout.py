@@ -72,24 +72,25 @@ def form_sel(dict_, f):
 
 
 def apply_node_records(w, q, h0, h1, h2, form, J, Z):
-    """mono_kernel's record runs (by kind) and two-form records on (J, Z); returns the new position."""
-    for kind, n in ((REC_ADD, h1 & 0xFF), (REC_SUB, (h1 >> 8) & 0xFF), (REC_ADD2, (h1 >> 16) & 0xFF),
-                    (REC_Z, h1 >> 24), (REC_ZN, h2 & 0xFF)):
-        for _ in range(n):
-            r = int(w[q])
-            q += 1
-            assert r >> 28 == kind
-            a = form(r & 0xFFF)
-            if kind == REC_ADD:
-                J += a
-            elif kind == REC_SUB:
-                J -= a
-            elif kind == REC_ADD2:
-                J += 2 * a
-            elif kind == REC_Z:
-                Z |= a == 1
-            else:
-                Z |= a == 0
+    """mono_kernel's one-form records (any kind order) and two-form records on (J, Z);
+    returns the new position."""
+    ns = (h1 & 0xFF) + ((h1 >> 8) & 0xFF) + ((h1 >> 16) & 0xFF) + (h1 >> 24) + (h2 & 0xFF)
+    for _ in range(ns):
+        r = int(w[q])
+        q += 1
+        kind = r >> 28
+        a = form(r & 0xFFF)
+        if kind == REC_ADD:
+            J += a
+        elif kind == REC_SUB:
+            J -= a
+        elif kind == REC_ADD2:
+            J += 2 * a
+        elif kind == REC_Z:
+            Z |= a == 1
+        else:
+            assert kind == REC_ZN
+            Z |= a == 0
     for _ in range(h0 & 0xFF):
         r, g = int(w[q]), int(w[q + 1])
         q += 2

@@ -305,6 +305,15 @@ zxs_status zxs_probability_of_at(zxs_sampler *s, const uint8_t *outcome, uint32_
  */
 zxs_status zxs_probability_of(zxs_sampler *s, const uint8_t *outcome, uint32_t n_outcome, double *out);
 
+/*
+ * Health check of the compiled tensors (SURVEY finding 3): the reference
+ * computes max |Im P| / |P| (phase_terms.cpp:134-141) but never checks it;
+ * physically P is real. Evaluates every chain tensor with the exact kernel on
+ * `samples` random parameter vectors; out[num_components] receives each
+ * component's maximum ratio.
+ */
+zxs_status zxs_imag_health(zxs_sampler *s, uint64_t samples, uint64_t seed, double *out);
+
 /* Philox4x32-10 uniform_at (rng.hpp:31-41) evaluated on the device, n draws
    at indices first_index .. first_index+n-1. */
 zxs_status zxs_philox_uniform(int device, uint64_t seed, uint32_t stream, uint64_t first_index,

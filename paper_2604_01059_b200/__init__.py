@@ -19,6 +19,7 @@ from .sampler import (  # noqa: F401
     encode_shots,
     eval_batch,
     eval_batch_mono,
+    imag_health,
     measure_fp64_peak,
     measure_philox_peak,
     measure_smem_peak,
@@ -35,7 +36,7 @@ from .sampler import (  # noqa: F401
 
 __all__ = [
     "FORMAT_01", "FORMAT_B8", "encode_shots", "sample_encoded", "MODE_DETECTORS", "MODE_MEASUREMENTS", "BatchEvalResult", "CompiledSampler", "SampleRecord",
-    "SamplerOptions", "count_outputs", "eval_batch", "eval_batch_mono", "measure_fp64_peak", "measure_philox_peak", "measure_smem_peak",
+    "SamplerOptions", "count_outputs", "eval_batch", "eval_batch_mono", "imag_health", "measure_fp64_peak", "measure_philox_peak", "measure_smem_peak",
     "philox_uniform", "probability_of", "probability_of_at",
     "sample_detectors", "sample_error_batch", "sample_given_f", "sample_measurements", "sparse_eligible",
 ]

@@ -78,6 +78,7 @@ SIGNATURES = (
     ("zxs_sample_given_f", ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _u64p, _dp,
                                           _u64p]),
     ("zxs_probability_of", ctypes.c_int, [_vp, _u8p, ctypes.c_uint32, _dp]),
+    ("zxs_imag_health", ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint64, _dp]),
     ("zxs_probability_of_at", ctypes.c_int, [_vp, _u8p, ctypes.c_uint32, _u8p, ctypes.c_uint32, _dp]),
     ("zxs_philox_uniform", ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
                                           ctypes.c_uint64, _dp]),

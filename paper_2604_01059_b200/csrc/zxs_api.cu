@@ -2388,6 +2388,44 @@ zxs_status zxs_eval_batch_mono(zxs_sampler *s, uint32_t component, uint32_t chai
     });
 }
 
+// Compile-time health check (SURVEY finding 3): the reference records
+// max |Im P| / |P| over a batch (phase_terms.cpp:134-141) but never checks it.
+// Here every chain tensor of every component is evaluated with the exact
+// kernel on `samples` uniformly random parameter vectors; out[c] = the
+// component's maximum ratio.
+zxs_status zxs_imag_health(zxs_sampler *s, uint64_t samples, uint64_t seed, double *out) {
+    return guarded([&] {
+        if (!s || !out) fail(ZXS_INVALID_ARGUMENT, "null argument");
+        if (samples == 0) fail(ZXS_INVALID_ARGUMENT, "samples must be positive");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard g(s->device);
+        uint64_t x = seed ^ 0x9E3779B97F4A7C15ull;
+        auto next = [&]() {  // splitmix64
+            uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+            return z ^ (z >> 31);
+        };
+        const uint64_t words = (samples + 63) / 64;
+        std::vector<double> vals(samples);
+        for (size_t c = 0; c + 1 < s->comp_out_begin.size(); c++) {
+            double worst = 0.0;
+            for (uint32_t t = s->comp_tensor_begin[c]; t < s->comp_tensor_begin[c + 1]; t++) {
+                const uint32_t W = std::max<uint32_t>(1, s->tensor_width[t]);
+                std::vector<uint64_t> params(size_t(W) * words);
+                for (auto &w : params) w = next();
+                if (samples & 63) {
+                    for (uint32_t p = 0; p < W; p++) params[p * words + words - 1] &= (uint64_t(1) << (samples & 63)) - 1;
+                }
+                double mi = 0.0;
+                eval_on_device(s, t, params.data(), W, samples, vals.data(), &mi);
+                worst = std::max(worst, mi);
+            }
+            out[c] = worst;
+        }
+    });
+}
+
 // probability_of_at (sampler.cpp:360-368) -> outcome_probability_given
 // (sampler.cpp:324-356), every eval on the device.
 zxs_status zxs_probability_of_at(zxs_sampler *s, const uint8_t *outcome, uint32_t n_outcome,

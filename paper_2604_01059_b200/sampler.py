@@ -312,6 +312,14 @@ def probability_of(cs: CompiledSampler, outcome) -> float:
     return out.value
 
 
+def imag_health(cs: CompiledSampler, samples: int = 4096, seed: int = 1) -> np.ndarray:
+    """Per component, max |Im P| / |P| over random parameter vectors (phase_terms.cpp:134-141;
+    SURVEY finding 3: the reference never checks it)."""
+    out = np.zeros(max(len(cs.components), 1), np.float64)
+    _native.check(_native.lib().zxs_imag_health(cs.handle, samples, seed, out.ctypes.data_as(_dp)))
+    return out[:len(cs.components)]
+
+
 def measure_philox_peak(device: int = 0) -> float:
     """Philox4x32-10 blocks/s of the draw code alone (same-op-mix roofline)."""
     out = ctypes.c_double()

@@ -376,3 +376,20 @@ def test_kernel_timing_counts_launches():
     t = cm.kernel_times()
     cm.kernel_timing(False)
     assert t["shot_kernel"][1] == 1 and t["mono_kernel"][1] == 1
+
+
+def test_imag_health_check():
+    """SURVEY finding 3: clean circuits report ~1e-15; the 9-T proxy's magic
+    component carries non-vanishing imaginary parts (the reference never checks)."""
+    clean = zx.imag_health(model("c2_surface_d3_xmem_t"), samples=2048)
+    assert clean.max() < 1e-9
+    dirty = zx.imag_health(model("surface_d3_xmem_9t"), samples=2048)
+    assert dirty.max() > 1e-4
+    # the same metric as the reference's eval_batch on the same parameters
+    orc = coracle.OracleModel.load(golden_path("c2_surface_d3_xmem_t"))
+    rng = np.random.default_rng(3)
+    cs = model("c2_surface_d3_xmem_t")
+    P = rng.integers(0, 2**63, size=(int(orc.arrays["tensor_param_width"][1]), 32), dtype=np.uint64)
+    mi_dev = zx.eval_batch(cs, 0, 1, P, 2048).max_imag_ratio
+    _, mi_ref = orc.eval_batch(int(orc.arrays["comp_tensor_begin"][0]) + 1, P, 2048)
+    assert abs(mi_dev - mi_ref) <= 1e-9 * max(mi_ref, 1e-300)  # hypot may differ in the last ulp

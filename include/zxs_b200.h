@@ -310,7 +310,7 @@ zxs_status zxs_probability_of(zxs_sampler *s, const uint8_t *outcome, uint32_t n
  * computes max |Im P| / |P| (phase_terms.cpp:134-141) but never checks it;
  * physically P is real. Evaluates every chain tensor with the exact kernel on
  * `samples` random parameter vectors; out[num_components] receives each
- * component's maximum ratio.
+ * component's largest max|Im P| / max|Re P| over its chain tensors.
  */
 zxs_status zxs_imag_health(zxs_sampler *s, uint64_t samples, uint64_t seed, double *out);
 

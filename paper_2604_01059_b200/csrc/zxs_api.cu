@@ -120,6 +120,7 @@ struct zxs_sampler {
     int device = 0;
     uint32_t mode = 0;
     int fw_template = 1;
+    int shots_per_lane = 2;  // shot_kernel S (ZXS_SHOTS_PER_LANE)
     DevModel m{};
     zxs_sampler_info info{};
     bool all_outputs_covered = true;
@@ -239,19 +240,25 @@ struct zxs_sampler {
 
 namespace {
 
-template <int FW>
+template <int FW, int S>
 const void *kernel_ptr(bool param_mechs) {
-    return param_mechs ? reinterpret_cast<const void *>(&zxs_dev::shot_kernel<FW, true>)
-                       : reinterpret_cast<const void *>(&zxs_dev::shot_kernel<FW, false>);
+    return param_mechs ? reinterpret_cast<const void *>(&zxs_dev::shot_kernel<FW, true, S>)
+                       : reinterpret_cast<const void *>(&zxs_dev::shot_kernel<FW, false, S>);
 }
 
-const void *shot_kernel_for(int fw, bool param_mechs) {
+// S = shots per lane: 4 for narrow f (FW <= 2: the f register file stays small),
+// else 2.
+const void *shot_kernel_for(int fw, bool param_mechs, int S) {
+    if (S == 4) {
+        if (fw == 1) return kernel_ptr<1, 4>(param_mechs);
+        if (fw == 2) return kernel_ptr<2, 4>(param_mechs);
+    }
     switch (fw) {
-        case 1: return kernel_ptr<1>(param_mechs);
-        case 2: return kernel_ptr<2>(param_mechs);
-        case 4: return kernel_ptr<4>(param_mechs);
-        case 8: return kernel_ptr<8>(param_mechs);
-        case 16: return kernel_ptr<16>(param_mechs);
+        case 1: return kernel_ptr<1, 2>(param_mechs);
+        case 2: return kernel_ptr<2, 2>(param_mechs);
+        case 4: return kernel_ptr<4, 2>(param_mechs);
+        case 8: return kernel_ptr<8, 2>(param_mechs);
+        case 16: return kernel_ptr<16, 2>(param_mechs);
     }
     fail(ZXS_UNSUPPORTED, "f_width above 1024 is not supported");
 }
@@ -260,7 +267,7 @@ constexpr int kThreads = 256;
 
 size_t shot_smem_bytes(const zxs_sampler *s) {  // one warp per CTA
     const size_t sh_off = (2 * size_t(s->m.num_outputs) + 3) & ~size_t(3);
-    return (sh_off + 16 * size_t(s->light_tables)) * 4 + size_t(zxs_dev::kS) * s->m.col_stride * 4;
+    return (sh_off + 16 * size_t(s->light_tables)) * 4 + size_t(s->shots_per_lane) * s->m.col_stride * 4;
 }
 
 void validate_csr(const char *name, const uint32_t *b, size_t n, size_t total) {
@@ -1695,7 +1702,9 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         CK(cudaEventCreateWithFlags(&s->ev_copied[i], cudaEventDisableTiming));
     }
     CK(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, s->device));
-    const void *kern = shot_kernel_for(FW, s->param_mechs);
+    s->shots_per_lane = FW <= 2 ? 4 : 2;
+    if (const char *e = std::getenv("ZXS_SHOTS_PER_LANE")) s->shots_per_lane = (std::atoi(e) == 4 && FW <= 2) ? 4 : 2;
+    const void *kern = shot_kernel_for(FW, s->param_mechs, s->shots_per_lane);
     size_t smem = shot_smem_bytes(s);
     if (smem > 48 * 1024) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -1765,8 +1774,9 @@ void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
     a.ext = s->ext;
     a.err = s->dev_err;
     for (int i = 0; i < 10; i++) a.k0_round[i] = uint32_t(a.seed) + uint32_t(i) * 0x9E3779B9u;
-    // One warp tile = 64 shots = one u64 output word, written in full.
-    a.n_tiles = (a.shots + zxs_dev::kTileShots - 1) / zxs_dev::kTileShots;
+    // One warp tile = 32 * S shots (S/2 u64 output words per output).
+    const uint64_t tile_shots = 32ull * s->shots_per_lane;
+    a.n_tiles = (a.shots + tile_shots - 1) / tile_shots;
     if (a.n_tiles == 0) return;
     uint64_t cap = uint64_t(s->sm_count) * s->blocks_per_sm;
     unsigned grid = unsigned(std::min(a.n_tiles, cap));
@@ -1779,7 +1789,8 @@ void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
     void *args[] = {&a, s->param_mechs ? static_cast<void *>(s->mech_table.get()) : static_cast<void *>(s->mech_table1.get())};
     cudaEvent_t t0 = nullptr;
     s->time_begin(0, st, t0);
-    CK(cudaLaunchKernel(shot_kernel_for(s->fw_template, s->param_mechs), dim3(grid), dim3(32), args, smem, st));
+    CK(cudaLaunchKernel(shot_kernel_for(s->fw_template, s->param_mechs, s->shots_per_lane), dim3(grid), dim3(32), args,
+                        smem, st));
     s->time_end(0, st, t0);
     if (heavy && s->has_mono) {
         s->time_begin(2, st, t0);
@@ -2305,16 +2316,17 @@ zxs_status zxs_sample_given_f(zxs_sampler *s, uint64_t seed, uint64_t first_shot
 
 namespace {
 void eval_on_device(zxs_sampler *s, uint32_t tensor, const uint64_t *host_params, uint32_t param_cols,
-                    uint64_t shots, double *host_values, double *max_imag) {
+                    uint64_t shots, double *host_values, double *max_imag, double *host_imag = nullptr) {
     const uint64_t words = (shots + 63) / 64;
     cudaStream_t st = s->stream;
     size_t pbytes = size_t(words) * param_cols * 8;
     size_t vbytes = size_t(shots) * 8;
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-    char *base = s->scratch_get(al(pbytes) + al(vbytes) + 256);
+    char *base = s->scratch_get(al(pbytes) + 2 * al(vbytes) + 256);
     auto *dp = reinterpret_cast<uint32_t *>(base);
     auto *dv = reinterpret_cast<double *>(base + al(pbytes));
     auto *dmi = reinterpret_cast<unsigned long long *>(base + al(pbytes) + al(vbytes));
+    auto *dimag = reinterpret_cast<double *>(base + al(pbytes) + al(vbytes) + 256);
     if (pbytes) CK(cudaMemcpyAsync(dp, host_params, pbytes, cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(dmi, 0, 8, st));
     uint32_t col_stride = std::max<uint32_t>(4, (param_cols + 3) & ~3u);
@@ -2326,9 +2338,10 @@ void eval_on_device(zxs_sampler *s, uint32_t tensor, const uint64_t *host_params
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     }
     zxs_dev::eval_kernel<<<grid, kThreads, smem, st>>>(s->m, tensor, dp, 2 * words, param_cols, col_stride, shots,
-                                                       n_tiles, dv, dmi);
+                                                       n_tiles, dv, dmi, host_imag ? dimag : nullptr);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(host_values, dv, vbytes, cudaMemcpyDeviceToHost, st));
+    if (host_imag) CK(cudaMemcpyAsync(host_imag, dimag, vbytes, cudaMemcpyDeviceToHost, st));
     unsigned long long mib = 0;
     CK(cudaMemcpyAsync(&mib, dmi, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -2389,10 +2402,11 @@ zxs_status zxs_eval_batch_mono(zxs_sampler *s, uint32_t component, uint32_t chai
 }
 
 // Compile-time health check (SURVEY finding 3): the reference records
-// max |Im P| / |P| over a batch (phase_terms.cpp:134-141) but never checks it.
+// max |Im P| / |P| per shot (phase_terms.cpp:134-141) but never checks it.
 // Here every chain tensor of every component is evaluated with the exact
 // kernel on `samples` uniformly random parameter vectors; out[c] = the
-// component's maximum ratio.
+// component's largest max|Im P| / max|Re P| over its tensors (relative to the
+// tensor's scale, so rounding noise on vanishing P does not register).
 zxs_status zxs_imag_health(zxs_sampler *s, uint64_t samples, uint64_t seed, double *out) {
     return guarded([&] {
         if (!s || !out) fail(ZXS_INVALID_ARGUMENT, "null argument");
@@ -2417,9 +2431,14 @@ zxs_status zxs_imag_health(zxs_sampler *s, uint64_t samples, uint64_t seed, doub
                 if (samples & 63) {
                     for (uint32_t p = 0; p < W; p++) params[p * words + words - 1] &= (uint64_t(1) << (samples & 63)) - 1;
                 }
-                double mi = 0.0;
-                eval_on_device(s, t, params.data(), W, samples, vals.data(), &mi);
-                worst = std::max(worst, mi);
+                std::vector<double> ims(samples);
+                eval_on_device(s, t, params.data(), W, samples, vals.data(), nullptr, ims.data());
+                double pmax = 0.0, imax = 0.0;
+                for (uint64_t i = 0; i < samples; i++) {
+                    pmax = std::max(pmax, std::fabs(vals[i]));
+                    imax = std::max(imax, std::fabs(ims[i]));
+                }
+                if (pmax > 0) worst = std::max(worst, imax / pmax);
             }
             out[c] = worst;
         }

@@ -85,7 +85,6 @@ struct MechTable {
     MechFast fast[N];
     LightProg prog;
 };
-static_assert(kS == 2, "output stores pack two 32-shot words");
 
 struct LaunchArgs {
     DevModel m;
@@ -189,79 +188,81 @@ __device__ __forceinline__ void philox_tail(const PhiloxPre (&p)[S], uint32_t k1
 // tile: acc[s] = sum_t c_t prod_k h_tk[(a<<1)|b] for this lane's shot in
 // sub-tile s, accumulated in the reference's order (terms in order, factors
 // in order, acc starting at 0), every product and sum rounded separately.
+template <int S = kS>
 __device__ __forceinline__ void eval_tensor(const DevModel &m, uint32_t t, const uint32_t *cols, uint32_t stride,
-                                            uint32_t lane, double2 (&acc)[kS]) {
+                                            uint32_t lane, double2 (&acc)[S]) {
 #pragma unroll
-    for (int s = 0; s < kS; s++) acc[s] = make_double2(0.0, 0.0);
+    for (int s = 0; s < S; s++) acc[s] = make_double2(0.0, 0.0);
     const uint32_t t0 = m.tensor_term_begin[t], t1 = m.tensor_term_begin[t + 1];
     for (uint32_t term = t0; term < t1; term++) {
         const double2 c = m.term_c[term];
-        double2 prod[kS];
+        double2 prod[S];
 #pragma unroll
-        for (int s = 0; s < kS; s++) prod[s] = c;
+        for (int s = 0; s < S; s++) prod[s] = c;
         const uint32_t k0 = m.term_factor_begin[term], k1 = m.term_factor_begin[term + 1];
         for (uint32_t k = k0; k < k1; k++) {
             const Factor fr = m.factors[k];
             const uint16_t *sel = m.selectors + fr.sel;
-            uint32_t aw[kS] = {}, bw[kS] = {};
+            uint32_t aw[S] = {}, bw[S] = {};
             for (uint32_t i = 0; i < fr.nu; i++) {
                 const uint32_t p = sel[i];
 #pragma unroll
-                for (int s = 0; s < kS; s++) aw[s] ^= cols[s * stride + p];
+                for (int s = 0; s < S; s++) aw[s] ^= cols[s * stride + p];
             }
             for (uint32_t i = 0; i < fr.nv; i++) {
                 const uint32_t p = sel[fr.nu + i];
 #pragma unroll
-                for (int s = 0; s < kS; s++) bw[s] ^= cols[s * stride + p];
+                for (int s = 0; s < S; s++) bw[s] ^= cols[s * stride + p];
             }
             const double2 *h = m.h_table + 4 * fr.table;
 #pragma unroll
-            for (int s = 0; s < kS; s++) {
+            for (int s = 0; s < S; s++) {
                 const uint32_t idx = (((aw[s] >> lane) & 1u) << 1) | ((bw[s] >> lane) & 1u);
                 prod[s] = cmul_rn(prod[s], h[idx]);
             }
         }
 #pragma unroll
-        for (int s = 0; s < kS; s++) acc[s] = cadd_rn(acc[s], prod[s]);
+        for (int s = 0; s < S; s++) acc[s] = cadd_rn(acc[s], prod[s]);
     }
 }
 
 // eval_tensor over the uniform LightProg: same products and sums in the
 // reference's order (phase_terms.cpp:121-131); h tables staged in shared
 // memory (sh, 4 entries per table), selected per lane by (a << 1) | b.
+template <int S = kS>
 __device__ __forceinline__ void eval_tensor_light(const LightProg &pg, uint32_t t, const uint32_t *cols,
                                                   uint32_t stride, uint32_t lane, const double2 *sh,
-                                                  double2 (&acc)[kS]) {
+                                                  double2 (&acc)[S]) {
 #pragma unroll
-    for (int s = 0; s < kS; s++) acc[s] = make_double2(0.0, 0.0);
+    for (int s = 0; s < S; s++) acc[s] = make_double2(0.0, 0.0);
     const uint32_t t0 = pg.tensor_term[t], t1 = pg.tensor_term[t + 1];
     for (uint32_t term = t0; term < t1; term++) {
         const double2 c = pg.term_c[term];
-        double2 prod[kS];
+        double2 prod[S];
 #pragma unroll
-        for (int s = 0; s < kS; s++) prod[s] = c;
+        for (int s = 0; s < S; s++) prod[s] = c;
         const uint32_t k0 = pg.term_factor[term], k1 = pg.term_factor[term + 1];
         for (uint32_t k = k0; k < k1; k++) {
-            uint32_t aw[kS] = {}, bw[kS] = {};
+            uint32_t aw[S] = {}, bw[S] = {};
             for (unsigned long long x = pg.fu[k]; x; x &= x - 1) {
                 const uint32_t p = __ffsll((long long)x) - 1;
 #pragma unroll
-                for (int s = 0; s < kS; s++) aw[s] ^= cols[s * stride + p];
+                for (int s = 0; s < S; s++) aw[s] ^= cols[s * stride + p];
             }
             for (unsigned long long x = pg.fv[k]; x; x &= x - 1) {
                 const uint32_t p = __ffsll((long long)x) - 1;
 #pragma unroll
-                for (int s = 0; s < kS; s++) bw[s] ^= cols[s * stride + p];
+                for (int s = 0; s < S; s++) bw[s] ^= cols[s * stride + p];
             }
             const double2 *h = sh + 4 * pg.ftable[k];
 #pragma unroll
-            for (int s = 0; s < kS; s++) {
+            for (int s = 0; s < S; s++) {
                 const uint32_t idx = (((aw[s] >> lane) & 1u) << 1) | ((bw[s] >> lane) & 1u);
                 prod[s] = cmul_rn(prod[s], h[idx]);
             }
         }
 #pragma unroll
-        for (int s = 0; s < kS; s++) acc[s] = cadd_rn(acc[s], prod[s]);
+        for (int s = 0; s < S; s++) acc[s] = cadd_rn(acc[s], prod[s]);
     }
 }
 
@@ -274,12 +275,11 @@ __device__ __forceinline__ void report_ratio_error(unsigned long long *err, uint
 // lane's two draws (first entry, then the rest of a joint table in order).
 // Kept out of line so the divergent scan does not pull the draw loop's
 // counters and Philox keys off the uniform datapath.
-__device__ __noinline__ uint2 resolve_flips(uint64_t r0, uint64_t r1, MechRec md, const uint32_t *ext_begin,
-                                            const ulonglong2 *ext, uint32_t mi) {
-    uint32_t out[kS];
-    const uint64_t r[kS] = {r0, r1};
+template <int S>
+__device__ __noinline__ void resolve_flips(const uint64_t (&r)[S], MechRec md, const uint32_t *ext_begin,
+                                           const ulonglong2 *ext, uint32_t mi, uint32_t (&out)[S]) {
 #pragma unroll
-    for (int s = 0; s < kS; s++) {
+    for (int s = 0; s < S; s++) {
         uint32_t flip = kNoFlip;
         if (r[s] <= md.lim0) {
             flip = md.flip0;
@@ -295,14 +295,37 @@ __device__ __noinline__ uint2 resolve_flips(uint64_t r0, uint64_t r1, MechRec md
         }
         out[s] = flip;
     }
-    return make_uint2(out[0], out[1]);
 }
 
-template <int FW, bool PARAM_MECHS>
+// Stores the lane group's S consecutive 32-bit output words of a tile (row
+// `row`, first word `w0`), only those below the row length `ld` (the last
+// tile of a range may be partial).
+template <int S>
+__device__ __forceinline__ void store_words(uint32_t *row, uint64_t w0, uint64_t ld, const uint32_t (&w)[S]) {
+    if constexpr (S == 2) {
+        *reinterpret_cast<uint2 *>(row + w0) = make_uint2(w[0], w[1]);  // ld is even: always in range
+    } else {
+        if (w0 + S <= ld) {
+            if ((reinterpret_cast<uintptr_t>(row + w0) & 15) == 0) {
+                *reinterpret_cast<uint4 *>(row + w0) = make_uint4(w[0], w[1], w[2], w[3]);
+            } else {  // odd 64-bit row pitch: rows are only 8-byte aligned
+                *reinterpret_cast<uint2 *>(row + w0) = make_uint2(w[0], w[1]);
+                *reinterpret_cast<uint2 *>(row + w0 + 2) = make_uint2(w[2], w[3]);
+            }
+        } else {
+#pragma unroll
+            for (int s = 0; s < S; s++) {
+                if (w0 + s < ld) row[w0 + s] = w[s];
+            }
+        }
+    }
+}
+
+template <int FW, bool PARAM_MECHS, int S>
 #ifndef ZXS_MAXNREG
 #define ZXS_MAXNREG 96
 #endif
-__global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ LaunchArgs a,
+__global__ void __maxnreg__(S == 4 ? 128 : ZXS_MAXNREG) shot_kernel(const __grid_constant__ LaunchArgs a,
                                                    const __grid_constant__ MechTable<PARAM_MECHS ? kParamMechs : 1> mt) {
     extern __shared__ __align__(16) uint32_t smem[];
     // One warp per CTA: the tile loop depends only on blockIdx, so the
@@ -327,12 +350,12 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
     const uint32_t k2c = uint32_t(kP1c) ^ a.k0_round[1];
 
     for (uint64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
-        uint64_t local[kS], shot[kS];
-        uint32_t vmask[kS];
-        PhiloxPre pre[kS];
+        uint64_t local[S], shot[S];
+        uint32_t vmask[S];
+        PhiloxPre pre[S];
 #pragma unroll
-        for (int s = 0; s < kS; s++) {
-            local[s] = tile * kTileShots + 32 * s + lane;
+        for (int s = 0; s < S; s++) {
+            local[s] = tile * (32 * S) + 32 * s + lane;
             vmask[s] = __ballot_sync(kFull, local[s] < a.shots);
             shot[s] = a.first_shot + local[s];
             pre[s] = philox_pre(uint32_t(shot[s]), uint32_t(shot[s] >> 32), a.k0_round[0]);
@@ -342,37 +365,41 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
         if (a.fcols_in) {
             for (uint32_t c = lane; c < m.f_width; c += 32) {
 #pragma unroll
-                for (int s = 0; s < kS; s++) cols[s * m.col_stride + c] = a.fcols_in[c * a.fcols_ld32 + tile * kS + s];
+                for (int s = 0; s < S; s++) {
+                    const uint64_t wi = tile * S + s;
+                    cols[s * m.col_stride + c] = wi < a.fcols_ld32 ? a.fcols_in[c * a.fcols_ld32 + wi] : 0u;
+                }
             }
         } else {
-            uint64_t f[kS][FW];
+            uint64_t f[S][FW];
 #pragma unroll
             for (int w = 0; w < FW; w++) {
                 const uint64_t b = m.base_offset[w];
 #pragma unroll
-                for (int s = 0; s < kS; s++) f[s][w] = b;
+                for (int s = 0; s < S; s++) f[s][w] = b;
             }
             for (uint32_t mi = 0; mi < a.num_mech; mi++) {
                 // No early-out for mechanisms that cannot flip anything: a
                 // data-dependent `continue` here moves the key schedule off the
                 // uniform datapath. Such records never flip.
                 const MechFast mf = PARAM_MECHS ? mt.fast[mi] : a.fast_global[mi];
-                uint32_t rhi[kS], rlo[kS];
-                philox_tail<kS>(pre, seed_hi ^ mi, a.k0_round, k2c, a.k0_round[9] ^ mf.sense, rhi, rlo);
+                uint32_t rhi[S], rlo[S];
+                philox_tail<S>(pre, seed_hi ^ mi, a.k0_round, k2c, a.k0_round[9] ^ mf.sense, rhi, rlo);
                 // Common case: every lane's draw certainly resolves to "no flip"
                 // (no error); anything else takes one warp-uniform branch, which
                 // keeps the loop (and the key schedule) uniform.
                 bool busy = false;
 #pragma unroll
-                for (int s = 0; s < kS; s++) busy |= !(rhi[s] < mf.thr);
+                for (int s = 0; s < S; s++) busy |= !(rhi[s] < mf.thr);
                 if (__any_sync(kFull, busy)) {
                     const MechRec md = a.mech_global[mi];
-                    const uint64_t r0 = (uint64_t(rhi[0] ^ mf.sense) << 32) | rlo[0];
-                    const uint64_t r1 = (uint64_t(rhi[1] ^ mf.sense) << 32) | rlo[1];
-                    const uint2 fl = resolve_flips(r0, r1, md, a.ext_begin, a.ext, mi);
-                    const uint32_t flip[kS] = {fl.x, fl.y};
+                    uint64_t rr[S];
 #pragma unroll
-                    for (int s = 0; s < kS; s++) {
+                    for (int s = 0; s < S; s++) rr[s] = (uint64_t(rhi[s] ^ mf.sense) << 32) | rlo[s];
+                    uint32_t flip[S];
+                    resolve_flips<S>(rr, md, a.ext_begin, a.ext, mi, flip);
+#pragma unroll
+                    for (int s = 0; s < S; s++) {
                         if (flip[s] != kNoFlip) {
                             const uint64_t *mask = m.flip_mask + size_t(flip[s]) * FW;
 #pragma unroll
@@ -382,7 +409,7 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
                 }
             }
 #pragma unroll
-            for (int s = 0; s < kS; s++) {
+            for (int s = 0; s < S; s++) {
 #pragma unroll
                 for (int w = 0; w < FW; w++) {
 #pragma unroll
@@ -400,50 +427,62 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
         if (a.heavy_fcols) {
             for (uint32_t c = lane; c < m.f_width; c += 32) {
 #pragma unroll
-                for (int s = 0; s < kS; s++) a.heavy_fcols[c * a.heavy_ld32 + tile * kS + s] = cols[s * m.col_stride + c];
+                for (int s = 0; s < S; s++) {
+                    if (tile * S + s < a.heavy_ld32) a.heavy_fcols[c * a.heavy_ld32 + tile * S + s] = cols[s * m.col_stride + c];
+                }
             }
         }
         if (a.fcols_out) {
             for (uint32_t c = lane; c < m.f_width; c += 32) {
 #pragma unroll
-                for (int s = 0; s < kS; s++) a.fcols_out[c * a.fcols_ld32 + tile * kS + s] = cols[s * m.col_stride + c] & vmask[s];
+                for (int s = 0; s < S; s++) {
+                    if (tile * S + s < a.fcols_ld32) a.fcols_out[c * a.fcols_ld32 + tile * S + s] = cols[s * m.col_stride + c] & vmask[s];
+                }
             }
             __syncwarp();
             continue;
         }
 
         // ---- (4): direct outputs, lane-parallel over outputs
-        uint32_t mism[kS] = {0u, 0u};  // probability mode: shots whose direct outputs differ from the outcome
+        uint32_t mism[S] = {};  // probability mode: shots whose direct outputs differ from the outcome
         for (uint32_t d = lane; d < m.num_direct; d += 32) {
             const uint32_t od = m.direct_out[d];
-            uint32_t w[kS];
+            uint32_t w[S];
 #pragma unroll
-            for (int s = 0; s < kS; s++) w[s] = (od >> 31) ? kFull : 0u;
+            for (int s = 0; s < S; s++) w[s] = (od >> 31) ? kFull : 0u;
             for (uint32_t b = m.direct_bit_begin[d]; b < m.direct_bit_begin[d + 1]; b++) {
                 const uint32_t fb = m.direct_bits[b];
 #pragma unroll
-                for (int s = 0; s < kS; s++) w[s] ^= cols[s * m.col_stride + fb];
+                for (int s = 0; s < S; s++) w[s] ^= cols[s * m.col_stride + fb];
             }
             const uint32_t o = od & 0x7fffffffu;
             if (a.forced) {
                 const uint32_t want = a.forced[o] ? kFull : 0u;
 #pragma unroll
-                for (int s = 0; s < kS; s++) mism[s] |= w[s] ^ want;
+                for (int s = 0; s < S; s++) mism[s] |= w[s] ^ want;
                 continue;
             }
 #pragma unroll
-            for (int s = 0; s < kS; s++) w[s] &= vmask[s];
-            if (a.out32) {
-                *reinterpret_cast<uint2 *>(a.out32 + o * a.ld32 + tile * kS) = make_uint2(w[0], w[1]);
+            for (int s = 0; s < S; s++) w[s] &= vmask[s];
+            if (a.out32) store_words<S>(a.out32 + o * a.ld32, tile * S, a.ld32, w);
+            if (a.counts) {
+                uint32_t ones = 0;
+#pragma unroll
+                for (int s = 0; s < S; s++) ones += __popc(w[s]);
+                if (ones) atomicAdd(&scount[o], (unsigned long long)ones);
             }
-            if (a.counts && (w[0] | w[1])) atomicAdd(&scount[o], (unsigned long long)(__popc(w[0]) + __popc(w[1])));
         }
 
-        double pgiven[kS] = {1.0, 1.0};
-        bool pzero[kS] = {false, false};
+        double pgiven[S];
+        bool pzero[S];
+#pragma unroll
+        for (int s = 0; s < S; s++) {
+            pgiven[s] = 1.0;
+            pzero[s] = false;
+        }
         if (a.forced) {
 #pragma unroll
-            for (int s = 0; s < kS; s++) {
+            for (int s = 0; s < S; s++) {
                 mism[s] = __reduce_or_sync(kFull, mism[s]);
                 pzero[s] = (mism[s] >> lane) & 1u;  // sampler.cpp:328-336: return 0.0 before any component
             }
@@ -461,28 +500,28 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
             if (mt.prog.tab_valid && ci < kTabComps && (mt.prog.tab.comp[ci] >> 31) && !a.forced) {
                 // ---- tabulated chain (TabProg): m_f form parities + sampled bits index the ratios
                 const uint32_t cw = mt.prog.tab.comp[ci], mf = (cw >> 24) & 0x7fu, f0 = cw & 0xffffu;
-                uint32_t idx[kS] = {};
+                uint32_t idx[S] = {};
                 for (uint32_t i = 0; i < mf; i++) {
-                    uint32_t w[kS] = {};
+                    uint32_t w[S] = {};
                     for (uint32_t q = mt.prog.tab.form_sel_begin[f0 + i]; q < mt.prog.tab.form_sel_begin[f0 + i + 1]; q++) {
                         const uint32_t pcol = mt.prog.tab.form_sel[q];
 #pragma unroll
-                        for (int s = 0; s < kS; s++) w[s] ^= cols[s * m.col_stride + pcol];
+                        for (int s = 0; s < S; s++) w[s] ^= cols[s * m.col_stride + pcol];
                     }
 #pragma unroll
-                    for (int s = 0; s < kS; s++) idx[s] |= ((w[s] >> lane) & 1u) << i;
+                    for (int s = 0; s < S; s++) idx[s] |= ((w[s] >> lane) & 1u) << i;
                 }
                 const double *tabp = a.tab + mt.prog.tab.base[ci];
                 for (uint32_t pos = 0; pos < n; pos++, upos++) {
-                    uint32_t rhi[kS], rlo[kS];
+                    uint32_t rhi[S], rlo[S];
                     if (!a.uniforms) {
                         const uint32_t stream = 0x80000000u ^ (ci << 12) ^ pos;  // sampler.cpp:37-39
-                        philox_tail<kS>(pre, seed_hi ^ stream, a.k0_round, k2c, a.k0_round[9], rhi, rlo);
+                        philox_tail<S>(pre, seed_hi ^ stream, a.k0_round, k2c, a.k0_round[9], rhi, rlo);
                     }
                     const double *tj = tabp + ((size_t((1u << pos) - 1u)) << mf);
-                    uint32_t word[kS];
+                    uint32_t word[S];
 #pragma unroll
-                    for (int s = 0; s < kS; s++) {
+                    for (int s = 0; s < S; s++) {
                         const bool valid = local[s] < a.shots;
                         const double cl = __ldg(tj + idx[s]);
                         if (isnan(cl) && valid) report_ratio_error(a.err, shot[s]);  // sampler.cpp:86-89
@@ -494,9 +533,12 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
                     }
                     if (lane == 0) {
                         const uint32_t o = m.comp_outputs[ob + pos];
-                        if (a.out32) *reinterpret_cast<uint2 *>(a.out32 + o * a.ld32 + tile * kS) = make_uint2(word[0], word[1]);
-                        if (a.counts && (word[0] | word[1])) {
-                            atomicAdd(&scount[o], (unsigned long long)(__popc(word[0]) + __popc(word[1])));
+                        if (a.out32) store_words<S>(a.out32 + o * a.ld32, tile * S, a.ld32, word);
+                        if (a.counts) {
+                            uint32_t ones = 0;
+#pragma unroll
+                            for (int s = 0; s < S; s++) ones += __popc(word[s]);
+                            if (ones) atomicAdd(&scount[o], (unsigned long long)ones);
                         }
                     }
                 }
@@ -505,48 +547,48 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
             const uint32_t tb = m.comp_tensor_begin[ci];
             for (uint32_t p = lane; p < n; p += 32) {
 #pragma unroll
-                for (int s = 0; s < kS; s++) cols[s * m.col_stride + m.f_width + p] = 0u;
+                for (int s = 0; s < S; s++) cols[s * m.col_stride + m.f_width + p] = 0u;
             }
             __syncwarp();
-            double2 acc[kS];
-            double prev[kS], norm[kS];
+            double2 acc[S];
+            double prev[S], norm[S];
             if (light) {
-                eval_tensor_light(mt.prog, tb, cols, m.col_stride, lane, sh, acc);
+                eval_tensor_light<S>(mt.prog, tb, cols, m.col_stride, lane, sh, acc);
             } else {
-                eval_tensor(m, tb, cols, m.col_stride, lane, acc);
+                eval_tensor<S>(m, tb, cols, m.col_stride, lane, acc);
             }
 #pragma unroll
-            for (int s = 0; s < kS; s++) {
+            for (int s = 0; s < S; s++) {
                 prev[s] = norm[s] = acc[s].x;
                 // sampler.cpp:343-345
                 if (a.forced && !pzero[s] && local[s] < a.shots && !(norm[s] > 0.0)) report_ratio_error(a.err, shot[s]);
             }
             for (uint32_t pos = 0; pos < n; pos++, upos++) {
                 if (light) {
-                    eval_tensor_light(mt.prog, tb + 1 + pos, cols, m.col_stride, lane, sh, acc);
+                    eval_tensor_light<S>(mt.prog, tb + 1 + pos, cols, m.col_stride, lane, sh, acc);
                 } else {
-                    eval_tensor(m, tb + 1 + pos, cols, m.col_stride, lane, acc);
+                    eval_tensor<S>(m, tb + 1 + pos, cols, m.col_stride, lane, acc);
                 }
                 if (a.forced) {  // sampler.cpp:346-352: forced outcome bit
                     const uint32_t o = m.comp_outputs[ob + pos];
                     const bool bit = a.forced[o] != 0;
 #pragma unroll
-                    for (int s = 0; s < kS; s++) prev[s] = bit ? __dsub_rn(prev[s], acc[s].x) : acc[s].x;
+                    for (int s = 0; s < S; s++) prev[s] = bit ? __dsub_rn(prev[s], acc[s].x) : acc[s].x;
                     if (lane == 0) {
 #pragma unroll
-                        for (int s = 0; s < kS; s++) cols[s * m.col_stride + m.f_width + pos] = bit ? kFull : 0u;
+                        for (int s = 0; s < S; s++) cols[s * m.col_stride + m.f_width + pos] = bit ? kFull : 0u;
                     }
                     __syncwarp();
                     continue;
                 }
-                uint32_t rhi[kS], rlo[kS];
+                uint32_t rhi[S], rlo[S];
                 if (!a.uniforms) {
                     const uint32_t stream = 0x80000000u ^ (ci << 12) ^ pos;  // sampler.cpp:37-39
-                    philox_tail<kS>(pre, seed_hi ^ stream, a.k0_round, k2c, a.k0_round[9], rhi, rlo);
+                    philox_tail<S>(pre, seed_hi ^ stream, a.k0_round, k2c, a.k0_round[9], rhi, rlo);
                 }
-                uint32_t word[kS];
+                uint32_t word[S];
 #pragma unroll
-                for (int s = 0; s < kS; s++) {
+                for (int s = 0; s < S; s++) {
                     const bool valid = local[s] < a.shots;
                     const double cur = acc[s].x;
                     const double ratio = __ddiv_rn(cur, prev[s]);
@@ -561,23 +603,26 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
                 }
                 if (lane == 0) {
 #pragma unroll
-                    for (int s = 0; s < kS; s++) cols[s * m.col_stride + m.f_width + pos] = word[s];
+                    for (int s = 0; s < S; s++) cols[s * m.col_stride + m.f_width + pos] = word[s];
                     const uint32_t o = m.comp_outputs[ob + pos];
-                    if (a.out32) *reinterpret_cast<uint2 *>(a.out32 + o * a.ld32 + tile * kS) = make_uint2(word[0], word[1]);
-                    if (a.counts && (word[0] | word[1])) {
-                        atomicAdd(&scount[o], (unsigned long long)(__popc(word[0]) + __popc(word[1])));
+                    if (a.out32) store_words<S>(a.out32 + o * a.ld32, tile * S, a.ld32, word);
+                    if (a.counts) {
+                        uint32_t ones = 0;
+#pragma unroll
+                        for (int s = 0; s < S; s++) ones += __popc(word[s]);
+                        if (ones) atomicAdd(&scount[o], (unsigned long long)ones);
                     }
                 }
                 __syncwarp();
             }
             if (a.forced) {
 #pragma unroll
-                for (int s = 0; s < kS; s++) pgiven[s] = __dmul_rn(pgiven[s], __ddiv_rn(prev[s], norm[s]));  // sampler.cpp:353
+                for (int s = 0; s < S; s++) pgiven[s] = __dmul_rn(pgiven[s], __ddiv_rn(prev[s], norm[s]));  // sampler.cpp:353
             }
         }
         if (a.forced) {
 #pragma unroll
-            for (int s = 0; s < kS; s++) {
+            for (int s = 0; s < S; s++) {
                 if (local[s] < a.shots) a.prob[local[s]] = pzero[s] ? 0.0 : pgiven[s];
             }
         }
@@ -595,7 +640,7 @@ __global__ void __maxnreg__(ZXS_MAXNREG) shot_kernel(const __grid_constant__ Lau
 __global__ void __launch_bounds__(256) eval_kernel(DevModel m, uint32_t tensor, const uint32_t *params,
                                                    uint64_t ld32, uint32_t ncols, uint32_t stride, uint64_t shots,
                                                    uint64_t n_tiles, double *values,
-                                                   unsigned long long *max_imag_bits) {
+                                                   unsigned long long *max_imag_bits, double *imag_values) {
     extern __shared__ __align__(16) uint32_t smem[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
     uint32_t *cols = smem + warp * (kS * stride);
@@ -612,6 +657,7 @@ __global__ void __launch_bounds__(256) eval_kernel(DevModel m, uint32_t tensor, 
             const uint64_t local = tile * kTileShots + 32 * s + lane;
             if (local < shots) {
                 values[local] = acc[s].x;
+                if (imag_values) imag_values[local] = acc[s].y;
                 const double mag = hypot(acc[s].x, acc[s].y);
                 if (mag > 0) {
                     const double ratio = fabs(acc[s].y) / (mag + 1e-300);  // phase_terms.cpp:137-141

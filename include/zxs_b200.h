@@ -224,6 +224,10 @@ zxs_status zxs_count(zxs_sampler *s, uint64_t seed, uint64_t first_shot, uint64_
  */
 zxs_status zxs_kernel_timing(zxs_sampler *s, int enable);
 zxs_status zxs_kernel_times(zxs_sampler *s, double *ms /*[3]*/, uint64_t *launches /*[3]*/);
+/* The same for the first n timing slots: [3] the deduplicated path's
+ * contraction kernel (dedup_eval_kernel), [4] its per-shot and reduction
+ * kernels (key hashing, autoregressive steps, segment folds, table clears). */
+zxs_status zxs_kernel_times_n(zxs_sampler *s, double *ms, uint64_t *launches, uint32_t n);
 
 /* Synchronizes `stream` and reports (then clears) a device-side ratio breakdown. */
 zxs_status zxs_check_errors(zxs_sampler *s, void *stream);

@@ -34,6 +34,7 @@
 #include "zxs_b200.h"
 #include "zxs_heavy.cuh"
 #include "zxs_mono.cuh"
+#include "zxs_dedup.cuh"
 #include "zxs_encode.cuh"
 #include "zxs_sparse.cuh"
 
@@ -166,6 +167,20 @@ struct zxs_sampler {
     std::map<uint32_t, uint32_t> mono_tensor;  // model tensor -> mono tensor index
     char *mono_scratch = nullptr;
     size_t mono_scratch_bytes = 0;
+
+    // deduplicated large-chi path (zxs_dedup.cuh; ZXS_DEDUP, default on)
+    bool dedup = false;
+    const uint32_t *dd_words = nullptr;  // segment streams (device)
+    const uint4 *dd_segs = nullptr;
+    std::vector<uint32_t> dd_tsb, dd_tdb, dd_tw, dd_tbb;  // host copies per mono tensor
+    std::vector<unsigned long long> dd_key_mask;          // per mono component
+    size_t dd_smem = 0;
+    char *dd_buf = nullptr;  // keys, slots, prev, values, partials, two tables
+    size_t dd_buf_bytes = 0;
+    uint64_t dd_cap_shots = 0;
+    uint32_t dd_table_slots = 0;
+    bool dd_dirty = true;  // tables need a full reset
+    uint32_t *dd_pinned = nullptr;
 
     // error model kept on the host for probability_of's enumeration
     // (sampler.cpp:370-429): per mechanism the f_vectors as FW-word masks and
@@ -461,6 +476,12 @@ struct MonoHost {
     uint32_t all_plane = 0;                    // plane index of the per-tensor ALL plane
     uint32_t max_dict = 1;
     uint32_t max_depth = 1;  // deepest tree node + 1
+    // summation segments (zxs_dedup.cuh): per mono tensor, up to kDedupSegs
+    // self-contained node streams (each replays its first node's ancestors)
+    std::vector<uint32_t> seg_words;
+    std::vector<uint4> segs;                   // {word_begin, n_words, n_nodes, 0}
+    std::vector<uint32_t> tensor_seg_begin{0};
+    std::vector<unsigned long long> comp_key_mask;  // per mono component: raw params any tensor reads
 };
 
 // One term after lowering: its records as sorted tokens (record word, plus
@@ -758,6 +779,9 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
         std::vector<uint32_t> w;
         std::vector<uint4> ch;
         std::vector<uint32_t> tcb;
+        std::vector<uint32_t> sw;   // segment streams of this component
+        std::vector<uint4> sg;      // segments (word_begin relative to sw)
+        std::vector<uint32_t> tsb;  // per tensor: first segment (relative to sg)
         uint64_t recs = 0, dead = 0, nsel = 0, loads = 0, nodes_total = 0;
         for (uint32_t t = t0; ok && t < t1; t++) {
             form_id.clear();
@@ -934,7 +958,27 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             tcb.push_back(uint32_t(H.chunks.size() + ch.size()));
             if (H.dict.size() - dict_base >= 0xfffu) ok = false;  // 12-bit form ids
             comp_max_dict = std::max<uint32_t>(comp_max_dict, uint32_t(H.dict.size() - dict_base));
+            // summation segments: contiguous node ranges of about equal cost (records + leaf
+            // epilogue), the tensor value being the ordered sum of the segment sums
+            std::vector<uint8_t> seg_start(nodes.size(), 0);
+            {
+                const uint32_t G = std::max<uint32_t>(
+                    1, std::min<uint32_t>(zxs_dev::kDedupSegs, uint32_t(nodes.size() / 8)));
+                uint64_t total = 0;
+                for (const MonoNode &nd : nodes) total += nd.recs.size() + (nd.leaf ? 8 : 1);
+                uint64_t cum = 0, k = 1;
+                for (size_t i = 0; i < nodes.size(); i++) {
+                    if (i == 0) seg_start[i] = 1;
+                    else if (k < G && cum * G >= total * k) {
+                        seg_start[i] = 1;
+                        while (k < G && cum * G >= total * k) k++;
+                    }
+                    cum += nodes[i].recs.size() + (nodes[i].leaf ? 8 : 1);
+                }
+            }
+            std::vector<uint32_t> node_off(nodes.size()), node_len(nodes.size());
             std::vector<uint32_t> nw;
+            size_t node_i = 0;
             for (const MonoNode &nd : nodes) {
                 if (!ok) break;
                 // node: {leaf << 31 | depth << 24 | n_gen, n_add | n_sub << 8 | n_add2 << 16 | n_z << 24, n_zn}
@@ -944,7 +988,8 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                 for (int k = 0; k < 16; k++) ok &= cnt[k] < 256;
                 if (!ok) break;
                 nw.clear();
-                nw.push_back((nd.leaf ? 0x80000000u : 0u) | uint32_t(nd.depth) << 24 | cnt[zxs_dev::kRecGen]);
+                nw.push_back((nd.leaf ? 0x80000000u : 0u) | (seg_start[node_i] ? zxs_dev::kMonoSegStart : 0u) |
+                             uint32_t(nd.depth) << 24 | cnt[zxs_dev::kRecGen]);
                 nw.push_back(cnt[zxs_dev::kRecAdd] | cnt[zxs_dev::kRecSub] << 8 | cnt[zxs_dev::kRecAdd2] << 16 |
                              cnt[zxs_dev::kRecZ] << 24);
                 nw.push_back(cnt[zxs_dev::kRecZn]);
@@ -982,10 +1027,38 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                     break;
                 }
                 if (H.words.size() + w.size() + nw.size() - cur_begin > zxs_dev::kMonoChunkWords) close_chunk();
+                node_off[node_i] = uint32_t(w.size());
+                node_len[node_i] = uint32_t(nw.size());
+                node_i++;
                 w.insert(w.end(), nw.begin(), nw.end());
                 cur_nodes++;
             }
             if (ok) close_chunk();
+            // segment streams: each starts with its first node's ancestors (internal nodes,
+            // replayed to rebuild the stack), then the segment's own nodes; flags cleared
+            tsb.push_back(uint32_t(sg.size()));
+            if (ok) {
+                std::vector<size_t> anc(zxs_dev::kMonoMaxDepth, 0);
+                for (size_t i = 0; i < nodes.size();) {
+                    size_t j = i + 1;
+                    while (j < nodes.size() && !seg_start[j]) j++;
+                    const uint32_t b = uint32_t(sw.size());
+                    uint32_t nn = 0;
+                    auto copy_node = [&](size_t x) {
+                        const size_t o = sw.size();
+                        sw.insert(sw.end(), w.begin() + node_off[x], w.begin() + node_off[x] + node_len[x]);
+                        sw[o] &= ~zxs_dev::kMonoSegStart;
+                        nn++;
+                    };
+                    for (uint32_t dd = 0; dd < nodes[i].depth; dd++) copy_node(anc[dd]);
+                    for (size_t x = i; x < j; x++) {
+                        copy_node(x);
+                        anc[nodes[x].depth] = x;
+                    }
+                    sg.push_back(make_uint4(b, uint32_t(sw.size()) - b, nn, 0));
+                    i = j;
+                }
+            }
             nodes_total += nodes.size();
         }
         if (ok && mono_smem_bytes(fwid + 2 * max_chain + 2, std::max(comp_max_dict, H.max_dict), 1,
@@ -1002,6 +1075,16 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             for (uint32_t t = t0; t < t1; t++) H.tensor_index[t] = hc.first_tensor + (t - t0);
             H.words.insert(H.words.end(), w.begin(), w.end());
             H.chunks.insert(H.chunks.end(), ch.begin(), ch.end());
+            {
+                const uint32_t wb = uint32_t(H.seg_words.size()), sb = uint32_t(H.segs.size());
+                H.seg_words.insert(H.seg_words.end(), sw.begin(), sw.end());
+                for (uint4 x : sg) H.segs.push_back(make_uint4(x.x + wb, x.y, x.z, 0));
+                for (size_t i = 1; i < tsb.size(); i++) H.tensor_seg_begin.push_back(tsb[i] + sb);
+                H.tensor_seg_begin.push_back(uint32_t(H.segs.size()));
+                unsigned long long km = 0;
+                for (uint64_t v : cb) km |= v;
+                H.comp_key_mask.push_back(km);
+            }
             for (size_t i = 1; i < tcb.size(); i++) H.tensor_chunk_begin.push_back(tcb[i]);
             H.tensor_chunk_begin.push_back(uint32_t(H.chunks.size()));
             H.tensor_dict_begin.insert(H.tensor_dict_begin.end(), tdb.begin(), tdb.end());
@@ -1550,6 +1633,10 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     size_t o_mtw = ar.add(MH.tensor_width);
     size_t o_mtbb = ar.add(MH.tensor_basis_begin);
     size_t o_mbasis = ar.add(MH.basis);
+    if (MH.seg_words.empty()) MH.seg_words.assign(4, 0);
+    if (MH.segs.empty()) MH.segs.push_back(make_uint4(0, 0, 0, 0));
+    size_t o_sw = ar.add(MH.seg_words);
+    size_t o_sg = ar.add(MH.segs);
 
     CK(cudaMalloc(&s->dev_model, ar.host.size()));
     s->dev_model_bytes = ar.host.size();
@@ -1654,6 +1741,17 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         if (const char *e = std::getenv("ZXS_MONO_WORDS")) s->mono_nw = std::atoi(e) == 1 ? 1 : 2;
         if (mono_smem_bytes(ma.n_planes, ma.max_dict, s->mono_nw, ma.stack_depth) > 227 * 1024) s->mono_nw = 1;
         s->mono_smem = mono_smem_bytes(ma.n_planes, ma.max_dict, s->mono_nw, ma.stack_depth);
+        s->dd_words = reinterpret_cast<const uint32_t *>(b + o_sw);
+        s->dd_segs = reinterpret_cast<const uint4 *>(b + o_sg);
+        s->dd_tsb = MH.tensor_seg_begin;
+        s->dd_tdb = MH.tensor_dict_begin;
+        s->dd_tw = MH.tensor_width;
+        s->dd_tbb = MH.tensor_basis_begin;
+        s->dd_key_mask = MH.comp_key_mask;
+        s->dd_smem = size_t(ma.max_dict) * 16 + size_t(MH.all_plane + 2) * 32 * 4 +
+                     size_t(zxs_dev::kDedupWarps) * ma.stack_depth * 96 * 4;
+        s->dedup = s->dd_smem <= 227 * 1024 && s->dd_key_mask.size() == MH.comps.size();
+        if (const char *e = std::getenv("ZXS_DEDUP")) s->dedup = s->dedup && std::atoi(e) != 0;
     }
     s->info.num_mono_components = uint32_t(MH.comps.size());
     s->info.num_mono_records = MH.records;
@@ -1724,6 +1822,11 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->mono_blocks_per_sm, mk, mono_warps(s->mono_nw) * 32,
                                                          s->mono_smem));
         if (s->mono_blocks_per_sm < 1) fail(ZXS_UNSUPPORTED, "mono kernel does not fit on an SM");
+        if (s->dedup) {
+            CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(&zxs_dev::dedup_eval_kernel),
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->dd_smem)));
+            CK(cudaMallocHost(&s->dd_pinned, 64));
+        }
     }
 }
 
@@ -1752,7 +1855,7 @@ void launch_mono(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *f
     const uint64_t per_cta = uint64_t(mono_warps(nw)) * 1024 * nw;
     h.n_cta_tiles = (a.shots + per_cta - 1) / per_cta;
     if (h.n_cta_tiles == 0) return;
-    h.scratch = s->mono_scratch_get(size_t(2) * h.n_cta_tiles * per_cta * 8);
+    h.scratch = s->mono_scratch_get(size_t(3) * h.n_cta_tiles * per_cta * 8);
     const size_t smem = mono_smem_bytes(h.n_planes, h.max_dict, nw, h.stack_depth);
     if (smem > s->mono_smem) {
         CK(cudaFuncSetAttribute(mono_kernel_ptr(nw), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -1760,6 +1863,187 @@ void launch_mono(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *f
     const unsigned grid = unsigned(std::min<uint64_t>(h.n_cta_tiles, uint64_t(s->sm_count) * std::max(1, s->mono_blocks_per_sm)));
     void *args[] = {&h};
     CK(cudaLaunchKernel(mono_kernel_ptr(nw), dim3(grid), dim3(mono_warps(nw) * 32), args, smem, st));
+}
+
+// ---- deduplicated large-chi path (zxs_dedup.cuh)
+constexpr uint32_t kDedupRoundKeys = 16384;  // keys per eval round (partials: segments x round keys)
+
+struct DedupBufs {
+    unsigned long long *key;
+    uint32_t *slot;
+    double *prev, *value0, *value, *partial;
+    zxs_dev::DedupTable table[2];
+};
+
+DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
+    uint64_t cap = std::max<uint64_t>(s->dd_cap_shots, 1024);
+    while (cap < shots) cap *= 2;
+    uint32_t slots = 2048;
+    while (slots < 2 * cap) slots *= 2;
+    uint32_t max_segs = 1;
+    for (size_t t = 0; t + 1 < s->dd_tsb.size(); t++) max_segs = std::max(max_segs, s->dd_tsb[t + 1] - s->dd_tsb[t]);
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const size_t per_table = al(size_t(slots) * 8) + al(size_t(slots) * 4) + al(4) + al(size_t(cap) * 8) + al(size_t(cap) * 4);
+    const size_t bytes = al(cap * 8) + al(cap * 4) + 3 * al(cap * 8) + al(size_t(max_segs) * kDedupRoundKeys * 8) + 2 * per_table;
+    if (bytes > s->dd_buf_bytes) {
+        if (s->dd_buf) CK(cudaFree(s->dd_buf));
+        s->dd_buf = nullptr;
+        s->dd_buf_bytes = 0;
+        CK(cudaMalloc(&s->dd_buf, bytes));
+        s->dd_buf_bytes = bytes;
+        s->dd_dirty = true;
+    }
+    s->dd_cap_shots = cap;
+    DedupBufs d;
+    char *p = s->dd_buf;
+    auto take = [&](size_t n) { char *r = p; p += al(n); return r; };
+    d.key = reinterpret_cast<unsigned long long *>(take(cap * 8));
+    d.slot = reinterpret_cast<uint32_t *>(take(cap * 4));
+    d.prev = reinterpret_cast<double *>(take(cap * 8));
+    d.value0 = reinterpret_cast<double *>(take(cap * 8));
+    d.value = reinterpret_cast<double *>(take(cap * 8));
+    d.partial = reinterpret_cast<double *>(take(size_t(max_segs) * kDedupRoundKeys * 8));
+    for (int i = 0; i < 2; i++) {
+        zxs_dev::DedupTable &t = d.table[i];
+        t.keys = reinterpret_cast<unsigned long long *>(take(size_t(slots) * 8));
+        t.ids = reinterpret_cast<uint32_t *>(take(size_t(slots) * 4));
+        t.mask = slots - 1;
+        t.count = reinterpret_cast<uint32_t *>(take(4));
+        t.ukeys = reinterpret_cast<unsigned long long *>(take(cap * 8));
+        t.uslot = reinterpret_cast<uint32_t *>(take(cap * 4));
+    }
+    if (s->dd_dirty || slots != s->dd_table_slots) {
+        for (int i = 0; i < 2; i++) {
+            CK(cudaMemset(d.table[i].keys, 0xff, size_t(slots) * 8));
+            CK(cudaMemset(d.table[i].count, 0, 4));
+        }
+        CK(cudaDeviceSynchronize());
+        s->dd_table_slots = slots;
+        s->dd_dirty = false;
+    }
+    return d;
+}
+
+uint32_t dedup_count(zxs_sampler *s, const zxs_dev::DedupTable &t, cudaStream_t st) {
+    CK(cudaMemcpyAsync(s->dd_pinned, t.count, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return s->dd_pinned[0];
+}
+
+// Values of mono tensor `mt` for the table's n distinct keys, in id order.
+void dedup_eval(zxs_sampler *s, uint32_t mt, const zxs_dev::DedupTable &t, uint32_t n, double *value, double *partial,
+                cudaStream_t st) {
+    const uint32_t g0 = s->dd_tsb[mt], ng = s->dd_tsb[mt + 1] - g0;
+    if (n == 0) return;
+    if (ng == 0) {  // every term dead: the value is exactly 0
+        CK(cudaMemsetAsync(value, 0, size_t(n) * 8, st));
+        return;
+    }
+    const zxs_dev::MonoArgs &m = s->mono;
+    for (uint32_t r0 = 0; r0 < n; r0 += kDedupRoundKeys) {
+        zxs_dev::DedupEvalArgs e{};
+        e.words = s->dd_words;
+        e.segs = s->dd_segs + g0;
+        e.n_segs = ng;
+        e.dict = m.dict + s->dd_tdb[mt];
+        e.n_dict = s->dd_tdb[mt + 1] - s->dd_tdb[mt];
+        e.basis = m.basis + s->dd_tbb[mt];
+        e.width = std::min(s->dd_tw[mt], m.all_plane);
+        e.all_plane = m.all_plane;
+        e.n_planes = m.all_plane + 2;
+        e.stack_depth = m.stack_depth;
+        e.keys = t.ukeys + r0;
+        e.n_keys = std::min(kDedupRoundKeys, n - r0);
+        e.partial = partial;
+        const uint64_t items = uint64_t((e.n_keys + zxs_dev::kDedupKeysPerWarp - 1) / zxs_dev::kDedupKeysPerWarp) *
+                               ((ng + zxs_dev::kDedupWarps - 1) / zxs_dev::kDedupWarps);
+        const unsigned grid = unsigned(std::min<uint64_t>(items, uint64_t(s->sm_count)));
+        cudaEvent_t t0 = nullptr;
+        s->time_begin(3, st, t0);
+        void *args[] = {&e};
+        CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_eval_kernel), dim3(grid),
+                            dim3(zxs_dev::kDedupWarps * 32), args, s->dd_smem, st));
+        s->time_end(3, st, t0);
+        s->time_begin(4, st, t0);
+        zxs_dev::dedup_reduce_kernel<<<(e.n_keys + 255) / 256, 256, 0, st>>>(partial, ng, e.n_keys, value + r0);
+        CK(cudaGetLastError());
+        s->time_end(4, st, t0);
+    }
+}
+
+// The large-chi components of shots [first_shot, first_shot + shots) on the
+// deduplicated path, after shot_kernel left their f-columns in `fcols`.
+void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *fcols, uint64_t fcols_ld32,
+                  cudaStream_t st) {
+    if (a.shots == 0) return;
+    DedupBufs d = dedup_reserve(s, a.shots);
+    const zxs_dev::MonoArgs &m = s->mono;
+    const unsigned pgrid = unsigned(std::min<uint64_t>((a.shots + 255) / 256, uint64_t(s->sm_count) * 8));
+    s->dd_dirty = true;  // until the chain completes
+    cudaEvent_t t0 = nullptr;
+    for (uint32_t hc = 0; hc < m.n_comps; hc++) {
+        const zxs_dev::HeavyComp cd = m.comps[hc];
+        zxs_dev::DedupInitArgs ia{};
+        ia.shots = a.shots;
+        ia.fcols = fcols;
+        ia.fcols_ld32 = fcols_ld32;
+        ia.f_width = m.f_width;
+        ia.key_mask = s->dd_key_mask[hc];
+        ia.key = d.key;
+        ia.slot = d.slot;
+        ia.table = d.table[0];
+        s->time_begin(4, st, t0);
+        void *iargs[] = {&ia};
+        CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_init_kernel), dim3(pgrid), dim3(256), iargs, 0,
+                            st));
+        s->time_end(4, st, t0);
+        uint32_t n = dedup_count(s, d.table[0], st);
+        dedup_eval(s, cd.first_tensor, d.table[0], n, d.value0, d.partial, st);
+        for (uint32_t j = 0; j < cd.n_out; j++) {
+            const zxs_dev::DedupTable &cur = d.table[j & 1], &nxt = d.table[(j + 1) & 1];
+            dedup_eval(s, cd.first_tensor + 1 + j, cur, n, d.value, d.partial, st);
+            zxs_dev::DedupArArgs ra{};
+            ra.seed = a.seed;
+            ra.first_shot = a.first_shot;
+            ra.shots = a.shots;
+            for (int i = 0; i < 10; i++) ra.k0_round[i] = a.k0_round[i];
+            ra.ci = cd.ci;
+            ra.j = j;
+            ra.out = s->comp_outputs[cd.out_begin + j];
+            ra.f_width = m.f_width;
+            ra.key_mask = s->dd_key_mask[hc];
+            ra.key = d.key;
+            ra.slot = d.slot;
+            ra.prev = d.prev;
+            ra.value0 = d.value0;
+            ra.value = d.value;
+            ra.cur = cur;
+            ra.next = nxt;
+            ra.insert_next = j + 1 < cd.n_out;
+            ra.out32 = a.out32;
+            ra.out_ld32 = a.ld32;
+            ra.counts = a.counts;
+            ra.uniforms = a.uniforms;
+            ra.uniforms_ld = a.uniforms_ld;
+            ra.upos = cd.upos_base + j;
+            ra.err = s->dev_err;
+            s->time_begin(4, st, t0);
+            void *rargs[] = {&ra};
+            CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_ar_kernel), dim3(pgrid), dim3(256), rargs,
+                                0, st));
+            s->time_end(4, st, t0);
+            s->time_begin(4, st, t0);
+            zxs_dev::dedup_clear_kernel<<<std::max(1u, std::min((n + 255) / 256, 1024u)), 256, 0, st>>>(cur, n);
+            CK(cudaGetLastError());
+            s->time_end(4, st, t0);
+            if (ra.insert_next) n = dedup_count(s, nxt, st);
+        }
+        if (cd.n_out == 0) {  // no autoregressive step cleared the first table
+            zxs_dev::dedup_clear_kernel<<<std::max(1u, std::min((n + 255) / 256, 1024u)), 256, 0, st>>>(d.table[0], n);
+            CK(cudaGetLastError());
+        }
+    }
+    s->dd_dirty = false;
 }
 
 void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
@@ -1792,7 +2076,9 @@ void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
     CK(cudaLaunchKernel(shot_kernel_for(s->fw_template, s->param_mechs, s->shots_per_lane), dim3(grid), dim3(32), args,
                         smem, st));
     s->time_end(0, st, t0);
-    if (heavy && s->has_mono) {
+    if (heavy && s->has_mono && s->dedup) {
+        launch_dedup(s, a, a.heavy_fcols, a.heavy_ld32, st);
+    } else if (heavy && s->has_mono) {
         s->time_begin(2, st, t0);
         launch_mono(s, a, a.heavy_fcols, a.heavy_ld32, -1, nullptr, 0, st);
         s->time_end(2, st, t0);
@@ -1931,6 +2217,8 @@ void zxs_sampler_destroy(zxs_sampler *s) {
     if (s->dev_flip_begin) cudaFree(s->dev_flip_begin);
     if (s->dev_flip_out) cudaFree(s->dev_flip_out);
     if (s->mono_scratch) cudaFree(s->mono_scratch);
+    if (s->dd_buf) cudaFree(s->dd_buf);
+    if (s->dd_pinned) cudaFreeHost(s->dd_pinned);
     for (auto &t : s->timed) {
         cudaEventDestroy(t.second.first);
         cudaEventDestroy(t.second.second);
@@ -1991,14 +2279,19 @@ zxs_status zxs_kernel_timing(zxs_sampler *s, int enable) {
 }
 
 zxs_status zxs_kernel_times(zxs_sampler *s, double *ms, uint64_t *launches) {
+    return zxs_kernel_times_n(s, ms, launches, 3);
+}
+
+zxs_status zxs_kernel_times_n(zxs_sampler *s, double *ms, uint64_t *launches, uint32_t n) {
     return guarded([&] {
-        if (!s || !ms || !launches) fail(ZXS_INVALID_ARGUMENT, "null argument");
+        if (!s || (n && (!ms || !launches))) fail(ZXS_INVALID_ARGUMENT, "null argument");
         DeviceGuard g(s->device);
-        for (int i = 0; i < 3; i++) {
+        for (uint32_t i = 0; i < n; i++) {
             ms[i] = 0.0;
             launches[i] = 0;
         }
         for (auto &t : s->timed) {
+            if (uint32_t(t.first) >= n) continue;
             CK(cudaEventSynchronize(t.second.second));
             float e = 0.f;
             CK(cudaEventElapsedTime(&e, t.second.first, t.second.second));
@@ -2650,6 +2943,20 @@ zxs_status zxs_debug_mono_layout(const zxs_model_desc *desc, uint64_t min_factor
         blob.push_back(uint32_t(H.basis.size()));
         for (unsigned long long x : H.basis) blob.insert(blob.end(), {uint32_t(x), uint32_t(x >> 32)});
         blob.insert(blob.end(), H.words.begin(), H.words.end());
+        // summation segments (zxs_dedup.cuh): counts, tensor_seg_begin, segments, streams, key masks
+        blob.insert(blob.end(), {uint32_t(H.tensor_seg_begin.size()), uint32_t(H.segs.size()),
+                                 uint32_t(H.seg_words.size()), uint32_t(H.comp_key_mask.size())});
+        blob.insert(blob.end(), H.tensor_seg_begin.begin(), H.tensor_seg_begin.end());
+        for (const uint4 &c : H.segs) blob.insert(blob.end(), {c.x, c.y, c.z, c.w});
+        blob.insert(blob.end(), H.seg_words.begin(), H.seg_words.end());
+        for (unsigned long long x : H.comp_key_mask) blob.insert(blob.end(), {uint32_t(x), uint32_t(x >> 32)});
+        // summation segments (zxs_dedup.cuh): counts, tensor_seg_begin, segments, streams, key masks
+        blob.insert(blob.end(), {uint32_t(H.tensor_seg_begin.size()), uint32_t(H.segs.size()),
+                                 uint32_t(H.seg_words.size()), uint32_t(H.comp_key_mask.size())});
+        blob.insert(blob.end(), H.tensor_seg_begin.begin(), H.tensor_seg_begin.end());
+        for (const uint4 &c : H.segs) blob.insert(blob.end(), {c.x, c.y, c.z, c.w});
+        blob.insert(blob.end(), H.seg_words.begin(), H.seg_words.end());
+        for (unsigned long long x : H.comp_key_mask) blob.insert(blob.end(), {uint32_t(x), uint32_t(x >> 32)});
         *needed = blob.size();
         if (out && cap >= blob.size()) std::memcpy(out, blob.data(), blob.size() * 4);
     });

@@ -60,6 +60,8 @@ constexpr uint32_t kMonoChunkWords = 2048;   // 8 KiB per chunk buffer
 constexpr uint32_t kMonoNoForm = 0xfffu;     // "no form" (parity 0) in the 12-bit form fields
 constexpr int kMaxMonoComps = 8;
 constexpr uint32_t kMonoMaxDepth = 8;        // levels of the shared-prefix term tree
+constexpr uint32_t kMonoSegStart = 1u << 30; // node header flag: first node of a summation segment
+constexpr uint32_t kDedupSegs = 2368;        // summation segments per tensor (148 SMs x 16 warps)
 
 // record kinds (bits 28..31 of a record word; first form in bits 0..11,
 // second form in bits 16..27; ids index the tensor's dictionary)
@@ -89,7 +91,7 @@ struct MonoArgs {
     const double *uniforms;           // injected AR uniforms (nullable)
     uint64_t uniforms_ld;
     unsigned long long *err;
-    double *scratch;                  // [2][n_cta_tiles * kMonoWarps * 1024]: prev, cur per shot
+    double *scratch;                  // [3][n_cta_tiles * warps * shots per warp]: prev, cur, folded sum per shot
     const uint32_t *words;            // record streams
     const uint4 *chunks;              // {word_begin, n_words (multiple of 4), n_terms, 0}
     const uint32_t *tensor_chunk_begin;
@@ -311,6 +313,104 @@ __device__ __forceinline__ void j_add(BW<NW> &j0, BW<NW> &j1, const BW<NW> &x, u
 #define ZXS_OP_ZN(x) { z = bw_or<NW>(z, bw_not<NW>(x)); }
 #define ZXS_OP_ANY(r, x) ZXS_OP_KIND(r, x)
 
+// Walks `nnodes` nodes of a record stream (node layout in zxs_api.cu
+// encode_mono) on top of the per-level (Z, J0, J1) stack `stk`; leaves add
+// Re(c' i^J) of their non-zero shots to acc. FOLD: a node flagged
+// kMonoSegStart first folds the running segment sum into tot (tot += acc,
+// acc = 0), so the tensor value is the canonical
+//   ((0 + S_0) + S_1) + ... + S_{G-1},   S_k = segment k's terms in order
+// that the deduplicated path (zxs_dedup.cuh) computes segment by segment.
+template <int NW, bool FOLD>
+__device__ __forceinline__ void mono_walk(const uint32_t *w, uint32_t nnodes, const uint4 *sd, const char *pl,
+                                          BW<NW> *stk, double (&acc)[32 * NW], double *tot) {
+    uint32_t q = 0;
+    for (uint32_t nn = 0; nn < nnodes; nn++) {
+        // node: {leaf << 31 | seg_start << 30 | depth << 24 | n_gen, n_add | n_sub << 8 | n_add2 << 16 | n_z << 24,
+        // n_zn} [re, im], records grouped by kind
+        const uint32_t h0 = w[q], h1 = w[q + 1], h2 = w[q + 2];
+        const uint32_t depth = (h0 >> 24) & 0x3fu;
+        const bool leaf = (h0 >> 31) != 0;
+        if (FOLD && (h0 & kMonoSegStart)) {
+            // eight at a time (compiler barriers keep the loads from being hoisted
+            // together: the accumulators already fill the register file)
+#pragma unroll
+            for (int g = 0; g < 4 * NW; g++) {
+                asm volatile("" ::: "memory");
+                double t[8];
+#pragma unroll
+                for (int s = 0; s < 8; s++) t[s] = tot[8 * g + s];
+#pragma unroll
+                for (int s = 0; s < 8; s++) {
+                    tot[8 * g + s] = __dadd_rn(t[s], acc[8 * g + s]);
+                    acc[8 * g + s] = 0.0;
+                }
+            }
+            asm volatile("" ::: "memory");
+        }
+        q += 3;
+        double re = 0.0, im = 0.0;
+        if (leaf) {
+            re = __hiloint2double(int(w[q + 1]), int(w[q]));
+            im = __hiloint2double(int(w[q + 3]), int(w[q + 2]));
+            q += 4;
+        }
+        // state of the parent (depth - 1), or the empty product at the root
+        BW<NW> z = bw_zero<NW>(), j0 = bw_zero<NW>(), j1 = bw_zero<NW>();
+        if (depth) {
+            const BW<NW> *ps = stk + (depth - 1) * 96;
+            z = ps[0];
+            j0 = ps[32];
+            j1 = ps[64];
+        }
+        {
+            // one-form records (any kind, ordered by size class): one copy of the
+            // form code for all kinds keeps the kernel within the instruction cache
+            const uint32_t ns = (h1 & 0xffu) + ((h1 >> 8) & 0xffu) + ((h1 >> 16) & 0xffu) + (h1 >> 24) + (h2 & 0xffu);
+            ZXS_MONO_RUN(ns, ZXS_OP_ANY)
+        }
+        for (uint32_t g = 0; g < (h0 & 0xffu); g++) {  // two-form records
+            const uint32_t r = w[q], gw = w[q + 1];
+            q += 2;
+            const uint32_t fa = r & 0xfffu, fb = (r >> 16) & 0xfffu;
+            const BW<NW> a = fa == kMonoNoForm ? bw_zero<NW>() : mono_form<NW>(sd, fa, pl);
+            const BW<NW> bb = fb == kMonoNoForm ? bw_zero<NW>() : mono_form<NW>(sd, fb, pl);
+            const uint32_t zl = gw >> 6;
+#pragma unroll
+            for (int i = 0; i < NW; i++) {
+                z.w[i] |= ((zl & 1u) ? (~a.w[i] & ~bb.w[i]) : 0u) | ((zl & 2u) ? (~a.w[i] & bb.w[i]) : 0u) |
+                          ((zl & 4u) ? (a.w[i] & ~bb.w[i]) : 0u) | ((zl & 8u) ? (a.w[i] & bb.w[i]) : 0u);
+            }
+            j_add<NW>(j0, j1, a, gw & 3u);
+            j_add<NW>(j0, j1, bb, (gw >> 2) & 3u);
+            j_add<NW>(j0, j1, bw_and<NW>(a, bb), (gw >> 4) & 3u);
+        }
+        if (!leaf) {
+            BW<NW> *ns = stk + depth * 96;
+            ns[0] = z;
+            ns[32] = j0;
+            ns[64] = j1;
+            continue;
+        }
+        // epilogue: acc[s] += Re(c' i^J) = {re, -im, -re, im}[J] for the non-zero shots,
+        // in term order; the sign is a flip of the high word's sign bit
+        const uint32_t re_lo = uint32_t(__double2loint(re)), re_hi = uint32_t(__double2hiint(re));
+        const uint32_t im_lo = uint32_t(__double2loint(im)), im_hi = uint32_t(__double2hiint(im));
+#pragma unroll
+        for (int i = 0; i < NW; i++) {
+            const uint32_t neg = j0.w[i] ^ j1.w[i];
+#pragma unroll
+            for (int s = 0; s < 32; s++) {
+                const bool odd = (j0.w[i] >> s) & 1u;
+                const uint32_t lo = odd ? im_lo : re_lo;
+                const uint32_t hi = (odd ? im_hi : re_hi) ^ ((neg << (31 - s)) & 0x80000000u);
+                if (!((z.w[i] >> s) & 1u)) {
+                    acc[i * 32 + s] = __dadd_rn(acc[i * 32 + s], __hiloint2double(int(hi), int(lo)));
+                }
+            }
+        }
+    }
+}
+
 template <int NW>
 __global__ void __launch_bounds__(MonoCfg<NW>::kWarps * 32, 1) mono_kernel(const __grid_constant__ MonoArgs h) {
     constexpr int kW = MonoCfg<NW>::kWarps;
@@ -380,6 +480,7 @@ __global__ void __launch_bounds__(MonoCfg<NW>::kWarps * 32, 1) mono_kernel(const
         __syncwarp();
         double *prev_g = h.scratch + wrd * 32;
         double *cur_g = h.scratch + (h.n_cta_tiles * kW * kWarpShots) + wrd * 32;
+        double *tot_g = h.scratch + 2 * (h.n_cta_tiles * kW * kWarpShots) + wrd * 32;  // folded segment sums
 
         const uint32_t ncomp = h.eval_tensor >= 0 ? 1u : h.n_comps;
         for (uint32_t hc = 0; hc < ncomp; hc++) {
@@ -421,85 +522,32 @@ __global__ void __launch_bounds__(MonoCfg<NW>::kWarps * 32, 1) mono_kernel(const
                 }
                 double acc[kLaneShots];
 #pragma unroll
-                for (int s = 0; s < int(kLaneShots); s++) acc[s] = 0.0;
+                for (int s = 0; s < int(kLaneShots); s++) {
+                    acc[s] = 0.0;
+                    tot_g[s] = 0.0;
+                }
                 for (uint32_t c = h.tensor_chunk_begin[t]; c < h.tensor_chunk_begin[t + 1]; c++, use++) {
                     const uint32_t b = uint32_t(use & 1);
                     mbar_wait(&bars[b], uint32_t((use >> 1) & 1));
                     const uint32_t *w = buf0 + b * kMonoChunkWords;
-                    const uint32_t nnodes = h.chunks[c].z;
-                    uint32_t q = 0;
-                    for (uint32_t nn = 0; nn < nnodes; nn++) {
-                        // node: {leaf << 31 | depth << 24 | n_gen, n_add | n_sub << 8 | n_add2 << 16 | n_z << 24,
-                        // n_zn} [re, im], records grouped by kind
-                        const uint32_t h0 = w[q], h1 = w[q + 1], h2 = w[q + 2];
-                        const uint32_t depth = (h0 >> 24) & 0x7fu;
-                        const bool leaf = (h0 >> 31) != 0;
-                        q += 3;
-                        double re = 0.0, im = 0.0;
-                        if (leaf) {
-                            re = __hiloint2double(int(w[q + 1]), int(w[q]));
-                            im = __hiloint2double(int(w[q + 3]), int(w[q + 2]));
-                            q += 4;
-                        }
-                        // state of the parent (depth - 1), or the empty product at the root
-                        BW<NW> z = bw_zero<NW>(), j0 = bw_zero<NW>(), j1 = bw_zero<NW>();
-                        if (depth) {
-                            const BW<NW> *ps = stk + (depth - 1) * 96;
-                            z = ps[0];
-                            j0 = ps[32];
-                            j1 = ps[64];
-                        }
-                        {
-                            // one-form records (any kind, ordered by size class): one copy of the
-                            // form code for all kinds keeps the kernel within the instruction cache
-                            const uint32_t ns = (h1 & 0xffu) + ((h1 >> 8) & 0xffu) + ((h1 >> 16) & 0xffu) + (h1 >> 24) +
-                                                (h2 & 0xffu);
-                            ZXS_MONO_RUN(ns, ZXS_OP_ANY)
-                        }
-                        for (uint32_t g = 0; g < (h0 & 0xffu); g++) {  // two-form records
-                            const uint32_t r = w[q], gw = w[q + 1];
-                            q += 2;
-                            const uint32_t fa = r & 0xfffu, fb = (r >> 16) & 0xfffu;
-                            const BW<NW> a = fa == kMonoNoForm ? bw_zero<NW>() : mono_form<NW>(sd, fa, pl);
-                            const BW<NW> bb = fb == kMonoNoForm ? bw_zero<NW>() : mono_form<NW>(sd, fb, pl);
-                            const uint32_t zl = gw >> 6;
-#pragma unroll
-                            for (int i = 0; i < NW; i++) {
-                                z.w[i] |= ((zl & 1u) ? (~a.w[i] & ~bb.w[i]) : 0u) | ((zl & 2u) ? (~a.w[i] & bb.w[i]) : 0u) |
-                                          ((zl & 4u) ? (a.w[i] & ~bb.w[i]) : 0u) | ((zl & 8u) ? (a.w[i] & bb.w[i]) : 0u);
-                            }
-                            j_add<NW>(j0, j1, a, gw & 3u);
-                            j_add<NW>(j0, j1, bb, (gw >> 2) & 3u);
-                            j_add<NW>(j0, j1, bw_and<NW>(a, bb), (gw >> 4) & 3u);
-                        }
-                        if (!leaf) {
-                            BW<NW> *ns = stk + depth * 96;
-                            ns[0] = z;
-                            ns[32] = j0;
-                            ns[64] = j1;
-                            continue;
-                        }
-                        // epilogue: acc[s] += Re(c' i^J) = {re, -im, -re, im}[J] for the non-zero shots,
-                        // in term order; the sign is a flip of the high word's sign bit
-                        const uint32_t re_lo = uint32_t(__double2loint(re)), re_hi = uint32_t(__double2hiint(re));
-                        const uint32_t im_lo = uint32_t(__double2loint(im)), im_hi = uint32_t(__double2hiint(im));
-#pragma unroll
-                        for (int i = 0; i < NW; i++) {
-                            const uint32_t neg = j0.w[i] ^ j1.w[i];
-#pragma unroll
-                            for (int s = 0; s < 32; s++) {
-                                const bool odd = (j0.w[i] >> s) & 1u;
-                                const uint32_t lo = odd ? im_lo : re_lo;
-                                const uint32_t hi = (odd ? im_hi : re_hi) ^ ((neg << (31 - s)) & 0x80000000u);
-                                if (!((z.w[i] >> s) & 1u)) {
-                                    acc[i * 32 + s] = __dadd_rn(acc[i * 32 + s], __hiloint2double(int(hi), int(lo)));
-                                }
-                            }
-                        }
-                    }
+#ifdef ZXS_MONO_NOFOLD  // A/B timing only: not the canonical order
+                    mono_walk<NW, false>(w, h.chunks[c].z, sd, pl, stk, acc, tot_g);
+#else
+                    mono_walk<NW, true>(w, h.chunks[c].z, sd, pl, stk, acc, tot_g);
+#endif
                     __syncthreads();  // buffer b fully consumed by every warp
                     if (threadIdx.x == 0 && use + 2 < total_uses) issue(use + 2);
                 }
+#pragma unroll
+                for (int g = 0; g < int(kLaneShots) / 8; g++) {  // last segment, eight at a time
+                    asm volatile("" ::: "memory");
+                    double t[8];
+#pragma unroll
+                    for (int s = 0; s < 8; s++) t[s] = tot_g[8 * g + s];
+#pragma unroll
+                    for (int s = 0; s < 8; s++) acc[8 * g + s] = __dadd_rn(t[s], acc[8 * g + s]);
+                }
+                asm volatile("" ::: "memory");
                 if (h.eval_tensor >= 0) {
 #pragma unroll
                     for (int s = 0; s < int(kLaneShots); s++) {

@@ -130,11 +130,13 @@ class CompiledSampler:
         _native.check(_native.lib().zxs_kernel_timing(self._h, 1 if enable else 0))
 
     def kernel_times(self) -> dict:
-        """{kernel: (total ms, launches)} for shot_kernel, heavy_kernel, mono_kernel."""
-        ms = (ctypes.c_double * 3)()
-        n = (ctypes.c_uint64 * 3)()
-        _native.check(_native.lib().zxs_kernel_times(self._h, ms, n))
-        return {k: (ms[i], int(n[i])) for i, k in enumerate(("shot_kernel", "heavy_kernel", "mono_kernel"))}
+        """{kernel: (total ms, launches)} for shot_kernel, heavy_kernel, mono_kernel and the
+        deduplicated path's dedup_eval_kernel and its per-shot/reduction kernels (dedup_aux)."""
+        names = ("shot_kernel", "heavy_kernel", "mono_kernel", "dedup_eval_kernel", "dedup_aux")
+        ms = (ctypes.c_double * len(names))()
+        n = (ctypes.c_uint64 * len(names))()
+        _native.check(_native.lib().zxs_kernel_times_n(self._h, ms, n, len(names)))
+        return {k: (ms[i], int(n[i])) for i, k in enumerate(names)}
 
     # ---- host-buffer entry points --------------------------------------
     def sample_into(self, expected_mode: int, seed: int, first_shot: int, shots: int, out: np.ndarray,

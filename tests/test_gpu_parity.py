@@ -197,12 +197,13 @@ def test_empty_and_tiny_ranges():
         assert np.array_equal(sample(cs, shots, 4, first), orc.sample(shots, 4, first))
 
 
-def _heavy_model(name, min_factors="1", mono="0"):
+def _heavy_model(name, min_factors="1", mono="0", dedup="1"):
     """Sampler whose components (with >= min_factors factors) all run in
-    heavy_kernel (mono="0": exact FP64 path) or mono_kernel (mono="1":
-    integer monomial path, where eligible)."""
+    heavy_kernel (mono="0": exact FP64 path) or on the integer monomial path
+    (mono="1", where eligible): deduplicated (dedup="1", zxs_dedup.cuh) or
+    per shot in mono_kernel (dedup="0")."""
     import os
-    keys = {"ZXS_HEAVY_MIN_FACTORS": min_factors, "ZXS_MONO": mono}
+    keys = {"ZXS_HEAVY_MIN_FACTORS": min_factors, "ZXS_MONO": mono, "ZXS_DEDUP": dedup}
     old = {k: os.environ.get(k) for k in keys}
     os.environ.update(keys)
     try:
@@ -303,24 +304,26 @@ def test_mono_eval_matches_reference(name):
             assert err.max() < 1e-12, (name, ci, pos, float(err.max()))
 
 
+@pytest.mark.parametrize("dedup", ["1", "0"])
 @pytest.mark.parametrize("name", MONO_NAMES)
-def test_mono_path_matches_reference_goldens(name, goldens):
-    """Records of the monomial path == the reference's (bit-exact: a
-    difference could only come from a uniform falling between the two
-    ratios, ~1e-16 wide; none occurs in these goldens)."""
-    cs = _heavy_model(name, min_factors="0", mono="1")
+def test_mono_path_matches_reference_goldens(name, dedup, goldens):
+    """Records of the monomial path (deduplicated or per shot) == the
+    reference's (bit-exact: a difference could only come from a uniform
+    falling between the two ratios, ~1e-16 wide; none occurs in these goldens)."""
+    cs = _heavy_model(name, min_factors="0", mono="1", dedup=dedup)
     for s in goldens[name]["samples"]:
         if s["shots"] > 200000:
             continue
         assert sha(sample(cs, s["shots"], s["seed"], s["first_shot"])) == s["sha256"], (name, s)
 
 
-def test_mono_injected_noise_ties_counted():
+@pytest.mark.parametrize("dedup", ["1", "0"])
+def test_mono_injected_noise_ties_counted(dedup):
     """Injected f and uniforms: mono path vs the C oracle. Mismatching bits
     are allowed only at threshold ties (|u - ratio| < 1e-12 at the first
     differing position of a shot); the count is reported."""
     name = "surface_d3_xmem_9t"
-    cs = _heavy_model(name, min_factors="0", mono="1")
+    cs = _heavy_model(name, min_factors="0", mono="1", dedup=dedup)
     orc = coracle.OracleModel.load(golden_path(name))
     rng = np.random.default_rng(31)
     shots = 20000
@@ -334,9 +337,10 @@ def test_mono_injected_noise_ties_counted():
     assert ties == 0, f"{ties} shots differ (threshold ties)"
 
 
-def test_mono_counts_and_shards():
+@pytest.mark.parametrize("dedup", ["1", "0"])
+def test_mono_counts_and_shards(dedup):
     name = "c4_color_d5_rz3"
-    cs = _heavy_model(name, min_factors="0", mono="1")
+    cs = _heavy_model(name, min_factors="0", mono="1", dedup=dedup)
     full = sample(cs, 70000, 3, 123)
     pc = np.unpackbits(full.view(np.uint8), axis=1).sum(axis=1).astype(np.uint64)
     assert np.array_equal(zx.count_outputs(cs, 70000, seed=3, first_shot=123), pc)
@@ -345,13 +349,28 @@ def test_mono_counts_and_shards():
     assert np.array_equal(np.concatenate([a, b], axis=1)[:, :full.shape[1]], full)
 
 
-def test_cultivation_proxy_mono_against_reference():
+def _load_env(path, **env):
+    import os
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return zx.CompiledSampler.load(path)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("dedup", ["1", "0"])
+def test_cultivation_proxy_mono_against_reference(dedup):
     """Config-3 proxy on the monomial path vs the reference sampler itself."""
     import os
     path = os.path.join(os.path.dirname(golden_path("x")), "..", "..", "data", "c3_cultivation_proxy.zxs.gz")
     if not os.path.exists(path) or not refdriver.available():
         pytest.skip("cultivation proxy not generated (tools/make_fixtures.py --big)")
-    cs = zx.CompiledSampler.load(path)
+    cs = _load_env(path, ZXS_DEDUP=dedup)
     assert cs.info["num_mono_components"] == 1
     ref = refdriver.RefModel.load(path)
     shots, first = 640, 1 << 20
@@ -370,12 +389,41 @@ def test_kernel_timing_counts_launches():
     t = cs.kernel_times()
     cs.kernel_timing(False)
     assert t["shot_kernel"][1] == 2 and t["shot_kernel"][0] > 0 and t["mono_kernel"][1] == 0
-    cm = _heavy_model("surface_d3_xmem_9t", min_factors="0", mono="1")
+    cm = _heavy_model("surface_d3_xmem_9t", min_factors="0", mono="1", dedup="0")
     cm.kernel_timing(True)
     sample(cm, 5000, 1)
     t = cm.kernel_times()
     cm.kernel_timing(False)
-    assert t["shot_kernel"][1] == 1 and t["mono_kernel"][1] == 1
+    assert t["shot_kernel"][1] == 1 and t["mono_kernel"][1] == 1 and t["dedup_eval_kernel"][1] == 0
+    cd = _heavy_model("surface_d3_xmem_9t", min_factors="0", mono="1", dedup="1")
+    cd.kernel_timing(True)
+    sample(cd, 5000, 1)
+    t = cd.kernel_times()
+    cd.kernel_timing(False)
+    # one chain of 5 outputs (6 tensors): 6 evals; init + 6 folds + 5 AR steps + 5 table clears
+    assert t["shot_kernel"][1] == 1 and t["mono_kernel"][1] == 0
+    assert t["dedup_eval_kernel"][1] == 6 and t["dedup_aux"][1] == 17
+
+
+# ---------------------------------------------------------------- deduplicated path
+@pytest.mark.parametrize("name", ["surface_d3_xmem_9t", "surface_d3_xmem_rz5", "c4_color_d5_rz3", "steane_inject"])
+def test_dedup_bit_identical_to_per_shot(name):
+    """Deduplicated and per-shot monomial paths compute the same canonical
+    segment-ordered sums: identical records for every seed and range, and
+    identical counts (random f injected too: many distinct keys)."""
+    a = _heavy_model(name, min_factors="0", mono="1", dedup="1")
+    b = _heavy_model(name, min_factors="0", mono="1", dedup="0")
+    assert a.info["num_mono_components"] > 0
+    for shots, seed, first in ((1, 1, 0), (33, 2, 5), (100000, 3, 7), (4097, 4, 2**32 - 9)):
+        assert np.array_equal(sample(a, shots, seed, first), sample(b, shots, seed, first)), (shots, seed)
+    orc = coracle.OracleModel.load(golden_path(name))
+    rng = np.random.default_rng(41)
+    shots = 30000
+    f = rng.integers(0, 2**63, size=(orc.f_width, (shots + 63) // 64), dtype=np.uint64)
+    f[:, -1] &= np.uint64((1 << (shots & 63)) - 1)
+    u = rng.random((orc.num_positions, shots))
+    assert np.array_equal(zx.sample_given_f(a, f, shots, uniforms=u), zx.sample_given_f(b, f, shots, uniforms=u))
+    assert np.array_equal(zx.count_outputs(a, 50000, seed=9), zx.count_outputs(b, 50000, seed=9))
 
 
 def test_imag_health_check():

@@ -54,8 +54,19 @@ def mono_layout(arrays, min_factors=0):
     basis = [int(buf[o + 2 * i]) | (int(buf[o + 2 * i + 1]) << 32) for i in range(nb)]
     o += 2 * nb
     words = buf[o:o + n_words]
+    o += n_words
+    n_tsb, n_segs, n_sw, n_km = (int(x) for x in buf[o:o + 4])
+    o += 4
+    tsb = buf[o:o + n_tsb].astype(np.int64)
+    o += n_tsb
+    segs = buf[o:o + 4 * n_segs].reshape(n_segs, 4).astype(np.int64)
+    o += 4 * n_segs
+    seg_words = buf[o:o + n_sw]
+    o += n_sw
+    key_mask = [int(buf[o + 2 * i]) | (int(buf[o + 2 * i + 1]) << 32) for i in range(n_km)]
     return dict(comps=comps, flags=flags, tcb=tcb, chunks=chunks, dict=dict_, tdb=tdb, twidth=twidth,
-                tbb=tbb, basis=basis, all_plane=all_plane, words=words)
+                tbb=tbb, basis=basis, all_plane=all_plane, words=words, tsb=tsb, segs=segs,
+                seg_words=seg_words, key_mask=key_mask)
 
 
 def form_sel(dict_, f):
@@ -104,16 +115,42 @@ def apply_node_records(w, q, h0, h1, h2, form, J, Z):
     return q
 
 
-def emulate_tensor(lay, t, P, stats=None):
-    """mono_kernel's value of mono tensor t for parameter rows P [shots][W] (0/1):
-    DFS over the shared-prefix node stream, per-level (J, Z) stack, leaves in
-    term order run the epilogue."""
-    words = lay["words"]
-    cache = {}
+SEG_START = 1 << 30
+
+
+def walk_nodes(w, nnodes, form, S, stack, acc, tot, stats=None):
+    """mono_walk: nnodes nodes of stream w; FOLD when tot is given (segment starts
+    fold the running sum into tot)."""
+    q = 0
+    for _ in range(nnodes):
+        h0, h1, h2 = int(w[q]), int(w[q + 1]), int(w[q + 2])
+        depth, leaf = (h0 >> 24) & 0x3F, h0 >> 31
+        if tot is not None and h0 & SEG_START:
+            tot += acc
+            acc[:] = 0.0
+        q += 3
+        if leaf:
+            re = w[q:q + 2].copy().view(np.float64)[0]
+            im = w[q + 2:q + 4].copy().view(np.float64)[0]
+            q += 4
+        if depth:
+            J, Z = stack[depth - 1][0].copy(), stack[depth - 1][1].copy()
+        else:
+            J, Z = np.zeros(S, np.int64), np.zeros(S, bool)
+        q = apply_node_records(w, q, h0, h1, h2, form, J, Z)
+        if stats is not None:
+            stats["nodes"] = stats.get("nodes", 0) + 1
+        if not leaf:
+            stack[depth] = (J, Z)
+            continue
+        J &= 3
+        v = np.where(J == 0, re, np.where(J == 1, -im, np.where(J == 2, -re, im)))
+        acc[:] = np.where(Z, acc, acc + v)
+
+
+def tensor_forms(lay, t, P):
     d0 = int(lay["tdb"][t])
     W = int(lay["twidth"][t])
-    # planes: the tensor's W basis planes (parities of the raw params P), then ALL (XOR of the
-    # basis planes) at lay["all_plane"] and the all-zero plane after it
     planes = np.zeros((P.shape[0], lay["all_plane"] + 2), np.int64)
     b0 = int(lay["tbb"][t])
     for b in range(W):
@@ -121,41 +158,40 @@ def emulate_tensor(lay, t, P, stats=None):
         cols = [p for p in range(64) if (m >> p) & 1]
         planes[:, b] = P[:, cols].sum(1) & 1 if cols else 0
     planes[:, lay["all_plane"]] = planes[:, :W].sum(1) & 1
+    cache = {}
 
     def form(f):
         if f not in cache:
             cache[f] = (planes[:, form_sel(lay["dict"], d0 + f)].sum(1) & 1).astype(np.int64)
         return cache[f]
+    return form
 
+
+def emulate_segments(lay, t, P):
+    """dedup_eval_kernel + dedup_reduce_kernel: every summation segment walked on its
+    own (ancestors replayed), segment sums folded in order."""
+    form = tensor_forms(lay, t, P)
     S = P.shape[0]
-    acc = np.zeros(S)
-    stack = {}
+    tot = np.zeros(S)
+    for g in range(lay["tsb"][t], lay["tsb"][t + 1]):
+        wb, nw, nn = lay["segs"][g, :3]
+        acc = np.zeros(S)
+        walk_nodes(lay["seg_words"][wb:wb + nw], nn, form, S, {}, acc, None)
+        tot += acc
+    return tot
+
+
+def emulate_tensor(lay, t, P, stats=None):
+    """mono_kernel's value of mono tensor t for parameter rows P [shots][W] (0/1):
+    DFS over the shared-prefix node stream, per-level (J, Z) stack, leaves in
+    term order run the epilogue; segment starts fold into the running total."""
+    S = P.shape[0]
+    form = tensor_forms(lay, t, P)
+    acc, tot, stack = np.zeros(S), np.zeros(S), {}
     for c in range(lay["tcb"][t], lay["tcb"][t + 1]):
         wb, nw, nnodes = lay["chunks"][c, :3]
-        w = words[wb:wb + nw]
-        q = 0
-        for _ in range(nnodes):
-            h0, h1, h2 = int(w[q]), int(w[q + 1]), int(w[q + 2])
-            depth, leaf = (h0 >> 24) & 0x7F, h0 >> 31
-            q += 3
-            if leaf:
-                re = w[q:q + 2].copy().view(np.float64)[0]
-                im = w[q + 2:q + 4].copy().view(np.float64)[0]
-                q += 4
-            if depth:
-                J, Z = stack[depth - 1][0].copy(), stack[depth - 1][1].copy()
-            else:
-                J, Z = np.zeros(S, np.int64), np.zeros(S, bool)
-            q = apply_node_records(w, q, h0, h1, h2, form, J, Z)
-            if stats is not None:
-                stats["nodes"] = stats.get("nodes", 0) + 1
-            if not leaf:
-                stack[depth] = (J, Z)
-                continue
-            J &= 3
-            v = np.where(J == 0, re, np.where(J == 1, -im, np.where(J == 2, -re, im)))
-            acc = np.where(Z, acc, acc + v)
-    return acc
+        walk_nodes(lay["words"][wb:wb + nw], nnodes, form, S, stack, acc, tot, stats)
+    return tot + acc
 
 
 def term_scale(arrays, tensor, P):
@@ -218,12 +254,44 @@ def test_mono_values_match_oracle(name):
             shots = 64
             P = rng.integers(0, 2, (shots, max(W, 1))).astype(np.int64)
             got = emulate_tensor(lay, comp["first_tensor"] + pos, P)
+            # the deduplicated path's segment-by-segment order gives the same doubles
+            seg = emulate_segments(lay, comp["first_tensor"] + pos, P)
+            assert np.array_equal(got, seg), (name, ci, pos)
             want, _ = om.eval_batch(tensor, pack(P), shots)
             scale = term_scale(arrays, tensor, P) + 1e-300
             err = np.abs(got - want) / scale
             assert err.max() < 1e-12, (name, ci, pos, float(err.max()))
             checked += 1
     assert checked
+
+
+def test_summation_segments():
+    """Segments partition each tensor's node stream, every segment stream starts at
+    the root (depth 0) and the key mask covers every basis vector."""
+    arrays = zxs_format.load(golden_path("surface_d3_xmem_9t"))
+    lay = mono_layout(arrays)
+    nt = len(lay["tcb"]) - 1
+    assert len(lay["tsb"]) == nt + 1
+    for t in range(nt):
+        g0, g1 = lay["tsb"][t], lay["tsb"][t + 1]
+        assert 1 <= g1 - g0 <= 2368
+        starts = 0
+        for c in range(lay["tcb"][t], lay["tcb"][t + 1]):
+            wb, nw, nn = lay["chunks"][c, :3]
+            w, q = lay["words"][wb:wb + nw], 0
+            for _ in range(nn):
+                h0, h1, h2 = int(w[q]), int(w[q + 1]), int(w[q + 2])
+                starts += bool(h0 & SEG_START)
+                q += 3 + (4 if h0 >> 31 else 0)
+                q += (h1 & 0xFF) + ((h1 >> 8) & 0xFF) + ((h1 >> 16) & 0xFF) + (h1 >> 24) + (h2 & 0xFF) + 2 * (h0 & 0xFF)
+        assert starts == g1 - g0
+        for g in range(g0, g1):
+            wb = lay["segs"][g, 0]
+            assert (int(lay["seg_words"][wb]) >> 24) & 0x3F == 0
+    for comp, km in zip(lay["comps"], lay["key_mask"]):
+        for t in range(comp["first_tensor"], comp["first_tensor"] + comp["n_out"] + 1):
+            for b in range(int(lay["twidth"][t])):
+                assert lay["basis"][int(lay["tbb"][t]) + b] & ~km == 0
 
 
 def test_mono_record_kinds_and_dead_terms():

@@ -229,6 +229,16 @@ zxs_status zxs_kernel_times(zxs_sampler *s, double *ms /*[3]*/, uint64_t *launch
  * kernels (key hashing, autoregressive steps, segment folds, table clears). */
 zxs_status zxs_kernel_times_n(zxs_sampler *s, double *ms, uint64_t *launches, uint32_t n);
 
+/*
+ * Counters of the deduplicated large-chi path (zxs_dedup.cuh): out[0] batches,
+ * out[1] batches that fell back to the per-shot kernel (more distinct keys
+ * than ZXS_DEDUP_MAX_KEYS), out[2] distinct keys evaluated (summed over chain
+ * positions), out[3] algorithmic shared-memory plane-load bytes of those
+ * evaluations, out[4] dedup_eval_kernel launches, out[5] 1 if the path is
+ * enabled. reset != 0 clears the counters after reading.
+ */
+zxs_status zxs_dedup_stats(zxs_sampler *s, int reset, uint64_t *out /*[6]*/);
+
 /* Synchronizes `stream` and reports (then clears) a device-side ratio breakdown. */
 zxs_status zxs_check_errors(zxs_sampler *s, void *stream);
 

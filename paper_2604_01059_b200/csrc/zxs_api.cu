@@ -175,12 +175,15 @@ struct zxs_sampler {
     std::vector<uint32_t> dd_tsb, dd_tdb, dd_tw, dd_tbb;  // host copies per mono tensor
     std::vector<unsigned long long> dd_key_mask;          // per mono component
     size_t dd_smem = 0;
+    uint32_t dd_seg_buf_words = 0;  // per-warp segment copy in dedup_eval_kernel (0: from global)
     char *dd_buf = nullptr;  // keys, slots, prev, values, partials, two tables
     size_t dd_buf_bytes = 0;
     uint64_t dd_cap_shots = 0;
     uint32_t dd_table_slots = 0;
     bool dd_dirty = true;  // tables need a full reset
     uint32_t *dd_pinned = nullptr;
+    std::vector<uint64_t> dd_tloads;  // per mono tensor: plane loads per 32-key word
+    uint64_t dd_stats[5] = {};        // batches, fallbacks, evaluated keys, plane-load bytes, eval launches
 
     // error model kept on the host for probability_of's enumeration
     // (sampler.cpp:370-429): per mechanism the f_vectors as FW-word masks and
@@ -482,6 +485,7 @@ struct MonoHost {
     std::vector<uint4> segs;                   // {word_begin, n_words, n_nodes, 0}
     std::vector<uint32_t> tensor_seg_begin{0};
     std::vector<unsigned long long> comp_key_mask;  // per mono component: raw params any tensor reads
+    std::vector<uint64_t> tensor_loads;             // per mono tensor: plane loads per 32-shot word
 };
 
 // One term after lowering: its records as sorted tokens (record word, plus
@@ -782,6 +786,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
         std::vector<uint32_t> sw;   // segment streams of this component
         std::vector<uint4> sg;      // segments (word_begin relative to sw)
         std::vector<uint32_t> tsb;  // per tensor: first segment (relative to sg)
+        std::vector<uint64_t> tl;   // per tensor: plane loads per 32-shot word
         uint64_t recs = 0, dead = 0, nsel = 0, loads = 0, nodes_total = 0;
         for (uint32_t t = t0; ok && t < t1; t++) {
             form_id.clear();
@@ -976,6 +981,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                     cum += nodes[i].recs.size() + (nodes[i].leaf ? 8 : 1);
                 }
             }
+            const uint64_t loads_before = loads;
             std::vector<uint32_t> node_off(nodes.size()), node_len(nodes.size());
             std::vector<uint32_t> nw;
             size_t node_i = 0;
@@ -1034,6 +1040,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                 cur_nodes++;
             }
             if (ok) close_chunk();
+            tl.push_back(loads - loads_before);
             // segment streams: each starts with its first node's ancestors (internal nodes,
             // replayed to rebuild the stack), then the segment's own nodes; flags cleared
             tsb.push_back(uint32_t(sg.size()));
@@ -1084,6 +1091,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                 unsigned long long km = 0;
                 for (uint64_t v : cb) km |= v;
                 H.comp_key_mask.push_back(km);
+                H.tensor_loads.insert(H.tensor_loads.end(), tl.begin(), tl.end());
             }
             for (size_t i = 1; i < tcb.size(); i++) H.tensor_chunk_begin.push_back(tcb[i]);
             H.tensor_chunk_begin.push_back(uint32_t(H.chunks.size()));
@@ -1748,8 +1756,14 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         s->dd_tw = MH.tensor_width;
         s->dd_tbb = MH.tensor_basis_begin;
         s->dd_key_mask = MH.comp_key_mask;
+        s->dd_tloads = MH.tensor_loads;
         s->dd_smem = size_t(ma.max_dict) * 16 + size_t(MH.all_plane + 2) * 32 * 4 +
                      size_t(zxs_dev::kDedupWarps) * ma.stack_depth * 96 * 4;
+        uint32_t max_seg = 0;
+        for (const uint4 &g : MH.segs) max_seg = std::max(max_seg, g.y);
+        s->dd_seg_buf_words = (max_seg + 3) & ~3u;
+        if (s->dd_smem + size_t(zxs_dev::kDedupWarps) * s->dd_seg_buf_words * 4 > 227 * 1024) s->dd_seg_buf_words = 0;
+        s->dd_smem += size_t(zxs_dev::kDedupWarps) * s->dd_seg_buf_words * 4;
         s->dedup = s->dd_smem <= 227 * 1024 && s->dd_key_mask.size() == MH.comps.size();
         if (const char *e = std::getenv("ZXS_DEDUP")) s->dedup = s->dedup && std::atoi(e) != 0;
     }
@@ -1872,20 +1886,33 @@ struct DedupBufs {
     unsigned long long *key;
     uint32_t *slot;
     double *prev, *value0, *value, *partial;
+    unsigned long long *counts;  // per output, added to the caller's counts when the chain completes
     zxs_dev::DedupTable table[2];
 };
+
+// Distinct keys per chain position the tables hold (ZXS_DEDUP_MAX_KEYS, default
+// 2^20); a batch with more falls back to mono_kernel (bit-identical values).
+uint32_t dedup_max_keys() {
+    uint32_t m = 1u << 20;
+    if (const char *e = std::getenv("ZXS_DEDUP_MAX_KEYS")) m = uint32_t(std::max(16L, std::atol(e)));
+    return m;
+}
 
 DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
     uint64_t cap = std::max<uint64_t>(s->dd_cap_shots, 1024);
     while (cap < shots) cap *= 2;
-    uint32_t slots = 2048;
-    while (slots < 2 * cap) slots *= 2;
+    const uint32_t max_ids = uint32_t(std::min<uint64_t>(cap, dedup_max_keys()));
+    uint32_t slots = 4096;  // >= 2 max_ids + room for the inserts in flight when the limit is hit
+    while (slots < 2 * max_ids + 65536u) slots *= 2;
     uint32_t max_segs = 1;
     for (size_t t = 0; t + 1 < s->dd_tsb.size(); t++) max_segs = std::max(max_segs, s->dd_tsb[t + 1] - s->dd_tsb[t]);
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-    const size_t per_table = al(size_t(slots) * 8) + al(size_t(slots) * 4) + al(4) + al(size_t(cap) * 8) + al(size_t(cap) * 4);
-    const size_t bytes = al(cap * 8) + al(cap * 4) + 3 * al(cap * 8) + al(size_t(max_segs) * kDedupRoundKeys * 8) + 2 * per_table;
-    if (bytes > s->dd_buf_bytes) {
+    const size_t nout = std::max<uint32_t>(1, s->m.num_outputs);
+    const size_t per_table = al(size_t(slots) * 8) + al(size_t(slots) * 4) + al(4) + al(size_t(max_ids) * 8) +
+                             al(size_t(max_ids) * 4);
+    const size_t bytes = al(cap * 8) + al(cap * 4) + al(cap * 8) + 2 * al(size_t(max_ids) * 8) +
+                         al(size_t(max_segs) * kDedupRoundKeys * 8) + al(nout * 8) + 2 * per_table;
+    if (bytes > s->dd_buf_bytes || slots != s->dd_table_slots) {
         if (s->dd_buf) CK(cudaFree(s->dd_buf));
         s->dd_buf = nullptr;
         s->dd_buf_bytes = 0;
@@ -1900,19 +1927,21 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
     d.key = reinterpret_cast<unsigned long long *>(take(cap * 8));
     d.slot = reinterpret_cast<uint32_t *>(take(cap * 4));
     d.prev = reinterpret_cast<double *>(take(cap * 8));
-    d.value0 = reinterpret_cast<double *>(take(cap * 8));
-    d.value = reinterpret_cast<double *>(take(cap * 8));
+    d.value0 = reinterpret_cast<double *>(take(size_t(max_ids) * 8));
+    d.value = reinterpret_cast<double *>(take(size_t(max_ids) * 8));
     d.partial = reinterpret_cast<double *>(take(size_t(max_segs) * kDedupRoundKeys * 8));
+    d.counts = reinterpret_cast<unsigned long long *>(take(nout * 8));
     for (int i = 0; i < 2; i++) {
         zxs_dev::DedupTable &t = d.table[i];
         t.keys = reinterpret_cast<unsigned long long *>(take(size_t(slots) * 8));
         t.ids = reinterpret_cast<uint32_t *>(take(size_t(slots) * 4));
         t.mask = slots - 1;
+        t.max_ids = max_ids;
         t.count = reinterpret_cast<uint32_t *>(take(4));
-        t.ukeys = reinterpret_cast<unsigned long long *>(take(cap * 8));
-        t.uslot = reinterpret_cast<uint32_t *>(take(cap * 4));
+        t.ukeys = reinterpret_cast<unsigned long long *>(take(size_t(max_ids) * 8));
+        t.uslot = reinterpret_cast<uint32_t *>(take(size_t(max_ids) * 4));
     }
-    if (s->dd_dirty || slots != s->dd_table_slots) {
+    if (s->dd_dirty) {
         for (int i = 0; i < 2; i++) {
             CK(cudaMemset(d.table[i].keys, 0xff, size_t(slots) * 8));
             CK(cudaMemset(d.table[i].count, 0, 4));
@@ -1955,6 +1984,10 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const zxs_dev::DedupTable &t, uint3
         e.keys = t.ukeys + r0;
         e.n_keys = std::min(kDedupRoundKeys, n - r0);
         e.partial = partial;
+        e.seg_buf_words = s->dd_seg_buf_words;
+        s->dd_stats[2] += e.n_keys;
+        s->dd_stats[3] += (mt < s->dd_tloads.size() ? s->dd_tloads[mt] : 0) * ((e.n_keys + 31) / 32) * 4;
+        s->dd_stats[4] += 1;
         const uint64_t items = uint64_t((e.n_keys + zxs_dev::kDedupKeysPerWarp - 1) / zxs_dev::kDedupKeysPerWarp) *
                                ((ng + zxs_dev::kDedupWarps - 1) / zxs_dev::kDedupWarps);
         const unsigned grid = unsigned(std::min<uint64_t>(items, uint64_t(s->sm_count)));
@@ -1965,30 +1998,48 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const zxs_dev::DedupTable &t, uint3
                             dim3(zxs_dev::kDedupWarps * 32), args, s->dd_smem, st));
         s->time_end(3, st, t0);
         s->time_begin(4, st, t0);
-        zxs_dev::dedup_reduce_kernel<<<(e.n_keys + 255) / 256, 256, 0, st>>>(partial, ng, e.n_keys, value + r0);
+        zxs_dev::dedup_reduce_kernel<<<(e.n_keys + 63) / 64, 64, 0, st>>>(partial, ng, e.n_keys, value + r0);
         CK(cudaGetLastError());
         s->time_end(4, st, t0);
     }
 }
 
 // The large-chi components of shots [first_shot, first_shot + shots) on the
-// deduplicated path, after shot_kernel left their f-columns in `fcols`.
+// deduplicated path, after shot_kernel left their f-columns in `fcols`. A
+// chain position with more distinct keys than the tables hold sends the
+// whole batch to mono_kernel instead (same canonical values, so the same bits).
 void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *fcols, uint64_t fcols_ld32,
                   cudaStream_t st) {
     if (a.shots == 0) return;
     DedupBufs d = dedup_reserve(s, a.shots);
     const zxs_dev::MonoArgs &m = s->mono;
     const unsigned pgrid = unsigned(std::min<uint64_t>((a.shots + 255) / 256, uint64_t(s->sm_count) * 8));
+    const uint32_t nout = s->m.num_outputs;
     s->dd_dirty = true;  // until the chain completes
+    if (a.counts) CK(cudaMemsetAsync(d.counts, 0, size_t(std::max<uint32_t>(nout, 1)) * 8, st));
     cudaEvent_t t0 = nullptr;
+    auto clear = [&](const zxs_dev::DedupTable &t, uint32_t n) {
+        s->time_begin(4, st, t0);
+        zxs_dev::dedup_clear_kernel<<<std::max(1u, std::min((n + 255) / 256, 1024u)), 256, 0, st>>>(t, n);
+        CK(cudaGetLastError());
+        s->time_end(4, st, t0);
+    };
+    s->dd_stats[0] += 1;
+    auto fallback = [&]() {  // tables left dirty: reset on the next call
+        s->dd_stats[1] += 1;
+        s->time_begin(2, st, t0);
+        launch_mono(s, a, fcols, fcols_ld32, -1, nullptr, 0, st);
+        s->time_end(2, st, t0);
+    };
     for (uint32_t hc = 0; hc < m.n_comps; hc++) {
         const zxs_dev::HeavyComp cd = m.comps[hc];
         zxs_dev::DedupInitArgs ia{};
         ia.shots = a.shots;
         ia.fcols = fcols;
         ia.fcols_ld32 = fcols_ld32;
-        ia.f_width = m.f_width;
-        ia.key_mask = s->dd_key_mask[hc];
+        for (uint32_t p = 0; p < std::min(m.f_width, 63u); p++) {
+            if ((s->dd_key_mask[hc] >> p) & 1ull) ia.bits[ia.n_bits++] = uint8_t(p);
+        }
         ia.key = d.key;
         ia.slot = d.slot;
         ia.table = d.table[0];
@@ -1998,6 +2049,7 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
                             st));
         s->time_end(4, st, t0);
         uint32_t n = dedup_count(s, d.table[0], st);
+        if (n > d.table[0].max_ids) return fallback();
         dedup_eval(s, cd.first_tensor, d.table[0], n, d.value0, d.partial, st);
         for (uint32_t j = 0; j < cd.n_out; j++) {
             const zxs_dev::DedupTable &cur = d.table[j & 1], &nxt = d.table[(j + 1) & 1];
@@ -2022,7 +2074,7 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
             ra.insert_next = j + 1 < cd.n_out;
             ra.out32 = a.out32;
             ra.out_ld32 = a.ld32;
-            ra.counts = a.counts;
+            ra.counts = a.counts ? d.counts : nullptr;
             ra.uniforms = a.uniforms;
             ra.uniforms_ld = a.uniforms_ld;
             ra.upos = cd.upos_base + j;
@@ -2032,16 +2084,19 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
             CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_ar_kernel), dim3(pgrid), dim3(256), rargs,
                                 0, st));
             s->time_end(4, st, t0);
-            s->time_begin(4, st, t0);
-            zxs_dev::dedup_clear_kernel<<<std::max(1u, std::min((n + 255) / 256, 1024u)), 256, 0, st>>>(cur, n);
-            CK(cudaGetLastError());
-            s->time_end(4, st, t0);
-            if (ra.insert_next) n = dedup_count(s, nxt, st);
+            clear(cur, n);
+            if (ra.insert_next) {
+                n = dedup_count(s, nxt, st);
+                if (n > nxt.max_ids) return fallback();
+            }
         }
-        if (cd.n_out == 0) {  // no autoregressive step cleared the first table
-            zxs_dev::dedup_clear_kernel<<<std::max(1u, std::min((n + 255) / 256, 1024u)), 256, 0, st>>>(d.table[0], n);
-            CK(cudaGetLastError());
-        }
+        if (cd.n_out == 0) clear(d.table[0], n);  // no autoregressive step cleared it
+    }
+    if (a.counts) {
+        s->time_begin(4, st, t0);
+        zxs_dev::dedup_add_counts_kernel<<<(nout + 255) / 256, 256, 0, st>>>(d.counts, a.counts, nout);
+        CK(cudaGetLastError());
+        s->time_end(4, st, t0);
     }
     s->dd_dirty = false;
 }
@@ -2298,6 +2353,16 @@ zxs_status zxs_kernel_times_n(zxs_sampler *s, double *ms, uint64_t *launches, ui
             ms[t.first] += e;
             launches[t.first]++;
         }
+    });
+}
+
+zxs_status zxs_dedup_stats(zxs_sampler *s, int reset, uint64_t *out) {
+    return guarded([&] {
+        if (!s || !out) fail(ZXS_INVALID_ARGUMENT, "null argument");
+        std::lock_guard<std::mutex> lk(s->mu);
+        for (int i = 0; i < 5; i++) out[i] = s->dd_stats[i];
+        out[5] = s->dedup ? 1 : 0;
+        if (reset) std::memset(s->dd_stats, 0, sizeof(s->dd_stats));
     });
 }
 

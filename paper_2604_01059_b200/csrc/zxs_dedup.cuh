@@ -36,6 +36,7 @@ struct DedupTable {
     unsigned long long *keys;  // [mask + 1], kDedupEmpty when free
     uint32_t *ids;             // [mask + 1] dense id of the key in the slot
     uint32_t mask;
+    uint32_t max_ids;          // ukeys / uslot capacity; more keys = overflow (host falls back)
     uint32_t *count;           // distinct keys inserted
     unsigned long long *ukeys; // [id] key
     uint32_t *uslot;           // [id] slot (for clearing)
@@ -55,15 +56,18 @@ __device__ __forceinline__ uint32_t dedup_hash(unsigned long long k, uint32_t ma
 __device__ __forceinline__ uint32_t dedup_insert(const DedupTable &t, unsigned long long key) {
     uint32_t slot = dedup_hash(key, t.mask);
     while (true) {
+        if (*reinterpret_cast<volatile uint32_t *>(t.count) >= t.max_ids) return 0;  // overflow: batch falls back
         const unsigned long long k = *reinterpret_cast<volatile unsigned long long *>(&t.keys[slot]);
         if (k == key) return slot;
         if (k == kDedupEmpty) {
             const unsigned long long old = atomicCAS(&t.keys[slot], kDedupEmpty, key);
             if (old == kDedupEmpty) {
                 const uint32_t id = atomicAdd(t.count, 1u);
-                t.ids[slot] = id;
-                t.ukeys[id] = key;
-                t.uslot[id] = slot;
+                if (id < t.max_ids) {
+                    t.ids[slot] = id;
+                    t.ukeys[id] = key;
+                    t.uslot[id] = slot;
+                }
                 return slot;
             }
             if (old == key) return slot;
@@ -72,23 +76,60 @@ __device__ __forceinline__ uint32_t dedup_insert(const DedupTable &t, unsigned l
     }
 }
 
-// Warp-cooperative insert: one insert per distinct key of the warp.
-__device__ __forceinline__ uint32_t dedup_insert_warp(const DedupTable &t, unsigned long long key, bool valid,
-                                                      uint32_t lane) {
-    const unsigned long long k = valid ? key : kDedupEmpty;
-    const uint32_t peers = __match_any_sync(kFull, k);
-    const uint32_t leader = __ffs(peers) - 1;
+// Per-warp cache of recent (key, slot) pairs, one pair per lane (lanes 0..7
+// used): the key distribution is extremely skewed (most shots carry the
+// all-zero key), so most shots resolve here instead of hammering one table
+// line in L2.
+struct DedupWarpCache {
+    unsigned long long key = kDedupEmpty;
     uint32_t slot = 0;
-    if (lane == leader && valid) slot = dedup_insert(t, k);
-    return __shfl_sync(kFull, slot, leader);
+    uint32_t next = 0;  // round-robin victim (warp-uniform)
+};
+constexpr uint32_t kDedupCacheWays = 8;
+
+// Warp-cooperative insert: cache lookup, then one table insert per distinct
+// missing key of the warp.
+__device__ __forceinline__ uint32_t dedup_insert_warp(const DedupTable &t, unsigned long long key, bool valid,
+                                                      uint32_t lane, DedupWarpCache &c) {
+    const unsigned long long k = valid ? key : kDedupEmpty;
+    uint32_t slot = 0;
+    bool hit = !valid;
+#pragma unroll
+    for (uint32_t i = 0; i < kDedupCacheWays; i++) {
+        const unsigned long long ck = __shfl_sync(kFull, c.key, i);
+        const uint32_t cs = __shfl_sync(kFull, c.slot, i);
+        if (!hit && ck == k) {
+            hit = true;
+            slot = cs;
+        }
+    }
+    const uint32_t miss = __ballot_sync(kFull, !hit);
+    if (miss) {
+        const uint32_t peers = __match_any_sync(kFull, hit ? kDedupEmpty : k);
+        const uint32_t leader = __ffs(peers) - 1;
+        uint32_t ns = 0;
+        if (!hit && lane == leader) ns = dedup_insert(t, k);
+        ns = __shfl_sync(kFull, ns, leader);
+        if (!hit) slot = ns;
+        // the first missing key enters the cache
+        const uint32_t first = __ffs(miss) - 1;
+        const unsigned long long fk = __shfl_sync(kFull, k, first);
+        const uint32_t fs = __shfl_sync(kFull, slot, first);
+        if (lane == c.next) {
+            c.key = fk;
+            c.slot = fs;
+        }
+        c.next = (c.next + 1) % kDedupCacheWays;
+    }
+    return slot;
 }
 
 struct DedupInitArgs {
     uint64_t shots;
     const uint32_t *fcols;  // [f_width][fcols_ld32]
     uint64_t fcols_ld32;
-    uint32_t f_width;
-    unsigned long long key_mask;
+    uint32_t n_bits;          // f columns the component's tensors read
+    uint8_t bits[64];
     unsigned long long *key;  // [shots]
     uint32_t *slot;           // [shots]
     DedupTable table;
@@ -98,18 +139,24 @@ struct DedupInitArgs {
 // the warp's 32 shots share every f-column word (broadcast loads).
 __global__ void __launch_bounds__(256) dedup_init_kernel(const __grid_constant__ DedupInitArgs a) {
     const uint32_t lane = threadIdx.x & 31u;
+    DedupWarpCache cache;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint64_t s0 = uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); s0 < a.shots; s0 += stride) {
         const uint64_t s = s0 + lane, wd = s0 >> 5;
         const bool valid = s < a.shots;
         unsigned long long key = 0;
-        const uint32_t nf = min(a.f_width, 63u);
-        for (uint32_t p = 0; p < nf; p++) {
-            if (!((a.key_mask >> p) & 1ull)) continue;
-            const uint32_t word = __ldg(a.fcols + p * a.fcols_ld32 + wd);
-            key |= (unsigned long long)((word >> lane) & 1u) << p;
+        for (uint32_t i0 = 0; i0 < a.n_bits; i0 += 16) {  // 16 column loads in flight
+            uint32_t wv[16];
+#pragma unroll
+            for (uint32_t i = 0; i < 16; i++) {
+                wv[i] = i0 + i < a.n_bits ? __ldg(a.fcols + a.bits[i0 + i] * a.fcols_ld32 + wd) : 0u;
+            }
+#pragma unroll
+            for (uint32_t i = 0; i < 16; i++) {
+                if (i0 + i < a.n_bits) key |= (unsigned long long)((wv[i] >> lane) & 1u) << a.bits[i0 + i];
+            }
         }
-        const uint32_t slot = dedup_insert_warp(a.table, key, valid, lane);
+        const uint32_t slot = dedup_insert_warp(a.table, key, valid, lane, cache);
         if (valid) {
             a.key[s] = key;
             a.slot[s] = slot;
@@ -130,6 +177,7 @@ struct DedupEvalArgs {
     const unsigned long long *keys;   // the round's keys
     uint32_t n_keys;
     double *partial;                  // [n_segs][n_keys]
+    uint32_t seg_buf_words;           // per-warp shared-memory copy of its segment (0: walk from global)
 };
 
 // Items = (key group of 1024, block of kDedupWarps segments); a CTA builds the
@@ -142,6 +190,8 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
     uint32_t *stack_all = planes + h.n_planes * 32;                  // per warp [depth][3][lane]
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     BW<1> *stk = reinterpret_cast<BW<1> *>(stack_all + warp * h.stack_depth * 96) + lane;
+    uint32_t *segbuf = stack_all + kDedupWarps * h.stack_depth * 96 + warp * h.seg_buf_words;
+    uint32_t have_seg = 0xffffffffu;  // segment currently in segbuf
     const char *pl = reinterpret_cast<const char *>(planes + lane);
 
     for (uint32_t i = threadIdx.x; i < h.n_dict; i += blockDim.x) sd[i] = __ldg(h.dict + i);
@@ -174,10 +224,24 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
         const uint32_t seg = blk * kDedupWarps + warp;
         if (seg >= h.n_segs) continue;
         const uint4 sgd = __ldg(h.segs + seg);
+        // the warp's segment into shared memory once (the walk's record loads are
+        // warp-uniform and serial: broadcast LDS instead of L1/L2 round trips); a CTA
+        // keeps its segment block across key groups
+        const uint32_t *w = h.words + sgd.x;
+        if (sgd.y <= h.seg_buf_words) {
+            if (have_seg != seg) {
+                const uint32_t *src = h.words + sgd.x;
+#pragma unroll 4
+                for (uint32_t i = lane; i < sgd.y; i += 32) segbuf[i] = __ldg(src + i);
+                __syncwarp();
+                have_seg = seg;
+            }
+            w = segbuf;
+        }
         double acc[32];
 #pragma unroll
         for (int s = 0; s < 32; s++) acc[s] = 0.0;
-        mono_walk<1, false>(h.words + sgd.x, sgd.z, sd, pl, stk, acc, nullptr);
+        mono_walk<1, false>(w, sgd.z, sd, pl, stk, acc, nullptr);
         const uint32_t k0 = kg * kDedupKeysPerWarp + lane * 32;
         double *out = h.partial + uint64_t(seg) * h.n_keys + k0;
 #pragma unroll
@@ -192,9 +256,22 @@ __global__ void dedup_reduce_kernel(const double *__restrict__ partial, uint32_t
                                     double *__restrict__ value) {
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n_keys; k += gridDim.x * blockDim.x) {
         double v = 0.0;
-        for (uint32_t g = 0; g < n_segs; g++) v = __dadd_rn(v, partial[uint64_t(g) * n_keys + k]);
+        uint32_t g = 0;
+        for (; g + 16 <= n_segs; g += 16) {  // 16 independent loads in flight, adds in order
+            double x[16];
+#pragma unroll
+            for (int i = 0; i < 16; i++) x[i] = __ldg(partial + uint64_t(g + i) * n_keys + k);
+#pragma unroll
+            for (int i = 0; i < 16; i++) v = __dadd_rn(v, x[i]);
+        }
+        for (; g < n_segs; g++) v = __dadd_rn(v, __ldg(partial + uint64_t(g) * n_keys + k));
         value[k] = v;
     }
+}
+
+__global__ void dedup_add_counts_kernel(const unsigned long long *__restrict__ src, unsigned long long *dst, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && src[i]) dst[i] += src[i];
 }
 
 // Frees the slots of the table's keys and resets its count (the next
@@ -237,6 +314,7 @@ __global__ void __launch_bounds__(256) dedup_ar_kernel(const __grid_constant__ D
     const uint32_t stream = 0x80000000u ^ (a.ci << 12) ^ a.j;  // sampler.cpp:37-39
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     unsigned long long ones = 0;
+    DedupWarpCache cache;
     // up to the 64-shot boundary: the record's last 64-bit word gets zero tail bits
     const uint64_t shots64 = (a.shots + 63) & ~uint64_t(63);
     for (uint64_t s0 = uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); s0 < shots64; s0 += stride) {
@@ -274,7 +352,7 @@ __global__ void __launch_bounds__(256) dedup_ar_kernel(const __grid_constant__ D
             ones += __popc(word);
         }
         if (a.insert_next) {
-            const uint32_t ns = dedup_insert_warp(a.next, key, valid, lane);
+            const uint32_t ns = dedup_insert_warp(a.next, key, valid, lane, cache);
             if (valid) {
                 a.key[s] = key;
                 a.slot[s] = ns;

@@ -138,6 +138,13 @@ class CompiledSampler:
         _native.check(_native.lib().zxs_kernel_times_n(self._h, ms, n, len(names)))
         return {k: (ms[i], int(n[i])) for i, k in enumerate(names)}
 
+    def dedup_stats(self, reset: bool = False) -> dict:
+        """Counters of the deduplicated large-chi path (include/zxs_b200.h zxs_dedup_stats)."""
+        out = (ctypes.c_uint64 * 6)()
+        _native.check(_native.lib().zxs_dedup_stats(self._h, int(reset), out))
+        return dict(zip(("batches", "fallbacks", "keys", "plane_load_bytes", "eval_launches", "enabled"),
+                        (int(x) for x in out)))
+
     # ---- host-buffer entry points --------------------------------------
     def sample_into(self, expected_mode: int, seed: int, first_shot: int, shots: int, out: np.ndarray,
                     stream: int = 0) -> np.ndarray:

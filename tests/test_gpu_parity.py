@@ -452,3 +452,28 @@ def test_imag_health_check():
     mi_dev = zx.eval_batch(cs, 0, 1, P, 2048).max_imag_ratio
     _, mi_ref = orc.eval_batch(int(orc.arrays["comp_tensor_begin"][0]) + 1, P, 2048)
     assert abs(mi_dev - mi_ref) <= 1e-9 * max(mi_ref, 1e-300)  # hypot may differ in the last ulp
+
+
+def test_dedup_overflow_falls_back_bit_identical():
+    """More distinct keys than the tables hold (ZXS_DEDUP_MAX_KEYS=64): the batch
+    goes to mono_kernel; records and counts stay identical."""
+    import os
+    name = "surface_d3_xmem_9t"
+    os.environ["ZXS_DEDUP_MAX_KEYS"] = "64"
+    try:
+        a = _heavy_model(name, min_factors="0", mono="1", dedup="1")
+        orc = coracle.OracleModel.load(golden_path(name))
+        rng = np.random.default_rng(43)
+        shots = 5000
+        f = rng.integers(0, 2**63, size=(orc.f_width, (shots + 63) // 64), dtype=np.uint64)
+        f[:, -1] &= np.uint64((1 << (shots & 63)) - 1)
+        u = rng.random((orc.num_positions, shots))
+        got = zx.sample_given_f(a, f, shots, uniforms=u)
+        cnt = zx.count_outputs(a, 20000, seed=5)
+        small = sample(a, 3000, 2, 11)  # few keys: stays on the deduplicated path after the overflow
+    finally:
+        del os.environ["ZXS_DEDUP_MAX_KEYS"]
+    b = _heavy_model(name, min_factors="0", mono="1", dedup="0")
+    assert np.array_equal(got, zx.sample_given_f(b, f, shots, uniforms=u))
+    assert np.array_equal(cnt, zx.count_outputs(b, 20000, seed=5))
+    assert np.array_equal(small, sample(b, 3000, 2, 11))

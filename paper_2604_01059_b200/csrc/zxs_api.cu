@@ -176,6 +176,9 @@ struct zxs_sampler {
     std::vector<unsigned long long> dd_key_mask;          // per mono component
     size_t dd_smem = 0;
     uint32_t dd_seg_buf_words = 0;  // per-warp segment copy in dedup_eval_kernel (0: from global)
+    const uint32_t *dd_block_forms = nullptr, *dd_block_form_begin = nullptr;
+    std::vector<uint32_t> dd_tfb;    // per mono tensor: first block form table (~0: dictionary ids)
+    uint32_t dd_table_bytes = 0;
     char *dd_buf = nullptr;  // keys, slots, prev, values, partials, two tables
     size_t dd_buf_bytes = 0;
     uint64_t dd_cap_shots = 0;
@@ -486,6 +489,12 @@ struct MonoHost {
     std::vector<uint32_t> tensor_seg_begin{0};
     std::vector<unsigned long long> comp_key_mask;  // per mono component: raw params any tensor reads
     std::vector<uint64_t> tensor_loads;             // per mono tensor: plane loads per 32-shot word
+    // block form tables (dedup_eval_kernel): per block of kDedupWarps segments the
+    // tensor dictionary entries its records use; segment streams carry block-local ids
+    std::vector<uint32_t> block_forms;
+    std::vector<uint32_t> block_form_begin{0};
+    std::vector<uint32_t> tensor_first_block;  // per mono tensor
+    uint32_t max_block_forms = 0;
 };
 
 // One term after lowering: its records as sorted tokens (record word, plus
@@ -787,6 +796,8 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
         std::vector<uint4> sg;      // segments (word_begin relative to sw)
         std::vector<uint32_t> tsb;  // per tensor: first segment (relative to sg)
         std::vector<uint64_t> tl;   // per tensor: plane loads per 32-shot word
+        std::vector<uint32_t> bf, bfb, tfb;  // block forms, block ends (relative), per tensor first block
+        uint32_t max_bf = 0;
         uint64_t recs = 0, dead = 0, nsel = 0, loads = 0, nodes_total = 0;
         for (uint32_t t = t0; ok && t < t1; t++) {
             form_id.clear();
@@ -1065,6 +1076,52 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                     sg.push_back(make_uint4(b, uint32_t(sw.size()) - b, nn, 0));
                     i = j;
                 }
+                // block form tables: the dictionary entries each block of kDedupWarps segments
+                // uses; its records are rewritten to block-local ids (kept global when a block
+                // needs more than kDedupMaxBlockForms: tensor_first_block = ~0)
+                const uint32_t s0 = tsb.back(), s1 = uint32_t(sg.size());
+                auto for_forms = [&](uint32_t b0, const std::function<uint32_t(uint32_t)> &fn) {
+                    for (uint32_t g = b0; g < std::min(s1, b0 + uint32_t(zxs_dev::kDedupWarps)); g++) {
+                        uint32_t q = sg[g].x;
+                        for (uint32_t nn2 = 0; nn2 < sg[g].z; nn2++) {
+                            const uint32_t h0 = sw[q], h1 = sw[q + 1], h2 = sw[q + 2];
+                            q += 3 + ((h0 >> 31) ? 4 : 0);
+                            const uint32_t ns = (h1 & 0xffu) + ((h1 >> 8) & 0xffu) + ((h1 >> 16) & 0xffu) + (h1 >> 24) +
+                                                (h2 & 0xffu);
+                            for (uint32_t r = 0; r < ns; r++, q++) sw[q] = (sw[q] & ~0xfffu) | fn(sw[q] & 0xfffu);
+                            for (uint32_t gg = 0; gg < (h0 & 0xffu); gg++, q += 2) {
+                                const uint32_t r = sw[q];
+                                sw[q] = (r & 0xf000f000u) | (fn((r >> 16) & 0xfffu) << 16) | fn(r & 0xfffu);
+                            }
+                        }
+                    }
+                };
+                std::vector<std::vector<uint32_t>> lists;
+                bool fits = true;
+                for (uint32_t b0 = s0; b0 < s1; b0 += zxs_dev::kDedupWarps) {
+                    std::map<uint32_t, uint32_t> local;
+                    std::vector<uint32_t> list;
+                    for_forms(b0, [&](uint32_t f) {  // identity pass: collect
+                        if (f != zxs_dev::kMonoNoForm && local.emplace(f, uint32_t(list.size())).second) list.push_back(f);
+                        return f;
+                    });
+                    fits = fits && list.size() <= zxs_dev::kDedupMaxBlockForms;
+                    lists.push_back(std::move(list));
+                }
+                if (!fits) {
+                    tfb.push_back(0xffffffffu);
+                } else {
+                    tfb.push_back(uint32_t(bfb.size()));
+                    size_t k = 0;
+                    for (uint32_t b0 = s0; b0 < s1; b0 += zxs_dev::kDedupWarps, k++) {
+                        std::map<uint32_t, uint32_t> local;
+                        for (uint32_t i = 0; i < lists[k].size(); i++) local.emplace(lists[k][i], i);
+                        for_forms(b0, [&](uint32_t f) { return f == zxs_dev::kMonoNoForm ? f : local.at(f); });
+                        max_bf = std::max(max_bf, uint32_t(lists[k].size()));
+                        bf.insert(bf.end(), lists[k].begin(), lists[k].end());
+                        bfb.push_back(uint32_t(bf.size()));
+                    }
+                }
             }
             nodes_total += nodes.size();
         }
@@ -1092,6 +1149,11 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                 for (uint64_t v : cb) km |= v;
                 H.comp_key_mask.push_back(km);
                 H.tensor_loads.insert(H.tensor_loads.end(), tl.begin(), tl.end());
+                const uint32_t fb0 = uint32_t(H.block_forms.size()), blk0 = uint32_t(H.block_form_begin.size() - 1);
+                H.block_forms.insert(H.block_forms.end(), bf.begin(), bf.end());
+                for (uint32_t x : bfb) H.block_form_begin.push_back(x + fb0);
+                for (uint32_t x : tfb) H.tensor_first_block.push_back(x == 0xffffffffu ? x : x + blk0);
+                H.max_block_forms = std::max(H.max_block_forms, max_bf);
             }
             for (size_t i = 1; i < tcb.size(); i++) H.tensor_chunk_begin.push_back(tcb[i]);
             H.tensor_chunk_begin.push_back(uint32_t(H.chunks.size()));
@@ -1641,6 +1703,9 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     size_t o_mtw = ar.add(MH.tensor_width);
     size_t o_mtbb = ar.add(MH.tensor_basis_begin);
     size_t o_mbasis = ar.add(MH.basis);
+    if (MH.block_forms.empty()) MH.block_forms.push_back(0);
+    size_t o_bf = ar.add(MH.block_forms);
+    size_t o_bfb = ar.add(MH.block_form_begin);
     if (MH.seg_words.empty()) MH.seg_words.assign(4, 0);
     if (MH.segs.empty()) MH.segs.push_back(make_uint4(0, 0, 0, 0));
     size_t o_sw = ar.add(MH.seg_words);
@@ -1757,7 +1822,11 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         s->dd_tbb = MH.tensor_basis_begin;
         s->dd_key_mask = MH.comp_key_mask;
         s->dd_tloads = MH.tensor_loads;
-        s->dd_smem = size_t(ma.max_dict) * 16 + size_t(MH.all_plane + 2) * 32 * 4 +
+        s->dd_block_forms = reinterpret_cast<const uint32_t *>(b + o_bf);
+        s->dd_block_form_begin = reinterpret_cast<const uint32_t *>(b + o_bfb);
+        s->dd_tfb = MH.tensor_first_block;
+        s->dd_table_bytes = uint32_t(std::max<size_t>(size_t(ma.max_dict) * 16, size_t(MH.max_block_forms) * 128));
+        s->dd_smem = size_t(s->dd_table_bytes) + size_t(MH.all_plane + 2) * 32 * 4 +
                      size_t(zxs_dev::kDedupWarps) * ma.stack_depth * 96 * 4;
         uint32_t max_seg = 0;
         for (const uint4 &g : MH.segs) max_seg = std::max(max_seg, g.y);
@@ -1910,7 +1979,7 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
     const size_t nout = std::max<uint32_t>(1, s->m.num_outputs);
     const size_t per_table = al(size_t(slots) * 8) + al(size_t(slots) * 4) + al(4) + al(size_t(max_ids) * 8) +
                              al(size_t(max_ids) * 4);
-    const size_t bytes = al(cap * 8) + al(cap * 4) + al(cap * 8) + 2 * al(size_t(max_ids) * 8) +
+    const size_t bytes = al(cap * 8) + al(cap * 4) + al(cap * 8) + 2 * al(size_t(slots) * 8) +
                          al(size_t(max_segs) * kDedupRoundKeys * 8) + al(nout * 8) + 2 * per_table;
     if (bytes > s->dd_buf_bytes || slots != s->dd_table_slots) {
         if (s->dd_buf) CK(cudaFree(s->dd_buf));
@@ -1927,8 +1996,8 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
     d.key = reinterpret_cast<unsigned long long *>(take(cap * 8));
     d.slot = reinterpret_cast<uint32_t *>(take(cap * 4));
     d.prev = reinterpret_cast<double *>(take(cap * 8));
-    d.value0 = reinterpret_cast<double *>(take(size_t(max_ids) * 8));
-    d.value = reinterpret_cast<double *>(take(size_t(max_ids) * 8));
+    d.value0 = reinterpret_cast<double *>(take(size_t(slots) * 8));
+    d.value = reinterpret_cast<double *>(take(size_t(slots) * 8));
     d.partial = reinterpret_cast<double *>(take(size_t(max_segs) * kDedupRoundKeys * 8));
     d.counts = reinterpret_cast<unsigned long long *>(take(nout * 8));
     for (int i = 0; i < 2; i++) {
@@ -1964,8 +2033,8 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const zxs_dev::DedupTable &t, uint3
                 cudaStream_t st) {
     const uint32_t g0 = s->dd_tsb[mt], ng = s->dd_tsb[mt + 1] - g0;
     if (n == 0) return;
-    if (ng == 0) {  // every term dead: the value is exactly 0
-        CK(cudaMemsetAsync(value, 0, size_t(n) * 8, st));
+    if (ng == 0) {  // every term dead: the value is exactly 0 (for every slot)
+        CK(cudaMemsetAsync(value, 0, size_t(t.mask + 1) * 8, st));
         return;
     }
     const zxs_dev::MonoArgs &m = s->mono;
@@ -1985,6 +2054,12 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const zxs_dev::DedupTable &t, uint3
         e.n_keys = std::min(kDedupRoundKeys, n - r0);
         e.partial = partial;
         e.seg_buf_words = s->dd_seg_buf_words;
+        e.table_bytes = s->dd_table_bytes;
+        if (mt < s->dd_tfb.size() && s->dd_tfb[mt] != 0xffffffffu) {
+            e.block_forms = s->dd_block_forms;
+            e.block_form_begin = s->dd_block_form_begin;
+            e.first_block = s->dd_tfb[mt];
+        }
         s->dd_stats[2] += e.n_keys;
         s->dd_stats[3] += (mt < s->dd_tloads.size() ? s->dd_tloads[mt] : 0) * ((e.n_keys + 31) / 32) * 4;
         s->dd_stats[4] += 1;
@@ -1998,7 +2073,7 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const zxs_dev::DedupTable &t, uint3
                             dim3(zxs_dev::kDedupWarps * 32), args, s->dd_smem, st));
         s->time_end(3, st, t0);
         s->time_begin(4, st, t0);
-        zxs_dev::dedup_reduce_kernel<<<(e.n_keys + 63) / 64, 64, 0, st>>>(partial, ng, e.n_keys, value + r0);
+        zxs_dev::dedup_reduce_kernel<<<(e.n_keys + 63) / 64, 64, 0, st>>>(partial, ng, e.n_keys, t.uslot + r0, value);
         CK(cudaGetLastError());
         s->time_end(4, st, t0);
     }
@@ -2038,15 +2113,18 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
         ia.fcols = fcols;
         ia.fcols_ld32 = fcols_ld32;
         for (uint32_t p = 0; p < std::min(m.f_width, 63u); p++) {
-            if ((s->dd_key_mask[hc] >> p) & 1ull) ia.bits[ia.n_bits++] = uint8_t(p);
+            if ((s->dd_key_mask[hc] >> p) & 1ull) ia.cols[ia.n_cols++] = uint8_t(p);
         }
         ia.key = d.key;
         ia.slot = d.slot;
         ia.table = d.table[0];
         s->time_begin(4, st, t0);
         void *iargs[] = {&ia};
-        CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_init_kernel), dim3(pgrid), dim3(256), iargs, 0,
-                            st));
+        const uint64_t iwarps = (a.shots + 1023) / 1024;
+        const unsigned igrid = unsigned(std::min<uint64_t>((iwarps + zxs_dev::kDedupInitWarps - 1) / zxs_dev::kDedupInitWarps,
+                                                           uint64_t(s->sm_count) * 8));
+        CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_init_kernel), dim3(igrid),
+                            dim3(zxs_dev::kDedupInitWarps * 32), iargs, 0, st));
         s->time_end(4, st, t0);
         uint32_t n = dedup_count(s, d.table[0], st);
         if (n > d.table[0].max_ids) return fallback();
@@ -2081,7 +2159,8 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
             ra.err = s->dev_err;
             s->time_begin(4, st, t0);
             void *rargs[] = {&ra};
-            CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_ar_kernel), dim3(pgrid), dim3(256), rargs,
+            const unsigned agrid = unsigned(std::min<uint64_t>((a.shots + 511) / 512, uint64_t(s->sm_count) * 8));
+            CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_ar_kernel), dim3(agrid), dim3(256), rargs,
                                 0, st));
             s->time_end(4, st, t0);
             clear(cur, n);
@@ -3015,13 +3094,12 @@ zxs_status zxs_debug_mono_layout(const zxs_model_desc *desc, uint64_t min_factor
         for (const uint4 &c : H.segs) blob.insert(blob.end(), {c.x, c.y, c.z, c.w});
         blob.insert(blob.end(), H.seg_words.begin(), H.seg_words.end());
         for (unsigned long long x : H.comp_key_mask) blob.insert(blob.end(), {uint32_t(x), uint32_t(x >> 32)});
-        // summation segments (zxs_dedup.cuh): counts, tensor_seg_begin, segments, streams, key masks
-        blob.insert(blob.end(), {uint32_t(H.tensor_seg_begin.size()), uint32_t(H.segs.size()),
-                                 uint32_t(H.seg_words.size()), uint32_t(H.comp_key_mask.size())});
-        blob.insert(blob.end(), H.tensor_seg_begin.begin(), H.tensor_seg_begin.end());
-        for (const uint4 &c : H.segs) blob.insert(blob.end(), {c.x, c.y, c.z, c.w});
-        blob.insert(blob.end(), H.seg_words.begin(), H.seg_words.end());
-        for (unsigned long long x : H.comp_key_mask) blob.insert(blob.end(), {uint32_t(x), uint32_t(x >> 32)});
+        // block form tables: counts, tensor_first_block, block_form_begin, block_forms
+        blob.insert(blob.end(), {uint32_t(H.tensor_first_block.size()), uint32_t(H.block_form_begin.size()),
+                                 uint32_t(H.block_forms.size())});
+        blob.insert(blob.end(), H.tensor_first_block.begin(), H.tensor_first_block.end());
+        blob.insert(blob.end(), H.block_form_begin.begin(), H.block_form_begin.end());
+        blob.insert(blob.end(), H.block_forms.begin(), H.block_forms.end());
         *needed = blob.size();
         if (out && cap >= blob.size()) std::memcpy(out, blob.data(), blob.size() * 4);
     });

@@ -31,6 +31,7 @@ namespace zxs_dev {
 constexpr unsigned long long kDedupEmpty = ~0ull;  // keys use at most 63 raw parameter bits
 constexpr int kDedupWarps = 16;                    // dedup_eval_kernel: warps per CTA (one segment each)
 constexpr uint32_t kDedupKeysPerWarp = 1024;       // 32 keys per lane (NW = 1)
+constexpr uint32_t kDedupMaxBlockForms = 1024;     // form values per block table (128 B each in shared memory)
 
 struct DedupTable {
     unsigned long long *keys;  // [mask + 1], kDedupEmpty when free
@@ -41,6 +42,8 @@ struct DedupTable {
     unsigned long long *ukeys; // [id] key
     uint32_t *uslot;           // [id] slot (for clearing)
 };
+
+constexpr uint32_t kDedupMaxProbes = 256;
 
 __device__ __forceinline__ uint32_t dedup_hash(unsigned long long k, uint32_t mask) {
     k ^= k >> 33;
@@ -55,8 +58,11 @@ __device__ __forceinline__ uint32_t dedup_hash(unsigned long long k, uint32_t ma
 // are found without atomics.
 __device__ __forceinline__ uint32_t dedup_insert(const DedupTable &t, unsigned long long key) {
     uint32_t slot = dedup_hash(key, t.mask);
-    while (true) {
-        if (*reinterpret_cast<volatile uint32_t *>(t.count) >= t.max_ids) return 0;  // overflow: batch falls back
+    for (uint32_t probe = 0;; probe++) {
+        if (probe == kDedupMaxProbes) {  // congested (more keys than the table is sized for): fall back
+            atomicMax(t.count, t.max_ids + 1);
+            return 0;
+        }
         const unsigned long long k = *reinterpret_cast<volatile unsigned long long *>(&t.keys[slot]);
         if (k == key) return slot;
         if (k == kDedupEmpty) {
@@ -76,48 +82,49 @@ __device__ __forceinline__ uint32_t dedup_insert(const DedupTable &t, unsigned l
     }
 }
 
-// Per-warp cache of recent (key, slot) pairs, one pair per lane (lanes 0..7
-// used): the key distribution is extremely skewed (most shots carry the
-// all-zero key), so most shots resolve here instead of hammering one table
-// line in L2.
-struct DedupWarpCache {
-    unsigned long long key = kDedupEmpty;
-    uint32_t slot = 0;
-    uint32_t next = 0;  // round-robin victim (warp-uniform)
-};
+// Per-warp cache of recent (key, slot) pairs, replicated in every lane (warp-
+// uniform registers): the key distribution is extremely skewed (most shots
+// carry the all-zero key), so most shots resolve here instead of hammering one
+// table line in L2.
 constexpr uint32_t kDedupCacheWays = 8;
+struct DedupWarpCache {
+    unsigned long long key[kDedupCacheWays];
+    uint32_t slot[kDedupCacheWays];
+    uint32_t next;  // round-robin victim
+    __device__ DedupWarpCache() : next(0) {
+#pragma unroll
+        for (uint32_t i = 0; i < kDedupCacheWays; i++) {
+            key[i] = kDedupEmpty;
+            slot[i] = 0;
+        }
+    }
+};
 
-// Warp-cooperative insert: cache lookup, then one table insert per distinct
-// missing key of the warp.
+// Warp-cooperative insert: cache lookup; lanes whose key missed insert into
+// the table themselves (duplicates of a warp resolve to the same slot); the
+// first missing key enters the cache.
 __device__ __forceinline__ uint32_t dedup_insert_warp(const DedupTable &t, unsigned long long key, bool valid,
                                                       uint32_t lane, DedupWarpCache &c) {
-    const unsigned long long k = valid ? key : kDedupEmpty;
     uint32_t slot = 0;
     bool hit = !valid;
 #pragma unroll
     for (uint32_t i = 0; i < kDedupCacheWays; i++) {
-        const unsigned long long ck = __shfl_sync(kFull, c.key, i);
-        const uint32_t cs = __shfl_sync(kFull, c.slot, i);
-        if (!hit && ck == k) {
-            hit = true;
-            slot = cs;
-        }
+        const bool m = key == c.key[i];
+        slot = (m && !hit) ? c.slot[i] : slot;
+        hit = hit || m;
     }
     const uint32_t miss = __ballot_sync(kFull, !hit);
     if (miss) {
-        const uint32_t peers = __match_any_sync(kFull, hit ? kDedupEmpty : k);
-        const uint32_t leader = __ffs(peers) - 1;
-        uint32_t ns = 0;
-        if (!hit && lane == leader) ns = dedup_insert(t, k);
-        ns = __shfl_sync(kFull, ns, leader);
-        if (!hit) slot = ns;
-        // the first missing key enters the cache
+        if (!hit) slot = dedup_insert(t, key);
         const uint32_t first = __ffs(miss) - 1;
-        const unsigned long long fk = __shfl_sync(kFull, k, first);
+        const unsigned long long fk = __shfl_sync(kFull, key, first);
         const uint32_t fs = __shfl_sync(kFull, slot, first);
-        if (lane == c.next) {
-            c.key = fk;
-            c.slot = fs;
+#pragma unroll
+        for (uint32_t i = 0; i < kDedupCacheWays; i++) {
+            if (i == c.next) {
+                c.key[i] = fk;
+                c.slot[i] = fs;
+            }
         }
         c.next = (c.next + 1) % kDedupCacheWays;
     }
@@ -128,39 +135,63 @@ struct DedupInitArgs {
     uint64_t shots;
     const uint32_t *fcols;  // [f_width][fcols_ld32]
     uint64_t fcols_ld32;
-    uint32_t n_bits;          // f columns the component's tensors read
-    uint8_t bits[64];
+    uint32_t n_cols;            // f columns the component's tensors read (< 63)
+    uint8_t cols[64];
     unsigned long long *key;  // [shots]
     uint32_t *slot;           // [shots]
     DedupTable table;
 };
 
-// Keys of the chain's first tensors (no sampled bits yet): thread = shot,
-// the warp's 32 shots share every f-column word (broadcast loads).
-__global__ void __launch_bounds__(256) dedup_init_kernel(const __grid_constant__ DedupInitArgs a) {
-    const uint32_t lane = threadIdx.x & 31u;
+// Keys of the chain's first tensors (no sampled bits yet). A warp takes 1024
+// shots: lane l loads its own 32-shot word of every f column the component
+// reads (coalesced), scatters the few set bits into per-shot keys in shared
+// memory, then the warp resolves the keys 32 shots at a time (lane = shot):
+// the all-zero key (most shots) by a compare, the rest through the warp cache
+// and the table.
+constexpr uint32_t kDedupInitWarps = 4;
+__global__ void __launch_bounds__(kDedupInitWarps * 32) dedup_init_kernel(const __grid_constant__ DedupInitArgs a) {
+    __shared__ unsigned long long skeys[kDedupInitWarps][32 * 33];  // [shot bit][lane], padded
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    unsigned long long *kw = skeys[warp];
     DedupWarpCache cache;
-    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-    for (uint64_t s0 = uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); s0 < a.shots; s0 += stride) {
-        const uint64_t s = s0 + lane, wd = s0 >> 5;
-        const bool valid = s < a.shots;
-        unsigned long long key = 0;
-        for (uint32_t i0 = 0; i0 < a.n_bits; i0 += 16) {  // 16 column loads in flight
-            uint32_t wv[16];
+    // slot of the all-zero key (inserted once per warp; harmless if no shot has it)
+    uint32_t slot0 = 0;
+    if (lane == 0) slot0 = dedup_insert(a.table, 0ull);
+    slot0 = __shfl_sync(kFull, slot0, 0);
+    const uint64_t n_words = (a.shots + 31) / 32;
+    const uint64_t wstride = uint64_t(gridDim.x) * kDedupInitWarps * 32;
+    for (uint64_t w0 = (uint64_t(blockIdx.x) * kDedupInitWarps + warp) * 32; w0 < n_words; w0 += wstride) {
+        const uint64_t wd = w0 + lane;  // this lane's 32-shot word
 #pragma unroll
-            for (uint32_t i = 0; i < 16; i++) {
-                wv[i] = i0 + i < a.n_bits ? __ldg(a.fcols + a.bits[i0 + i] * a.fcols_ld32 + wd) : 0u;
-            }
-#pragma unroll
-            for (uint32_t i = 0; i < 16; i++) {
-                if (i0 + i < a.n_bits) key |= (unsigned long long)((wv[i] >> lane) & 1u) << a.bits[i0 + i];
+        for (int s = 0; s < 32; s++) kw[s * 33 + lane] = 0ull;
+        if (wd < n_words) {
+            for (uint32_t i = 0; i < a.n_cols; i++) {
+                const uint32_t p = a.cols[i];
+                uint32_t w = __ldg(a.fcols + uint64_t(p) * a.fcols_ld32 + wd);
+                while (w) {
+                    const uint32_t sb = __ffs(w) - 1;
+                    w &= w - 1;
+                    kw[sb * 33 + lane] |= 1ull << p;
+                }
             }
         }
-        const uint32_t slot = dedup_insert_warp(a.table, key, valid, lane, cache);
-        if (valid) {
-            a.key[s] = key;
-            a.slot[s] = slot;
+        __syncwarp();
+        for (uint32_t r = 0; r < 32; r++) {
+            const uint64_t sh = (w0 + r) * 32 + lane;  // shot: word w0 + r, bit lane
+            const bool valid = sh < a.shots;
+            const unsigned long long key = kw[lane * 33 + r];
+            const uint32_t nz = __ballot_sync(kFull, valid && key != 0ull);
+            uint32_t slot = slot0;
+            if (nz) {
+                const uint32_t sl = dedup_insert_warp(a.table, key, valid && key != 0ull, lane, cache);
+                if (key != 0ull) slot = sl;
+            }
+            if (valid) {
+                a.key[sh] = key;
+                a.slot[sh] = slot;
+            }
         }
+        __syncwarp();
     }
 }
 
@@ -178,15 +209,82 @@ struct DedupEvalArgs {
     uint32_t n_keys;
     double *partial;                  // [n_segs][n_keys]
     uint32_t seg_buf_words;           // per-warp shared-memory copy of its segment (0: walk from global)
+    // block form tables (null: records carry tensor dictionary ids): the forms block
+    // `first_block + blk` of kDedupWarps segments uses, as tensor dictionary entries
+    const uint32_t *block_forms;
+    const uint32_t *block_form_begin;
+    uint32_t first_block;
+    uint32_t table_bytes;  // shared memory before the planes: dictionary or form values
 };
+
+// mono_walk for one 32-key word per lane when every form value of the block
+// is precomputed in shared memory (fv[local form * 32 + lane]): a form costs
+// one conflict-free LDS instead of its dictionary entry and selector loads.
+__device__ __forceinline__ void mono_walk_fv(const uint32_t *w, uint32_t nnodes, const uint32_t *fv, BW<1> *stk,
+                                             double (&acc)[32]) {
+    constexpr int NW = 1;
+    uint32_t q = 0;
+    for (uint32_t nn = 0; nn < nnodes; nn++) {
+        const uint32_t h0 = w[q], h1 = w[q + 1], h2 = w[q + 2];
+        const uint32_t depth = (h0 >> 24) & 0x3fu;
+        const bool leaf = (h0 >> 31) != 0;
+        q += 3;
+        double re = 0.0, im = 0.0;
+        if (leaf) {
+            re = __hiloint2double(int(w[q + 1]), int(w[q]));
+            im = __hiloint2double(int(w[q + 3]), int(w[q + 2]));
+            q += 4;
+        }
+        BW<1> z = bw_zero<1>(), j0 = bw_zero<1>(), j1 = bw_zero<1>();
+        if (depth) {
+            const BW<1> *ps = stk + (depth - 1) * 96;
+            z = ps[0];
+            j0 = ps[32];
+            j1 = ps[64];
+        }
+        const uint32_t ns = (h1 & 0xffu) + ((h1 >> 8) & 0xffu) + ((h1 >> 16) & 0xffu) + (h1 >> 24) + (h2 & 0xffu);
+#pragma unroll 4
+        for (uint32_t i = 0; i < ns; i++) {
+            const uint32_t r = w[q + i];
+            BW<1> x;
+            x.w[0] = fv[(r & 0xfffu) * 32];
+            ZXS_OP_ANY(r, x)
+        }
+        q += ns;
+        for (uint32_t g = 0; g < (h0 & 0xffu); g++) {  // two-form records
+            const uint32_t r = w[q], gw = w[q + 1];
+            q += 2;
+            const uint32_t fa = r & 0xfffu, fb = (r >> 16) & 0xfffu;
+            BW<1> a, bb;
+            a.w[0] = fa == kMonoNoForm ? 0u : fv[fa * 32];
+            bb.w[0] = fb == kMonoNoForm ? 0u : fv[fb * 32];
+            const uint32_t zl = gw >> 6;
+            z.w[0] |= ((zl & 1u) ? (~a.w[0] & ~bb.w[0]) : 0u) | ((zl & 2u) ? (~a.w[0] & bb.w[0]) : 0u) |
+                      ((zl & 4u) ? (a.w[0] & ~bb.w[0]) : 0u) | ((zl & 8u) ? (a.w[0] & bb.w[0]) : 0u);
+            j_add<1>(j0, j1, a, gw & 3u);
+            j_add<1>(j0, j1, bb, (gw >> 2) & 3u);
+            j_add<1>(j0, j1, bw_and<1>(a, bb), (gw >> 4) & 3u);
+        }
+        if (!leaf) {
+            BW<1> *nsp = stk + depth * 96;
+            nsp[0] = z;
+            nsp[32] = j0;
+            nsp[64] = j1;
+            continue;
+        }
+        mono_leaf<1>(acc, z, j0, j1, re, im);
+    }
+}
 
 // Items = (key group of 1024, block of kDedupWarps segments); a CTA builds the
 // key group's parameter planes once in shared memory (shared by its warps),
 // every warp walks one segment for all 1024 keys.
 __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const __grid_constant__ DedupEvalArgs h) {
     extern __shared__ __align__(128) uint8_t dsm[];
-    uint4 *sd = reinterpret_cast<uint4 *>(dsm);
-    uint32_t *planes = reinterpret_cast<uint32_t *>(sd + h.n_dict);  // [p][lane]
+    const bool fvm = h.block_forms != nullptr;
+    uint4 *sd = reinterpret_cast<uint4 *>(dsm);  // dictionary (fvm: form values [f][lane])
+    uint32_t *fv = reinterpret_cast<uint32_t *>(dsm);
+    uint32_t *planes = reinterpret_cast<uint32_t *>(dsm + h.table_bytes);  // [p][lane]
     uint32_t *stack_all = planes + h.n_planes * 32;                  // per warp [depth][3][lane]
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     BW<1> *stk = reinterpret_cast<BW<1> *>(stack_all + warp * h.stack_depth * 96) + lane;
@@ -194,7 +292,10 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
     uint32_t have_seg = 0xffffffffu;  // segment currently in segbuf
     const char *pl = reinterpret_cast<const char *>(planes + lane);
 
-    for (uint32_t i = threadIdx.x; i < h.n_dict; i += blockDim.x) sd[i] = __ldg(h.dict + i);
+    if (!fvm) {
+        for (uint32_t i = threadIdx.x; i < h.n_dict; i += blockDim.x) sd[i] = __ldg(h.dict + i);
+    }
+    uint32_t cur_blk = 0xffffffffu;
     const uint32_t n_kg = (h.n_keys + kDedupKeysPerWarp - 1) / kDedupKeysPerWarp;
     const uint32_t n_blk = (h.n_segs + kDedupWarps - 1) / kDedupWarps;
     const uint64_t n_items = uint64_t(n_kg) * n_blk;
@@ -220,6 +321,18 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
             }
             __syncthreads();
             cur_kg = kg;
+            cur_blk = 0xffffffffu;
+        }
+        if (fvm && blk != cur_blk) {
+            // the block's form values for this key group: warp w computes forms w, w + 16, ...
+            const uint32_t f0 = __ldg(h.block_form_begin + h.first_block + blk);
+            const uint32_t nf = __ldg(h.block_form_begin + h.first_block + blk + 1) - f0;
+            __syncthreads();  // every warp is done with the previous block's values
+            for (uint32_t f = warp; f < nf; f += kDedupWarps) {
+                fv[f * 32 + lane] = mono_form<1>(h.dict, __ldg(h.block_forms + f0 + f), pl).w[0];
+            }
+            __syncthreads();
+            cur_blk = blk;
         }
         const uint32_t seg = blk * kDedupWarps + warp;
         if (seg >= h.n_segs) continue;
@@ -241,7 +354,11 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
         double acc[32];
 #pragma unroll
         for (int s = 0; s < 32; s++) acc[s] = 0.0;
-        mono_walk<1, false>(w, sgd.z, sd, pl, stk, acc, nullptr);
+        if (fvm) {
+            mono_walk_fv(w, sgd.z, fv + lane, stk, acc);
+        } else {
+            mono_walk<1, false>(w, sgd.z, sd, pl, stk, acc, nullptr);
+        }
         const uint32_t k0 = kg * kDedupKeysPerWarp + lane * 32;
         double *out = h.partial + uint64_t(seg) * h.n_keys + k0;
 #pragma unroll
@@ -251,21 +368,22 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
     }
 }
 
-// value[k] = ((0 + S_0[k]) + S_1[k]) + ... in segment order.
+// value[slot of key k] = ((0 + S_0[k]) + S_1[k]) + ... in segment order (values
+// are stored by table slot: the autoregressive step looks them up directly).
 __global__ void dedup_reduce_kernel(const double *__restrict__ partial, uint32_t n_segs, uint32_t n_keys,
-                                    double *__restrict__ value) {
+                                    const uint32_t *__restrict__ uslot, double *__restrict__ value) {
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n_keys; k += gridDim.x * blockDim.x) {
         double v = 0.0;
         uint32_t g = 0;
-        for (; g + 16 <= n_segs; g += 16) {  // 16 independent loads in flight, adds in order
-            double x[16];
+        for (; g + 48 <= n_segs; g += 48) {  // 48 independent loads in flight, adds in order
+            double x[48];
 #pragma unroll
-            for (int i = 0; i < 16; i++) x[i] = __ldg(partial + uint64_t(g + i) * n_keys + k);
+            for (int i = 0; i < 48; i++) x[i] = __ldg(partial + uint64_t(g + i) * n_keys + k);
 #pragma unroll
-            for (int i = 0; i < 16; i++) v = __dadd_rn(v, x[i]);
+            for (int i = 0; i < 48; i++) v = __dadd_rn(v, x[i]);
         }
         for (; g < n_segs; g++) v = __dadd_rn(v, __ldg(partial + uint64_t(g) * n_keys + k));
-        value[k] = v;
+        value[uslot[k]] = v;
     }
 }
 
@@ -293,8 +411,8 @@ struct DedupArArgs {
     unsigned long long *key;    // [shots]
     uint32_t *slot;             // [shots] slot in `cur`; replaced by the slot in `next`
     double *prev;               // [shots]
-    const double *value0;       // j == 0: the normalization's values (same keys)
-    const double *value;        // this tensor's values by id
+    const double *value0;       // j == 0: the normalization's values by slot (same table)
+    const double *value;        // this tensor's values by slot of `cur`
     DedupTable cur;
     DedupTable next;            // insertion table for the next tensor (unused when last)
     bool insert_next;
@@ -306,56 +424,85 @@ struct DedupArArgs {
     unsigned long long *err;
 };
 
-// One autoregressive step (sampler.cpp:84-99) for every shot: thread = shot.
+// One autoregressive step (sampler.cpp:84-99) for every shot. A warp takes 64
+// consecutive shots per iteration, lane = shots s and s + 32: both groups'
+// loads, divisions and Philox draws are independent (two chains in flight).
+constexpr int kDedupArGroups = 2;
 __global__ void __launch_bounds__(256) dedup_ar_kernel(const __grid_constant__ DedupArArgs a) {
+    constexpr int G = kDedupArGroups;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t seed_hi = uint32_t(a.seed >> 32);
     const uint32_t k2c = uint32_t(kP1c) ^ a.k0_round[1];
     const uint32_t stream = 0x80000000u ^ (a.ci << 12) ^ a.j;  // sampler.cpp:37-39
-    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    const uint32_t p = a.f_width + a.j;
+    const bool key_bit = p < 63 && ((a.key_mask >> p) & 1ull);  // later tensors read sampled bit j
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * G;
     unsigned long long ones = 0;
     DedupWarpCache cache;
     // up to the 64-shot boundary: the record's last 64-bit word gets zero tail bits
     const uint64_t shots64 = (a.shots + 63) & ~uint64_t(63);
-    for (uint64_t s0 = uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); s0 < shots64; s0 += stride) {
-        const uint64_t s = s0 + lane;
-        const bool valid = s < a.shots;
-        bool bit = false;
-        unsigned long long key = 0;
-        if (valid) {
-            const uint32_t id = a.cur.ids[a.slot[s]];
-            const double cur = a.value[id];
-            const double pv = a.j == 0 ? a.value0[id] : a.prev[s];
-            const double ratio = __ddiv_rn(cur, pv);
-            if (!(ratio > -1e-6 && ratio < 1.0 + 1e-6)) report_ratio_error(a.err, a.first_shot + s);
-            double cl = (0.0 < ratio) ? ratio : 0.0;
-            cl = (cl < 1.0) ? cl : 1.0;
-            double u;
-            if (a.uniforms) {
-                u = a.uniforms[a.upos * a.uniforms_ld + s];
-            } else {
-                const uint64_t shot = a.first_shot + s;
-                PhiloxPre pre[1] = {philox_pre(uint32_t(shot), uint32_t(shot >> 32), a.k0_round[0])};
-                uint32_t rhi[1], rlo[1];
-                philox_tail<1>(pre, seed_hi ^ stream, a.k0_round, k2c, a.k0_round[9], rhi, rlo);
-                u = philox_uniform((uint64_t(rhi[0]) << 32) | rlo[0]);
-            }
-            bit = !(u < cl);
-            a.prev[s] = bit ? __dsub_rn(pv, cur) : cur;
-            key = a.key[s];
-            const uint32_t p = a.f_width + a.j;
-            if (bit && p < 63 && ((a.key_mask >> p) & 1ull)) key |= 1ull << p;
+    for (uint64_t s0 = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * G; s0 < shots64; s0 += stride) {
+        uint64_t s[G];
+        bool valid[G], bit[G];
+        uint32_t sl[G];
+        double cur[G], pv[G];
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            s[g] = s0 + 32 * g + lane;
+            valid[g] = s[g] < a.shots;
+            sl[g] = valid[g] ? a.slot[s[g]] : 0u;
+            if (a.j != 0 && valid[g]) pv[g] = a.prev[s[g]];
         }
-        const uint32_t word = __ballot_sync(kFull, bit);
-        if (lane == 0) {
-            if (a.out32 && (s0 >> 5) < a.out_ld32) a.out32[a.out * a.out_ld32 + (s0 >> 5)] = word;
-            ones += __popc(word);
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            cur[g] = a.value[sl[g]];
+            if (a.j == 0) pv[g] = a.value0[sl[g]];
+        }
+        double u[G];
+        if (a.uniforms) {
+#pragma unroll
+            for (int g = 0; g < G; g++) u[g] = valid[g] ? a.uniforms[a.upos * a.uniforms_ld + s[g]] : 0.0;
+        } else {
+            PhiloxPre pre[G];
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+                const uint64_t shot = a.first_shot + s[g];
+                pre[g] = philox_pre(uint32_t(shot), uint32_t(shot >> 32), a.k0_round[0]);
+            }
+            uint32_t rhi[G], rlo[G];
+            philox_tail<G>(pre, seed_hi ^ stream, a.k0_round, k2c, a.k0_round[9], rhi, rlo);
+#pragma unroll
+            for (int g = 0; g < G; g++) u[g] = philox_uniform((uint64_t(rhi[g]) << 32) | rlo[g]);
+        }
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            bit[g] = false;
+            if (valid[g]) {
+                const double ratio = __ddiv_rn(cur[g], pv[g]);
+                if (!(ratio > -1e-6 && ratio < 1.0 + 1e-6)) report_ratio_error(a.err, a.first_shot + s[g]);
+                double cl = (0.0 < ratio) ? ratio : 0.0;
+                cl = (cl < 1.0) ? cl : 1.0;
+                bit[g] = !(u[g] < cl);
+                a.prev[s[g]] = bit[g] ? __dsub_rn(pv[g], cur[g]) : cur[g];
+            }
+            const uint32_t word = __ballot_sync(kFull, bit[g]);
+            if (lane == 0) {
+                const uint64_t wi = (s0 >> 5) + g;
+                if (a.out32 && wi < a.out_ld32) a.out32[a.out * a.out_ld32 + wi] = word;
+                ones += __popc(word);
+            }
         }
         if (a.insert_next) {
-            const uint32_t ns = dedup_insert_warp(a.next, key, valid, lane, cache);
-            if (valid) {
-                a.key[s] = key;
-                a.slot[s] = ns;
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+                unsigned long long key = valid[g] ? a.key[s[g]] : 0ull;
+                const bool grows = key_bit && bit[g];  // the key gains bit j
+                if (grows) key |= 1ull << p;
+                const uint32_t ns = dedup_insert_warp(a.next, key, valid[g], lane, cache);
+                if (valid[g]) {
+                    if (grows) a.key[s[g]] = key;
+                    a.slot[s[g]] = ns;
+                }
             }
         }
     }

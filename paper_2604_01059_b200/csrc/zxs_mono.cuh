@@ -234,8 +234,16 @@ __device__ __forceinline__ void mono_entry2(const uint4 e0, const uint4 e1, cons
     }
 }
 
+#ifndef ZXS_FORM_NOINLINE
+#define ZXS_FORM_NOINLINE 0
+#endif
 template <int NW>
-__device__ __forceinline__ BW<NW> mono_form(const uint4 *sd, uint32_t f, const char *lb) {
+#if ZXS_FORM_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+BW<NW> mono_form(const uint4 *sd, uint32_t f, const char *lb) {
     uint4 e = sd[f];
     BW<NW> acc = mono_entry<NW>(e, lb);
     while (e.x & 0x80u) {
@@ -256,12 +264,20 @@ __device__ __forceinline__ void j_add(BW<NW> &j0, BW<NW> &j1, const BW<NW> &x, u
     }
 }
 
-// One-form records, forms of four (NW = 1) or two (NW = 2) records formed
+// Groups of four one-form records per pass (NW = 1) cost instruction-cache
+// misses in the term-parallel dedup_eval_kernel (16 warps walking different
+// segments); pairs keep the hot loop small.
+#ifndef ZXS_MONO_QUAD
+#define ZXS_MONO_QUAD 0
+#endif
+constexpr bool kMonoQuad = ZXS_MONO_QUAD != 0;
+
+// One-form records, forms of four (NW = 1, kMonoQuad) or two records formed
 // together (independent shared loads in flight), then applied by kind.
 #define ZXS_MONO_RUN(N, OP)                                                              \
     {                                                                                    \
         uint32_t i_ = 0;                                                                 \
-        if constexpr (NW == 1) {                                                         \
+        if constexpr (NW == 1 && kMonoQuad) {                                            \
             for (; i_ + 4 <= (N); i_ += 4) {                                             \
                 const uint32_t r0_ = w[q + i_], r1_ = w[q + i_ + 1];                     \
                 const uint32_t r2_ = w[q + i_ + 2], r3_ = w[q + i_ + 3];                 \
@@ -312,6 +328,28 @@ __device__ __forceinline__ void j_add(BW<NW> &j0, BW<NW> &j1, const BW<NW> &x, u
 #define ZXS_OP_Z(x) { z = bw_or<NW>(z, x); }
 #define ZXS_OP_ZN(x) { z = bw_or<NW>(z, bw_not<NW>(x)); }
 #define ZXS_OP_ANY(r, x) ZXS_OP_KIND(r, x)
+
+// Leaf epilogue: acc[s] += Re(c' i^J) = {re, -im, -re, im}[J] for the non-zero
+// shots, in term order; the sign is a flip of the high word's sign bit.
+template <int NW>
+__device__ __forceinline__ void mono_leaf(double (&acc)[32 * NW], const BW<NW> &z, const BW<NW> &j0, const BW<NW> &j1,
+                                          double re, double im) {
+    const uint32_t re_lo = uint32_t(__double2loint(re)), re_hi = uint32_t(__double2hiint(re));
+    const uint32_t im_lo = uint32_t(__double2loint(im)), im_hi = uint32_t(__double2hiint(im));
+#pragma unroll
+    for (int i = 0; i < NW; i++) {
+        const uint32_t neg = j0.w[i] ^ j1.w[i];
+#pragma unroll
+        for (int s = 0; s < 32; s++) {
+            const bool odd = (j0.w[i] >> s) & 1u;
+            const uint32_t lo = odd ? im_lo : re_lo;
+            const uint32_t hi = (odd ? im_hi : re_hi) ^ ((neg << (31 - s)) & 0x80000000u);
+            if (!((z.w[i] >> s) & 1u)) {
+                acc[i * 32 + s] = __dadd_rn(acc[i * 32 + s], __hiloint2double(int(hi), int(lo)));
+            }
+        }
+    }
+}
 
 // Walks `nnodes` nodes of a record stream (node layout in zxs_api.cu
 // encode_mono) on top of the per-level (Z, J0, J1) stack `stk`; leaves add
@@ -391,23 +429,7 @@ __device__ __forceinline__ void mono_walk(const uint32_t *w, uint32_t nnodes, co
             ns[64] = j1;
             continue;
         }
-        // epilogue: acc[s] += Re(c' i^J) = {re, -im, -re, im}[J] for the non-zero shots,
-        // in term order; the sign is a flip of the high word's sign bit
-        const uint32_t re_lo = uint32_t(__double2loint(re)), re_hi = uint32_t(__double2hiint(re));
-        const uint32_t im_lo = uint32_t(__double2loint(im)), im_hi = uint32_t(__double2hiint(im));
-#pragma unroll
-        for (int i = 0; i < NW; i++) {
-            const uint32_t neg = j0.w[i] ^ j1.w[i];
-#pragma unroll
-            for (int s = 0; s < 32; s++) {
-                const bool odd = (j0.w[i] >> s) & 1u;
-                const uint32_t lo = odd ? im_lo : re_lo;
-                const uint32_t hi = (odd ? im_hi : re_hi) ^ ((neg << (31 - s)) & 0x80000000u);
-                if (!((z.w[i] >> s) & 1u)) {
-                    acc[i * 32 + s] = __dadd_rn(acc[i * 32 + s], __hiloint2double(int(hi), int(lo)));
-                }
-            }
-        }
+        mono_leaf<NW>(acc, z, j0, j1, re, im);
     }
 }
 

@@ -64,7 +64,15 @@ def mono_layout(arrays, min_factors=0):
     seg_words = buf[o:o + n_sw]
     o += n_sw
     key_mask = [int(buf[o + 2 * i]) | (int(buf[o + 2 * i + 1]) << 32) for i in range(n_km)]
-    return dict(comps=comps, flags=flags, tcb=tcb, chunks=chunks, dict=dict_, tdb=tdb, twidth=twidth,
+    o += 2 * n_km
+    n_tfb, n_bfb, n_bf = (int(x) for x in buf[o:o + 3])
+    o += 3
+    tfb = buf[o:o + n_tfb].astype(np.int64)
+    o += n_tfb
+    bfb = buf[o:o + n_bfb].astype(np.int64)
+    o += n_bfb
+    bforms = buf[o:o + n_bf].astype(np.int64)
+    return dict(tfb=tfb, bfb=bfb, bforms=bforms, comps=comps, flags=flags, tcb=tcb, chunks=chunks, dict=dict_, tdb=tdb, twidth=twidth,
                 tbb=tbb, basis=basis, all_plane=all_plane, words=words, tsb=tsb, segs=segs,
                 seg_words=seg_words, key_mask=key_mask)
 
@@ -173,10 +181,18 @@ def emulate_segments(lay, t, P):
     form = tensor_forms(lay, t, P)
     S = P.shape[0]
     tot = np.zeros(S)
-    for g in range(lay["tsb"][t], lay["tsb"][t + 1]):
+    g0 = lay["tsb"][t]
+    for g in range(g0, lay["tsb"][t + 1]):
         wb, nw, nn = lay["segs"][g, :3]
         acc = np.zeros(S)
-        walk_nodes(lay["seg_words"][wb:wb + nw], nn, form, S, {}, acc, None)
+        fb = int(lay["tfb"][t])
+        if fb != 0xFFFFFFFF:  # block-local form ids -> the tensor dictionary's
+            blk = fb + (g - g0) // 16
+            table = lay["bforms"][lay["bfb"][blk]:lay["bfb"][blk + 1]]
+            f = (lambda x, table=table: form(int(table[x])))
+        else:
+            f = form
+        walk_nodes(lay["seg_words"][wb:wb + nw], nn, f, S, {}, acc, None)
         tot += acc
     return tot
 

@@ -2073,7 +2073,8 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const zxs_dev::DedupTable &t, uint3
                             dim3(zxs_dev::kDedupWarps * 32), args, s->dd_smem, st));
         s->time_end(3, st, t0);
         s->time_begin(4, st, t0);
-        zxs_dev::dedup_reduce_kernel<<<(e.n_keys + 63) / 64, 64, 0, st>>>(partial, ng, e.n_keys, t.uslot + r0, value);
+        zxs_dev::dedup_reduce_kernel<<<std::min((e.n_keys + 7) / 8, uint32_t(s->sm_count) * 8), 256, 0, st>>>(
+            partial, ng, e.n_keys, t.uslot + r0, value);
         CK(cudaGetLastError());
         s->time_end(4, st, t0);
     }

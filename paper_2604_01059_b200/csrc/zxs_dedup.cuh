@@ -360,30 +360,33 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
             mono_walk<1, false>(w, sgd.z, sd, pl, stk, acc, nullptr);
         }
         const uint32_t k0 = kg * kDedupKeysPerWarp + lane * 32;
-        double *out = h.partial + uint64_t(seg) * h.n_keys + k0;
+        double *out = h.partial + uint64_t(k0) * h.n_segs + seg;  // [key][segment]
 #pragma unroll
         for (int s = 0; s < 32; s++) {
-            if (k0 + s < h.n_keys) out[s] = acc[s];
+            if (k0 + s < h.n_keys) out[uint64_t(s) * h.n_segs] = acc[s];
         }
     }
 }
 
 // value[slot of key k] = ((0 + S_0[k]) + S_1[k]) + ... in segment order (values
 // are stored by table slot: the autoregressive step looks them up directly).
+// One warp per key: lanes load 32 consecutive segment sums, the warp adds them
+// in order through shuffles.
 __global__ void dedup_reduce_kernel(const double *__restrict__ partial, uint32_t n_segs, uint32_t n_keys,
                                     const uint32_t *__restrict__ uslot, double *__restrict__ value) {
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n_keys; k += gridDim.x * blockDim.x) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < n_keys; k += warps) {
+        const double *row = partial + uint64_t(k) * n_segs;
         double v = 0.0;
-        uint32_t g = 0;
-        for (; g + 48 <= n_segs; g += 48) {  // 48 independent loads in flight, adds in order
-            double x[48];
-#pragma unroll
-            for (int i = 0; i < 48; i++) x[i] = __ldg(partial + uint64_t(g + i) * n_keys + k);
-#pragma unroll
-            for (int i = 0; i < 48; i++) v = __dadd_rn(v, x[i]);
+        double x = lane < n_segs ? __ldg(row + lane) : 0.0;
+        for (uint32_t g0 = 0; g0 < n_segs; g0 += 32) {
+            const double nx = g0 + 32 + lane < n_segs ? __ldg(row + g0 + 32 + lane) : 0.0;  // next chunk in flight
+            const uint32_t n = min(32u, n_segs - g0);
+            for (uint32_t i = 0; i < n; i++) v = __dadd_rn(v, __shfl_sync(kFull, x, i));
+            x = nx;
         }
-        for (; g < n_segs; g++) v = __dadd_rn(v, __ldg(partial + uint64_t(g) * n_keys + k));
-        value[uslot[k]] = v;
+        if (lane == 0) value[uslot[k]] = v;
     }
 }
 

@@ -179,6 +179,7 @@ struct zxs_sampler {
     const uint32_t *dd_block_forms = nullptr, *dd_block_form_begin = nullptr;
     std::vector<uint32_t> dd_tfb;    // per mono tensor: first block form table (~0: dictionary ids)
     uint32_t dd_table_bytes = 0;
+    bool dd_stage_entries = false;
     char *dd_buf = nullptr;  // keys, slots, prev, values, partials, two tables
     size_t dd_buf_bytes = 0;
     uint64_t dd_cap_shots = 0;
@@ -1833,6 +1834,8 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         s->dd_seg_buf_words = (max_seg + 3) & ~3u;
         if (s->dd_smem + size_t(zxs_dev::kDedupWarps) * s->dd_seg_buf_words * 4 > 227 * 1024) s->dd_seg_buf_words = 0;
         s->dd_smem += size_t(zxs_dev::kDedupWarps) * s->dd_seg_buf_words * 4;
+        s->dd_stage_entries = MH.max_block_forms > 0 && s->dd_smem + size_t(MH.max_block_forms) * 16 <= 227 * 1024;
+        if (s->dd_stage_entries) s->dd_smem += size_t(MH.max_block_forms) * 16;
         s->dedup = s->dd_smem <= 227 * 1024 && s->dd_key_mask.size() == MH.comps.size();
         if (const char *e = std::getenv("ZXS_DEDUP")) s->dedup = s->dedup && std::atoi(e) != 0;
     }
@@ -2059,6 +2062,7 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const zxs_dev::DedupTable &t, uint3
             e.block_forms = s->dd_block_forms;
             e.block_form_begin = s->dd_block_form_begin;
             e.first_block = s->dd_tfb[mt];
+            e.stage_entries = s->dd_stage_entries ? 1u : 0u;
         }
         s->dd_stats[2] += e.n_keys;
         s->dd_stats[3] += (mt < s->dd_tloads.size() ? s->dd_tloads[mt] : 0) * ((e.n_keys + 31) / 32) * 4;

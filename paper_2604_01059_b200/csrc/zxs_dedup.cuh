@@ -215,6 +215,7 @@ struct DedupEvalArgs {
     const uint32_t *block_form_begin;
     uint32_t first_block;
     uint32_t table_bytes;  // shared memory before the planes: dictionary or form values
+    uint32_t stage_entries;  // block tables: stage the forms' first dictionary entries in shared memory
 };
 
 // mono_walk for one 32-key word per lane when every form value of the block
@@ -289,6 +290,7 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     BW<1> *stk = reinterpret_cast<BW<1> *>(stack_all + warp * h.stack_depth * 96) + lane;
     uint32_t *segbuf = stack_all + kDedupWarps * h.stack_depth * 96 + warp * h.seg_buf_words;
+    uint4 *sent = reinterpret_cast<uint4 *>(stack_all + kDedupWarps * h.stack_depth * 96 + kDedupWarps * h.seg_buf_words);
     uint32_t have_seg = 0xffffffffu;  // segment currently in segbuf
     const char *pl = reinterpret_cast<const char *>(planes + lane);
 
@@ -328,8 +330,26 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
             const uint32_t f0 = __ldg(h.block_form_begin + h.first_block + blk);
             const uint32_t nf = __ldg(h.block_form_begin + h.first_block + blk + 1) - f0;
             __syncthreads();  // every warp is done with the previous block's values
-            for (uint32_t f = warp; f < nf; f += kDedupWarps) {
-                fv[f * 32 + lane] = mono_form<1>(h.dict, __ldg(h.block_forms + f0 + f), pl).w[0];
+            if (h.stage_entries) {
+                // first dictionary entry of every form, gathered once (L2 -> shared)
+                for (uint32_t i = threadIdx.x; i < nf; i += blockDim.x) sent[i] = __ldg(h.dict + __ldg(h.block_forms + f0 + i));
+                __syncthreads();
+                for (uint32_t f = warp; f < nf; f += kDedupWarps) {
+                    uint4 e = sent[f];
+                    BW<1> v = mono_entry<1>(e, pl);
+                    if (e.x & 0x80u) {  // continuation entries (forms of more than 15 selectors)
+                        uint32_t gi = __ldg(h.block_forms + f0 + f);
+                        do {
+                            e = __ldg(h.dict + ++gi);
+                            v = bw_xor<1>(v, mono_entry<1>(e, pl));
+                        } while (e.x & 0x80u);
+                    }
+                    fv[f * 32 + lane] = v.w[0];
+                }
+            } else {
+                for (uint32_t f = warp; f < nf; f += kDedupWarps) {
+                    fv[f * 32 + lane] = mono_form<1>(h.dict, __ldg(h.block_forms + f0 + f), pl).w[0];
+                }
             }
             __syncthreads();
             cur_blk = blk;

@@ -180,6 +180,7 @@ struct zxs_sampler {
     std::vector<uint32_t> dd_tfb;    // per mono tensor: first block form table (~0: dictionary ids)
     uint32_t dd_table_bytes = 0;
     bool dd_stage_entries = false;
+    int dd_init_occ = 1, dd_ar_occ = 1;  // resident blocks per SM of the per-shot dedup kernels
     char *dd_buf = nullptr;  // keys, slots, prev, values, partials, two tables
     size_t dd_buf_bytes = 0;
     uint64_t dd_cap_shots = 0;
@@ -1912,6 +1913,11 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
             CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(&zxs_dev::dedup_eval_kernel),
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->dd_smem)));
             CK(cudaMallocHost(&s->dd_pinned, 64));
+            // per-shot kernels: one full wave of resident blocks (grid-stride loops, no tail wave)
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &s->dd_init_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_init_kernel), zxs_dev::kDedupInitWarps * 32, 0));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &s->dd_ar_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_ar_kernel), 256, 0));
         }
     }
 }
@@ -2127,7 +2133,7 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
         void *iargs[] = {&ia};
         const uint64_t iwarps = (a.shots + 1023) / 1024;
         const unsigned igrid = unsigned(std::min<uint64_t>((iwarps + zxs_dev::kDedupInitWarps - 1) / zxs_dev::kDedupInitWarps,
-                                                           uint64_t(s->sm_count) * 8));
+                                                           uint64_t(s->sm_count) * std::max(1, s->dd_init_occ)));
         CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_init_kernel), dim3(igrid),
                             dim3(zxs_dev::kDedupInitWarps * 32), iargs, 0, st));
         s->time_end(4, st, t0);
@@ -2164,7 +2170,8 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
             ra.err = s->dev_err;
             s->time_begin(4, st, t0);
             void *rargs[] = {&ra};
-            const unsigned agrid = unsigned(std::min<uint64_t>((a.shots + 511) / 512, uint64_t(s->sm_count) * 8));
+            const unsigned agrid =
+                unsigned(std::min<uint64_t>((a.shots + 511) / 512, uint64_t(s->sm_count) * std::max(1, s->dd_ar_occ)));
             CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_ar_kernel), dim3(agrid), dim3(256), rargs,
                                 0, st));
             s->time_end(4, st, t0);

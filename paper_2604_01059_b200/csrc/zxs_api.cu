@@ -1119,6 +1119,20 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                         std::map<uint32_t, uint32_t> local;
                         for (uint32_t i = 0; i < lists[k].size(); i++) local.emplace(lists[k][i], i);
                         for_forms(b0, [&](uint32_t f) { return f == zxs_dev::kMonoNoForm ? f : local.at(f); });
+                        // one-form records grouped by kind (ADD, SUB, ADD2, Z, ZN: the header's counts),
+                        // so mono_walk_fv runs one fixed operation per loop
+                        for (uint32_t g = b0; g < std::min(s1, b0 + uint32_t(zxs_dev::kDedupWarps)); g++) {
+                            uint32_t q = sg[g].x;
+                            for (uint32_t nn2 = 0; nn2 < sg[g].z; nn2++) {
+                                const uint32_t h0 = sw[q], h1 = sw[q + 1], h2 = sw[q + 2];
+                                q += 3 + ((h0 >> 31) ? 4 : 0);
+                                const uint32_t ns = (h1 & 0xffu) + ((h1 >> 8) & 0xffu) + ((h1 >> 16) & 0xffu) +
+                                                    (h1 >> 24) + (h2 & 0xffu);
+                                std::stable_sort(sw.begin() + q, sw.begin() + q + ns,
+                                                 [](uint32_t x, uint32_t y) { return (x >> 28) < (y >> 28); });
+                                q += ns + 2 * (h0 & 0xffu);
+                            }
+                        }
                         max_bf = std::max(max_bf, uint32_t(lists[k].size()));
                         bf.insert(bf.end(), lists[k].begin(), lists[k].end());
                         bfb.push_back(uint32_t(bf.size()));

@@ -243,15 +243,29 @@ __device__ __forceinline__ void mono_walk_fv(const uint32_t *w, uint32_t nnodes,
             j0 = ps[32];
             j1 = ps[64];
         }
-        const uint32_t ns = (h1 & 0xffu) + ((h1 >> 8) & 0xffu) + ((h1 >> 16) & 0xffu) + (h1 >> 24) + (h2 & 0xffu);
-#pragma unroll 4
-        for (uint32_t i = 0; i < ns; i++) {
-            const uint32_t r = w[q + i];
-            BW<1> x;
-            x.w[0] = fv[(r & 0xfffu) * 32];
-            ZXS_OP_ANY(r, x)
+        // one-form records grouped by kind (host: encode_mono block tables): one fixed op per loop
+        {
+            uint32_t zz = z.w[0], a0 = j0.w[0], a1 = j1.w[0];
+            const uint32_t n_add = h1 & 0xffu, n_sub = (h1 >> 8) & 0xffu, n_add2 = (h1 >> 16) & 0xffu;
+            const uint32_t n_z = h1 >> 24, n_zn = h2 & 0xffu;
+            uint32_t e = q + n_add;
+            for (; q < e; q++) {  // J += a
+                const uint32_t x = fv[(w[q] & 0xfffu) * 32];
+                a1 ^= a0 & x;
+                a0 ^= x;
+            }
+            for (e += n_sub; q < e; q++) {  // J -= a
+                const uint32_t x = fv[(w[q] & 0xfffu) * 32];
+                a1 ^= ~a0 & x;
+                a0 ^= x;
+            }
+            for (e += n_add2; q < e; q++) a1 ^= fv[(w[q] & 0xfffu) * 32];  // J += 2a
+            for (e += n_z; q < e; q++) zz |= fv[(w[q] & 0xfffu) * 32];     // Z |= a
+            for (e += n_zn; q < e; q++) zz |= ~fv[(w[q] & 0xfffu) * 32];   // Z |= ~a
+            z.w[0] = zz;
+            j0.w[0] = a0;
+            j1.w[0] = a1;
         }
-        q += ns;
         for (uint32_t g = 0; g < (h0 & 0xffu); g++) {  // two-form records
             const uint32_t r = w[q], gw = w[q + 1];
             q += 2;
@@ -374,8 +388,10 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
         double acc[32];
 #pragma unroll
         for (int s = 0; s < 32; s++) acc[s] = 0.0;
-        if (fvm) {
-            mono_walk_fv(w, sgd.z, fv + lane, stk, acc);
+        if (fvm && w == segbuf) {  // record words in shared memory: LDS (a separate instantiation)
+            mono_walk_fv(segbuf, sgd.z, fv + lane, stk, acc);
+        } else if (fvm) {
+            mono_walk_fv(h.words + sgd.x, sgd.z, fv + lane, stk, acc);
         } else {
             mono_walk<1, false>(w, sgd.z, sd, pl, stk, acc, nullptr);
         }

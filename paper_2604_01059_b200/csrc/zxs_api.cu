@@ -181,6 +181,8 @@ struct zxs_sampler {
     uint32_t dd_table_bytes = 0;
     bool dd_stage_entries = false;
     int dd_init_occ = 1, dd_ar_occ = 1;  // resident blocks per SM of the per-shot dedup kernels
+    bool dd_async = true;                 // key counts stay on the device (ZXS_DEDUP_SYNC=1: host round trips)
+    unsigned long long *dd_dev_stats = nullptr;  // {keys, plane-load bytes} accumulated by dedup_eval_kernel
     char *dd_buf = nullptr;  // keys, slots, prev, values, partials, two tables
     size_t dd_buf_bytes = 0;
     uint64_t dd_cap_shots = 0;
@@ -1927,6 +1929,9 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
             CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(&zxs_dev::dedup_eval_kernel),
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->dd_smem)));
             CK(cudaMallocHost(&s->dd_pinned, 64));
+            CK(cudaMalloc(&s->dd_dev_stats, 16));
+            CK(cudaMemset(s->dd_dev_stats, 0, 16));
+            if (const char *e = std::getenv("ZXS_DEDUP_SYNC")) s->dd_async = std::atoi(e) == 0;
             // per-shot kernels: one full wave of resident blocks (grid-stride loops, no tail wave)
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &s->dd_init_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_init_kernel), zxs_dev::kDedupInitWarps * 32, 0));
@@ -1979,6 +1984,8 @@ struct DedupBufs {
     uint32_t *slot;
     double *prev, *value0, *value, *partial;
     unsigned long long *counts;  // per output, added to the caller's counts when the chain completes
+    unsigned int *max_count;     // largest key count of the batch (sync-free path)
+    unsigned long long *err;     // staged ratio-breakdown report of the sync-free path
     zxs_dev::DedupTable table[2];
 };
 
@@ -2003,7 +2010,7 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
     const size_t per_table = al(size_t(slots) * 8) + al(size_t(slots) * 4) + al(4) + al(size_t(max_ids) * 8) +
                              al(size_t(max_ids) * 4);
     const size_t bytes = al(cap * 8) + al(cap * 4) + al(cap * 8) + 2 * al(size_t(slots) * 8) +
-                         al(size_t(max_segs) * kDedupRoundKeys * 8) + al(nout * 8) + 2 * per_table;
+                         al(size_t(max_segs) * kDedupRoundKeys * 8) + al(nout * 8) + al(4) + al(16) + 2 * per_table;
     if (bytes > s->dd_buf_bytes || slots != s->dd_table_slots) {
         if (s->dd_buf) CK(cudaFree(s->dd_buf));
         s->dd_buf = nullptr;
@@ -2023,6 +2030,8 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
     d.value = reinterpret_cast<double *>(take(size_t(slots) * 8));
     d.partial = reinterpret_cast<double *>(take(size_t(max_segs) * kDedupRoundKeys * 8));
     d.counts = reinterpret_cast<unsigned long long *>(take(nout * 8));
+    d.max_count = reinterpret_cast<unsigned int *>(take(4));
+    d.err = reinterpret_cast<unsigned long long *>(take(16));
     for (int i = 0; i < 2; i++) {
         zxs_dev::DedupTable &t = d.table[i];
         t.keys = reinterpret_cast<unsigned long long *>(take(size_t(slots) * 8));
@@ -2052,8 +2061,9 @@ uint32_t dedup_count(zxs_sampler *s, const zxs_dev::DedupTable &t, cudaStream_t 
 }
 
 // Values of mono tensor `mt` for the table's n distinct keys, in id order.
+// n_dev: the key count is read on the device (one round of at most n = kDedupRoundKeys keys).
 void dedup_eval(zxs_sampler *s, uint32_t mt, const zxs_dev::DedupTable &t, uint32_t n, double *value, double *partial,
-                cudaStream_t st) {
+                cudaStream_t st, const uint32_t *n_dev = nullptr) {
     const uint32_t g0 = s->dd_tsb[mt], ng = s->dd_tsb[mt + 1] - g0;
     if (n == 0) return;
     if (ng == 0) {  // every term dead: the value is exactly 0 (for every slot)
@@ -2084,8 +2094,9 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const zxs_dev::DedupTable &t, uint3
             e.first_block = s->dd_tfb[mt];
             e.stage_entries = s->dd_stage_entries ? 1u : 0u;
         }
-        s->dd_stats[2] += e.n_keys;
-        s->dd_stats[3] += (mt < s->dd_tloads.size() ? s->dd_tloads[mt] : 0) * ((e.n_keys + 31) / 32) * 4;
+        e.n_dev = n_dev;
+        e.stats = s->dd_dev_stats;
+        e.tensor_loads = mt < s->dd_tloads.size() ? s->dd_tloads[mt] : 0;
         s->dd_stats[4] += 1;
         const uint64_t items = uint64_t((e.n_keys + zxs_dev::kDedupKeysPerWarp - 1) / zxs_dev::kDedupKeysPerWarp) *
                                ((ng + zxs_dev::kDedupWarps - 1) / zxs_dev::kDedupWarps);
@@ -2098,7 +2109,7 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const zxs_dev::DedupTable &t, uint3
         s->time_end(3, st, t0);
         s->time_begin(4, st, t0);
         zxs_dev::dedup_reduce_kernel<<<std::min((e.n_keys + 7) / 8, uint32_t(s->sm_count) * 8), 256, 0, st>>>(
-            partial, ng, e.n_keys, t.uslot + r0, value);
+            partial, ng, e.n_keys, n_dev, t.uslot + r0, value);
         CK(cudaGetLastError());
         s->time_end(4, st, t0);
     }
@@ -2108,8 +2119,8 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const zxs_dev::DedupTable &t, uint3
 // deduplicated path, after shot_kernel left their f-columns in `fcols`. A
 // chain position with more distinct keys than the tables hold sends the
 // whole batch to mono_kernel instead (same canonical values, so the same bits).
-void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *fcols, uint64_t fcols_ld32,
-                  cudaStream_t st) {
+void launch_dedup_sync(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *fcols, uint64_t fcols_ld32,
+                       cudaStream_t st) {
     if (a.shots == 0) return;
     DedupBufs d = dedup_reserve(s, a.shots);
     const zxs_dev::MonoArgs &m = s->mono;
@@ -2197,6 +2208,115 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
         }
         if (cd.n_out == 0) clear(d.table[0], n);  // no autoregressive step cleared it
     }
+    if (a.counts) {
+        s->time_begin(4, st, t0);
+        zxs_dev::dedup_add_counts_kernel<<<(nout + 255) / 256, 256, 0, st>>>(d.counts, a.counts, nout);
+        CK(cudaGetLastError());
+        s->time_end(4, st, t0);
+    }
+    s->dd_dirty = false;
+}
+
+// The same chain without host round trips: key counts stay on the device (one
+// evaluation round of at most kDedupRoundKeys keys per position), the largest
+// count is checked once at the end; a batch that needed more rounds (or
+// overflowed the tables) is redone on the synchronous path, which overwrites
+// every output it wrote (counts are staged, so nothing is added twice).
+void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *fcols, uint64_t fcols_ld32,
+                  cudaStream_t st) {
+    if (a.shots == 0) return;
+    if (!s->dd_async) return launch_dedup_sync(s, a, fcols, fcols_ld32, st);
+    DedupBufs d = dedup_reserve(s, a.shots);
+    const zxs_dev::MonoArgs &m = s->mono;
+    const uint32_t nout = s->m.num_outputs;
+    const uint32_t limit = std::min(kDedupRoundKeys, d.table[0].max_ids);
+    s->dd_dirty = true;  // until the chain completes
+    CK(cudaMemsetAsync(d.max_count, 0, 4, st));
+    if (a.counts) CK(cudaMemsetAsync(d.counts, 0, size_t(std::max<uint32_t>(nout, 1)) * 8, st));
+    zxs_dev::dedup_err_init_kernel<<<1, 1, 0, st>>>(d.err);
+    CK(cudaGetLastError());
+    cudaEvent_t t0 = nullptr;
+    const unsigned cgrid = unsigned(s->sm_count) * 2;
+    auto clear = [&](const zxs_dev::DedupTable &t) {
+        s->time_begin(4, st, t0);
+        zxs_dev::dedup_clear_dev_kernel<<<cgrid, 256, 0, st>>>(t, d.max_count);
+        CK(cudaGetLastError());
+        s->time_end(4, st, t0);
+        s->time_begin(4, st, t0);
+        zxs_dev::dedup_reset_kernel<<<1, 1, 0, st>>>(t.count);
+        CK(cudaGetLastError());
+        s->time_end(4, st, t0);
+    };
+    s->dd_stats[0] += 1;
+    for (uint32_t hc = 0; hc < m.n_comps; hc++) {
+        const zxs_dev::HeavyComp cd = m.comps[hc];
+        zxs_dev::DedupInitArgs ia{};
+        ia.shots = a.shots;
+        ia.fcols = fcols;
+        ia.fcols_ld32 = fcols_ld32;
+        for (uint32_t p = 0; p < std::min(m.f_width, 63u); p++) {
+            if ((s->dd_key_mask[hc] >> p) & 1ull) ia.cols[ia.n_cols++] = uint8_t(p);
+        }
+        ia.key = d.key;
+        ia.slot = d.slot;
+        ia.table = d.table[0];
+        const uint64_t iwarps = (a.shots + 1023) / 1024;
+        const unsigned igrid = unsigned(std::min<uint64_t>((iwarps + zxs_dev::kDedupInitWarps - 1) / zxs_dev::kDedupInitWarps,
+                                                           uint64_t(s->sm_count) * std::max(1, s->dd_init_occ)));
+        s->time_begin(4, st, t0);
+        void *iargs[] = {&ia};
+        CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_init_kernel), dim3(igrid),
+                            dim3(zxs_dev::kDedupInitWarps * 32), iargs, 0, st));
+        s->time_end(4, st, t0);
+        dedup_eval(s, cd.first_tensor, d.table[0], limit, d.value0, d.partial, st, d.table[0].count);
+        for (uint32_t j = 0; j < cd.n_out; j++) {
+            const zxs_dev::DedupTable &cur = d.table[j & 1], &nxt = d.table[(j + 1) & 1];
+            dedup_eval(s, cd.first_tensor + 1 + j, cur, limit, d.value, d.partial, st, cur.count);
+            zxs_dev::DedupArArgs ra{};
+            ra.seed = a.seed;
+            ra.first_shot = a.first_shot;
+            ra.shots = a.shots;
+            for (int i = 0; i < 10; i++) ra.k0_round[i] = a.k0_round[i];
+            ra.ci = cd.ci;
+            ra.j = j;
+            ra.out = s->comp_outputs[cd.out_begin + j];
+            ra.f_width = m.f_width;
+            ra.key_mask = s->dd_key_mask[hc];
+            ra.key = d.key;
+            ra.slot = d.slot;
+            ra.prev = d.prev;
+            ra.value0 = d.value0;
+            ra.value = d.value;
+            ra.cur = cur;
+            ra.next = nxt;
+            ra.insert_next = j + 1 < cd.n_out;
+            ra.out32 = a.out32;
+            ra.out_ld32 = a.ld32;
+            ra.counts = a.counts ? d.counts : nullptr;
+            ra.uniforms = a.uniforms;
+            ra.uniforms_ld = a.uniforms_ld;
+            ra.upos = cd.upos_base + j;
+            ra.err = d.err;
+            s->time_begin(4, st, t0);
+            void *rargs[] = {&ra};
+            const unsigned agrid =
+                unsigned(std::min<uint64_t>((a.shots + 511) / 512, uint64_t(s->sm_count) * std::max(1, s->dd_ar_occ)));
+            CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_ar_kernel), dim3(agrid), dim3(256), rargs,
+                                0, st));
+            s->time_end(4, st, t0);
+            clear(cur);
+        }
+        if (cd.n_out == 0) clear(d.table[0]);
+    }
+    CK(cudaMemcpyAsync(s->dd_pinned, d.max_count, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (s->dd_pinned[0] > limit) {  // more keys than one round (or the tables) hold: redo synchronously
+        s->dd_dirty = true;
+        s->dd_stats[0] -= 1;
+        return launch_dedup_sync(s, a, fcols, fcols_ld32, st);
+    }
+    zxs_dev::dedup_err_merge_kernel<<<1, 1, 0, st>>>(d.err, s->dev_err);
+    CK(cudaGetLastError());
     if (a.counts) {
         s->time_begin(4, st, t0);
         zxs_dev::dedup_add_counts_kernel<<<(nout + 255) / 256, 256, 0, st>>>(d.counts, a.counts, nout);
@@ -2379,6 +2499,7 @@ void zxs_sampler_destroy(zxs_sampler *s) {
     if (s->mono_scratch) cudaFree(s->mono_scratch);
     if (s->dd_buf) cudaFree(s->dd_buf);
     if (s->dd_pinned) cudaFreeHost(s->dd_pinned);
+    if (s->dd_dev_stats) cudaFree(s->dd_dev_stats);
     for (auto &t : s->timed) {
         cudaEventDestroy(t.second.first);
         cudaEventDestroy(t.second.second);
@@ -2465,9 +2586,20 @@ zxs_status zxs_dedup_stats(zxs_sampler *s, int reset, uint64_t *out) {
     return guarded([&] {
         if (!s || !out) fail(ZXS_INVALID_ARGUMENT, "null argument");
         std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard g(s->device);
+        unsigned long long dev[2] = {0, 0};
+        if (s->dd_dev_stats) {
+            CK(cudaDeviceSynchronize());
+            CK(cudaMemcpy(dev, s->dd_dev_stats, 16, cudaMemcpyDeviceToHost));
+        }
         for (int i = 0; i < 5; i++) out[i] = s->dd_stats[i];
+        out[2] += dev[0];
+        out[3] += dev[1];
         out[5] = s->dedup ? 1 : 0;
-        if (reset) std::memset(s->dd_stats, 0, sizeof(s->dd_stats));
+        if (reset) {
+            std::memset(s->dd_stats, 0, sizeof(s->dd_stats));
+            if (s->dd_dev_stats) CK(cudaMemset(s->dd_dev_stats, 0, 16));
+        }
     });
 }
 

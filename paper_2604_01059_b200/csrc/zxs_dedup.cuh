@@ -210,8 +210,11 @@ struct DedupEvalArgs {
     uint32_t all_plane, n_planes;     // plane indices the dictionary uses: [0, W), ALL, ZERO = ALL + 1
     uint32_t stack_depth;
     const unsigned long long *keys;   // the round's keys
-    uint32_t n_keys;
-    double *partial;                  // [n_segs][n_keys]
+    uint32_t n_keys;                  // keys (n_dev: at most this many, the rest read from n_dev)
+    const uint32_t *n_dev;            // device-side key count (the table's), or null
+    unsigned long long *stats;        // device counters {keys, plane-load bytes} (nullable)
+    unsigned long long tensor_loads;  // plane loads per 32-key word of this tensor
+    double *partial;                  // [keys][n_segs]
     uint32_t seg_buf_words;           // per-warp shared-memory copy of its segment (0: walk from global)
     // block form tables (null: records carry tensor dictionary ids): the forms block
     // `first_block + blk` of kDedupWarps segments uses, as tensor dictionary entries
@@ -316,7 +319,12 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
         for (uint32_t i = threadIdx.x; i < h.n_dict; i += blockDim.x) sd[i] = __ldg(h.dict + i);
     }
     uint32_t cur_blk = 0xffffffffu;
-    const uint32_t n_kg = (h.n_keys + kDedupKeysPerWarp - 1) / kDedupKeysPerWarp;
+    const uint32_t n_keys = h.n_dev ? min(*h.n_dev, h.n_keys) : h.n_keys;
+    if (h.stats && blockIdx.x == 0 && threadIdx.x == 0) {
+        atomicAdd(&h.stats[0], (unsigned long long)n_keys);
+        atomicAdd(&h.stats[1], h.tensor_loads * ((n_keys + 31) / 32) * 4);
+    }
+    const uint32_t n_kg = (n_keys + kDedupKeysPerWarp - 1) / kDedupKeysPerWarp;
     const uint32_t n_blk = (h.n_segs + kDedupWarps - 1) / kDedupWarps;
     const uint64_t n_items = uint64_t(n_kg) * n_blk;
     uint32_t cur_kg = 0xffffffffu;
@@ -327,7 +335,7 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
             // plane b, lane l, bit s = parity(basis_b & key[kg * 1024 + 32 l + s])
             for (uint32_t l = warp; l < 32; l += kDedupWarps) {
                 const uint32_t ki = kg * kDedupKeysPerWarp + l * 32 + lane;
-                const unsigned long long key = ki < h.n_keys ? __ldg(h.keys + ki) : 0ull;
+                const unsigned long long key = ki < n_keys ? __ldg(h.keys + ki) : 0ull;
                 uint32_t all = 0;
                 for (uint32_t b = 0; b < h.width; b++) {
                     const uint32_t v = __ballot_sync(kFull, __popcll(key & __ldg(h.basis + b)) & 1);
@@ -403,7 +411,7 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
         double *out = h.partial + uint64_t(k0) * h.n_segs + seg;  // [key][segment]
 #pragma unroll
         for (int s = 0; s < 32; s++) {
-            if (k0 + s < h.n_keys) out[uint64_t(s) * h.n_segs] = acc[s];
+            if (k0 + s < n_keys) out[uint64_t(s) * h.n_segs] = acc[s];
         }
     }
 }
@@ -412,9 +420,11 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
 // are stored by table slot: the autoregressive step looks them up directly).
 // One warp per key: lanes load 32 consecutive segment sums, the warp adds them
 // in order through shuffles.
-__global__ void dedup_reduce_kernel(const double *__restrict__ partial, uint32_t n_segs, uint32_t n_keys,
-                                    const uint32_t *__restrict__ uslot, double *__restrict__ value) {
+__global__ void dedup_reduce_kernel(const double *__restrict__ partial, uint32_t n_segs, uint32_t max_keys,
+                                    const uint32_t *n_dev, const uint32_t *__restrict__ uslot,
+                                    double *__restrict__ value) {
     const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t n_keys = n_dev ? min(*n_dev, max_keys) : max_keys;
     const uint32_t warps = gridDim.x * (blockDim.x >> 5);
     for (uint32_t k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < n_keys; k += warps) {
         const double *row = partial + uint64_t(k) * n_segs;
@@ -442,6 +452,29 @@ __global__ void dedup_clear_kernel(DedupTable t, uint32_t n) {
         t.keys[t.uslot[i]] = kDedupEmpty;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) *t.count = 0;
+}
+
+// The same with the key count read on the device (no host round trip); the
+// largest count seen goes to *max_count (the host checks it once per batch).
+// The count itself is reset by dedup_reset_kernel after this kernel.
+__global__ void dedup_clear_dev_kernel(DedupTable t, unsigned int *max_count) {
+    const uint32_t n = min(*t.count, t.max_ids);
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(max_count, *t.count);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        t.keys[t.uslot[i]] = kDedupEmpty;
+    }
+}
+__global__ void dedup_reset_kernel(uint32_t *count) { *count = 0; }
+
+// Ratio-breakdown reports of the sync-free chain are staged (a batch that is
+// redone must not report the garbage of its first attempt) and merged into
+// the sampler's error state when the batch is accepted.
+__global__ void dedup_err_init_kernel(unsigned long long *e) {
+    e[0] = 0ull;
+    e[1] = ~0ull;
+}
+__global__ void dedup_err_merge_kernel(const unsigned long long *e, unsigned long long *err) {
+    if (e[0]) report_ratio_error(err, e[1]);
 }
 
 struct DedupArArgs {

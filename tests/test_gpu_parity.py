@@ -400,9 +400,9 @@ def test_kernel_timing_counts_launches():
     sample(cd, 5000, 1)
     t = cd.kernel_times()
     cd.kernel_timing(False)
-    # one chain of 5 outputs (6 tensors): 6 evals; init + 6 folds + 5 AR steps + 5 table clears
+    # one chain of 5 outputs (6 tensors): 6 evals; init + 6 folds + 5 AR steps + 5 table clears + 5 count resets
     assert t["shot_kernel"][1] == 1 and t["mono_kernel"][1] == 0
-    assert t["dedup_eval_kernel"][1] == 6 and t["dedup_aux"][1] == 17
+    assert t["dedup_eval_kernel"][1] == 6 and t["dedup_aux"][1] == 22
 
 
 # ---------------------------------------------------------------- deduplicated path
@@ -477,3 +477,28 @@ def test_dedup_overflow_falls_back_bit_identical():
     assert np.array_equal(got, zx.sample_given_f(b, f, shots, uniforms=u))
     assert np.array_equal(cnt, zx.count_outputs(b, 20000, seed=5))
     assert np.array_equal(small, sample(b, 3000, 2, 11))
+
+
+def test_dedup_sync_and_async_paths_identical():
+    """Device-side key counts (default) and host round trips (ZXS_DEDUP_SYNC=1) give the
+    same records; a batch with more keys than one evaluation round is redone synchronously."""
+    import os
+    name = "surface_d3_xmem_9t"
+    a = _heavy_model(name, min_factors="0", mono="1", dedup="1")
+    os.environ["ZXS_DEDUP_SYNC"] = "1"
+    try:
+        b = _heavy_model(name, min_factors="0", mono="1", dedup="1")
+    finally:
+        del os.environ["ZXS_DEDUP_SYNC"]
+    for shots, seed, first in ((5000, 1, 0), (300000, 2, 77)):
+        assert np.array_equal(sample(a, shots, seed, first), sample(b, shots, seed, first))
+    orc = coracle.OracleModel.load(golden_path(name))
+    rng = np.random.default_rng(47)
+    shots = 40000  # random f: ~40000 distinct keys > one round of 16384
+    f = rng.integers(0, 2**63, size=(orc.f_width, (shots + 63) // 64), dtype=np.uint64)
+    f[:, -1] &= np.uint64((1 << (shots & 63)) - 1)
+    u = rng.random((orc.num_positions, shots))
+    a.dedup_stats(reset=True)
+    got = zx.sample_given_f(a, f, shots, uniforms=u)
+    assert np.array_equal(got, zx.sample_given_f(b, f, shots, uniforms=u))
+    assert np.array_equal(got, orc.sample(shots, 0, fcols=f, uniforms=u))

@@ -180,8 +180,9 @@ struct zxs_sampler {
     std::vector<uint32_t> dd_tfb;    // per mono tensor: first block form table (~0: dictionary ids)
     uint32_t dd_table_bytes = 0;
     bool dd_stage_entries = false;
-    int dd_init_occ = 1, dd_ar_occ = 1;  // resident blocks per SM of the per-shot dedup kernels
+    int dd_init_occ = 1, dd_ar_occ = 1, dd_fused_occ = 1;  // resident blocks per SM of the per-shot dedup kernels
     bool dd_async = true;                 // key counts stay on the device (ZXS_DEDUP_SYNC=1: host round trips)
+    bool dd_fused = true;                 // short chains in one per-shot kernel (ZXS_DEDUP_FUSED=0: step by step)
     unsigned long long *dd_dev_stats = nullptr;  // {keys, plane-load bytes} accumulated by dedup_eval_kernel
     char *dd_buf = nullptr;  // keys, slots, prev, values, partials, two tables
     size_t dd_buf_bytes = 0;
@@ -1932,11 +1933,14 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
             CK(cudaMalloc(&s->dd_dev_stats, 16));
             CK(cudaMemset(s->dd_dev_stats, 0, 16));
             if (const char *e = std::getenv("ZXS_DEDUP_SYNC")) s->dd_async = std::atoi(e) == 0;
+            if (const char *e = std::getenv("ZXS_DEDUP_FUSED")) s->dd_fused = std::atoi(e) != 0;
             // per-shot kernels: one full wave of resident blocks (grid-stride loops, no tail wave)
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &s->dd_init_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_init_kernel), zxs_dev::kDedupInitWarps * 32, 0));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &s->dd_ar_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_ar_kernel), 256, 0));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &s->dd_fused_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_fused_ar_kernel), 256, 0));
         }
     }
 }
@@ -1977,7 +1981,7 @@ void launch_mono(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *f
 }
 
 // ---- deduplicated large-chi path (zxs_dedup.cuh)
-constexpr uint32_t kDedupRoundKeys = 16384;  // keys per eval round (partials: segments x round keys)
+constexpr uint32_t kDedupRoundKeys = 65536;  // keys per eval round (partials: segments x round keys)
 
 struct DedupBufs {
     unsigned long long *key;
@@ -1986,6 +1990,8 @@ struct DedupBufs {
     unsigned long long *counts;  // per output, added to the caller's counts when the chain completes
     unsigned int *max_count;     // largest key count of the batch (sync-free path)
     unsigned long long *err;     // staged ratio-breakdown report of the sync-free path
+    unsigned long long *xkeys;   // expanded keys of one chain position (fused chains)
+    double *fvals[zxs_dev::kDedupMaxFused + 1];  // dense values per chain position (fused chains)
     zxs_dev::DedupTable table[2];
 };
 
@@ -2010,7 +2016,8 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
     const size_t per_table = al(size_t(slots) * 8) + al(size_t(slots) * 4) + al(4) + al(size_t(max_ids) * 8) +
                              al(size_t(max_ids) * 4);
     const size_t bytes = al(cap * 8) + al(cap * 4) + al(cap * 8) + 2 * al(size_t(slots) * 8) +
-                         al(size_t(max_segs) * kDedupRoundKeys * 8) + al(nout * 8) + al(4) + al(16) + 2 * per_table;
+                         al(size_t(max_segs) * kDedupRoundKeys * 8) + al(nout * 8) + al(4) + al(16) + al(size_t(kDedupRoundKeys) * 8) +
+                         (zxs_dev::kDedupMaxFused + 1) * al(size_t(kDedupRoundKeys) * 8) + 2 * per_table;
     if (bytes > s->dd_buf_bytes || slots != s->dd_table_slots) {
         if (s->dd_buf) CK(cudaFree(s->dd_buf));
         s->dd_buf = nullptr;
@@ -2032,6 +2039,8 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
     d.counts = reinterpret_cast<unsigned long long *>(take(nout * 8));
     d.max_count = reinterpret_cast<unsigned int *>(take(4));
     d.err = reinterpret_cast<unsigned long long *>(take(16));
+    d.xkeys = reinterpret_cast<unsigned long long *>(take(size_t(kDedupRoundKeys) * 8));
+    for (uint32_t i = 0; i <= zxs_dev::kDedupMaxFused; i++) d.fvals[i] = reinterpret_cast<double *>(take(size_t(kDedupRoundKeys) * 8));
     for (int i = 0; i < 2; i++) {
         zxs_dev::DedupTable &t = d.table[i];
         t.keys = reinterpret_cast<unsigned long long *>(take(size_t(slots) * 8));
@@ -2062,12 +2071,15 @@ uint32_t dedup_count(zxs_sampler *s, const zxs_dev::DedupTable &t, cudaStream_t 
 
 // Values of mono tensor `mt` for the table's n distinct keys, in id order.
 // n_dev: the key count is read on the device (one round of at most n = kDedupRoundKeys keys).
-void dedup_eval(zxs_sampler *s, uint32_t mt, const zxs_dev::DedupTable &t, uint32_t n, double *value, double *partial,
-                cudaStream_t st, const uint32_t *n_dev = nullptr) {
+// keys/uslot: the keys to contract and where their values go (value[uslot[k]], or value[k] when
+// uslot is null); n_dev/n_mult: n = min(*n_dev x n_mult, n) read on the device.
+void dedup_eval(zxs_sampler *s, uint32_t mt, const unsigned long long *keys, const uint32_t *uslot, uint32_t n,
+                double *value, double *partial, cudaStream_t st, const uint32_t *n_dev = nullptr, uint32_t n_mult = 1,
+                size_t value_slots = 0) {
     const uint32_t g0 = s->dd_tsb[mt], ng = s->dd_tsb[mt + 1] - g0;
     if (n == 0) return;
     if (ng == 0) {  // every term dead: the value is exactly 0 (for every slot)
-        CK(cudaMemsetAsync(value, 0, size_t(t.mask + 1) * 8, st));
+        CK(cudaMemsetAsync(value, 0, value_slots * 8, st));
         return;
     }
     const zxs_dev::MonoArgs &m = s->mono;
@@ -2083,7 +2095,7 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const zxs_dev::DedupTable &t, uint3
         e.all_plane = m.all_plane;
         e.n_planes = m.all_plane + 2;
         e.stack_depth = m.stack_depth;
-        e.keys = t.ukeys + r0;
+        e.keys = keys + r0;
         e.n_keys = std::min(kDedupRoundKeys, n - r0);
         e.partial = partial;
         e.seg_buf_words = s->dd_seg_buf_words;
@@ -2095,6 +2107,7 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const zxs_dev::DedupTable &t, uint3
             e.stage_entries = s->dd_stage_entries ? 1u : 0u;
         }
         e.n_dev = n_dev;
+        e.n_mult = n_mult;
         e.stats = s->dd_dev_stats;
         e.tensor_loads = mt < s->dd_tloads.size() ? s->dd_tloads[mt] : 0;
         s->dd_stats[4] += 1;
@@ -2109,7 +2122,7 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const zxs_dev::DedupTable &t, uint3
         s->time_end(3, st, t0);
         s->time_begin(4, st, t0);
         zxs_dev::dedup_reduce_kernel<<<std::min((e.n_keys + 7) / 8, uint32_t(s->sm_count) * 8), 256, 0, st>>>(
-            partial, ng, e.n_keys, n_dev, t.uslot + r0, value);
+            partial, ng, e.n_keys, n_dev, n_mult, uslot ? uslot + r0 : nullptr, value);
         CK(cudaGetLastError());
         s->time_end(4, st, t0);
     }
@@ -2164,10 +2177,12 @@ void launch_dedup_sync(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint3
         s->time_end(4, st, t0);
         uint32_t n = dedup_count(s, d.table[0], st);
         if (n > d.table[0].max_ids) return fallback();
-        dedup_eval(s, cd.first_tensor, d.table[0], n, d.value0, d.partial, st);
+        dedup_eval(s, cd.first_tensor, d.table[0].ukeys, d.table[0].uslot, n, d.value0, d.partial, st, nullptr, 1,
+                   d.table[0].mask + 1);
         for (uint32_t j = 0; j < cd.n_out; j++) {
             const zxs_dev::DedupTable &cur = d.table[j & 1], &nxt = d.table[(j + 1) & 1];
-            dedup_eval(s, cd.first_tensor + 1 + j, cur, n, d.value, d.partial, st);
+            dedup_eval(s, cd.first_tensor + 1 + j, cur.ukeys, cur.uslot, n, d.value, d.partial, st, nullptr, 1,
+                       cur.mask + 1);
             zxs_dev::DedupArArgs ra{};
             ra.seed = a.seed;
             ra.first_shot = a.first_shot;
@@ -2237,9 +2252,9 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
     CK(cudaGetLastError());
     cudaEvent_t t0 = nullptr;
     const unsigned cgrid = unsigned(s->sm_count) * 2;
-    auto clear = [&](const zxs_dev::DedupTable &t) {
+    auto clear = [&](const zxs_dev::DedupTable &t, uint32_t mult = 1) {
         s->time_begin(4, st, t0);
-        zxs_dev::dedup_clear_dev_kernel<<<cgrid, 256, 0, st>>>(t, d.max_count);
+        zxs_dev::dedup_clear_dev_kernel<<<cgrid, 256, 0, st>>>(t, d.max_count, mult);
         CK(cudaGetLastError());
         s->time_end(4, st, t0);
         s->time_begin(4, st, t0);
@@ -2268,10 +2283,70 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
         CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_init_kernel), dim3(igrid),
                             dim3(zxs_dev::kDedupInitWarps * 32), iargs, 0, st));
         s->time_end(4, st, t0);
-        dedup_eval(s, cd.first_tensor, d.table[0], limit, d.value0, d.partial, st, d.table[0].count);
+        // fused chain: every position's keys = base keys x patterns of the sampled bits it reads
+        uint32_t relevant = 0, nrel = 0;
+        uint64_t relpos = 0;
+        for (uint32_t j = 0; j + 1 < cd.n_out; j++) {
+            const uint32_t p = m.f_width + j;
+            if (p < 63 && ((s->dd_key_mask[hc] >> p) & 1ull)) {
+                relevant |= 1u << j;
+                if (nrel < 8) relpos |= uint64_t(p) << (8 * nrel);
+                nrel++;
+            }
+        }
+        auto nb_of = [&](uint32_t pos) { return pos < 2 ? 0u : uint32_t(__builtin_popcount(relevant & ((1u << (pos - 1)) - 1))); };
+        uint32_t sum_p = 0;
+        for (uint32_t pos = 0; pos <= cd.n_out; pos++) sum_p += 1u << nb_of(pos);
+        if (s->dd_fused && cd.n_out >= 1 && cd.n_out <= zxs_dev::kDedupMaxFused && sum_p <= 16) {
+            for (uint32_t pos = 0; pos <= cd.n_out; pos++) {
+                const uint32_t nb = nb_of(pos);
+                const unsigned long long *keys = d.table[0].ukeys;
+                if (nb) {
+                    s->time_begin(4, st, t0);
+                    zxs_dev::dedup_expand_kernel<<<unsigned(s->sm_count) * 4, 256, 0, st>>>(
+                        d.table[0].ukeys, d.table[0].count, nb, relpos, limit, d.xkeys);
+                    CK(cudaGetLastError());
+                    s->time_end(4, st, t0);
+                    keys = d.xkeys;
+                }
+                dedup_eval(s, cd.first_tensor + pos, keys, nullptr, limit, d.fvals[pos], d.partial, st, d.table[0].count,
+                           1u << nb, limit);
+            }
+            zxs_dev::DedupFusedArgs fa{};
+            fa.seed = a.seed;
+            fa.first_shot = a.first_shot;
+            fa.shots = a.shots;
+            for (int i = 0; i < 10; i++) fa.k0_round[i] = a.k0_round[i];
+            fa.ci = cd.ci;
+            fa.n_out = cd.n_out;
+            for (uint32_t j = 0; j < cd.n_out; j++) fa.out[j] = s->comp_outputs[cd.out_begin + j];
+            fa.relevant = relevant;
+            fa.slot = d.slot;
+            fa.ids = d.table[0].ids;
+            for (uint32_t pos = 0; pos <= cd.n_out; pos++) fa.value[pos] = d.fvals[pos];
+            fa.out32 = a.out32;
+            fa.out_ld32 = a.ld32;
+            fa.counts = a.counts ? d.counts : nullptr;
+            fa.uniforms = a.uniforms;
+            fa.uniforms_ld = a.uniforms_ld;
+            fa.upos_base = cd.upos_base;
+            fa.err = d.err;
+            const unsigned fgrid =
+                unsigned(std::min<uint64_t>((a.shots + 511) / 512, uint64_t(s->sm_count) * std::max(1, s->dd_fused_occ)));
+            s->time_begin(4, st, t0);
+            void *fargs[] = {&fa};
+            CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_fused_ar_kernel), dim3(fgrid), dim3(256),
+                                fargs, 0, st));
+            s->time_end(4, st, t0);
+            clear(d.table[0], 1u << nb_of(cd.n_out));
+            continue;
+        }
+        dedup_eval(s, cd.first_tensor, d.table[0].ukeys, d.table[0].uslot, limit, d.value0, d.partial, st,
+                   d.table[0].count, 1, d.table[0].mask + 1);
         for (uint32_t j = 0; j < cd.n_out; j++) {
             const zxs_dev::DedupTable &cur = d.table[j & 1], &nxt = d.table[(j + 1) & 1];
-            dedup_eval(s, cd.first_tensor + 1 + j, cur, limit, d.value, d.partial, st, cur.count);
+            dedup_eval(s, cd.first_tensor + 1 + j, cur.ukeys, cur.uslot, limit, d.value, d.partial, st, cur.count, 1,
+                       cur.mask + 1);
             zxs_dev::DedupArArgs ra{};
             ra.seed = a.seed;
             ra.first_shot = a.first_shot;

@@ -212,6 +212,7 @@ struct DedupEvalArgs {
     const unsigned long long *keys;   // the round's keys
     uint32_t n_keys;                  // keys (n_dev: at most this many, the rest read from n_dev)
     const uint32_t *n_dev;            // device-side key count (the table's), or null
+    uint32_t n_mult;                  // keys = *n_dev x n_mult (expanded keys: base key x sampled-bit pattern)
     unsigned long long *stats;        // device counters {keys, plane-load bytes} (nullable)
     unsigned long long tensor_loads;  // plane loads per 32-key word of this tensor
     double *partial;                  // [keys][n_segs]
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
         for (uint32_t i = threadIdx.x; i < h.n_dict; i += blockDim.x) sd[i] = __ldg(h.dict + i);
     }
     uint32_t cur_blk = 0xffffffffu;
-    const uint32_t n_keys = h.n_dev ? min(*h.n_dev, h.n_keys) : h.n_keys;
+    const uint32_t n_keys = h.n_dev ? uint32_t(min(uint64_t(*h.n_dev) * max(h.n_mult, 1u), uint64_t(h.n_keys))) : h.n_keys;
     if (h.stats && blockIdx.x == 0 && threadIdx.x == 0) {
         atomicAdd(&h.stats[0], (unsigned long long)n_keys);
         atomicAdd(&h.stats[1], h.tensor_loads * ((n_keys + 31) / 32) * 4);
@@ -421,10 +422,10 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
 // One warp per key: lanes load 32 consecutive segment sums, the warp adds them
 // in order through shuffles.
 __global__ void dedup_reduce_kernel(const double *__restrict__ partial, uint32_t n_segs, uint32_t max_keys,
-                                    const uint32_t *n_dev, const uint32_t *__restrict__ uslot,
+                                    const uint32_t *n_dev, uint32_t n_mult, const uint32_t *__restrict__ uslot,
                                     double *__restrict__ value) {
     const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t n_keys = n_dev ? min(*n_dev, max_keys) : max_keys;
+    const uint32_t n_keys = n_dev ? uint32_t(min(uint64_t(*n_dev) * max(n_mult, 1u), uint64_t(max_keys))) : max_keys;
     const uint32_t warps = gridDim.x * (blockDim.x >> 5);
     for (uint32_t k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < n_keys; k += warps) {
         const double *row = partial + uint64_t(k) * n_segs;
@@ -436,7 +437,7 @@ __global__ void dedup_reduce_kernel(const double *__restrict__ partial, uint32_t
             for (uint32_t i = 0; i < n; i++) v = __dadd_rn(v, __shfl_sync(kFull, x, i));
             x = nx;
         }
-        if (lane == 0) value[uslot[k]] = v;
+        if (lane == 0) value[uslot ? uslot[k] : k] = v;  // by table slot, or dense (expanded keys)
     }
 }
 
@@ -457,9 +458,12 @@ __global__ void dedup_clear_kernel(DedupTable t, uint32_t n) {
 // The same with the key count read on the device (no host round trip); the
 // largest count seen goes to *max_count (the host checks it once per batch).
 // The count itself is reset by dedup_reset_kernel after this kernel.
-__global__ void dedup_clear_dev_kernel(DedupTable t, unsigned int *max_count) {
+__global__ void dedup_clear_dev_kernel(DedupTable t, unsigned int *max_count, uint32_t mult = 1) {
     const uint32_t n = min(*t.count, t.max_ids);
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(max_count, *t.count);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const unsigned long long v = (unsigned long long)(*t.count) * mult;
+        atomicMax(max_count, *t.count > t.max_ids || v > 0xffffffffull ? 0xffffffffu : uint32_t(v));
+    }
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         t.keys[t.uslot[i]] = kDedupEmpty;
     }
@@ -583,6 +587,126 @@ __global__ void __launch_bounds__(256) dedup_ar_kernel(const __grid_constant__ D
         }
     }
     if (a.counts && lane == 0 && ones) atomicAdd(&a.counts[a.out], ones);
+}
+
+// ---- fused chain (short chains): every position's keys are the base keys
+// (f bits) times the patterns of the sampled bits the tensor reads, so all
+// tensors are contracted before any draw and one per-shot kernel runs the
+// whole autoregressive chain with its state in registers.
+constexpr uint32_t kDedupMaxFused = 6;  // outputs per fused chain
+
+// keys_out[id * P + pat] = base key id | pattern bits at their raw parameter positions.
+__global__ void dedup_expand_kernel(const unsigned long long *__restrict__ ukeys0, const uint32_t *n0, uint32_t nbits,
+                                    uint64_t relpos, uint32_t cap, unsigned long long *__restrict__ keys_out) {
+    const uint32_t P = 1u << nbits;
+    const uint32_t n = uint32_t(min(uint64_t(*n0) * P, uint64_t(cap)));
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        unsigned long long key = __ldg(ukeys0 + (k >> nbits));
+        for (uint32_t b = 0; b < nbits; b++) {
+            if ((k >> b) & 1u) key |= 1ull << ((relpos >> (8 * b)) & 0xffu);
+        }
+        keys_out[k] = key;
+    }
+}
+
+struct DedupFusedArgs {
+    uint64_t seed, first_shot, shots;
+    uint32_t k0_round[10];
+    uint32_t ci, n_out;
+    uint32_t out[kDedupMaxFused];
+    uint32_t relevant;           // bit j: a later tensor reads sampled bit j
+    const uint32_t *slot;        // [shots] slot in the base table
+    const uint32_t *ids;         // base table: slot -> id
+    const double *value[kDedupMaxFused + 1];  // tensor pos: [id << nb + pattern]
+    uint32_t *out32;
+    uint64_t out_ld32;
+    unsigned long long *counts;
+    const double *uniforms;
+    uint64_t uniforms_ld, upos_base;
+    unsigned long long *err;
+};
+
+// The whole chain (sampler.cpp:84-99) per shot: lane = shots s, s + 32.
+// (Drawing every position's uniform first and loading both candidates of the
+// next position while deciding this one measured slower: 102 registers.)
+__global__ void __launch_bounds__(256) dedup_fused_ar_kernel(const __grid_constant__ DedupFusedArgs a) {
+    constexpr int G = 2;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t seed_hi = uint32_t(a.seed >> 32);
+    const uint32_t k2c = uint32_t(kP1c) ^ a.k0_round[1];
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * G;
+    unsigned long long ones[kDedupMaxFused] = {};
+    const uint64_t shots64 = (a.shots + 63) & ~uint64_t(63);
+    for (uint64_t s0 = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * G; s0 < shots64; s0 += stride) {
+        uint64_t s[G];
+        bool valid[G];
+        uint32_t id[G], pat[G];
+        double prev[G];
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            s[g] = s0 + 32 * g + lane;
+            valid[g] = s[g] < a.shots;
+            id[g] = valid[g] ? a.ids[a.slot[s[g]]] : 0u;
+            prev[g] = a.value[0][id[g]];
+            pat[g] = 0;
+        }
+        uint32_t nb = 0;
+#pragma unroll 1
+        for (uint32_t j = 0; j < a.n_out; j++) {
+            const uint32_t stream = 0x80000000u ^ (a.ci << 12) ^ j;  // sampler.cpp:37-39
+            double u[G];
+            if (a.uniforms) {
+#pragma unroll
+                for (int g = 0; g < G; g++) u[g] = valid[g] ? a.uniforms[(a.upos_base + j) * a.uniforms_ld + s[g]] : 0.0;
+            } else {
+                PhiloxPre pre[G];
+#pragma unroll
+                for (int g = 0; g < G; g++) {
+                    const uint64_t shot = a.first_shot + s[g];
+                    pre[g] = philox_pre(uint32_t(shot), uint32_t(shot >> 32), a.k0_round[0]);
+                }
+                uint32_t rhi[G], rlo[G];
+                philox_tail<G>(pre, seed_hi ^ stream, a.k0_round, k2c, a.k0_round[9], rhi, rlo);
+#pragma unroll
+                for (int g = 0; g < G; g++) u[g] = philox_uniform((uint64_t(rhi[g]) << 32) | rlo[g]);
+            }
+            const double *vj = a.value[j + 1];
+            bool bit[G];
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+                bit[g] = false;
+                if (valid[g]) {
+                    const double cur = vj[(id[g] << nb) | pat[g]];
+                    const double ratio = __ddiv_rn(cur, prev[g]);
+                    if (!(ratio > -1e-6 && ratio < 1.0 + 1e-6)) report_ratio_error(a.err, a.first_shot + s[g]);
+                    double cl = (0.0 < ratio) ? ratio : 0.0;
+                    cl = (cl < 1.0) ? cl : 1.0;
+                    bit[g] = !(u[g] < cl);
+                    prev[g] = bit[g] ? __dsub_rn(prev[g], cur) : cur;
+                }
+                const uint32_t word = __ballot_sync(kFull, bit[g]);
+                if (lane == 0) {
+                    const uint64_t wi = (s0 >> 5) + g;
+                    if (a.out32 && wi < a.out_ld32) a.out32[a.out[j] * a.out_ld32 + wi] = word;
+#pragma unroll
+                    for (uint32_t q = 0; q < kDedupMaxFused; q++) {
+                        if (q == j) ones[q] += __popc(word);
+                    }
+                }
+            }
+            if ((a.relevant >> j) & 1u) {
+#pragma unroll
+                for (int g = 0; g < G; g++) pat[g] |= uint32_t(bit[g]) << nb;
+                nb++;
+            }
+        }
+    }
+    if (a.counts && lane == 0) {
+#pragma unroll
+        for (uint32_t q = 0; q < kDedupMaxFused; q++) {
+            if (q < a.n_out && ones[q]) atomicAdd(&a.counts[a.out[q]], ones[q]);
+        }
+    }
 }
 
 }  // namespace zxs_dev

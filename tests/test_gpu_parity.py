@@ -502,3 +502,27 @@ def test_dedup_sync_and_async_paths_identical():
     got = zx.sample_given_f(a, f, shots, uniforms=u)
     assert np.array_equal(got, zx.sample_given_f(b, f, shots, uniforms=u))
     assert np.array_equal(got, orc.sample(shots, 0, fcols=f, uniforms=u))
+
+
+@pytest.mark.parametrize("name", ["surface_d3_xmem_rz5", "c4_color_d5_rz3", "steane_inject"])
+def test_dedup_fused_chain_identical(name):
+    """Short chains run fused (every position's keys expanded over the sampled-bit
+    patterns, one per-shot kernel for the whole chain): same records and counts as the
+    step-by-step chain (ZXS_DEDUP_FUSED=0) and as the oracle under injected noise."""
+    import os
+    a = _heavy_model(name, min_factors="0", mono="1", dedup="1")
+    os.environ["ZXS_DEDUP_FUSED"] = "0"
+    try:
+        b = _heavy_model(name, min_factors="0", mono="1", dedup="1")
+    finally:
+        del os.environ["ZXS_DEDUP_FUSED"]
+    for shots, seed, first in ((4097, 1, 12345), (200000, 2, 0)):
+        assert np.array_equal(sample(a, shots, seed, first), sample(b, shots, seed, first))
+    assert np.array_equal(zx.count_outputs(a, 100000, seed=5), zx.count_outputs(b, 100000, seed=5))
+    orc = coracle.OracleModel.load(golden_path(name))
+    rng = np.random.default_rng(53)
+    shots = 6000
+    f = rng.integers(0, 2**63, size=(orc.f_width, (shots + 63) // 64), dtype=np.uint64)
+    f[:, -1] &= np.uint64((1 << (shots & 63)) - 1)
+    u = rng.random((orc.num_positions, shots))
+    assert np.array_equal(zx.sample_given_f(a, f, shots, uniforms=u), orc.sample(shots, 0, fcols=f, uniforms=u))

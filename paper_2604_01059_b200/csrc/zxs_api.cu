@@ -2265,24 +2265,6 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
     s->dd_stats[0] += 1;
     for (uint32_t hc = 0; hc < m.n_comps; hc++) {
         const zxs_dev::HeavyComp cd = m.comps[hc];
-        zxs_dev::DedupInitArgs ia{};
-        ia.shots = a.shots;
-        ia.fcols = fcols;
-        ia.fcols_ld32 = fcols_ld32;
-        for (uint32_t p = 0; p < std::min(m.f_width, 63u); p++) {
-            if ((s->dd_key_mask[hc] >> p) & 1ull) ia.cols[ia.n_cols++] = uint8_t(p);
-        }
-        ia.key = d.key;
-        ia.slot = d.slot;
-        ia.table = d.table[0];
-        const uint64_t iwarps = (a.shots + 1023) / 1024;
-        const unsigned igrid = unsigned(std::min<uint64_t>((iwarps + zxs_dev::kDedupInitWarps - 1) / zxs_dev::kDedupInitWarps,
-                                                           uint64_t(s->sm_count) * std::max(1, s->dd_init_occ)));
-        s->time_begin(4, st, t0);
-        void *iargs[] = {&ia};
-        CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_init_kernel), dim3(igrid),
-                            dim3(zxs_dev::kDedupInitWarps * 32), iargs, 0, st));
-        s->time_end(4, st, t0);
         // fused chain: every position's keys = base keys x patterns of the sampled bits it reads
         uint32_t relevant = 0, nrel = 0;
         uint64_t relpos = 0;
@@ -2297,7 +2279,26 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
         auto nb_of = [&](uint32_t pos) { return pos < 2 ? 0u : uint32_t(__builtin_popcount(relevant & ((1u << (pos - 1)) - 1))); };
         uint32_t sum_p = 0;
         for (uint32_t pos = 0; pos <= cd.n_out; pos++) sum_p += 1u << nb_of(pos);
-        if (s->dd_fused && cd.n_out >= 1 && cd.n_out <= zxs_dev::kDedupMaxFused && sum_p <= 16) {
+        const bool fused = s->dd_fused && cd.n_out >= 1 && cd.n_out <= zxs_dev::kDedupMaxFused && sum_p <= 16;
+        zxs_dev::DedupInitArgs ia{};
+        ia.shots = a.shots;
+        ia.fcols = fcols;
+        ia.fcols_ld32 = fcols_ld32;
+        for (uint32_t p = 0; p < std::min(m.f_width, 63u); p++) {
+            if ((s->dd_key_mask[hc] >> p) & 1ull) ia.cols[ia.n_cols++] = uint8_t(p);
+        }
+        ia.key = fused ? nullptr : d.key;
+        ia.slot = d.slot;
+        ia.table = d.table[0];
+        const uint64_t iwarps = (a.shots + 1023) / 1024;
+        const unsigned igrid = unsigned(std::min<uint64_t>((iwarps + zxs_dev::kDedupInitWarps - 1) / zxs_dev::kDedupInitWarps,
+                                                           uint64_t(s->sm_count) * std::max(1, s->dd_init_occ)));
+        s->time_begin(4, st, t0);
+        void *iargs[] = {&ia};
+        CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_init_kernel), dim3(igrid),
+                            dim3(zxs_dev::kDedupInitWarps * 32), iargs, 0, st));
+        s->time_end(4, st, t0);
+        if (fused) {
             for (uint32_t pos = 0; pos <= cd.n_out; pos++) {
                 const uint32_t nb = nb_of(pos);
                 const unsigned long long *keys = d.table[0].ukeys;

@@ -141,7 +141,7 @@ struct DedupInitArgs {
     uint64_t fcols_ld32;
     uint32_t n_cols;            // f columns the component's tensors read (< 63)
     uint8_t cols[64];
-    unsigned long long *key;  // [shots]
+    unsigned long long *key;  // [shots] (nullable)
     uint32_t *slot;           // [shots]
     DedupTable table;
 };
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kDedupInitWarps * 32) dedup_init_kernel(const 
                 if (key != 0ull) slot = sl;
             }
             if (valid) {
-                a.key[sh] = key;
+                if (a.key) a.key[sh] = key;  // null: the fused chain never extends keys
                 a.slot[sh] = slot;
             }
         }

@@ -481,6 +481,29 @@ __global__ void dedup_err_merge_kernel(const unsigned long long *e, unsigned lon
     if (e[0]) report_ratio_error(err, e[1]);
 }
 
+// One autoregressive decision, exactly the reference's (sampler.cpp:84-99):
+// ratio = cur / prev (IEEE), error outside (-1e-6, 1 + 1e-6), clamp to [0, 1],
+// bit = !(u < ratio). The IEEE quotient only matters when u (or an error
+// bound) lies within the float estimate's error of it: a float quotient with
+// a 4e-7 relative margin (conversion + division error <= 2.4e-7) decides every
+// other case with the same result, the rest take __ddiv_rn.
+__device__ __forceinline__ bool ar_decide(double cur, double prev, double u, unsigned long long *err, uint64_t shot) {
+    const double ac = fabs(cur), ap = fabs(prev);
+    if (ap > 1e-30 && ap < 1e30 && (ac == 0.0 || (ac > 1e-30 && ac < 1e30))) {
+        const float qf = __fdividef(float(cur), float(prev));
+        const double q = double(qf), d = 4e-7 * fabs(q) + 1e-37;
+        if (q - d > -1e-6 && q + d < 1.0 + 1e-6) {  // certainly no ratio error
+            if (u < q - d) return false;            // u < ratio <= 1 (or ratio clamped to 1)
+            if (u > q + d) return true;             // u > max(ratio, 0) >= clamp(ratio)
+        }
+    }
+    const double ratio = __ddiv_rn(cur, prev);
+    if (!(ratio > -1e-6 && ratio < 1.0 + 1e-6)) report_ratio_error(err, shot);
+    double cl = (0.0 < ratio) ? ratio : 0.0;
+    cl = (cl < 1.0) ? cl : 1.0;
+    return !(u < cl);
+}
+
 struct DedupArArgs {
     uint64_t seed, first_shot, shots;
     uint32_t k0_round[10];
@@ -558,11 +581,7 @@ __global__ void __launch_bounds__(256) dedup_ar_kernel(const __grid_constant__ D
         for (int g = 0; g < G; g++) {
             bit[g] = false;
             if (valid[g]) {
-                const double ratio = __ddiv_rn(cur[g], pv[g]);
-                if (!(ratio > -1e-6 && ratio < 1.0 + 1e-6)) report_ratio_error(a.err, a.first_shot + s[g]);
-                double cl = (0.0 < ratio) ? ratio : 0.0;
-                cl = (cl < 1.0) ? cl : 1.0;
-                bit[g] = !(u[g] < cl);
+                bit[g] = ar_decide(cur[g], pv[g], u[g], a.err, a.first_shot + s[g]);
                 a.prev[s[g]] = bit[g] ? __dsub_rn(pv[g], cur[g]) : cur[g];
             }
             const uint32_t word = __ballot_sync(kFull, bit[g]);
@@ -677,11 +696,7 @@ __global__ void __launch_bounds__(256) dedup_fused_ar_kernel(const __grid_consta
                 bit[g] = false;
                 if (valid[g]) {
                     const double cur = vj[(id[g] << nb) | pat[g]];
-                    const double ratio = __ddiv_rn(cur, prev[g]);
-                    if (!(ratio > -1e-6 && ratio < 1.0 + 1e-6)) report_ratio_error(a.err, a.first_shot + s[g]);
-                    double cl = (0.0 < ratio) ? ratio : 0.0;
-                    cl = (cl < 1.0) ? cl : 1.0;
-                    bit[g] = !(u[g] < cl);
+                    bit[g] = ar_decide(cur, prev[g], u[g], a.err, a.first_shot + s[g]);
                     prev[g] = bit[g] ? __dsub_rn(prev[g], cur) : cur;
                 }
                 const uint32_t word = __ballot_sync(kFull, bit[g]);

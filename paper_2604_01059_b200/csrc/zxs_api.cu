@@ -180,7 +180,7 @@ struct zxs_sampler {
     std::vector<uint32_t> dd_tfb;    // per mono tensor: first block form table (~0: dictionary ids)
     uint32_t dd_table_bytes = 0;
     bool dd_stage_entries = false;
-    int dd_init_occ = 1, dd_ar_occ = 1, dd_fused_occ = 1;  // resident blocks per SM of the per-shot dedup kernels
+    int dd_init_occ = 1, dd_ar_occ = 1, dd_fused_occ = 1, dd_raw_occ = 1;  // resident blocks per SM (per-shot dedup kernels)
     bool dd_async = true;                 // key counts stay on the device (ZXS_DEDUP_SYNC=1: host round trips)
     bool dd_fused = true;                 // short chains in one per-shot kernel (ZXS_DEDUP_FUSED=0: step by step)
     unsigned long long *dd_dev_stats = nullptr;  // {keys, plane-load bytes} accumulated by dedup_eval_kernel
@@ -1941,6 +1941,8 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
                 &s->dd_ar_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_ar_kernel), 256, 0));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &s->dd_fused_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_fused_ar_kernel), 256, 0));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &s->dd_raw_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_init_raw_kernel), 256, 0));
         }
     }
 }
@@ -2294,9 +2296,17 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
         const unsigned igrid = unsigned(std::min<uint64_t>((iwarps + zxs_dev::kDedupInitWarps - 1) / zxs_dev::kDedupInitWarps,
                                                            uint64_t(s->sm_count) * std::max(1, s->dd_init_occ)));
         s->time_begin(4, st, t0);
-        void *iargs[] = {&ia};
-        CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_init_kernel), dim3(igrid),
-                            dim3(zxs_dev::kDedupInitWarps * 32), iargs, 0, st));
+        if (a.heavy_fraw) {  // per-shot f words from shot_kernel
+            const unsigned long long fm = s->dd_key_mask[hc] & (m.f_width >= 63 ? (1ull << 63) - 1 : (1ull << m.f_width) - 1);
+            const unsigned rgrid =
+                unsigned(std::min<uint64_t>((a.shots + 255) / 256, uint64_t(s->sm_count) * std::max(1, s->dd_raw_occ)));
+            zxs_dev::dedup_init_raw_kernel<<<rgrid, 256, 0, st>>>(a.heavy_fraw, fm, a.shots, ia.key, d.slot, d.table[0]);
+            CK(cudaGetLastError());
+        } else {
+            void *iargs[] = {&ia};
+            CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_init_kernel), dim3(igrid),
+                                dim3(zxs_dev::kDedupInitWarps * 32), iargs, 0, st));
+        }
         s->time_end(4, st, t0);
         if (fused) {
             for (uint32_t pos = 0; pos <= cd.n_out; pos++) {
@@ -2424,7 +2434,11 @@ void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
     const bool heavy = (s->has_heavy || s->has_mono) && !a.fcols_out && !a.forced;
     if (heavy) {
         a.heavy_ld32 = 2 * ((a.shots + 63) / 64);
-        a.heavy_fcols = s->heavy_fcols_get(std::max<size_t>(16, size_t(s->m.f_width) * a.heavy_ld32 * 4));
+        const size_t fc_bytes = (std::max<size_t>(16, size_t(s->m.f_width) * a.heavy_ld32 * 4) + 255) & ~size_t(255);
+        const bool raw = s->has_mono && s->dedup && s->dd_async && s->fw_template == 1 && !a.fcols_in;
+        char *hb = reinterpret_cast<char *>(s->heavy_fcols_get(fc_bytes + (raw ? size_t(a.shots) * 8 : 0)));
+        a.heavy_fcols = reinterpret_cast<uint32_t *>(hb);
+        a.heavy_fraw = raw ? reinterpret_cast<unsigned long long *>(hb + fc_bytes) : nullptr;
     }
     void *args[] = {&a, s->param_mechs ? static_cast<void *>(s->mech_table.get()) : static_cast<void *>(s->mech_table1.get())};
     cudaEvent_t t0 = nullptr;

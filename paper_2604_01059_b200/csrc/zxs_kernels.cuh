@@ -106,6 +106,7 @@ struct LaunchArgs {
     unsigned long long *err;       // [0] = flag, [1] = first failing shot
     uint32_t *heavy_fcols;         // f-columns for heavy_kernel: [f_width][heavy_ld32] (nullable)
     uint64_t heavy_ld32;
+    unsigned long long *heavy_fraw;  // per shot f word (f_width <= 64) for the deduplicated path's keys (nullable)
     uint32_t debug_ar_components;  // profiling only (ZXS_DEBUG_AR_COMPONENTS): evaluate this many components
     const double *tab;             // tabulated chains (LightProg.tab), clamped ratios / NaN
     // probability mode (outcome_probability_given, sampler.cpp:324-356): the
@@ -405,6 +406,14 @@ __global__ void __maxnreg__(S == 4 ? 128 : ZXS_MAXNREG) shot_kernel(const __grid
 #pragma unroll
                             for (int w = 0; w < FW; w++) f[s][w] ^= mask[w];
                         }
+                    }
+                }
+            }
+            if constexpr (FW == 1) {
+                if (a.heavy_fraw) {  // lane = shot: coalesced 8-byte stores
+#pragma unroll
+                    for (int s = 0; s < S; s++) {
+                        if (local[s] < a.shots) a.heavy_fraw[local[s]] = f[s][0];
                     }
                 }
             }

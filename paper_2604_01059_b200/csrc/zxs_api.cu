@@ -2123,7 +2123,7 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const unsigned long long *keys, con
                             dim3(zxs_dev::kDedupWarps * 32), args, s->dd_smem, st));
         s->time_end(3, st, t0);
         s->time_begin(4, st, t0);
-        zxs_dev::dedup_reduce_kernel<<<std::min((e.n_keys + 7) / 8, uint32_t(s->sm_count) * 8), 256, 0, st>>>(
+        zxs_dev::dedup_reduce_kernel<<<std::min((e.n_keys + 127) / 128, uint32_t(s->sm_count) * 8), 128, 0, st>>>(
             partial, ng, e.n_keys, n_dev, n_mult, uslot ? uslot + r0 : nullptr, value);
         CK(cudaGetLastError());
         s->time_end(4, st, t0);

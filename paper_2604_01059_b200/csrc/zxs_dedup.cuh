@@ -447,26 +447,32 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
 }
 
 // value[slot of key k] = ((0 + S_0[k]) + S_1[k]) + ... in segment order (values
-// are stored by table slot: the autoregressive step looks them up directly).
-// One warp per key: lanes load 32 consecutive segment sums, the warp adds them
-// in order through shuffles.
+// are stored by table slot, or densely for expanded keys). Thread = key: it
+// streams its own row of segment sums (16 B loads, eight in flight) and adds
+// them in order.
 __global__ void dedup_reduce_kernel(const double *__restrict__ partial, uint32_t n_segs, uint32_t max_keys,
                                     const uint32_t *n_dev, uint32_t n_mult, const uint32_t *__restrict__ uslot,
                                     double *__restrict__ value) {
-    const uint32_t lane = threadIdx.x & 31u;
     const uint32_t n_keys = n_dev ? uint32_t(min(uint64_t(*n_dev) * max(n_mult, 1u), uint64_t(max_keys))) : max_keys;
-    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < n_keys; k += warps) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n_keys; k += gridDim.x * blockDim.x) {
         const double *row = partial + uint64_t(k) * n_segs;
         double v = 0.0;
-        double x = lane < n_segs ? __ldg(row + lane) : 0.0;
-        for (uint32_t g0 = 0; g0 < n_segs; g0 += 32) {
-            const double nx = g0 + 32 + lane < n_segs ? __ldg(row + g0 + 32 + lane) : 0.0;  // next chunk in flight
-            const uint32_t n = min(32u, n_segs - g0);
-            for (uint32_t i = 0; i < n; i++) v = __dadd_rn(v, __shfl_sync(kFull, x, i));
-            x = nx;
+        uint32_t g = 0;
+        if (!(n_segs & 1u)) {  // rows are 16-byte aligned
+            const double2 *r2 = reinterpret_cast<const double2 *>(row);
+            for (; g + 16 <= n_segs; g += 16) {
+                double2 x[8];
+#pragma unroll
+                for (int i = 0; i < 8; i++) x[i] = __ldg(r2 + (g >> 1) + i);
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    v = __dadd_rn(v, x[i].x);
+                    v = __dadd_rn(v, x[i].y);
+                }
+            }
         }
-        if (lane == 0) value[uslot ? uslot[k] : k] = v;  // by table slot, or dense (expanded keys)
+        for (; g < n_segs; g++) v = __dadd_rn(v, __ldg(row + g));
+        value[uslot ? uslot[k] : k] = v;
     }
 }
 

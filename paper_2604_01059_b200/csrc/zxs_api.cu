@@ -2343,7 +2343,8 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
             fa.upos_base = cd.upos_base;
             fa.err = d.err;
             const unsigned fgrid =
-                unsigned(std::min<uint64_t>((a.shots + 511) / 512, uint64_t(s->sm_count) * std::max(1, s->dd_fused_occ)));
+                unsigned(std::min<uint64_t>((a.shots + 256 * ZXS_FUSED_G - 1) / (256 * ZXS_FUSED_G),
+                                            uint64_t(s->sm_count) * std::max(1, s->dd_fused_occ)));
             s->time_begin(4, st, t0);
             void *fargs[] = {&fa};
             CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_fused_ar_kernel), dim3(fgrid), dim3(256),

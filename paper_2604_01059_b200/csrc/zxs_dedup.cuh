@@ -683,8 +683,11 @@ struct DedupFusedArgs {
 // The whole chain (sampler.cpp:84-99) per shot: lane = shots s, s + 32.
 // (Drawing every position's uniform first and loading both candidates of the
 // next position while deciding this one measured slower: 102 registers.)
+#ifndef ZXS_FUSED_G
+#define ZXS_FUSED_G 1  // measured: 1 < 2 < 4 shots per lane in time (register pressure)
+#endif
 __global__ void __launch_bounds__(256) dedup_fused_ar_kernel(const __grid_constant__ DedupFusedArgs a) {
-    constexpr int G = 2;
+    constexpr int G = ZXS_FUSED_G;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t seed_hi = uint32_t(a.seed >> 32);
     const uint32_t k2c = uint32_t(kP1c) ^ a.k0_round[1];

@@ -2213,7 +2213,7 @@ void launch_dedup_sync(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint3
             s->time_begin(4, st, t0);
             void *rargs[] = {&ra};
             const unsigned agrid =
-                unsigned(std::min<uint64_t>((a.shots + 511) / 512, uint64_t(s->sm_count) * std::max(1, s->dd_ar_occ)));
+                unsigned(std::min<uint64_t>((a.shots + 256 * zxs_dev::kDedupArGroups - 1) / (256 * zxs_dev::kDedupArGroups), uint64_t(s->sm_count) * std::max(1, s->dd_ar_occ)));
             CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_ar_kernel), dim3(agrid), dim3(256), rargs,
                                 0, st));
             s->time_end(4, st, t0);
@@ -2387,7 +2387,7 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
             s->time_begin(4, st, t0);
             void *rargs[] = {&ra};
             const unsigned agrid =
-                unsigned(std::min<uint64_t>((a.shots + 511) / 512, uint64_t(s->sm_count) * std::max(1, s->dd_ar_occ)));
+                unsigned(std::min<uint64_t>((a.shots + 256 * zxs_dev::kDedupArGroups - 1) / (256 * zxs_dev::kDedupArGroups), uint64_t(s->sm_count) * std::max(1, s->dd_ar_occ)));
             CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_ar_kernel), dim3(agrid), dim3(256), rargs,
                                 0, st));
             s->time_end(4, st, t0);

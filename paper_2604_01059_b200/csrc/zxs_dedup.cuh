@@ -565,7 +565,10 @@ struct DedupArArgs {
 // One autoregressive step (sampler.cpp:84-99) for every shot. A warp takes 64
 // consecutive shots per iteration, lane = shots s and s + 32: both groups'
 // loads, divisions and Philox draws are independent (two chains in flight).
-constexpr int kDedupArGroups = 2;
+#ifndef ZXS_AR_G
+#define ZXS_AR_G 2
+#endif
+constexpr int kDedupArGroups = ZXS_AR_G;
 __global__ void __launch_bounds__(256) dedup_ar_kernel(const __grid_constant__ DedupArArgs a) {
     constexpr int G = kDedupArGroups;
     const uint32_t lane = threadIdx.x & 31u;

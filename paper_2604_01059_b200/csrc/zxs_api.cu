@@ -2770,8 +2770,10 @@ zxs_status zxs_sample(zxs_sampler *s, uint32_t expected_mode, uint64_t seed, uin
             check_ratio_error(s, st);
             return;
         }
-        // chunk: multiple of 64 shots, ~64 MiB of output per buffer
+        // chunk: multiple of 64 shots, ~64 MiB of output per buffer (copies overlap the next chunk);
+        // 2^28 shots at least on the deduplicated path, whose per-batch contraction amortises
         uint64_t chunk_words = std::max<uint64_t>(1, (uint64_t(64) << 20) / (8ull * nout));
+        if (s->has_mono && s->dedup) chunk_words = std::max<uint64_t>(chunk_words, uint64_t(1) << 22);
         chunk_words = std::min(chunk_words, words);
         const size_t buf_bytes = size_t(chunk_words) * nout * 8;
         char *scratch = s->scratch_get(2 * buf_bytes);

@@ -138,6 +138,24 @@ class CompiledSampler:
         _native.check(_native.lib().zxs_kernel_times_n(self._h, ms, n, len(names)))
         return {k: (ms[i], int(n[i])) for i, k in enumerate(names)}
 
+    def mono_chain_positions(self) -> int:
+        """Autoregressive positions of the components on the large-chi integer path (their draws
+        run in the deduplicated / mono kernels, not in shot_kernel): zxs_debug_mono_layout with
+        the sampler's threshold (ZXS_MONO_MIN_FACTORS / ZXS_HEAVY_MIN_FACTORS, default 2000)."""
+        import os
+        if not self.info["num_mono_components"]:
+            return 0
+        mf = int(os.environ.get("ZXS_MONO_MIN_FACTORS", os.environ.get("ZXS_HEAVY_MIN_FACTORS", "2000")))
+        desc = zxs_format.make_desc(self.arrays)
+        need = ctypes.c_uint64()
+        L = _native.lib()
+        _native.check(L.zxs_debug_mono_layout(ctypes.byref(desc), mf, None, 0, ctypes.byref(need)))
+        buf = np.zeros(need.value, np.uint32)
+        _native.check(L.zxs_debug_mono_layout(ctypes.byref(desc), mf, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+                                              buf.size, ctypes.byref(need)))
+        n_comps = int(buf[4])
+        return int(sum(int(buf[8 + 5 * i + 1]) for i in range(n_comps)))
+
     def dedup_stats(self, reset: bool = False) -> dict:
         """Counters of the deduplicated large-chi path (include/zxs_b200.h zxs_dedup_stats)."""
         out = (ctypes.c_uint64 * 6)()

@@ -275,27 +275,39 @@ __device__ __forceinline__ void report_ratio_error(unsigned long long *err, uint
 // Rare path of the mechanism draw: the flip set selected by each of the
 // lane's two draws (first entry, then the rest of a joint table in order).
 // Kept out of line so the divergent scan does not pull the draw loop's
-// counters and Philox keys off the uniform datapath.
+// counters and Philox keys off the uniform datapath. Draws and results travel
+// by value (registers under the ABI) rather than through arrays passed by
+// reference (local memory).
 template <int S>
-__device__ __noinline__ void resolve_flips(const uint64_t (&r)[S], MechRec md, const uint32_t *ext_begin,
-                                           const ulonglong2 *ext, uint32_t mi, uint32_t (&out)[S]) {
+struct DrawsS {
+    uint64_t v[S];
+};
+template <int S>
+struct FlipsS {
+    uint32_t v[S];
+};
+template <int S>
+__device__ __noinline__ FlipsS<S> resolve_flips(const DrawsS<S> r, MechRec md, const uint32_t *ext_begin,
+                                                const ulonglong2 *ext, uint32_t mi) {
+    FlipsS<S> out;
 #pragma unroll
     for (int s = 0; s < S; s++) {
         uint32_t flip = kNoFlip;
-        if (r[s] <= md.lim0) {
+        if (r.v[s] <= md.lim0) {
             flip = md.flip0;
         } else if (md.n_extra) {
             const uint32_t e0 = ext_begin[mi];
             for (uint32_t e = e0; e < e0 + md.n_extra; e++) {
                 const ulonglong2 en = ext[e];
-                if (r[s] <= en.x) {
+                if (r.v[s] <= en.x) {
                     flip = uint32_t(en.y);
                     break;
                 }
             }
         }
-        out[s] = flip;
+        out.v[s] = flip;
     }
+    return out;
 }
 
 // Stores the lane group's S consecutive 32-bit output words of a tile (row
@@ -394,15 +406,14 @@ __global__ void __maxnreg__(S == 4 ? 128 : ZXS_MAXNREG) shot_kernel(const __grid
                 for (int s = 0; s < S; s++) busy |= !(rhi[s] < mf.thr);
                 if (__any_sync(kFull, busy)) {
                     const MechRec md = a.mech_global[mi];
-                    uint64_t rr[S];
+                    DrawsS<S> rr;
 #pragma unroll
-                    for (int s = 0; s < S; s++) rr[s] = (uint64_t(rhi[s] ^ mf.sense) << 32) | rlo[s];
-                    uint32_t flip[S];
-                    resolve_flips<S>(rr, md, a.ext_begin, a.ext, mi, flip);
+                    for (int s = 0; s < S; s++) rr.v[s] = (uint64_t(rhi[s] ^ mf.sense) << 32) | rlo[s];
+                    const FlipsS<S> flip = resolve_flips<S>(rr, md, a.ext_begin, a.ext, mi);
 #pragma unroll
                     for (int s = 0; s < S; s++) {
-                        if (flip[s] != kNoFlip) {
-                            const uint64_t *mask = m.flip_mask + size_t(flip[s]) * FW;
+                        if (flip.v[s] != kNoFlip) {
+                            const uint64_t *mask = m.flip_mask + size_t(flip.v[s]) * FW;
 #pragma unroll
                             for (int w = 0; w < FW; w++) f[s][w] ^= mask[w];
                         }

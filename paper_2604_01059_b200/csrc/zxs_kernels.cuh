@@ -338,7 +338,10 @@ template <int FW, bool PARAM_MECHS, int S>
 #ifndef ZXS_MAXNREG
 #define ZXS_MAXNREG 96
 #endif
-__global__ void __maxnreg__(S == 4 ? 128 : ZXS_MAXNREG) shot_kernel(const __grid_constant__ LaunchArgs a,
+#ifndef ZXS_MAXNREG4
+#define ZXS_MAXNREG4 128  // measured: 128 (80 B of spills) beats 144 / 160 without spills
+#endif
+__global__ void __maxnreg__(S == 4 ? ZXS_MAXNREG4 : ZXS_MAXNREG) shot_kernel(const __grid_constant__ LaunchArgs a,
                                                    const __grid_constant__ MechTable<PARAM_MECHS ? kParamMechs : 1> mt) {
     extern __shared__ __align__(16) uint32_t smem[];
     // One warp per CTA: the tile loop depends only on blockIdx, so the

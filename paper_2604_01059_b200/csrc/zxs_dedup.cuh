@@ -8,20 +8,27 @@
 // 338 distinct f vectors. Per chain position the path therefore
 //   1. hashes each shot's key (its raw parameter bits restricted to the ones
 //      the component's tensors read) into an open-addressing table, giving
-//      the batch's U distinct keys (dedup_init_kernel / dedup_ar_kernel);
+//      the batch's U distinct keys (dedup_init_raw_kernel from the f words
+//      shot_kernel stores, dedup_init_kernel from f columns, dedup_ar_kernel
+//      for keys extended by a sampled bit);
 //   2. contracts the tensor for those U keys only, term-parallel: the
 //      tensor's terms are cut into G fixed summation segments (host,
-//      encode_mono), a warp walks one segment for 1024 keys (mono_walk,
-//      the same record code as mono_kernel) and writes the segment sums
-//      (dedup_eval_kernel);
+//      encode_mono), a warp walks one segment for 1024 keys (mono_walk_fv
+//      over block form tables, or mono_walk -- the record code of
+//      mono_kernel) and writes the segment sums (dedup_eval_kernel);
 //   3. folds the segment sums in order, ((0 + S_0) + S_1) + ... + S_{G-1}
 //      (dedup_reduce_kernel) -- the same canonical order mono_kernel uses
 //      per shot, so both paths give bit-identical values and a shot's value
 //      does not depend on which other shots share its batch;
-//   4. runs the autoregressive draw per shot (sampler.cpp:84-99) with the
-//      value looked up by key, and inserts the extended key (plus the new
-//      bit) for the next tensor (dedup_ar_kernel).
-// Every step is recomputed per batch (nothing is cached across calls).
+//   4. runs the autoregressive draws per shot (sampler.cpp:84-99) with the
+//      values looked up by key: for short chains every position's keys are
+//      expanded over the sampled-bit patterns up front and one kernel runs
+//      the whole chain (dedup_expand_kernel, dedup_fused_ar_kernel);
+//      otherwise one dedup_ar_kernel per position inserts the extended keys
+//      for the next tensor.
+// Key counts stay on the device; the host checks once per batch and redoes
+// a batch that needed more than one evaluation round synchronously. Every
+// step is recomputed per batch (nothing is cached across calls).
 #pragma once
 
 #include "zxs_mono.cuh"

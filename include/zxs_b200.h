@@ -200,15 +200,20 @@ zxs_status zxs_sparse_eligible(const zxs_sampler *s, const zxs_sample_options *o
  * Device-resident variant: dev_columns is device memory [num_outputs][ld_words]
  * uint64 with ld_words >= ceil(shots/64). dev_counts (nullable, device,
  * [num_outputs] uint64) is incremented by the per-output number of set bits.
- * Asynchronous on `stream` (a cudaStream_t; NULL is the legacy default
- * stream). Errors in the autoregressive ratio check are reported by the next
- * zxs_check_errors / synchronous call.
+ * Enqueued on `stream` (a cudaStream_t; NULL is the legacy default stream).
+ * Calls on one sampler are serialised (its per-shot scratch is shared by
+ * every entry point), so concurrent calls on different streams do not
+ * overlap. Large-chi components on the deduplicated path synchronise the
+ * stream once per batch (key counts); everything else returns without
+ * waiting. Shots are processed in batches of at most 2^28. Errors in the
+ * autoregressive ratio check are reported by the next zxs_check_errors /
+ * synchronous call.
  */
 zxs_status zxs_sample_device(zxs_sampler *s, uint64_t seed, uint64_t first_shot,
                              uint64_t shots, uint64_t *dev_columns, uint64_t ld_words,
                              uint64_t *dev_counts, void *stream);
 
-/* Counts only (no bit record): dev_counts[num_outputs] += flips. Asynchronous. */
+/* Counts only (no bit record): dev_counts[num_outputs] += flips. Enqueued like zxs_sample_device. */
 zxs_status zxs_count_device(zxs_sampler *s, uint64_t seed, uint64_t first_shot,
                             uint64_t shots, uint64_t *dev_counts, void *stream);
 /* Host variant of the above: host_counts[num_outputs] is overwritten. Synchronous. */

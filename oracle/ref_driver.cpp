@@ -35,6 +35,10 @@
 #include "zxs_flat.hpp"
 #include "zxsim/circuit.hpp"
 #include "zxsim/compile.hpp"
+#include "zxsim/decompose.hpp"
+#include "zxsim/lowering.hpp"
+#include "zxsim/oracle.hpp"
+#include "zxsim/simplify.hpp"
 #include "zxsim/encode.hpp"
 #include "zxsim/rng.hpp"
 #include "zxsim/sampler.hpp"
@@ -470,6 +474,47 @@ int zr_encode(const uint64_t *cols, uint32_t width, uint64_t shots, int format, 
         if (s.size() > cap) throw std::invalid_argument("encode buffer too small");
         std::memcpy(out, s.data(), s.size());
         *written = s.size();
+    });
+}
+
+// Front-end probe without the tensor build (compile.cpp:126-127, 249):
+// lower -> undouble -> clifford_simplify -> plan_decomposition over the whole
+// reduced diagram. out[0..4] = doubled magic spiders, total terms (chi),
+// surviving vertices, error parameters, channel groups. Seconds where the
+// full compile of a chi ~ 5e4 circuit takes minutes.
+int zr_plan(const char *text, int mode, uint64_t *out) {
+    return guarded([&] {
+        zxsim::Circuit c = zxsim::parse_circuit(text);
+        zxsim::LoweredProgram lp = zxsim::lower(c, mode == 0 ? zxsim::SampleMode::detectors
+                                                             : zxsim::SampleMode::measurements);
+        auto [reduced, trace] = zxsim::clifford_simplify(zxsim::undouble(lp.diagram));
+        zxsim::DecompositionPlan plan = zxsim::plan_decomposition(reduced);
+        out[0] = plan.num_magic;
+        out[1] = plan.total_terms;
+        out[2] = reduced.vertex_count();
+        out[3] = lp.e_param_count;
+        out[4] = lp.channels.size();
+    });
+}
+
+// The reference's exact branching statevector oracle (oracle.cpp:494-542;
+// <= 12 qubits, <= 16 measurements): outcome keys (bit i = output i) and
+// their probabilities.
+int zr_oracle_distribution(const char *text, int mode, uint64_t *keys, double *probs, uint64_t cap,
+                           uint64_t *n) {
+    return guarded([&] {
+        zxsim::Circuit c = zxsim::parse_circuit(text);
+        zxsim::OutcomeDistribution d = zxsim::oracle_distribution(
+            c, mode == 0 ? zxsim::SampleMode::detectors : zxsim::SampleMode::measurements);
+        uint64_t i = 0;
+        for (const auto &[k, p] : d.probs) {
+            if (i < cap) {
+                keys[i] = k;
+                probs[i] = p;
+            }
+            i++;
+        }
+        *n = i;
     });
 }
 

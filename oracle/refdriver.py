@@ -59,6 +59,8 @@ def lib():
         L.zr_uniform_at.restype = ctypes.c_double
         L.zr_encode.argtypes = [_u64p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int,
                                 ctypes.c_char_p, ctypes.c_uint64, _u64p]
+        L.zr_plan.argtypes = [ctypes.c_char_p, ctypes.c_int, _u64p]
+        L.zr_oracle_distribution.argtypes = [ctypes.c_char_p, ctypes.c_int, _u64p, _dp, ctypes.c_uint64, _u64p]
         _lib = L
     return _lib
 
@@ -190,6 +192,24 @@ class RefModel:
         out = ctypes.c_double()
         _check(lib().zr_probability_of(self._h, _ptr(o, _u8p), ctypes.byref(out)))
         return out.value
+
+
+def plan(text: str, mode: int = 0) -> dict:
+    """Front-end probe (lower, simplify, plan_decomposition; no tensors)."""
+    out = np.zeros(5, np.uint64)
+    _check(lib().zr_plan(text.encode(), mode, _ptr(out)))
+    return dict(zip(("num_magic", "chi", "vertices", "e_params", "channels"), (int(x) for x in out)))
+
+
+def oracle_distribution(text: str, mode: int = 0) -> dict:
+    """The reference's exact statevector oracle: {outcome key: probability}."""
+    cap = 1 << 16
+    keys = np.zeros(cap, np.uint64)
+    probs = np.zeros(cap, np.float64)
+    n = ctypes.c_uint64()
+    _check(lib().zr_oracle_distribution(text.encode(), mode, _ptr(keys), _ptr(probs, _dp), cap, ctypes.byref(n)))
+    m = min(n.value, cap)
+    return {int(k): float(p) for k, p in zip(keys[:m], probs[:m])}
 
 
 def uniform_at(seed: int, stream: int, index: int) -> float:

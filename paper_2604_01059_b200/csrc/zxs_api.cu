@@ -2056,6 +2056,7 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
     if (s->dd_dirty) {
         for (int i = 0; i < 2; i++) {
             CK(cudaMemset(d.table[i].keys, 0xff, size_t(slots) * 8));
+            CK(cudaMemset(d.table[i].ids, 0, size_t(slots) * 4));  // ids stay in range (dedup_insert)
             CK(cudaMemset(d.table[i].count, 0, 4));
         }
         CK(cudaDeviceSynchronize());
@@ -2335,6 +2336,7 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
             fa.slot = d.slot;
             fa.ids = d.table[0].ids;
             for (uint32_t pos = 0; pos <= cd.n_out; pos++) fa.value[pos] = d.fvals[pos];
+            fa.value_cap = limit;
             fa.out32 = a.out32;
             fa.out_ld32 = a.ld32;
             fa.counts = a.counts ? d.counts : nullptr;
@@ -2606,11 +2608,30 @@ zxs_status zxs_sampler_get_info(const zxs_sampler *s, zxs_sampler_info *info) {
     });
 }
 
+// Shots per launch_shots batch on the device-buffer and count entry points:
+// per-shot scratch (f columns, f words, dedup keys/slots/marginals) is sized
+// by the batch, so a 1e10-shot sweep runs as 2^28-shot batches (a multiple of
+// 64: every batch starts on a record word).
+constexpr uint64_t kMaxBatchShots = uint64_t(1) << 28;
+
+void launch_shots_chunked(zxs_sampler *s, const zxs_dev::LaunchArgs &tmpl, cudaStream_t st) {
+    for (uint64_t done = 0; done < tmpl.shots; done += kMaxBatchShots) {
+        zxs_dev::LaunchArgs a = tmpl;
+        a.first_shot = tmpl.first_shot + done;
+        a.shots = std::min(kMaxBatchShots, tmpl.shots - done);
+        if (a.out32) a.out32 = tmpl.out32 + done / 32;  // done is a multiple of 64
+        launch_shots(s, a, st);
+        CK(cudaGetLastError());
+    }
+}
+
 zxs_status zxs_sample_device(zxs_sampler *s, uint64_t seed, uint64_t first_shot, uint64_t shots,
                              uint64_t *dev_columns, uint64_t ld_words, uint64_t *dev_counts, void *stream) {
     return guarded([&] {
         if (!s) fail(ZXS_INVALID_ARGUMENT, "null sampler");
         if (dev_columns && ld_words < (shots + 63) / 64) fail(ZXS_INVALID_ARGUMENT, "ld_words < ceil(shots/64)");
+        // the sampler's per-shot scratch is shared by every entry point: calls are serialised
+        std::lock_guard<std::mutex> lk(s->mu);
         DeviceGuard g(s->device);
         cudaStream_t st = device_stream(stream);
         if (dev_columns && !s->all_outputs_covered) {
@@ -2623,8 +2644,7 @@ zxs_status zxs_sample_device(zxs_sampler *s, uint64_t seed, uint64_t first_shot,
         a.out32 = reinterpret_cast<uint32_t *>(dev_columns);
         a.ld32 = 2 * ld_words;
         a.counts = reinterpret_cast<unsigned long long *>(dev_counts);
-        launch_shots(s, a, st);
-        CK(cudaGetLastError());
+        launch_shots_chunked(s, a, st);
     });
 }
 
@@ -2744,8 +2764,7 @@ zxs_status zxs_count(zxs_sampler *s, uint64_t seed, uint64_t first_shot, uint64_
         a.first_shot = first_shot;
         a.shots = shots;
         a.counts = dc;
-        launch_shots(s, a, st);
-        CK(cudaGetLastError());
+        launch_shots_chunked(s, a, st);
         CK(cudaMemcpyAsync(host_counts, dc, bytes, cudaMemcpyDeviceToHost, st));
         check_ratio_error(s, st);
     });
@@ -2771,9 +2790,12 @@ zxs_status zxs_sample(zxs_sampler *s, uint32_t expected_mode, uint64_t seed, uin
             return;
         }
         // chunk: multiple of 64 shots, ~64 MiB of output per buffer (copies overlap the next chunk);
-        // 2^28 shots at least on the deduplicated path, whose per-batch contraction amortises
+        // on the deduplicated path, whose per-batch contraction amortises, up to 2^28 shots while
+        // a buffer stays within 512 MiB
         uint64_t chunk_words = std::max<uint64_t>(1, (uint64_t(64) << 20) / (8ull * nout));
-        if (s->has_mono && s->dedup) chunk_words = std::max<uint64_t>(chunk_words, uint64_t(1) << 22);
+        if (s->has_mono && s->dedup) {
+            chunk_words = std::max<uint64_t>(chunk_words, std::min<uint64_t>(kMaxBatchShots / 64, (uint64_t(512) << 20) / (8ull * nout)));
+        }
         chunk_words = std::min(chunk_words, words);
         const size_t buf_bytes = size_t(chunk_words) * nout * 8;
         char *scratch = s->scratch_get(2 * buf_bytes);

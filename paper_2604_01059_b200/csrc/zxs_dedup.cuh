@@ -68,7 +68,7 @@ __device__ __forceinline__ uint32_t dedup_insert(const DedupTable &t, unsigned l
     for (uint32_t probe = 0;; probe++) {
         if (probe == kDedupMaxProbes) {  // congested (more keys than the table is sized for): fall back
             atomicMax(t.count, t.max_ids + 1);
-            return 0;
+            return 0;  // any in-range slot: ids[] always holds an in-range id (dedup_reserve)
         }
         const unsigned long long k = *reinterpret_cast<volatile unsigned long long *>(&t.keys[slot]);
         if (k == key) return slot;
@@ -80,6 +80,8 @@ __device__ __forceinline__ uint32_t dedup_insert(const DedupTable &t, unsigned l
                     t.ids[slot] = id;
                     t.ukeys[id] = key;
                     t.uslot[id] = slot;
+                } else {
+                    t.ids[slot] = 0;  // overflowed key: an in-range id until the host redoes the batch
                 }
                 return slot;
             }
@@ -682,6 +684,7 @@ struct DedupFusedArgs {
     const uint32_t *slot;        // [shots] slot in the base table
     const uint32_t *ids;         // base table: slot -> id
     const double *value[kDedupMaxFused + 1];  // tensor pos: [id << nb + pattern]
+    uint32_t value_cap;                       // entries per value array
     uint32_t *out32;
     uint64_t out_ld32;
     unsigned long long *counts;
@@ -714,7 +717,7 @@ __global__ void __launch_bounds__(256) dedup_fused_ar_kernel(const __grid_consta
             s[g] = s0 + 32 * g + lane;
             valid[g] = s[g] < a.shots;
             id[g] = valid[g] ? a.ids[a.slot[s[g]]] : 0u;
-            prev[g] = a.value[0][id[g]];
+            prev[g] = a.value[0][min(id[g], a.value_cap - 1)];
             pat[g] = 0;
         }
         uint32_t nb = 0;
@@ -743,7 +746,9 @@ __global__ void __launch_bounds__(256) dedup_fused_ar_kernel(const __grid_consta
             for (int g = 0; g < G; g++) {
                 bit[g] = false;
                 if (valid[g]) {
-                    const double cur = vj[(id[g] << nb) | pat[g]];
+                    // clamped: after a table overflow (the host redoes the batch) ids can exceed the
+                    // values the round computed; the garbage pass must stay in bounds
+                    const double cur = vj[min((id[g] << nb) | pat[g], a.value_cap - 1)];
                     bit[g] = ar_decide(cur, prev[g], u[g], a.err, a.first_shot + s[g]);
                     prev[g] = bit[g] ? __dsub_rn(prev[g], cur) : cur;
                 }

@@ -17,13 +17,15 @@ def exact(cur, prev, u):
     return (not (u < cl)), err
 
 
-def shortcut(cur, prev, u):
+def shortcut(cur, prev, u, skew=0):
+    """The device rule with its float quotient moved `skew` float ulps off the
+    correctly rounded one (__fdividef is within 2 ulps)."""
     ac, ap = abs(cur), abs(prev)
     if 1e-30 < ap < 1e30 and (ac == 0.0 or 1e-30 < ac < 1e30):
         with np.errstate(all="ignore"):
             qf = np.float32(cur) / np.float32(prev)
-            # widen by 2 float ulps: the device's __fdividef may be 2 ulps off the rounded quotient
-            qf = np.nextafter(qf, np.float32(np.inf)) if np.random.rand() < 0.5 else np.nextafter(qf, np.float32(-np.inf))
+            for _ in range(abs(skew)):
+                qf = np.nextafter(qf, np.float32(np.inf if skew > 0 else -np.inf))
         q = float(qf)
         d = 4e-7 * abs(q) + 1e-37
         if q - d > -1e-6 and q + d < 1.0 + 1e-6:
@@ -57,6 +59,8 @@ def test_shortcut_matches_exact_rule():
         for u in us:
             u = min(max(float(u), 0.0), np.nextafter(1.0, 0.0))
             u = np.floor(u * 2.0 ** 53) / 2.0 ** 53  # uniform_at values are multiples of 2^-53
-            assert shortcut(cur, prev, u) == exact(cur, prev, u), (cur, prev, u)
+            want = exact(cur, prev, u)
+            for skew in (-2, -1, 0, 1, 2):
+                assert shortcut(cur, prev, u, skew) == want, (cur, prev, u, skew)
             n += 1
     assert n > 100000

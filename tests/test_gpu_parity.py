@@ -526,3 +526,27 @@ def test_dedup_fused_chain_identical(name):
     f[:, -1] &= np.uint64((1 << (shots & 63)) - 1)
     u = rng.random((orc.num_positions, shots))
     assert np.array_equal(zx.sample_given_f(a, f, shots, uniforms=u), orc.sample(shots, 0, fcols=f, uniforms=u))
+
+
+@pytest.mark.parametrize("name", ["c4_color_d5_rz3", "steane_inject"])
+def test_dedup_fused_chain_overflow(name):
+    """A fused chain whose batch has more distinct keys than the tables hold
+    (ZXS_DEDUP_MAX_KEYS=64): the garbage pass before the host's redo stays in
+    bounds (no sticky fault) and the records equal the per-shot path's."""
+    import os
+    os.environ["ZXS_DEDUP_MAX_KEYS"] = "64"
+    try:
+        a = _heavy_model(name, min_factors="0", mono="1", dedup="1")
+        orc = coracle.OracleModel.load(golden_path(name))
+        rng = np.random.default_rng(59)
+        shots = 20000
+        f = rng.integers(0, 2**63, size=(orc.f_width, (shots + 63) // 64), dtype=np.uint64)
+        f[:, -1] &= np.uint64((1 << (shots & 63)) - 1)
+        u = rng.random((orc.num_positions, shots))
+        got = zx.sample_given_f(a, f, shots, uniforms=u)
+        rec = sample(a, 50000, 3, 7)
+    finally:
+        del os.environ["ZXS_DEDUP_MAX_KEYS"]
+    assert np.array_equal(got, orc.sample(shots, 0, fcols=f, uniforms=u))
+    b = _heavy_model(name, min_factors="0", mono="1", dedup="0")
+    assert np.array_equal(rec, sample(b, 50000, 3, 7))

@@ -193,6 +193,13 @@ zxs_status zxs_sample(zxs_sampler *s, uint32_t expected_mode, uint64_t seed,
 zxs_status zxs_sample_opts(zxs_sampler *s, uint32_t expected_mode, uint64_t seed, uint64_t shots,
                            const zxs_sample_options *opts, uint64_t *host_columns, void *stream);
 
+/* Near-tie draws since the last reset: autoregressive draws of the integer
+ * (monomial / deduplicated) paths whose uniform fell within 1e-9 (relative)
+ * of the ratio -- the only draws whose bit could differ from the reference's
+ * (those paths reproduce the reference's values up to its own rounding of the
+ * h tables). The exact paths never count. reset != 0 clears the count. */
+zxs_status zxs_tie_count(zxs_sampler *s, int reset, uint64_t *out);
+
 /* 1 if zxs_sample_opts would take the sparse geometric path (sparse_eligible). */
 zxs_status zxs_sparse_eligible(const zxs_sampler *s, const zxs_sample_options *opts, int *eligible);
 

@@ -15,6 +15,11 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_ref", "libzxsim_ref.so")
+# The same library with the front-end's cat5 normalisation fixed (oracle/Makefile
+# `fixed`): only ever used to COMPILE a circuit to a .zxs file, which the
+# unmodified library then loads, samples and evaluates.
+FIXED_LIB_PATH = os.path.join(_HERE, "_ref", "libzxsim_fixed.so")
+_fixed_lib = None
 
 _u64p = ctypes.POINTER(ctypes.c_uint64)
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -95,6 +100,15 @@ class RefModel:
         h = ctypes.c_void_p()
         _check(lib().zr_compile(text.encode(), mode, ctypes.byref(h)))
         return cls(h)
+
+    @classmethod
+    def compile_fixed(cls, text: str, mode: int = 0) -> "RefModel":
+        """Compiled by the front-end with the cat5 fix (decompose.cpp:106), then
+        handed to the unmodified library through the lossless .zxs round trip."""
+        import tempfile
+        with tempfile.NamedTemporaryFile(suffix=".zxs") as tmp:
+            compile_fixed_to(text, mode, tmp.name)
+            return cls.load(tmp.name)
 
     @classmethod
     def load(cls, path: str) -> "RefModel":
@@ -192,6 +206,34 @@ class RefModel:
         out = ctypes.c_double()
         _check(lib().zr_probability_of(self._h, _ptr(o, _u8p), ctypes.byref(out)))
         return out.value
+
+
+def fixed_available() -> bool:
+    return os.path.exists(FIXED_LIB_PATH)
+
+
+def compile_fixed_to(text: str, mode: int, path: str) -> None:
+    """Compile with the fixed front-end and write the .zxs model to `path`."""
+    global _fixed_lib
+    if _fixed_lib is None:
+        if not fixed_available():
+            raise RuntimeError(f"fixed front-end not built: {FIXED_LIB_PATH} (run `make -C oracle fixed`)")
+        L = ctypes.CDLL(FIXED_LIB_PATH)
+        vp = ctypes.c_void_p
+        L.zr_last_error.restype = ctypes.c_char_p
+        L.zr_compile.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(vp)]
+        L.zr_save.argtypes = [vp, ctypes.c_char_p]
+        L.zr_free.argtypes = [vp]
+        L.zr_free.restype = None
+        _fixed_lib = L
+    h = ctypes.c_void_p()
+    if _fixed_lib.zr_compile(text.encode(), mode, ctypes.byref(h)) != 0:
+        raise RuntimeError(_fixed_lib.zr_last_error().decode())
+    try:
+        if _fixed_lib.zr_save(h, os.fsencode(path)) != 0:
+            raise RuntimeError(_fixed_lib.zr_last_error().decode())
+    finally:
+        _fixed_lib.zr_free(h)
 
 
 def plan(text: str, mode: int = 0) -> dict:

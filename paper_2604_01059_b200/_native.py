@@ -65,6 +65,7 @@ SIGNATURES = (
     ("zxs_kernel_times", ctypes.c_int, [_vp, _dp, _u64p]),
     ("zxs_kernel_times_n", ctypes.c_int, [_vp, _dp, _u64p, ctypes.c_uint32]),
     ("zxs_dedup_stats", ctypes.c_int, [_vp, ctypes.c_int, _u64p]),
+    ("zxs_tie_count", ctypes.c_int, [_vp, ctypes.c_int, _u64p]),
     ("zxs_encoded_bytes", ctypes.c_uint64, [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
                                             ctypes.c_uint32]),
     ("zxs_encode_shots_device", ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,

@@ -141,7 +141,7 @@ struct zxs_sampler {
     const uint32_t *ext_begin = nullptr;
     const ulonglong2 *ext = nullptr;
     uint32_t dead_mechanisms = 0;
-    unsigned long long *dev_err = nullptr;  // [2]
+    unsigned long long *dev_err = nullptr;  // [3]: ratio breakdown flag, first shot, near-tie draws
     cudaStream_t stream = nullptr, copy_stream = nullptr;
     cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
     char *scratch = nullptr;
@@ -173,7 +173,9 @@ struct zxs_sampler {
     const uint32_t *dd_words = nullptr;  // segment streams (device)
     const uint4 *dd_segs = nullptr;
     std::vector<uint32_t> dd_tsb, dd_tdb, dd_tw, dd_tbb;  // host copies per mono tensor
-    std::vector<unsigned long long> dd_key_mask;          // per mono component
+    std::vector<unsigned long long> dd_key_mask;          // per mono component (local parameters)
+    std::vector<uint16_t> dd_param_map;                   // MonoHost::param_map
+    bool dd_identity_map = true;                          // every mono component's local params = raw
     size_t dd_smem = 0;
     uint32_t dd_seg_buf_words = 0;  // per-warp segment copy in dedup_eval_kernel (0: from global)
     const uint32_t *dd_block_forms = nullptr, *dd_block_form_begin = nullptr;
@@ -492,7 +494,11 @@ struct MonoHost {
     std::vector<uint32_t> seg_words;
     std::vector<uint4> segs;                   // {word_begin, n_words, n_nodes, 0}
     std::vector<uint32_t> tensor_seg_begin{0};
-    std::vector<unsigned long long> comp_key_mask;  // per mono component: raw params any tensor reads
+    std::vector<unsigned long long> comp_key_mask;  // per mono component: local params any tensor reads
+    // component-local parameters: local p < nf -> raw f column param_map[pmap_begin + p];
+    // local nf + j -> sampled bit j (param_map holds f_width + j). Identity when
+    // f_width + chain <= 63, else the f columns the component's tensors read.
+    std::vector<uint16_t> param_map;
     std::vector<uint64_t> tensor_loads;             // per mono tensor: plane loads per 32-shot word
     // block form tables (dedup_eval_kernel): per block of kDedupWarps segments the
     // tensor dictionary entries its records use; segment streams carry block-local ids
@@ -626,11 +632,41 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
     // that basis -- the device forms the W basis planes once per tensor and
     // tile -- and, when longer than W/2, as its complement plus the ALL plane
     // (XOR of the W basis planes).
-    std::map<uint64_t, uint32_t> form_id;  // raw mask -> form id (per tensor)
+    // Component-local parameter spaces (the 64-bit form masks and dedup keys
+    // index parameters): a component whose raw width f_width + chain exceeds 63
+    // reads its tensors through the f columns they actually use, in column order.
+    std::vector<std::vector<uint32_t>> comp_local(d->num_components);  // local f param -> raw f column
+    uint32_t lf_max = 0;
+    for (uint32_t c = 0; c < d->num_components; c++) {
+        const uint32_t n = d->comp_out_begin[c + 1] - d->comp_out_begin[c];
+        std::vector<uint32_t> &loc = comp_local[c];
+        if (fwid + n <= 63) {
+            for (uint32_t p = 0; p < fwid; p++) loc.push_back(p);
+        } else {
+            std::vector<uint8_t> used(fwid, 0);
+            const uint32_t t0 = d->comp_tensor_begin[c], t1 = d->comp_tensor_begin[c + 1];
+            const uint64_t k0 = d->term_factor_begin[d->tensor_term_begin[t0]];
+            const uint64_t k1 = d->term_factor_begin[d->tensor_term_begin[t1]];
+            for (uint64_t x = d->factor_u_begin[k0]; x < d->factor_u_begin[k1]; x++) {
+                if (d->factor_u_bits[x] < fwid) used[d->factor_u_bits[x]] = 1;
+            }
+            for (uint64_t x = d->factor_v_begin[k0]; x < d->factor_v_begin[k1]; x++) {
+                if (d->factor_v_bits[x] < fwid) used[d->factor_v_bits[x]] = 1;
+            }
+            for (uint32_t p = 0; p < fwid; p++) {
+                if (used[p]) loc.push_back(p);
+            }
+        }
+        const uint64_t nfac = d->term_factor_begin[d->tensor_term_begin[d->comp_tensor_begin[c + 1]]] -
+                              d->term_factor_begin[d->tensor_term_begin[d->comp_tensor_begin[c]]];
+        if (nfac >= heavy_min && loc.size() + n <= 63) lf_max = std::max(lf_max, uint32_t(loc.size()));
+    }
+    std::map<uint64_t, uint32_t> form_id;  // local mask -> form id (per tensor)
     std::vector<uint64_t> form_mask;        // form id -> raw mask
     std::map<uint32_t, uint32_t> form_size; // dictionary entry index -> plane loads
     size_t dict_base = 0;
-    const uint32_t all_plane = fwid + max_chain;  // ALL plane; all_plane + 1: ZERO; + 2 + j: raw sampled bit j
+    // ALL plane (>= every mono tensor's local width); all_plane + 1: ZERO; + 2 + j: raw sampled bit j
+    const uint32_t all_plane = lf_max + max_chain;
     uint32_t cur_width = 0;                        // param width of the tensor being encoded
     auto dict_form = [&](const std::vector<uint32_t> &sel0) -> uint32_t {
         uint64_t m = 0;
@@ -787,7 +823,13 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
         const uint32_t n = d->comp_out_begin[c + 1] - d->comp_out_begin[c];
         const uint32_t t0 = d->comp_tensor_begin[c], t1 = d->comp_tensor_begin[c + 1];
         const uint64_t nf = d->term_factor_begin[d->tensor_term_begin[t1]] - d->term_factor_begin[d->tensor_term_begin[t0]];
-        bool ok = nf >= heavy_min && H.comps.size() < size_t(zxs_dev::kMaxMonoComps) && fwid + max_chain + 2 <= 255;
+        const std::vector<uint32_t> &loc = comp_local[c];
+        const uint32_t nloc = uint32_t(loc.size());
+        bool ok = nf >= heavy_min && H.comps.size() < size_t(zxs_dev::kMaxMonoComps) && nloc + n <= 63 &&
+                  all_plane + 2 <= 255;
+        std::vector<uint32_t> to_local(fwid + n, ~0u);  // raw param -> local param
+        for (uint32_t i = 0; i < nloc; i++) to_local[loc[i]] = i;
+        for (uint32_t j = 0; j < n; j++) to_local[fwid + j] = nloc + j;
         const size_t dict_mark = H.dict.size();
         std::vector<uint32_t> tdb;  // per tensor: first dictionary entry
         std::vector<uint32_t> twid;  // per tensor: param width (the ALL plane spans planes 0..W-1)
@@ -810,9 +852,9 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             form_size.clear();
             dict_base = H.dict.size();
             tdb.push_back(uint32_t(dict_base));
-            cur_width = d->tensor_param_width[t];
+            cur_width = nloc + n;  // the local width (reference width f_width + n, compile.cpp:256)
             twid.push_back(cur_width);
-            if (cur_width > 63) ok = false;  // raw forms as 64-bit masks
+            if (d->tensor_param_width[t] > fwid + n || cur_width > 63) ok = false;  // local forms as 64-bit masks
             // ---- lower every term of tensor t to record tokens (order-free: J and Z commute)
             std::vector<MonoTerm> terms;
             terms.reserve(size_t(d->tensor_term_begin[t + 1] - d->tensor_term_begin[t]));
@@ -826,12 +868,18 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                         ok = false;
                         break;
                     }
-                    const std::vector<uint32_t> us = sel_list(d->factor_u_bits + d->factor_u_begin[k],
-                                                              d->factor_u_begin[k + 1] - d->factor_u_begin[k]);
-                    const std::vector<uint32_t> vs = sel_list(d->factor_v_bits + d->factor_v_begin[k],
-                                                              d->factor_v_begin[k + 1] - d->factor_v_begin[k]);
-                    for (uint32_t p : us) ok &= p < fwid + n;
-                    for (uint32_t p : vs) ok &= p < fwid + n;
+                    std::vector<uint32_t> us = sel_list(d->factor_u_bits + d->factor_u_begin[k],
+                                                        d->factor_u_begin[k + 1] - d->factor_u_begin[k]);
+                    std::vector<uint32_t> vs = sel_list(d->factor_v_bits + d->factor_v_begin[k],
+                                                        d->factor_v_begin[k + 1] - d->factor_v_begin[k]);
+                    for (uint32_t &p : us) {
+                        ok &= p < fwid + n && to_local[p] != ~0u;
+                        p = ok ? to_local[p] : 0;
+                    }
+                    for (uint32_t &p : vs) {
+                        ok &= p < fwid + n && to_local[p] != ~0u;
+                        p = ok ? to_local[p] : 0;
+                    }
                     if (!ok) break;
                     const bool ua = !us.empty(), vb = !vs.empty();
                     // domain and non-zero set
@@ -1144,7 +1192,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             }
             nodes_total += nodes.size();
         }
-        if (ok && mono_smem_bytes(fwid + 2 * max_chain + 2, std::max(comp_max_dict, H.max_dict), 1,
+        if (ok && mono_smem_bytes(all_plane + max_chain + 2, std::max(comp_max_dict, H.max_dict), 1,
                                   std::max(comp_depth, H.max_depth)) > 227 * 1024) {
             ok = false;
         }
@@ -1155,6 +1203,10 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             hc.upos_base = upos;
             hc.out_begin = d->comp_out_begin[c];
             hc.first_tensor = uint32_t(H.tensor_chunk_begin.size() - 1);
+            hc.nf = nloc;
+            hc.pmap_begin = uint32_t(H.param_map.size());
+            for (uint32_t p : loc) H.param_map.push_back(uint16_t(p));
+            for (uint32_t j = 0; j < n; j++) H.param_map.push_back(uint16_t(fwid + j));
             for (uint32_t t = t0; t < t1; t++) H.tensor_index[t] = hc.first_tensor + (t - t0);
             H.words.insert(H.words.end(), w.begin(), w.end());
             H.chunks.insert(H.chunks.end(), ch.begin(), ch.end());
@@ -1204,7 +1256,8 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
     if (H.tensor_width.empty()) H.tensor_width.push_back(0);
     if (H.tensor_basis_begin.empty()) H.tensor_basis_begin.push_back(0);
     if (H.basis.empty()) H.basis.push_back(0);
-    H.all_plane = fwid + max_chain;
+    if (H.param_map.empty()) H.param_map.push_back(0);
+    H.all_plane = all_plane;
     return H;
 }
 
@@ -1722,6 +1775,7 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     size_t o_mtw = ar.add(MH.tensor_width);
     size_t o_mtbb = ar.add(MH.tensor_basis_begin);
     size_t o_mbasis = ar.add(MH.basis);
+    size_t o_mpmap = ar.add(MH.param_map);
     if (MH.block_forms.empty()) MH.block_forms.push_back(0);
     size_t o_bf = ar.add(MH.block_forms);
     size_t o_bfb = ar.add(MH.block_form_begin);
@@ -1817,6 +1871,7 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         ma.tensor_width = reinterpret_cast<const uint32_t *>(b + o_mtw);
         ma.tensor_basis_begin = reinterpret_cast<const uint32_t *>(b + o_mtbb);
         ma.basis = reinterpret_cast<const unsigned long long *>(b + o_mbasis);
+        ma.param_map = reinterpret_cast<const uint16_t *>(b + o_mpmap);
         ma.words = reinterpret_cast<const uint32_t *>(b + o_mw);
         ma.chunks = reinterpret_cast<const uint4 *>(b + o_mch);
         ma.tensor_chunk_begin = reinterpret_cast<const uint32_t *>(b + o_mtcb);
@@ -1840,6 +1895,11 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         s->dd_tw = MH.tensor_width;
         s->dd_tbb = MH.tensor_basis_begin;
         s->dd_key_mask = MH.comp_key_mask;
+        s->dd_param_map = MH.param_map;
+        s->dd_identity_map = true;  // every component reads its f columns at their raw positions
+        for (uint32_t hc = 0; hc < MH.comps.size(); hc++) {
+            s->dd_identity_map = s->dd_identity_map && MH.comps[hc].nf == fwid;
+        }
         s->dd_tloads = MH.tensor_loads;
         s->dd_block_forms = reinterpret_cast<const uint32_t *>(b + o_bf);
         s->dd_block_form_begin = reinterpret_cast<const uint32_t *>(b + o_bfb);
@@ -1894,8 +1954,8 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     in.device = s->device;
     in.monomial = monomial ? 1 : 0;
 
-    CK(cudaMalloc(&s->dev_err, 2 * sizeof(unsigned long long)));
-    unsigned long long init[2] = {0, ~0ull};
+    CK(cudaMalloc(&s->dev_err, 3 * sizeof(unsigned long long)));
+    unsigned long long init[3] = {0, ~0ull, 0};
     CK(cudaMemcpy(s->dev_err, init, sizeof(init), cudaMemcpyHostToDevice));
     CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
@@ -1967,7 +2027,15 @@ void launch_mono(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *f
     h.err = s->dev_err;
     h.eval_tensor = eval_tensor;
     h.eval_out = eval_out;
-    if (eval_tensor >= 0) h.f_width = std::min(f_width, h.all_plane);  // injected params; forms use < W
+    if (eval_tensor >= 0) {  // injected params: every raw parameter (f bits and sampled bits) is a column
+        h.f_width = f_width;
+        for (uint32_t hc = 0; hc < h.n_comps; hc++) {
+            if (uint32_t(eval_tensor) >= h.comps[hc].first_tensor &&
+                uint32_t(eval_tensor) <= h.comps[hc].first_tensor + h.comps[hc].n_out) {
+                h.eval_comp = hc;
+            }
+        }
+    }
     const int nw = s->mono_nw;
     const uint64_t per_cta = uint64_t(mono_warps(nw)) * 1024 * nw;
     h.n_cta_tiles = (a.shots + per_cta - 1) / per_cta;
@@ -2018,7 +2086,7 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
     const size_t per_table = al(size_t(slots) * 8) + al(size_t(slots) * 4) + al(4) + al(size_t(max_ids) * 8) +
                              al(size_t(max_ids) * 4);
     const size_t bytes = al(cap * 8) + al(cap * 4) + al(cap * 8) + 2 * al(size_t(slots) * 8) +
-                         al(size_t(max_segs) * kDedupRoundKeys * 8) + al(nout * 8) + al(4) + al(16) + al(size_t(kDedupRoundKeys) * 8) +
+                         al(size_t(max_segs) * kDedupRoundKeys * 8) + al(nout * 8) + al(4) + al(24) + al(size_t(kDedupRoundKeys) * 8) +
                          (zxs_dev::kDedupMaxFused + 1) * al(size_t(kDedupRoundKeys) * 8) + 2 * per_table;
     if (bytes > s->dd_buf_bytes || slots != s->dd_table_slots) {
         if (s->dd_buf) CK(cudaFree(s->dd_buf));
@@ -2040,7 +2108,7 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
     d.partial = reinterpret_cast<double *>(take(size_t(max_segs) * kDedupRoundKeys * 8));
     d.counts = reinterpret_cast<unsigned long long *>(take(nout * 8));
     d.max_count = reinterpret_cast<unsigned int *>(take(4));
-    d.err = reinterpret_cast<unsigned long long *>(take(16));
+    d.err = reinterpret_cast<unsigned long long *>(take(24));
     d.xkeys = reinterpret_cast<unsigned long long *>(take(size_t(kDedupRoundKeys) * 8));
     for (uint32_t i = 0; i <= zxs_dev::kDedupMaxFused; i++) d.fvals[i] = reinterpret_cast<double *>(take(size_t(kDedupRoundKeys) * 8));
     for (int i = 0; i < 2; i++) {
@@ -2164,8 +2232,11 @@ void launch_dedup_sync(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint3
         ia.shots = a.shots;
         ia.fcols = fcols;
         ia.fcols_ld32 = fcols_ld32;
-        for (uint32_t p = 0; p < std::min(m.f_width, 63u); p++) {
-            if ((s->dd_key_mask[hc] >> p) & 1ull) ia.cols[ia.n_cols++] = uint8_t(p);
+        for (uint32_t p = 0; p < cd.nf; p++) {  // key bit p = local f parameter p
+            if ((s->dd_key_mask[hc] >> p) & 1ull) {
+                ia.cols[ia.n_cols] = s->dd_param_map[cd.pmap_begin + p];
+                ia.bits[ia.n_cols++] = uint8_t(p);
+            }
         }
         ia.key = d.key;
         ia.slot = d.slot;
@@ -2194,7 +2265,7 @@ void launch_dedup_sync(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint3
             ra.ci = cd.ci;
             ra.j = j;
             ra.out = s->comp_outputs[cd.out_begin + j];
-            ra.f_width = m.f_width;
+            ra.f_width = cd.nf;  // the key's sampled bits follow the local f parameters
             ra.key_mask = s->dd_key_mask[hc];
             ra.key = d.key;
             ra.slot = d.slot;
@@ -2272,7 +2343,7 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
         uint32_t relevant = 0, nrel = 0;
         uint64_t relpos = 0;
         for (uint32_t j = 0; j + 1 < cd.n_out; j++) {
-            const uint32_t p = m.f_width + j;
+            const uint32_t p = cd.nf + j;
             if (p < 63 && ((s->dd_key_mask[hc] >> p) & 1ull)) {
                 relevant |= 1u << j;
                 if (nrel < 8) relpos |= uint64_t(p) << (8 * nrel);
@@ -2287,8 +2358,11 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
         ia.shots = a.shots;
         ia.fcols = fcols;
         ia.fcols_ld32 = fcols_ld32;
-        for (uint32_t p = 0; p < std::min(m.f_width, 63u); p++) {
-            if ((s->dd_key_mask[hc] >> p) & 1ull) ia.cols[ia.n_cols++] = uint8_t(p);
+        for (uint32_t p = 0; p < cd.nf; p++) {  // key bit p = local f parameter p
+            if ((s->dd_key_mask[hc] >> p) & 1ull) {
+                ia.cols[ia.n_cols] = s->dd_param_map[cd.pmap_begin + p];
+                ia.bits[ia.n_cols++] = uint8_t(p);
+            }
         }
         ia.key = fused ? nullptr : d.key;
         ia.slot = d.slot;
@@ -2297,8 +2371,8 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
         const unsigned igrid = unsigned(std::min<uint64_t>((iwarps + zxs_dev::kDedupInitWarps - 1) / zxs_dev::kDedupInitWarps,
                                                            uint64_t(s->sm_count) * std::max(1, s->dd_init_occ)));
         s->time_begin(4, st, t0);
-        if (a.heavy_fraw) {  // per-shot f words from shot_kernel
-            const unsigned long long fm = s->dd_key_mask[hc] & (m.f_width >= 63 ? (1ull << 63) - 1 : (1ull << m.f_width) - 1);
+        if (a.heavy_fraw) {  // per-shot f words from shot_kernel (identity parameter maps only)
+            const unsigned long long fm = s->dd_key_mask[hc] & (cd.nf >= 63 ? (1ull << 63) - 1 : (1ull << cd.nf) - 1);
             const unsigned rgrid =
                 unsigned(std::min<uint64_t>((a.shots + 255) / 256, uint64_t(s->sm_count) * std::max(1, s->dd_raw_occ)));
             zxs_dev::dedup_init_raw_kernel<<<rgrid, 256, 0, st>>>(a.heavy_fraw, fm, a.shots, ia.key, d.slot, d.table[0]);
@@ -2369,7 +2443,7 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
             ra.ci = cd.ci;
             ra.j = j;
             ra.out = s->comp_outputs[cd.out_begin + j];
-            ra.f_width = m.f_width;
+            ra.f_width = cd.nf;  // the key's sampled bits follow the local f parameters
             ra.key_mask = s->dd_key_mask[hc];
             ra.key = d.key;
             ra.slot = d.slot;
@@ -2438,7 +2512,7 @@ void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
     if (heavy) {
         a.heavy_ld32 = 2 * ((a.shots + 63) / 64);
         const size_t fc_bytes = (std::max<size_t>(16, size_t(s->m.f_width) * a.heavy_ld32 * 4) + 255) & ~size_t(255);
-        const bool raw = s->has_mono && s->dedup && s->dd_async && s->fw_template == 1 && !a.fcols_in;
+        const bool raw = s->has_mono && s->dedup && s->dd_async && s->fw_template == 1 && !a.fcols_in && s->dd_identity_map;
         char *hb = reinterpret_cast<char *>(s->heavy_fcols_get(fc_bytes + (raw ? size_t(a.shots) * 8 : 0)));
         a.heavy_fcols = reinterpret_cast<uint32_t *>(hb);
         a.heavy_fraw = raw ? reinterpret_cast<unsigned long long *>(hb + fc_bytes) : nullptr;
@@ -2711,6 +2785,19 @@ zxs_status zxs_dedup_stats(zxs_sampler *s, int reset, uint64_t *out) {
             std::memset(s->dd_stats, 0, sizeof(s->dd_stats));
             if (s->dd_dev_stats) CK(cudaMemset(s->dd_dev_stats, 0, 16));
         }
+    });
+}
+
+zxs_status zxs_tie_count(zxs_sampler *s, int reset, uint64_t *out) {
+    return guarded([&] {
+        if (!s || !out) fail(ZXS_INVALID_ARGUMENT, "null argument");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard g(s->device);
+        CK(cudaDeviceSynchronize());
+        unsigned long long t = 0;
+        CK(cudaMemcpy(&t, s->dev_err + 2, 8, cudaMemcpyDeviceToHost));
+        *out = t;
+        if (reset) CK(cudaMemset(s->dev_err + 2, 0, 8));
     });
 }
 

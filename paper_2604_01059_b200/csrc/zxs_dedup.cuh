@@ -149,7 +149,8 @@ struct DedupInitArgs {
     const uint32_t *fcols;  // [f_width][fcols_ld32]
     uint64_t fcols_ld32;
     uint32_t n_cols;            // f columns the component's tensors read (< 63)
-    uint8_t cols[64];
+    uint16_t cols[63];          // raw f column
+    uint8_t bits[63];           // its key bit (local parameter index)
     unsigned long long *key;  // [shots] (nullable)
     uint32_t *slot;           // [shots]
     DedupTable table;
@@ -180,11 +181,12 @@ __global__ void __launch_bounds__(kDedupInitWarps * 32) dedup_init_kernel(const 
         if (wd < n_words) {
             for (uint32_t i = 0; i < a.n_cols; i++) {
                 const uint32_t p = a.cols[i];
+                const unsigned long long kb = 1ull << a.bits[i];
                 uint32_t w = __ldg(a.fcols + uint64_t(p) * a.fcols_ld32 + wd);
                 while (w) {
                     const uint32_t sb = __ffs(w) - 1;
                     w &= w - 1;
-                    kw[sb * 33 + lane] |= 1ull << p;
+                    kw[sb * 33 + lane] |= kb;
                 }
             }
         }
@@ -520,9 +522,11 @@ __global__ void dedup_reset_kernel(uint32_t *count) { *count = 0; }
 __global__ void dedup_err_init_kernel(unsigned long long *e) {
     e[0] = 0ull;
     e[1] = ~0ull;
+    e[2] = 0ull;
 }
 __global__ void dedup_err_merge_kernel(const unsigned long long *e, unsigned long long *err) {
     if (e[0]) report_ratio_error(err, e[1]);
+    if (e[2]) err[2] += e[2];
 }
 
 // One autoregressive decision, exactly the reference's (sampler.cpp:84-99):
@@ -545,6 +549,7 @@ __device__ __forceinline__ bool ar_decide(double cur, double prev, double u, uns
     if (!(ratio > -1e-6 && ratio < 1.0 + 1e-6)) report_ratio_error(err, shot);
     double cl = (0.0 < ratio) ? ratio : 0.0;
     cl = (cl < 1.0) ? cl : 1.0;
+    count_near_tie(err, u, cl);
     return !(u < cl);
 }
 

@@ -36,6 +36,8 @@ struct HeavyComp {
     uint32_t upos_base;    // first chain position of this component in the global position order
     uint32_t out_begin;    // into comp_outputs
     uint32_t first_tensor; // index into tensor_chunk_begin (chain order: norm, marg0, ...)
+    uint32_t nf;           // monomial path: local f parameters (local nf + j = sampled bit j)
+    uint32_t pmap_begin;   // monomial path: MonoArgs::param_map[pmap_begin + local] = raw parameter
 };
 
 struct HeavyArgs {

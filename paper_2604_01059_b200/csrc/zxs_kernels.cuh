@@ -272,6 +272,15 @@ __device__ __forceinline__ void report_ratio_error(unsigned long long *err, uint
     atomicMin(&err[1], (unsigned long long)shot);
 }
 
+// Near-tie draws of the integer (monomial / deduplicated) paths, whose values
+// differ from the reference's by the reference's own rounding (<= 1e-12
+// relative of the term-magnitude sum, tests/test_gpu_parity.py): a draw whose
+// uniform lies within 1e-9 (relative) of the clamped ratio is one whose bit
+// could differ from the reference's. Counted in err[2] (zxs_tie_count).
+__device__ __forceinline__ void count_near_tie(unsigned long long *err, double u, double cl) {
+    if (fabs(u - cl) <= 1e-9 * fmax(cl, 1e-300)) atomicAdd(&err[2], 1ull);
+}
+
 // Rare path of the mechanism draw: the flip set selected by each of the
 // lane's two draws (first entry, then the rest of a joint table in order).
 // Kept out of line so the divergent scan does not pull the draw loop's

@@ -82,7 +82,8 @@ struct MonoArgs {
     uint32_t f_width, n_planes, all_plane;
     const uint32_t *tensor_width;     // [mono tensors] param width W
     const uint32_t *tensor_basis_begin;       // [mono tensors] first basis vector
-    const unsigned long long *basis;  // basis vectors: masks over the raw params (f bits, then sampled bits)
+    const unsigned long long *basis;  // basis vectors: masks over the component's local params
+    const uint16_t *param_map;        // local param -> raw param (f column, or f_width + sampled bit)
     const uint32_t *fcols;            // [f_width][fcols_ld32] from shot_kernel
     uint64_t fcols_ld32;
     uint32_t *out32;                  // [num_outputs][out_ld32] (nullable)
@@ -103,6 +104,7 @@ struct MonoArgs {
     const uint32_t *comp_outputs;
     // eval seam: evaluate one tensor and store the values (no chain)
     int eval_tensor;                  // -1: sample; else index into tensor_chunk_begin
+    uint32_t eval_comp;               // eval: index into comps of the tensor's component
     double *eval_out;                 // [shots]
     uint32_t n_comps;
     HeavyComp comps[kMaxMonoComps];
@@ -506,7 +508,7 @@ __global__ void __launch_bounds__(MonoCfg<NW>::kWarps * 32, 1) mono_kernel(const
 
         const uint32_t ncomp = h.eval_tensor >= 0 ? 1u : h.n_comps;
         for (uint32_t hc = 0; hc < ncomp; hc++) {
-            const HeavyComp cd = h.comps[hc];
+            const HeavyComp cd = h.comps[h.eval_tensor >= 0 ? h.eval_comp : hc];
             const uint32_t npos = h.eval_tensor >= 0 ? 1u : cd.n_out + 1;
             for (uint32_t pos = 0; pos < npos; pos++) {  // pos 0: normalization, pos j+1: marginal j
                 const uint32_t t = h.eval_tensor >= 0 ? uint32_t(h.eval_tensor) : cd.first_tensor + pos;
@@ -519,7 +521,7 @@ __global__ void __launch_bounds__(MonoCfg<NW>::kWarps * 32, 1) mono_kernel(const
                     for (uint32_t b = 0; b < W; b++) {
                         BW<NW> v = bw_zero<NW>();
                         for (unsigned long long x = bv[b]; x; x &= x - 1) {
-                            const uint32_t p = __ffsll((long long)x) - 1;
+                            const uint32_t p = __ldg(h.param_map + cd.pmap_begin + __ffsll((long long)x) - 1);  // raw
                             BW<NW> r;
                             if (p < h.f_width) {
 #pragma unroll
@@ -606,6 +608,7 @@ __global__ void __launch_bounds__(MonoCfg<NW>::kWarps * 32, 1) mono_kernel(const
                         philox_tail<1>(pre, seed_hi ^ stream, h.k0_round, k2c, h.k0_round[9], rhi, rlo);
                         u = philox_uniform((uint64_t(rhi[0]) << 32) | rlo[0]);
                     }
+                    if (valid) count_near_tie(h.err, u, cl);
                     const bool bit = !(u < cl) && valid;
                     prev_g[s] = bit ? __dsub_rn(pv, cur) : cur;
 #pragma unroll

@@ -163,6 +163,14 @@ class CompiledSampler:
         return dict(zip(("batches", "fallbacks", "keys", "plane_load_bytes", "eval_launches", "enabled"),
                         (int(x) for x in out)))
 
+    def tie_count(self, reset: bool = False) -> int:
+        """Near-tie autoregressive draws of the integer paths since the last reset
+        (include/zxs_b200.h zxs_tie_count): the only draws whose bit could differ
+        from the reference's."""
+        out = ctypes.c_uint64()
+        _native.check(_native.lib().zxs_tie_count(self._h, int(reset), ctypes.byref(out)))
+        return int(out.value)
+
     # ---- host-buffer entry points --------------------------------------
     def sample_into(self, expected_mode: int, seed: int, first_shot: int, shots: int, out: np.ndarray,
                     stream: int = 0) -> np.ndarray:

@@ -273,8 +273,11 @@ def test_cultivation_proxy_against_reference():
 
 
 # ---------------------------------------------------------------- monomial path
+# surface_d5_r5_xmem_rz3: f_width 122, so its magic component (raw width 125) runs through a
+# component-local parameter map (encode_mono)
 MONO_NAMES = ["c2_surface_d3_xmem_t", "c4_color_d5_rz3", "surface_d3_xmem_rz5", "surface_d3_xmem_9t", "h_t_h_m",
-              "oracle_mix_4", "random_02", "random_05", "steane_inject", "c1_surface_d3_zmem"]
+              "oracle_mix_4", "random_02", "random_05", "steane_inject", "c1_surface_d3_zmem",
+              "surface_d5_r5_xmem_rz3"]
 
 
 @pytest.mark.parametrize("name", MONO_NAMES)
@@ -406,7 +409,8 @@ def test_kernel_timing_counts_launches():
 
 
 # ---------------------------------------------------------------- deduplicated path
-@pytest.mark.parametrize("name", ["surface_d3_xmem_9t", "surface_d3_xmem_rz5", "c4_color_d5_rz3", "steane_inject"])
+@pytest.mark.parametrize("name", ["surface_d3_xmem_9t", "surface_d3_xmem_rz5", "c4_color_d5_rz3", "steane_inject",
+                                  "surface_d5_r5_xmem_rz3"])
 def test_dedup_bit_identical_to_per_shot(name):
     """Deduplicated and per-shot monomial paths compute the same canonical
     segment-ordered sums: identical records for every seed and range, and

@@ -7,13 +7,15 @@ regenerated from their textbook definitions:
   depolarizing noise, optional T gate on one data qubit after RX;
 * the [[19,1,5]] triangular 6.6.6 colour code memory with R_Z(theta)
   rotations on k data qubits (config 4);
-* a Steane-code cultivation proxy: T injection, Clifford encoder and c
-  transversal T checks (config 3 stand-in; Gidney et al.'s exact circuit
-  is not available offline);
+* d=3 magic-state cultivation on the Steane colour code with circuit-level
+  noise (config 3; Gidney et al.'s exact circuit is not available offline,
+  the structure is reconstructed: `cultivation_d3`), and the round-1 Steane
+  proxy (corrected checks);
 * random small circuits in the spirit of tests/test_util.hpp:13-115.
 
-Every generator is validated by compiling it noiselessly with the reference
-and checking that every detector and observable samples to 0.
+Every generator is checked noiselessly by tests/test_circuits.py: the
+reference's exact oracle (oracle.cpp:494) where the circuit is small enough,
+otherwise the reference's exact P(all outputs 0 | no error).
 """
 from __future__ import annotations
 
@@ -189,35 +191,159 @@ def color_code_memory(L: int, rounds: int, p: float, rz_count: int = 0, seed: in
     return "\n".join(lines) + "\n"
 
 
-# ---------------------------------------------------------------- cultivation proxy
-def steane_cultivation_proxy(checks: int, p: float) -> str:
-    """T-state injection into the Steane [[7,1,3]] code,
-    `checks` transversal T checks (T_DAG on all data, RX anc, CX anc->q for
-    all data, T on all data, MX anc, DETECTOR), final MX of all data with
-    observable = XOR of the 7. Noise: DEPOLARIZE1 after encoding, DEPOLARIZE2
-    on each check CX, Z_ERROR before each ancilla readout.
+# ---------------------------------------------------------------- cultivation
+# Steane [[7,1,3]] colour code, Hamming labels 1..7 -> qubits 0..6; the three
+# faces (weight-4 stabilisers, both X and Z type) are {4567}, {2367}, {1357}.
+STEANE_FACES = [[3, 4, 5, 6], [1, 2, 5, 6], [0, 2, 4, 6]]
+# Unitary encoder of the state on label 3 (qubit 2): X3 -> X3 X5 X6 (weight-3
+# logical X), then pivots 4, 2, 1 (qubits 3, 1, 0, in |+>) fan out over their
+# faces; qubits 4, 5, 6 start in |0>.
+STEANE_ENCODER = [(2, 4), (2, 5), (3, 4), (3, 5), (3, 6), (1, 2), (1, 5), (1, 6), (0, 2), (0, 4), (0, 6)]
 
-    Encoder (Hamming labels 1..7 -> qubits 0..6, stabilisers {4567}, {2367},
-    {1357}): the state T|+> is prepared on label 3, copied to labels 5 and 6
-    (X3 -> X3 X5 X6, a weight-3 logical X), then pivots 4, 2, 1 (in |+>)
-    fan out over their stabilisers."""
-    lines = ["RX 2", "T 2", "R 4 5 6", "RX 3 1 0", "CX 2 4 2 5",
-             "CX 3 4 3 5 3 6", "CX 1 2 1 5 1 6", "CX 0 2 0 4 0 6"]
+
+def steane_cultivation_proxy(checks: int, p: float) -> str:
+    """Round-1 proxy, corrected: T-state injection into the
+    Steane code, `checks` transversal H_XY checks (T on all data, RX anc,
+    CX anc->q for all data, MX anc, T_DAG on all data, DETECTOR), final T on
+    all data and MX of all data with observable = XOR of the 7. Noise only
+    after encoding, on the check CX and before each ancilla readout.
+
+    The round-1 version checked with T_DAG ... T, which measures a logical
+    operator the T state is not an eigenstate of (both detectors were coin
+    flips) and read the data out without the final T (a random observable).
+    tests/test_circuits.py checks every generator noiselessly."""
+    lines = ["RX 2", "T 2", "R 4 5 6", "RX 3 1 0"]
+    lines += [f"CX {a} {b}" for a, b in STEANE_ENCODER]
     lines.append(f"DEPOLARIZE1({_fmt(p)}) 0 1 2 3 4 5 6")
     anc = 7
     for _ in range(checks):
-        lines.append("T_DAG 0 1 2 3 4 5 6")
+        lines.append("T 0 1 2 3 4 5 6")
         lines.append(f"RX {anc}")
         for q in range(7):
             lines.append(f"CX {anc} {q}")
             lines.append(f"DEPOLARIZE2({_fmt(p)}) {anc} {q}")
-        lines.append("T 0 1 2 3 4 5 6")
+        lines.append("T_DAG 0 1 2 3 4 5 6")
         lines.append(f"Z_ERROR({_fmt(p)}) {anc}")
         lines.append(f"MX {anc}")
         lines.append("DETECTOR rec[-1]")
+    lines.append("T 0 1 2 3 4 5 6")
     lines.append("MX 0 1 2 3 4 5 6")
     lines.append("OBSERVABLE_INCLUDE(0) " + " ".join(f"rec[{-1 - i}]" for i in range(7)))
     return "\n".join(lines) + "\n"
+
+
+def cultivation_d3(p: float, checks: int = 2, z_rounds: bool = True, round0: bool = True) -> str:
+    """d=3 magic-state cultivation on the Steane colour code (the structure of
+    Gidney, Shutty & Jones 2024, reconstructed offline) with circuit-level
+    noise on every gate, reset and measurement:
+
+    1. Injection: T|+> on qubit 2, unitary encoder into the colour code.
+    2. Stabiliser round 0 (if round0): the three Z faces (R anc, CX q->anc,
+       M anc) and the three X faces (RX anc, CX anc->q, MX anc) through one
+       reused ancilla; every outcome is a detector (deterministic +1).
+    3. `checks` H_XY double checks: T on all data; a Z-face round (z_rounds:
+       detectors against the previous Z round -- Z faces commute with T, so
+       they are measured inside the check frame); the transversal logical X
+       measured through a fan-out from the ancilla (RX anc, CX anc->q x 7,
+       MX anc, detector); T_DAG on all data.
+    4. Readout: the inverse encoder (noisy), M of qubits 4 5 6 and MX of
+       qubits 3 1 0 (decoded stabilisers: detectors), T_DAG on qubit 2 and MX
+       (the logical T-basis readout: the observable).
+
+    Noise (p each): X_ERROR after R / Z_ERROR after RX, X_ERROR before M /
+    Z_ERROR before MX, DEPOLARIZE2 after every CX, DEPOLARIZE1 on every T /
+    T_DAG. A depolarizing channel commutes with any unitary on its qubit
+    (D(U rho U^+) = U D(rho) U^+), so the T gates' channel sits after T and
+    before T_DAG: the same noisy circuit, written so that the reference's
+    simplifier (simplify.cpp:67-103) still fuses a check's T_DAG with the next
+    check's T (an X-type error spider between them would block the fusion and
+    take chi from 93,312 to ~1.5e9). No idle noise.
+
+    Deterministic noiselessly: tests/test_circuits.py (the reference's exact
+    oracle on reduced variants, and P(all zero | no error) = 1 on the full
+    compiled circuit)."""
+    L: list[str] = []
+    nm = [0]
+    rec: dict = {}
+    anc = 7
+    pf = _fmt(p)
+
+    def meas(kind, q, key):
+        if p:
+            L.append(f"{'X' if kind == 'M' else 'Z'}_ERROR({pf}) {q}")
+        L.append(f"{kind} {q}")
+        rec[key] = nm[0]
+        nm[0] += 1
+
+    def det(keys):
+        L.append("DETECTOR " + " ".join(f"rec[{rec[k] - nm[0]}]" for k in keys))
+
+    def reset(kind, qs):
+        L.append(f"{kind} " + " ".join(map(str, qs)))
+        if p:
+            L.append(f"{'X' if kind == 'R' else 'Z'}_ERROR({pf}) " + " ".join(map(str, qs)))
+
+    def gate1(g, qs, noise_before=False):
+        if p and noise_before:
+            L.append(f"DEPOLARIZE1({pf}) " + " ".join(map(str, qs)))
+        L.append(f"{g} " + " ".join(map(str, qs)))
+        if p and not noise_before:
+            L.append(f"DEPOLARIZE1({pf}) " + " ".join(map(str, qs)))
+
+    def cx(a, b):
+        L.append(f"CX {a} {b}")
+        if p:
+            L.append(f"DEPOLARIZE2({pf}) {a} {b}")
+
+    D = list(range(7))
+    reset("RX", [2])
+    gate1("T", [2])
+    reset("R", [4, 5, 6])
+    reset("RX", [3, 1, 0])
+    for a, b in STEANE_ENCODER:
+        cx(a, b)
+    zr = [0]
+
+    def z_round():
+        r = zr[0]
+        for k, face in enumerate(STEANE_FACES):
+            reset("R", [anc])
+            for q in face:
+                cx(q, anc)
+            meas("M", anc, ("z", r, k))
+            det([("z", r, k)] if r == 0 else [("z", r, k), ("z", r - 1, k)])
+        zr[0] += 1
+
+    if round0:
+        z_round()
+        for k, face in enumerate(STEANE_FACES):
+            reset("RX", [anc])
+            for q in face:
+                cx(anc, q)
+            meas("MX", anc, ("x", k))
+            det([("x", k)])
+    for c in range(checks):
+        gate1("T", D)
+        if z_rounds:
+            z_round()
+        reset("RX", [anc])
+        for q in D:
+            cx(anc, q)
+        meas("MX", anc, ("c", c))
+        det([("c", c)])
+        gate1("T_DAG", D, noise_before=True)
+    for a, b in reversed(STEANE_ENCODER):
+        cx(a, b)
+    for q in (4, 5, 6):
+        meas("M", q, ("d", q))
+        det([("d", q)])
+    for q in (3, 1, 0):
+        meas("MX", q, ("d", q))
+        det([("d", q)])
+    gate1("T_DAG", [2], noise_before=True)
+    meas("MX", 2, ("d", 2))
+    L.append(f"OBSERVABLE_INCLUDE(0) rec[{rec[('d', 2)] - nm[0]}]")
+    return "\n".join(L) + "\n"
 
 
 # ---------------------------------------------------------------- random circuits

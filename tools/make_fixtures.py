@@ -12,7 +12,8 @@ unmodified reference compiled in place). For every fixture circuit it writes
                                   and of sample_error_batch f-columns
 
 Usage: python tools/make_fixtures.py [--only name,...] [--big]
-(--big also writes the cultivation proxy to data/, which is not committed).
+(--big also compiles the config-3 cultivation circuit into data/: minutes and
+~15 GB of host memory).
 """
 from __future__ import annotations
 
@@ -55,6 +56,9 @@ def fixtures():
     F.append(("c5_surface_d7_r7", 0, C.surface_code_memory(7, 7, 1e-3, "Z"), [(1, 0, 1000), (5, 777, 20000)]))
     F.append(("surface_d3_xmem_rz5", 0, _rz5(), big[:4]))
     F.append(("surface_d3_xmem_9t", 0, _nine_t(), big[:4]))
+    # f_width 122 > 63: the magic component reads its tensors through a component-local
+    # parameter map on the monomial / deduplicated path
+    F.append(("surface_d5_r5_xmem_rz3", 0, _rz_surface(5, 5, 3), big[:4]))
     small = [(1, 0, 1000), (9, 100, 777)]
     F.append(("h_t_h_m", 1, "H 0\nT 0\nH 0\nM 0\n", small))
     F.append(("bell_m", 1, "H 0\nCNOT 0 1\nM 0 1\n", small))
@@ -67,7 +71,7 @@ def fixtures():
     F.append(("oracle_mix_4", 1, "R_Y(0.23) 0\nE(0.15) X0 Z1\nH 1\nM 0 1\n", small))
     F.append(("xerror_merge", 0, "X_ERROR(0.1) 0\nX_ERROR(0.2) 0\nM 0\nDETECTOR rec[-1]\n", small))
     F.append(("norm_sum", 1, "H 0\nT 0\nCNOT 0 1\nX_ERROR(0.2) 0\nZ_ERROR(0.1) 1\nM 0 1\n", small))
-    F.append(("steane_inject", 0, C.steane_cultivation_proxy(0, 1e-3), small))
+    F.append(("steane_inject", 0, C.steane_cultivation_proxy(0, 1e-3), small, True))  # cat5 plan: fixed front-end
     # random circuits with magic (mixed component widths, R_Z/R_X, channels)
     import random
     rng = random.Random(20261017)
@@ -95,6 +99,15 @@ def _rz5() -> str:
     return "\n".join(lines[:3] + ins + lines[3:]) + "\n"
 
 
+def _rz_surface(d: int, rounds: int, k: int) -> str:
+    """d x d X-memory, `rounds` rounds, R_Z(0.1 pi) on the first k data qubits."""
+    t = C.surface_code_memory(d, rounds, 1e-3, "X")
+    lines = t.splitlines()
+    data = lines[1].split()[1:]
+    ins = [f"R_Z(0.1) {q}" for q in data[:k]]
+    return "\n".join(lines[:3] + ins + lines[3:]) + "\n"
+
+
 def _nine_t() -> str:
     """d=3 X-memory + T on all 9 data qubits (SURVEY '9-T proxy')."""
     t = C.surface_code_memory(3, 3, 1e-3, "X")
@@ -103,16 +116,19 @@ def _nine_t() -> str:
     return "\n".join(lines[:3] + ["T " + " ".join(data)] + lines[3:]) + "\n"
 
 
-def make(name, mode, text, plan, out_dir=GOLDEN, write_circuit=True):
+def make(name, mode, text, plan, out_dir=GOLDEN, write_circuit=True, fixed=False):
+    """fixed: compile with the front-end whose cat5 normalisation is fixed
+    (oracle/Makefile `fixed`); sampling and goldens always use the unmodified
+    reference library on the saved model."""
     if write_circuit:
         with open(os.path.join(CIRC, name + ".stim"), "w") as fp:
             fp.write(text)
     t0 = time.time()
-    m = R.RefModel.compile(text, mode)
+    m = R.RefModel.compile_fixed(text, mode) if fixed else R.RefModel.compile(text, mode)
     compile_s = time.time() - t0
     path = os.path.join(out_dir, name + ".zxs")
     m.save(path)
-    rec = {"mode": mode, "info": m.info, "compile_s": round(compile_s, 3),
+    rec = {"mode": mode, "info": m.info, "compile_s": round(compile_s, 3), "frontend": "fixed-cat5" if fixed else "reference",
            "circuit_sha256": hashlib.sha256(text.encode()).hexdigest(), "samples": [], "fcols": []}
     for seed, first, shots in plan:
         try:
@@ -147,11 +163,11 @@ def main():
     gpath = os.path.join(GOLDEN, "goldens.json")
     goldens = json.load(open(gpath)) if os.path.exists(gpath) else {}
     only = set(filter(None, args.only.split(",")))
-    for name, mode, text, plan in fixtures():
+    for name, mode, text, plan, *fixed in fixtures():
         if only and name not in only:
             continue
         t = time.time()
-        goldens[name] = make(name, mode, text, plan)
+        goldens[name] = make(name, mode, text, plan, fixed=bool(fixed and fixed[0]))
         print(f"{name}: {goldens[name]['info']['num_outputs']} outputs, chi={goldens[name]['info']['chi']}, "
               f"{time.time() - t:.1f}s", flush=True)
     goldens["_philox"] = [{"seed": s, "stream": st, "index": i, "u": R.uniform_at(s, st, i)}
@@ -160,12 +176,22 @@ def main():
     with open(gpath, "w") as fp:
         json.dump(goldens, fp, indent=1, sort_keys=True)
     if args.big:
+        # config 3: d=3 magic-state cultivation with circuit-level noise (tools/circuits.py
+        # cultivation_d3), compiled by the front-end with the cat5 fix -- the unmodified
+        # front-end's decomposition gives this circuit wrong marginals (tests/test_circuits.py)
         os.makedirs(os.path.join(ROOT, "data"), exist_ok=True)
-        text = C.steane_cultivation_proxy(2, 1e-3)
+        text = C.cultivation_d3(1e-3)
         t = time.time()
-        rec = make("c3_cultivation_proxy", 0, text, [(1, 0, 256)], out_dir=os.path.join(ROOT, "data"))
-        print(f"cultivation proxy: {rec['info']} {time.time() - t:.1f}s")
-        with open(os.path.join(ROOT, "data", "c3_cultivation_proxy.json"), "w") as fp:
+        rec = make("c3_cultivation_d3", 0, text, [(1, 0, 4096), (2, 1 << 20, 2048)], out_dir=os.path.join(ROOT, "data"),
+                   fixed=True)
+        print(f"cultivation d=3: {rec['info']} {time.time() - t:.1f}s", flush=True)
+        import gzip
+        import shutil
+        zp = os.path.join(ROOT, "data", "c3_cultivation_d3.zxs")
+        with open(zp, "rb") as src, gzip.open(zp + ".gz", "wb", compresslevel=9) as dst:
+            shutil.copyfileobj(src, dst, 1 << 24)
+        os.remove(zp)
+        with open(os.path.join(ROOT, "data", "c3_cultivation_d3.json"), "w") as fp:
             json.dump(rec, fp, indent=1)
 
 

@@ -51,12 +51,15 @@ def count_outputs_sharded(total_shots: int, seed: int, num_outputs: int,
     return counts.cpu().numpy().astype(np.uint64)
 
 
-def gpu_counter(cs, stream=None):
-    """counter() for count_outputs_sharded backed by the device sampler."""
+def gpu_counter(cs, stream=None, device=None):
+    """counter() for count_outputs_sharded backed by the device sampler
+    (zxs_count_device into a device tensor; `device` defaults to the sampler's
+    GPU -- the CPU tests pass a host device and a stand-in sampler)."""
     import torch
 
     def run(seed: int, first: int, shots: int):
-        counts = torch.zeros(cs.num_outputs, dtype=torch.int64, device=torch.device("cuda", cs.device))
+        dev = device if device is not None else torch.device("cuda", cs.device)
+        counts = torch.zeros(cs.num_outputs, dtype=torch.int64, device=dev)
         st = stream if stream is not None else torch.cuda.current_stream(cs.device).cuda_stream
         cs.count_device(seed, first, shots, counts.data_ptr(), st)
         cs.check_errors(st)

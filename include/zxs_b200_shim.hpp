@@ -15,6 +15,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <tuple>
 
@@ -76,6 +77,67 @@ class Sampler {
     zxs_sampler *s_ = nullptr;
 };
 
+// Uploaded samplers are cached per CompiledSampler (the reference's compiled
+// sampler is immutable, compile.hpp:57-58), so repeated calls on the same
+// object -- a CLI sweep, a decoder loop -- flatten and upload once. The key is
+// the object's address plus a fingerprint of its contents (sizes, error-model
+// probabilities, first/last term coefficients of every tensor), so a new
+// sampler allocated at a recycled address is not mistaken for the old one.
+struct CacheKey {
+    const void *addr;
+    uint64_t fingerprint;
+    int device;
+    bool operator<(const CacheKey &o) const {
+        return std::tie(addr, fingerprint, device) < std::tie(o.addr, o.fingerprint, o.device);
+    }
+};
+
+inline uint64_t fingerprint(const zxsim::CompiledSampler &cs) {
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](uint64_t x) { h = (h ^ x) * 1099511628211ull; };
+    auto mixd = [&](double d) { uint64_t x; std::memcpy(&x, &d, 8); mix(x); };
+    mix(cs.f_width);
+    mix(cs.num_outputs);
+    mix(uint64_t(cs.mode));
+    mix(cs.error_model.mechanisms.size());
+    for (const auto &m : cs.error_model.mechanisms) {
+        mixd(m.probability);
+        mix(m.table.size());
+        if (!m.table.empty()) mixd(m.table.back());
+        mix(m.f_vectors.size());
+    }
+    mix(cs.direct.size());
+    for (const auto &d : cs.direct) mix(d.output_index * 2 + d.flip_const + d.f_bits.size() * 1024);
+    mix(cs.components.size());
+    for (const auto &ac : cs.components) {
+        mix(ac.output_indices.size());
+        auto tens = [&](const zxsim::PhaseTermTensors &t) {
+            mix(t.terms.size());
+            if (!t.terms.empty()) {
+                mixd(t.terms.front().c.real());
+                mixd(t.terms.back().c.imag());
+                mix(t.terms.back().num_factors());
+            }
+        };
+        tens(ac.normalization);
+        for (const auto &t : ac.marginals) tens(t);
+    }
+    return h;
+}
+
+inline std::shared_ptr<Sampler> cached_sampler(const zxsim::CompiledSampler &cs, int device = 0) {
+    static std::mutex mu;
+    static std::map<CacheKey, std::shared_ptr<Sampler>> cache;
+    const CacheKey key{&cs, fingerprint(cs), device};
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    if (cache.size() >= 8) cache.erase(cache.begin());  // bounded: samplers hold device memory
+    auto s = std::make_shared<Sampler>(cs, device);
+    cache.emplace(key, s);
+    return s;
+}
+
 // Drop-in replacements for sampler.hpp:57-60. `seed`, `sparse_threshold` and
 // `force_dense` choose the bits exactly as in the reference (dense path, or
 // the sparse geometric path when sparse_eligible, sampler.cpp:104-147);
@@ -83,14 +145,12 @@ class Sampler {
 // are the same for any batch split (sampler.cpp:82, 91, 268-284).
 inline zxsim::SampleRecord sample_detectors(const zxsim::CompiledSampler &cs, size_t shots,
                                             const zxsim::SamplerOptions &opt) {
-    Sampler s(cs);
-    return s.sample(ZXS_MODE_DETECTORS, shots, opt);
+    return cached_sampler(cs)->sample(ZXS_MODE_DETECTORS, shots, opt);
 }
 
 inline zxsim::SampleRecord sample_measurements(const zxsim::CompiledSampler &cs, size_t shots,
                                                const zxsim::SamplerOptions &opt) {
-    Sampler s(cs);
-    return s.sample(ZXS_MODE_MEASUREMENTS, shots, opt);
+    return cached_sampler(cs)->sample(ZXS_MODE_MEASUREMENTS, shots, opt);
 }
 
 }  // namespace zxsim_b200

@@ -2002,7 +2002,7 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &s->dd_fused_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_fused_ar_kernel), 256, 0));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &s->dd_raw_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_init_raw_kernel), 256, 0));
+                &s->dd_raw_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_init_raw_kernel<unsigned long long>), 256, 0));
         }
     }
 }
@@ -2306,6 +2306,24 @@ void launch_dedup_sync(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint3
     s->dd_dirty = false;
 }
 
+void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st);
+
+// The f columns of a batch whose shot_kernel pass stored only per-shot f words
+// (raw keys): shot_kernel again in error-batch mode (no outputs), into the spare
+// buffer. Only a batch the deduplicated path must redo needs them.
+const uint32_t *regen_fcols(zxs_sampler *s, const zxs_dev::LaunchArgs &a, cudaStream_t st) {
+    zxs_dev::LaunchArgs b = a;
+    b.fcols_out = a.fcols_spare;
+    b.fcols_ld32 = a.heavy_ld32;
+    b.out32 = nullptr;
+    b.counts = nullptr;
+    b.heavy_fcols = nullptr;
+    b.heavy_fraw = nullptr;
+    launch_shots(s, b, st);
+    CK(cudaGetLastError());
+    return a.fcols_spare;
+}
+
 // The same chain without host round trips: key counts stay on the device (one
 // evaluation round of at most kDedupRoundKeys keys per position), the largest
 // count is checked once at the end; a batch that needed more rounds (or
@@ -2375,7 +2393,13 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
             const unsigned long long fm = s->dd_key_mask[hc] & (cd.nf >= 63 ? (1ull << 63) - 1 : (1ull << cd.nf) - 1);
             const unsigned rgrid =
                 unsigned(std::min<uint64_t>((a.shots + 255) / 256, uint64_t(s->sm_count) * std::max(1, s->dd_raw_occ)));
-            zxs_dev::dedup_init_raw_kernel<<<rgrid, 256, 0, st>>>(a.heavy_fraw, fm, a.shots, ia.key, d.slot, d.table[0]);
+            if (a.fraw_bytes == 4) {
+                zxs_dev::dedup_init_raw_kernel<uint32_t><<<rgrid, 256, 0, st>>>(
+                    static_cast<const uint32_t *>(a.heavy_fraw), fm, a.shots, ia.key, d.slot, d.table[0]);
+            } else {
+                zxs_dev::dedup_init_raw_kernel<unsigned long long><<<rgrid, 256, 0, st>>>(
+                    static_cast<const unsigned long long *>(a.heavy_fraw), fm, a.shots, ia.key, d.slot, d.table[0]);
+            }
             CK(cudaGetLastError());
         } else {
             void *iargs[] = {&ia};
@@ -2476,6 +2500,7 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
     if (s->dd_pinned[0] > limit) {  // more keys than one round (or the tables) hold: redo synchronously
         s->dd_dirty = true;
         s->dd_stats[0] -= 1;
+        if (!fcols) fcols = regen_fcols(s, a, st);
         return launch_dedup_sync(s, a, fcols, fcols_ld32, st);
     }
     zxs_dev::dedup_err_merge_kernel<<<1, 1, 0, st>>>(d.err, s->dev_err);
@@ -2513,9 +2538,14 @@ void launch_shots(zxs_sampler *s, zxs_dev::LaunchArgs &a, cudaStream_t st) {
         a.heavy_ld32 = 2 * ((a.shots + 63) / 64);
         const size_t fc_bytes = (std::max<size_t>(16, size_t(s->m.f_width) * a.heavy_ld32 * 4) + 255) & ~size_t(255);
         const bool raw = s->has_mono && s->dedup && s->dd_async && s->fw_template == 1 && !a.fcols_in && s->dd_identity_map;
-        char *hb = reinterpret_cast<char *>(s->heavy_fcols_get(fc_bytes + (raw ? size_t(a.shots) * 8 : 0)));
-        a.heavy_fcols = reinterpret_cast<uint32_t *>(hb);
-        a.heavy_fraw = raw ? reinterpret_cast<unsigned long long *>(hb + fc_bytes) : nullptr;
+        // raw keys: 4 B per shot when f fits 32 bits; the f columns are then not stored at all
+        // (no heavy_kernel component reads them; a batch the deduplicated path must redo
+        // regenerates them, launch_dedup)
+        a.fraw_bytes = s->m.f_width <= 32 ? 4 : 8;
+        char *hb = reinterpret_cast<char *>(s->heavy_fcols_get(fc_bytes + (raw ? size_t(a.shots) * a.fraw_bytes : 0)));
+        a.heavy_fcols = (raw && !s->has_heavy) ? nullptr : reinterpret_cast<uint32_t *>(hb);
+        a.heavy_fraw = raw ? static_cast<void *>(hb + fc_bytes) : nullptr;
+        a.fcols_spare = reinterpret_cast<uint32_t *>(hb);
     }
     void *args[] = {&a, s->param_mechs ? static_cast<void *>(s->mech_table.get()) : static_cast<void *>(s->mech_table1.get())};
     cudaEvent_t t0 = nullptr;

@@ -213,7 +213,8 @@ __global__ void __launch_bounds__(kDedupInitWarps * 32) dedup_init_kernel(const 
 // Keys from the per-shot f words shot_kernel stored (f_width <= 64): key =
 // f & mask; thread = shot, the all-zero key by a compare, the rest through the
 // warp cache and the table.
-__global__ void __launch_bounds__(256) dedup_init_raw_kernel(const unsigned long long *__restrict__ fraw,
+template <typename FW>  // uint32_t (f_width <= 32) or unsigned long long
+__global__ void __launch_bounds__(256) dedup_init_raw_kernel(const FW *__restrict__ fraw,
                                                              unsigned long long f_mask, uint64_t shots,
                                                              unsigned long long *key, uint32_t *slot_out,
                                                              DedupTable table) {
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(256) dedup_init_raw_kernel(const unsigned long
     for (uint64_t s0 = uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); s0 < shots; s0 += stride) {
         const uint64_t s = s0 + lane;
         const bool valid = s < shots;
-        const unsigned long long k = valid ? (__ldg(fraw + s) & f_mask) : 0ull;
+        const unsigned long long k = valid ? ((unsigned long long)__ldg(fraw + s) & f_mask) : 0ull;
         uint32_t sl = slot0;
         if (__ballot_sync(kFull, k != 0ull)) {
             const uint32_t g = dedup_insert_warp(table, k, k != 0ull, lane, cache);

@@ -106,7 +106,9 @@ struct LaunchArgs {
     unsigned long long *err;       // [0] = flag, [1] = first failing shot
     uint32_t *heavy_fcols;         // f-columns for heavy_kernel: [f_width][heavy_ld32] (nullable)
     uint64_t heavy_ld32;
-    unsigned long long *heavy_fraw;  // per shot f word (f_width <= 64) for the deduplicated path's keys (nullable)
+    void *heavy_fraw;              // per shot f word (f_width <= 64) for the deduplicated path's keys (nullable):
+    uint32_t fraw_bytes;           // 4 (f_width <= 32) or 8 bytes per shot
+    uint32_t *fcols_spare;         // host bookkeeping: where the f columns go if a batch must be redone
     uint32_t debug_ar_components;  // profiling only (ZXS_DEBUG_AR_COMPONENTS): evaluate this many components
     const double *tab;             // tabulated chains (LightProg.tab), clamped ratios / NaN
     // probability mode (outcome_probability_given, sampler.cpp:324-356): the
@@ -433,10 +435,16 @@ __global__ void __maxnreg__(S == 4 ? ZXS_MAXNREG4 : ZXS_MAXNREG) shot_kernel(con
                 }
             }
             if constexpr (FW == 1) {
-                if (a.heavy_fraw) {  // lane = shot: coalesced 8-byte stores
+                if (a.heavy_fraw) {  // lane = shot: coalesced 4- or 8-byte stores
 #pragma unroll
                     for (int s = 0; s < S; s++) {
-                        if (local[s] < a.shots) a.heavy_fraw[local[s]] = f[s][0];
+                        if (local[s] < a.shots) {
+                            if (a.fraw_bytes == 4) {
+                                static_cast<uint32_t *>(a.heavy_fraw)[local[s]] = uint32_t(f[s][0]);
+                            } else {
+                                static_cast<unsigned long long *>(a.heavy_fraw)[local[s]] = f[s][0];
+                            }
+                        }
                     }
                 }
             }
@@ -577,6 +585,9 @@ __global__ void __maxnreg__(S == 4 ? ZXS_MAXNREG4 : ZXS_MAXNREG) shot_kernel(con
                 continue;
             }
             const uint32_t tb = m.comp_tensor_begin[ci];
+            // the light program holds the non-heavy components' tensors only: a heavy one
+            // evaluated here (probability mode) reads the global tensors
+            const bool lightc = light && !m.comp_heavy[ci];
             for (uint32_t p = lane; p < n; p += 32) {
 #pragma unroll
                 for (int s = 0; s < S; s++) cols[s * m.col_stride + m.f_width + p] = 0u;
@@ -584,7 +595,7 @@ __global__ void __maxnreg__(S == 4 ? ZXS_MAXNREG4 : ZXS_MAXNREG) shot_kernel(con
             __syncwarp();
             double2 acc[S];
             double prev[S], norm[S];
-            if (light) {
+            if (lightc) {
                 eval_tensor_light<S>(mt.prog, tb, cols, m.col_stride, lane, sh, acc);
             } else {
                 eval_tensor<S>(m, tb, cols, m.col_stride, lane, acc);
@@ -596,7 +607,7 @@ __global__ void __maxnreg__(S == 4 ? ZXS_MAXNREG4 : ZXS_MAXNREG) shot_kernel(con
                 if (a.forced && !pzero[s] && local[s] < a.shots && !(norm[s] > 0.0)) report_ratio_error(a.err, shot[s]);
             }
             for (uint32_t pos = 0; pos < n; pos++, upos++) {
-                if (light) {
+                if (lightc) {
                     eval_tensor_light<S>(mt.prog, tb + 1 + pos, cols, m.col_stride, lane, sh, acc);
                 } else {
                     eval_tensor<S>(m, tb + 1 + pos, cols, m.col_stride, lane, acc);

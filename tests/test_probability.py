@@ -94,7 +94,7 @@ def test_probability_of_matches_reference(name):
 
 
 @pytest.mark.parametrize("name", ["oracle_mix_1", "oracle_mix_2", "random_05", "random_16", "steane_inject",
-                                  "bell_m", "h_t_h_m"])
+                                  "steane_inject_shipped", "bell_m", "h_t_h_m"])
 def test_probability_of_fixtures(name):
     if not refdriver.available():
         pytest.skip("reference library not built")

@@ -72,6 +72,9 @@ def fixtures():
     F.append(("xerror_merge", 0, "X_ERROR(0.1) 0\nX_ERROR(0.2) 0\nM 0\nDETECTOR rec[-1]\n", small))
     F.append(("norm_sum", 1, "H 0\nT 0\nCNOT 0 1\nX_ERROR(0.2) 0\nZ_ERROR(0.1) 1\nM 0 1\n", small))
     F.append(("steane_inject", 0, C.steane_cultivation_proxy(0, 1e-3), small, True))  # cat5 plan: fixed front-end
+    # the same circuit through the front-end as shipped (cat5 defect: wrong marginals, still a
+    # sampler parity case; its heavy component exercises probability_of's global-tensor path)
+    F.append(("steane_inject_shipped", 0, C.steane_cultivation_proxy(0, 1e-3), small, False))
     # random circuits with magic (mixed component widths, R_Z/R_X, channels)
     import random
     rng = random.Random(20261017)

@@ -2051,14 +2051,24 @@ void launch_mono(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *f
 }
 
 // ---- deduplicated large-chi path (zxs_dedup.cuh)
-constexpr uint32_t kDedupRoundKeys = 65536;  // keys per eval round (partials: segments x round keys)
+constexpr uint32_t kDedupRoundKeys = 65536;  // fused chains: expanded keys per position (one round)
+// Segment partial sums of one evaluation round live in one buffer of at most this many bytes; a
+// tensor of G segments is evaluated in rounds of about budget / (8 G) keys, each round reading the
+// device key count (rounds past it exit at once), so no host round trip decides how many run.
+size_t dedup_partial_budget() {
+    size_t mb = 1024;
+    if (const char *e = std::getenv("ZXS_DEDUP_PARTIAL_MB")) mb = size_t(std::max(64L, std::atol(e)));
+    return mb << 20;
+}
 
 struct DedupBufs {
     unsigned long long *key;
     uint32_t *slot;
     double *prev, *value0, *value, *partial;
+    size_t partial_bytes;
     unsigned long long *counts;  // per output, added to the caller's counts when the chain completes
-    unsigned int *max_count;     // largest key count of the batch (sync-free path)
+    unsigned int *max_count;     // sync-free path: [0] largest key count of a position, [1] largest
+                                 // expanded key count of a fused chain
     unsigned long long *err;     // staged ratio-breakdown report of the sync-free path
     unsigned long long *xkeys;   // expanded keys of one chain position (fused chains)
     double *fvals[zxs_dev::kDedupMaxFused + 1];  // dense values per chain position (fused chains)
@@ -2085,8 +2095,11 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
     const size_t nout = std::max<uint32_t>(1, s->m.num_outputs);
     const size_t per_table = al(size_t(slots) * 8) + al(size_t(slots) * 4) + al(4) + al(size_t(max_ids) * 8) +
                              al(size_t(max_ids) * 4);
+    // partials: one round of the fused chain's expanded keys at least, else the budget (or all keys)
+    const size_t partial_bytes = std::max(size_t(max_segs) * kDedupRoundKeys * 8,
+                                          std::min(dedup_partial_budget(), size_t(max_segs) * max_ids * 8));
     const size_t bytes = al(cap * 8) + al(cap * 4) + al(cap * 8) + 2 * al(size_t(slots) * 8) +
-                         al(size_t(max_segs) * kDedupRoundKeys * 8) + al(nout * 8) + al(4) + al(24) + al(size_t(kDedupRoundKeys) * 8) +
+                         al(partial_bytes) + al(nout * 8) + al(4) + al(24) + al(size_t(kDedupRoundKeys) * 8) +
                          (zxs_dev::kDedupMaxFused + 1) * al(size_t(kDedupRoundKeys) * 8) + 2 * per_table;
     if (bytes > s->dd_buf_bytes || slots != s->dd_table_slots) {
         if (s->dd_buf) CK(cudaFree(s->dd_buf));
@@ -2105,9 +2118,10 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
     d.prev = reinterpret_cast<double *>(take(cap * 8));
     d.value0 = reinterpret_cast<double *>(take(size_t(slots) * 8));
     d.value = reinterpret_cast<double *>(take(size_t(slots) * 8));
-    d.partial = reinterpret_cast<double *>(take(size_t(max_segs) * kDedupRoundKeys * 8));
+    d.partial = reinterpret_cast<double *>(take(partial_bytes));
+    d.partial_bytes = partial_bytes;
     d.counts = reinterpret_cast<unsigned long long *>(take(nout * 8));
-    d.max_count = reinterpret_cast<unsigned int *>(take(4));
+    d.max_count = reinterpret_cast<unsigned int *>(take(8));
     d.err = reinterpret_cast<unsigned long long *>(take(24));
     d.xkeys = reinterpret_cast<unsigned long long *>(take(size_t(kDedupRoundKeys) * 8));
     for (uint32_t i = 0; i <= zxs_dev::kDedupMaxFused; i++) d.fvals[i] = reinterpret_cast<double *>(take(size_t(kDedupRoundKeys) * 8));
@@ -2145,8 +2159,8 @@ uint32_t dedup_count(zxs_sampler *s, const zxs_dev::DedupTable &t, cudaStream_t 
 // keys/uslot: the keys to contract and where their values go (value[uslot[k]], or value[k] when
 // uslot is null); n_dev/n_mult: n = min(*n_dev x n_mult, n) read on the device.
 void dedup_eval(zxs_sampler *s, uint32_t mt, const unsigned long long *keys, const uint32_t *uslot, uint32_t n,
-                double *value, double *partial, cudaStream_t st, const uint32_t *n_dev = nullptr, uint32_t n_mult = 1,
-                size_t value_slots = 0) {
+                double *value, double *partial, size_t partial_bytes, cudaStream_t st, const uint32_t *n_dev = nullptr,
+                uint32_t n_mult = 1, size_t value_slots = 0) {
     const uint32_t g0 = s->dd_tsb[mt], ng = s->dd_tsb[mt + 1] - g0;
     if (n == 0) return;
     if (ng == 0) {  // every term dead: the value is exactly 0 (for every slot)
@@ -2154,7 +2168,12 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const unsigned long long *keys, con
         return;
     }
     const zxs_dev::MonoArgs &m = s->mono;
-    for (uint32_t r0 = 0; r0 < n; r0 += kDedupRoundKeys) {
+    // keys per round: as many as the partial buffer holds for this tensor's segments (whole key groups)
+    const uint64_t fit = partial_bytes / (uint64_t(ng) * 8);
+    const uint32_t round = uint32_t(std::max<uint64_t>(zxs_dev::kDedupKeysPerWarp,
+                                                       std::min<uint64_t>(n, fit) / zxs_dev::kDedupKeysPerWarp *
+                                                           zxs_dev::kDedupKeysPerWarp));
+    for (uint32_t r0 = 0; r0 < n; r0 += round) {
         zxs_dev::DedupEvalArgs e{};
         e.words = s->dd_words;
         e.segs = s->dd_segs + g0;
@@ -2167,7 +2186,8 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const unsigned long long *keys, con
         e.n_planes = m.all_plane + 2;
         e.stack_depth = m.stack_depth;
         e.keys = keys + r0;
-        e.n_keys = std::min(kDedupRoundKeys, n - r0);
+        e.n_keys = std::min(round, n - r0);
+        e.key_base = r0;
         e.partial = partial;
         e.seg_buf_words = s->dd_seg_buf_words;
         e.table_bytes = s->dd_table_bytes;
@@ -2193,7 +2213,7 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const unsigned long long *keys, con
         s->time_end(3, st, t0);
         s->time_begin(4, st, t0);
         zxs_dev::dedup_reduce_kernel<<<std::min((e.n_keys + 127) / 128, uint32_t(s->sm_count) * 8), 128, 0, st>>>(
-            partial, ng, e.n_keys, n_dev, n_mult, uslot ? uslot + r0 : nullptr, value);
+            partial, ng, e.n_keys, n_dev, n_mult, r0, uslot ? uslot + r0 : nullptr, uslot ? value : value + r0);
         CK(cudaGetLastError());
         s->time_end(4, st, t0);
     }
@@ -2251,11 +2271,11 @@ void launch_dedup_sync(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint3
         s->time_end(4, st, t0);
         uint32_t n = dedup_count(s, d.table[0], st);
         if (n > d.table[0].max_ids) return fallback();
-        dedup_eval(s, cd.first_tensor, d.table[0].ukeys, d.table[0].uslot, n, d.value0, d.partial, st, nullptr, 1,
+        dedup_eval(s, cd.first_tensor, d.table[0].ukeys, d.table[0].uslot, n, d.value0, d.partial, d.partial_bytes, st, nullptr, 1,
                    d.table[0].mask + 1);
         for (uint32_t j = 0; j < cd.n_out; j++) {
             const zxs_dev::DedupTable &cur = d.table[j & 1], &nxt = d.table[(j + 1) & 1];
-            dedup_eval(s, cd.first_tensor + 1 + j, cur.ukeys, cur.uslot, n, d.value, d.partial, st, nullptr, 1,
+            dedup_eval(s, cd.first_tensor + 1 + j, cur.ukeys, cur.uslot, n, d.value, d.partial, d.partial_bytes, st, nullptr, 1,
                        cur.mask + 1);
             zxs_dev::DedupArArgs ra{};
             ra.seed = a.seed;
@@ -2336,17 +2356,18 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
     DedupBufs d = dedup_reserve(s, a.shots);
     const zxs_dev::MonoArgs &m = s->mono;
     const uint32_t nout = s->m.num_outputs;
-    const uint32_t limit = std::min(kDedupRoundKeys, d.table[0].max_ids);
+    const uint32_t limit = d.table[0].max_ids;                               // keys per position (rounds)
+    const uint32_t flimit = std::min(kDedupRoundKeys, d.table[0].max_ids);   // fused chains: expanded keys
     s->dd_dirty = true;  // until the chain completes
-    CK(cudaMemsetAsync(d.max_count, 0, 4, st));
+    CK(cudaMemsetAsync(d.max_count, 0, 8, st));
     if (a.counts) CK(cudaMemsetAsync(d.counts, 0, size_t(std::max<uint32_t>(nout, 1)) * 8, st));
     zxs_dev::dedup_err_init_kernel<<<1, 1, 0, st>>>(d.err);
     CK(cudaGetLastError());
     cudaEvent_t t0 = nullptr;
     const unsigned cgrid = unsigned(s->sm_count) * 2;
-    auto clear = [&](const zxs_dev::DedupTable &t, uint32_t mult = 1) {
+    auto clear = [&](const zxs_dev::DedupTable &t, uint32_t mult = 1, unsigned int *maxc = nullptr) {
         s->time_begin(4, st, t0);
-        zxs_dev::dedup_clear_dev_kernel<<<cgrid, 256, 0, st>>>(t, d.max_count, mult);
+        zxs_dev::dedup_clear_dev_kernel<<<cgrid, 256, 0, st>>>(t, maxc ? maxc : d.max_count, mult);
         CK(cudaGetLastError());
         s->time_end(4, st, t0);
         s->time_begin(4, st, t0);
@@ -2414,13 +2435,13 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
                 if (nb) {
                     s->time_begin(4, st, t0);
                     zxs_dev::dedup_expand_kernel<<<unsigned(s->sm_count) * 4, 256, 0, st>>>(
-                        d.table[0].ukeys, d.table[0].count, nb, relpos, limit, d.xkeys);
+                        d.table[0].ukeys, d.table[0].count, nb, relpos, flimit, d.xkeys);
                     CK(cudaGetLastError());
                     s->time_end(4, st, t0);
                     keys = d.xkeys;
                 }
-                dedup_eval(s, cd.first_tensor + pos, keys, nullptr, limit, d.fvals[pos], d.partial, st, d.table[0].count,
-                           1u << nb, limit);
+                dedup_eval(s, cd.first_tensor + pos, keys, nullptr, flimit, d.fvals[pos], d.partial, d.partial_bytes, st,
+                           d.table[0].count, 1u << nb, flimit);
             }
             zxs_dev::DedupFusedArgs fa{};
             fa.seed = a.seed;
@@ -2434,7 +2455,7 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
             fa.slot = d.slot;
             fa.ids = d.table[0].ids;
             for (uint32_t pos = 0; pos <= cd.n_out; pos++) fa.value[pos] = d.fvals[pos];
-            fa.value_cap = limit;
+            fa.value_cap = flimit;
             fa.out32 = a.out32;
             fa.out_ld32 = a.ld32;
             fa.counts = a.counts ? d.counts : nullptr;
@@ -2450,14 +2471,14 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
             CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_fused_ar_kernel), dim3(fgrid), dim3(256),
                                 fargs, 0, st));
             s->time_end(4, st, t0);
-            clear(d.table[0], 1u << nb_of(cd.n_out));
+            clear(d.table[0], 1u << nb_of(cd.n_out), d.max_count + 1);
             continue;
         }
-        dedup_eval(s, cd.first_tensor, d.table[0].ukeys, d.table[0].uslot, limit, d.value0, d.partial, st,
+        dedup_eval(s, cd.first_tensor, d.table[0].ukeys, d.table[0].uslot, limit, d.value0, d.partial, d.partial_bytes, st,
                    d.table[0].count, 1, d.table[0].mask + 1);
         for (uint32_t j = 0; j < cd.n_out; j++) {
             const zxs_dev::DedupTable &cur = d.table[j & 1], &nxt = d.table[(j + 1) & 1];
-            dedup_eval(s, cd.first_tensor + 1 + j, cur.ukeys, cur.uslot, limit, d.value, d.partial, st, cur.count, 1,
+            dedup_eval(s, cd.first_tensor + 1 + j, cur.ukeys, cur.uslot, limit, d.value, d.partial, d.partial_bytes, st, cur.count, 1,
                        cur.mask + 1);
             zxs_dev::DedupArArgs ra{};
             ra.seed = a.seed;
@@ -2495,9 +2516,9 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
         }
         if (cd.n_out == 0) clear(d.table[0]);
     }
-    CK(cudaMemcpyAsync(s->dd_pinned, d.max_count, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(s->dd_pinned, d.max_count, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (s->dd_pinned[0] > limit) {  // more keys than one round (or the tables) hold: redo synchronously
+    if (s->dd_pinned[0] > limit || s->dd_pinned[1] > flimit) {  // more keys than the tables hold: redo synchronously
         s->dd_dirty = true;
         s->dd_stats[0] -= 1;
         if (!fcols) fcols = regen_fcols(s, a, st);

@@ -254,6 +254,7 @@ struct DedupEvalArgs {
     uint32_t n_keys;                  // keys (n_dev: at most this many, the rest read from n_dev)
     const uint32_t *n_dev;            // device-side key count (the table's), or null
     uint32_t n_mult;                  // keys = *n_dev x n_mult (expanded keys: base key x sampled-bit pattern)
+    uint32_t key_base;                // first key of this round (keys / partials are relative to it)
     unsigned long long *stats;        // device counters {keys, plane-load bytes} (nullable)
     unsigned long long tensor_loads;  // plane loads per 32-key word of this tensor
     double *partial;                  // [keys][n_segs]
@@ -361,7 +362,11 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
         for (uint32_t i = threadIdx.x; i < h.n_dict; i += blockDim.x) sd[i] = __ldg(h.dict + i);
     }
     uint32_t cur_blk = 0xffffffffu;
-    const uint32_t n_keys = h.n_dev ? uint32_t(min(uint64_t(*h.n_dev) * max(h.n_mult, 1u), uint64_t(h.n_keys))) : h.n_keys;
+    // keys of this round: the device count (minus the earlier rounds' keys), at most n_keys
+    const uint64_t dev_keys = h.n_dev ? uint64_t(*h.n_dev) * max(h.n_mult, 1u) : 0;
+    const uint32_t n_keys = h.n_dev ? uint32_t(min(dev_keys > h.key_base ? dev_keys - h.key_base : uint64_t(0), uint64_t(h.n_keys)))
+                                    : h.n_keys;
+    if (n_keys == 0) return;  // a round past the batch's key count
     if (h.stats && blockIdx.x == 0 && threadIdx.x == 0) {
         atomicAdd(&h.stats[0], (unsigned long long)n_keys);
         atomicAdd(&h.stats[1], h.tensor_loads * ((n_keys + 31) / 32) * 4);
@@ -463,9 +468,11 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
 // streams its own row of segment sums (16 B loads, eight in flight) and adds
 // them in order.
 __global__ void dedup_reduce_kernel(const double *__restrict__ partial, uint32_t n_segs, uint32_t max_keys,
-                                    const uint32_t *n_dev, uint32_t n_mult, const uint32_t *__restrict__ uslot,
-                                    double *__restrict__ value) {
-    const uint32_t n_keys = n_dev ? uint32_t(min(uint64_t(*n_dev) * max(n_mult, 1u), uint64_t(max_keys))) : max_keys;
+                                    const uint32_t *n_dev, uint32_t n_mult, uint32_t key_base,
+                                    const uint32_t *__restrict__ uslot, double *__restrict__ value) {
+    const uint64_t dev_keys = n_dev ? uint64_t(*n_dev) * max(n_mult, 1u) : 0;
+    const uint32_t n_keys = n_dev ? uint32_t(min(dev_keys > key_base ? dev_keys - key_base : uint64_t(0), uint64_t(max_keys)))
+                                  : max_keys;
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n_keys; k += gridDim.x * blockDim.x) {
         const double *row = partial + uint64_t(k) * n_segs;
         double v = 0.0;

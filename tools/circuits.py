@@ -232,7 +232,8 @@ def steane_cultivation_proxy(checks: int, p: float) -> str:
     return "\n".join(lines) + "\n"
 
 
-def cultivation_d3(p: float, checks: int = 2, z_rounds: bool = True, round0: bool = True) -> str:
+def cultivation_d3(p: float, checks: int = 2, z_rounds: bool = True, round0: bool = True,
+                   readout: str = "decode") -> str:
     """d=3 magic-state cultivation on the Steane colour code (the structure of
     Gidney, Shutty & Jones 2024, reconstructed offline) with circuit-level
     noise on every gate, reset and measurement:
@@ -246,9 +247,12 @@ def cultivation_d3(p: float, checks: int = 2, z_rounds: bool = True, round0: boo
        they are measured inside the check frame); the transversal logical X
        measured through a fan-out from the ancilla (RX anc, CX anc->q x 7,
        MX anc, detector); T_DAG on all data.
-    4. Readout: the inverse encoder (noisy), M of qubits 4 5 6 and MX of
-       qubits 3 1 0 (decoded stabilisers: detectors), T_DAG on qubit 2 and MX
-       (the logical T-basis readout: the observable).
+    4. Readout ("decode"): the inverse encoder (noisy), M of qubits 4 5 6 and
+       MX of qubits 3 1 0 (decoded stabilisers: detectors), T_DAG on qubit 2
+       and MX (the logical T-basis readout: the observable). Readout "frame":
+       T on all data and MX of all data, observable = XOR of the 7 (the H_XY
+       value read in the check frame); the reference's simplifier then fuses
+       the last check's T_DAG with that T, leaving chi = 432.
 
     Noise (p each): X_ERROR after R / Z_ERROR after RX, X_ERROR before M /
     Z_ERROR before MX, DEPOLARIZE2 after every CX, DEPOLARIZE1 on every T /
@@ -332,6 +336,12 @@ def cultivation_d3(p: float, checks: int = 2, z_rounds: bool = True, round0: boo
         meas("MX", anc, ("c", c))
         det([("c", c)])
         gate1("T_DAG", D, noise_before=True)
+    if readout == "frame":
+        gate1("T", D)
+        for q in D:
+            meas("MX", q, ("d", q))
+        L.append("OBSERVABLE_INCLUDE(0) " + " ".join(f"rec[{rec[('d', q)] - nm[0]}]" for q in D))
+        return "\n".join(L) + "\n"
     for a, b in reversed(STEANE_ENCODER):
         cx(a, b)
     for q in (4, 5, 6):

@@ -75,6 +75,9 @@ def fixtures():
     # the same circuit through the front-end as shipped (cat5 defect: wrong marginals, still a
     # sampler parity case; its heavy component exercises probability_of's global-tensor path)
     F.append(("steane_inject_shipped", 0, C.steane_cultivation_proxy(0, 1e-3), small, False))
+    # config 3 with the check-frame readout (chi = 432, chain of 9, circuit-level noise): the
+    # cultivation structure at a size the reference samples in seconds
+    F.append(("c3_cultivation_d3_frame", 0, C.cultivation_d3(1e-3, readout="frame"), big[:4], True))
     # random circuits with magic (mixed component widths, R_Z/R_X, channels)
     import random
     rng = random.Random(20261017)

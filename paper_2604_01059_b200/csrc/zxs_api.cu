@@ -182,7 +182,7 @@ struct zxs_sampler {
     std::vector<uint32_t> dd_tfb;    // per mono tensor: first block form table (~0: dictionary ids)
     uint32_t dd_table_bytes = 0;
     bool dd_stage_entries = false;
-    int dd_init_occ = 1, dd_ar_occ = 1, dd_fused_occ = 1, dd_raw_occ = 1;  // resident blocks per SM (per-shot dedup kernels)
+    int dd_init_occ = 1, dd_ar_occ = 1, dd_fused_occ = 1, dd_raw_occ = 1, dd_node_occ = 1;  // resident blocks per SM (per-shot dedup kernels)
     bool dd_async = true;                 // key counts stay on the device (ZXS_DEDUP_SYNC=1: host round trips)
     bool dd_fused = true;                 // short chains in one per-shot kernel (ZXS_DEDUP_FUSED=0: step by step)
     unsigned long long *dd_dev_stats = nullptr;  // {keys, plane-load bytes} accumulated by dedup_eval_kernel
@@ -2000,6 +2000,8 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &s->dd_ar_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_ar_kernel), 256, 0));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &s->dd_node_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_node_pass_kernel), 256, 0));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &s->dd_fused_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_fused_ar_kernel), 256, 0));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &s->dd_raw_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_init_raw_kernel<unsigned long long>), 256, 0));
@@ -2072,7 +2074,10 @@ struct DedupBufs {
     unsigned long long *err;     // staged ratio-breakdown report of the sync-free path
     unsigned long long *xkeys;   // expanded keys of one chain position (fused chains)
     double *fvals[zxs_dev::kDedupMaxFused + 1];  // dense values per chain position (fused chains)
-    zxs_dev::DedupTable table[2];
+    // [0] base keys (= level-0 nodes), [1], [2] node tables of the later levels (alternating),
+    // [3] the level's node keys (node levels); the step-by-step sync path uses [0], [1]
+    zxs_dev::DedupTable table[4];
+    zxs_dev::DedupNodeArrays nodes[2];  // node levels: per node key, prev, cur, key slot, decision
 };
 
 // Distinct keys per chain position the tables hold (ZXS_DEDUP_MAX_KEYS, default
@@ -2100,7 +2105,9 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
                                           std::min(dedup_partial_budget(), size_t(max_segs) * max_ids * 8));
     const size_t bytes = al(cap * 8) + al(cap * 4) + al(cap * 8) + 2 * al(size_t(slots) * 8) +
                          al(partial_bytes) + al(nout * 8) + al(4) + al(24) + al(size_t(kDedupRoundKeys) * 8) +
-                         (zxs_dev::kDedupMaxFused + 1) * al(size_t(kDedupRoundKeys) * 8) + 2 * per_table;
+                         (zxs_dev::kDedupMaxFused + 1) * al(size_t(kDedupRoundKeys) * 8) + 4 * per_table +
+                         2 * (3 * al(size_t(max_ids) * 8) + al(size_t(max_ids) * 4) +
+                              al(size_t(max_ids) * sizeof(zxs_dev::DedupNodeRec)));
     if (bytes > s->dd_buf_bytes || slots != s->dd_table_slots) {
         if (s->dd_buf) CK(cudaFree(s->dd_buf));
         s->dd_buf = nullptr;
@@ -2125,7 +2132,7 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
     d.err = reinterpret_cast<unsigned long long *>(take(24));
     d.xkeys = reinterpret_cast<unsigned long long *>(take(size_t(kDedupRoundKeys) * 8));
     for (uint32_t i = 0; i <= zxs_dev::kDedupMaxFused; i++) d.fvals[i] = reinterpret_cast<double *>(take(size_t(kDedupRoundKeys) * 8));
-    for (int i = 0; i < 2; i++) {
+    for (int i = 0; i < 4; i++) {
         zxs_dev::DedupTable &t = d.table[i];
         t.keys = reinterpret_cast<unsigned long long *>(take(size_t(slots) * 8));
         t.ids = reinterpret_cast<uint32_t *>(take(size_t(slots) * 4));
@@ -2135,8 +2142,16 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
         t.ukeys = reinterpret_cast<unsigned long long *>(take(size_t(max_ids) * 8));
         t.uslot = reinterpret_cast<uint32_t *>(take(size_t(max_ids) * 4));
     }
+    for (int i = 0; i < 2; i++) {
+        zxs_dev::DedupNodeArrays &na = d.nodes[i];
+        na.key = reinterpret_cast<unsigned long long *>(take(size_t(max_ids) * 8));
+        na.prev = reinterpret_cast<double *>(take(size_t(max_ids) * 8));
+        na.cur = reinterpret_cast<double *>(take(size_t(max_ids) * 8));
+        na.kslot = reinterpret_cast<uint32_t *>(take(size_t(max_ids) * 4));
+        na.rec = reinterpret_cast<zxs_dev::DedupNodeRec *>(take(size_t(max_ids) * sizeof(zxs_dev::DedupNodeRec)));
+    }
     if (s->dd_dirty) {
-        for (int i = 0; i < 2; i++) {
+        for (int i = 0; i < 4; i++) {
             CK(cudaMemset(d.table[i].keys, 0xff, size_t(slots) * 8));
             CK(cudaMemset(d.table[i].ids, 0, size_t(slots) * 4));  // ids stay in range (dedup_insert)
             CK(cudaMemset(d.table[i].count, 0, 4));
@@ -2474,13 +2489,41 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
             clear(d.table[0], 1u << nb_of(cd.n_out), d.max_count + 1);
             continue;
         }
+        // ---- node levels (zxs_dedup.cuh): level 0's nodes are the base keys
         dedup_eval(s, cd.first_tensor, d.table[0].ukeys, d.table[0].uslot, limit, d.value0, d.partial, d.partial_bytes, st,
                    d.table[0].count, 1, d.table[0].mask + 1);
+        if (cd.n_out == 0) {
+            clear(d.table[0]);
+            continue;
+        }
+        dedup_eval(s, cd.first_tensor + 1, d.table[0].ukeys, d.table[0].uslot, limit, d.value, d.partial, d.partial_bytes,
+                   st, d.table[0].count, 1, d.table[0].mask + 1);
+        const unsigned ngrid = unsigned(s->sm_count) * 4;
+        s->time_begin(4, st, t0);
+        zxs_dev::dedup_node_level0_kernel<<<ngrid, 256, 0, st>>>(d.table[0], d.value0, d.value, d.nodes[0]);
+        CK(cudaGetLastError());
+        s->time_end(4, st, t0);
+        auto node_table = [&](uint32_t j) -> const zxs_dev::DedupTable & { return j == 0 ? d.table[0] : d.table[1 + ((j - 1) & 1)]; };
         for (uint32_t j = 0; j < cd.n_out; j++) {
-            const zxs_dev::DedupTable &cur = d.table[j & 1], &nxt = d.table[(j + 1) & 1];
-            dedup_eval(s, cd.first_tensor + 1 + j, cur.ukeys, cur.uslot, limit, d.value, d.partial, d.partial_bytes, st, cur.count, 1,
-                       cur.mask + 1);
-            zxs_dev::DedupArArgs ra{};
+            const zxs_dev::DedupTable &cur = node_table(j);
+            const zxs_dev::DedupNodeArrays &na = d.nodes[j & 1];
+            if (j > 0) {
+                // the bit sampled at position j - 1 enters the key when a later tensor reads it
+                const uint32_t p = cd.nf + j - 1;
+                const uint32_t bit_pos = (p < 63 && ((s->dd_key_mask[hc] >> p) & 1ull)) ? p : 64u;
+                s->time_begin(4, st, t0);
+                zxs_dev::dedup_node_prep_kernel<<<ngrid, 256, 0, st>>>(cur, d.nodes[(j - 1) & 1], na, bit_pos, d.table[3]);
+                CK(cudaGetLastError());
+                s->time_end(4, st, t0);
+                dedup_eval(s, cd.first_tensor + 1 + j, d.table[3].ukeys, d.table[3].uslot, limit, d.value, d.partial,
+                           d.partial_bytes, st, d.table[3].count, 1, d.table[3].mask + 1);
+                s->time_begin(4, st, t0);
+                zxs_dev::dedup_node_decide_kernel<<<ngrid, 256, 0, st>>>(cur.count, cur.max_ids, d.value, na);
+                CK(cudaGetLastError());
+                s->time_end(4, st, t0);
+                clear(d.table[3]);
+            }
+            zxs_dev::DedupNodePassArgs ra{};
             ra.seed = a.seed;
             ra.first_shot = a.first_shot;
             ra.shots = a.shots;
@@ -2488,16 +2531,11 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
             ra.ci = cd.ci;
             ra.j = j;
             ra.out = s->comp_outputs[cd.out_begin + j];
-            ra.f_width = cd.nf;  // the key's sampled bits follow the local f parameters
-            ra.key_mask = s->dd_key_mask[hc];
-            ra.key = d.key;
             ra.slot = d.slot;
-            ra.prev = d.prev;
-            ra.value0 = d.value0;
-            ra.value = d.value;
             ra.cur = cur;
-            ra.next = nxt;
+            ra.next = node_table(j + 1);
             ra.insert_next = j + 1 < cd.n_out;
+            ra.rec = na.rec;
             ra.out32 = a.out32;
             ra.out_ld32 = a.ld32;
             ra.counts = a.counts ? d.counts : nullptr;
@@ -2507,14 +2545,14 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
             ra.err = d.err;
             s->time_begin(4, st, t0);
             void *rargs[] = {&ra};
-            const unsigned agrid =
-                unsigned(std::min<uint64_t>((a.shots + 256 * zxs_dev::kDedupArGroups - 1) / (256 * zxs_dev::kDedupArGroups), uint64_t(s->sm_count) * std::max(1, s->dd_ar_occ)));
-            CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_ar_kernel), dim3(agrid), dim3(256), rargs,
-                                0, st));
+            const unsigned agrid = unsigned(std::min<uint64_t>(
+                (a.shots + 256 * zxs_dev::kNodePassG - 1) / (256 * zxs_dev::kNodePassG),
+                uint64_t(s->sm_count) * std::max(1, s->dd_node_occ)));
+            CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_node_pass_kernel), dim3(agrid), dim3(256),
+                                rargs, 0, st));
             s->time_end(4, st, t0);
             clear(cur);
         }
-        if (cd.n_out == 0) clear(d.table[0]);
     }
     CK(cudaMemcpyAsync(s->dd_pinned, d.max_count, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

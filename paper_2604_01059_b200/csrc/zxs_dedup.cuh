@@ -668,6 +668,216 @@ __global__ void __launch_bounds__(256) dedup_ar_kernel(const __grid_constant__ D
     if (a.counts && lane == 0 && ones) atomicAdd(&a.counts[a.out], ones);
 }
 
+// ---- node levels (longer chains, the default when a chain is not fused).
+// A shot's state before position j is a NODE: its key (base key plus the
+// sampled bits the later tensors read) and its prev marginal; both are
+// functions of (base key, bits sampled so far), so they live per node, not
+// per shot. Per level: distinct node keys are contracted (dedup_eval), each
+// node's decision record is derived once (dedup_node_decide_kernel: the
+// IEEE ratio, its clamp, the reference's error test, and the integer draw
+// threshold T = ceil(cl 2^53): u = k 2^-53 < cl  <=>  k < T), and one
+// per-shot pass (dedup_node_pass_kernel) reads the shot's node slot, draws,
+// compares k >= T, and inserts the child node (parent id << 1 | bit) for
+// the next level: 4 B read + 4 B written per shot per position (the
+// step-by-step dedup_ar_kernel moves slot, key and prev per shot).
+struct DedupNodeRec {
+    unsigned long long T;       // bit = (k >= T); bit 63: ratio outside (-1e-6, 1 + 1e-6)
+    unsigned long long tie_lo;  // near-tie draws: k in [tie_lo, tie_hi]
+    unsigned long long tie_hi;
+    double cl;                  // clamped ratio (injected-uniform mode)
+};
+constexpr unsigned long long kNodeErr = 1ull << 63;
+
+struct DedupNodeArrays {
+    unsigned long long *key;  // [node] key (local parameter bits)
+    double *prev;             // [node] prev marginal
+    double *cur;              // [node] this level's marginal
+    uint32_t *kslot;          // [node] slot of the key in the level's key table
+    DedupNodeRec *rec;        // [node]
+};
+
+__device__ __forceinline__ DedupNodeRec node_rec(double cur, double pv) {
+    // sampler.cpp:84-99, per node: the same division, test and clamp as per shot
+    const double ratio = __ddiv_rn(cur, pv);
+    const bool err = !(ratio > -1e-6 && ratio < 1.0 + 1e-6);
+    double cl = (0.0 < ratio) ? ratio : 0.0;
+    cl = (cl < 1.0) ? cl : 1.0;
+    DedupNodeRec r;
+    r.cl = cl;
+    r.T = (unsigned long long)ceil(cl * 0x1.0p53) | (err ? kNodeErr : 0ull);  // cl 2^53 is exact
+    const double w = 1e-9 * fmax(cl, 1e-300);
+    const double lo = fmax(cl - w, 0.0) * 0x1.0p53, hi = fmin(cl + w, 1.0) * 0x1.0p53;
+    r.tie_lo = (unsigned long long)ceil(lo);
+    r.tie_hi = (unsigned long long)floor(hi);
+    return r;
+}
+
+// Level 0: the nodes are the base keys (table ids), already contracted for the
+// normalization (value0) and the first marginal (value), both by table slot.
+__global__ void dedup_node_level0_kernel(DedupTable t, const double *__restrict__ value0, const double *__restrict__ value,
+                                         DedupNodeArrays na) {
+    const uint32_t n = min(*t.count, t.max_ids);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t sl = t.uslot[i];
+        const double pv = value0[sl], cur = value[sl];
+        na.key[i] = t.ukeys[i];
+        na.prev[i] = pv;
+        na.cur[i] = cur;
+        na.kslot[i] = sl;
+        na.rec[i] = node_rec(cur, pv);
+    }
+}
+
+// Level j + 1's nodes (table entries parent << 1 | bit): key and prev from the
+// parent (prev = bit ? prev - cur : cur, sampler.cpp:95-98), the key extended
+// by the bit when a later tensor reads it (bit_pos < 64), inserted into the
+// level's key table.
+__global__ void dedup_node_prep_kernel(DedupTable nodes, DedupNodeArrays parent, DedupNodeArrays na, uint32_t bit_pos,
+                                       DedupTable keys) {
+    const uint32_t n = min(*nodes.count, nodes.max_ids);
+    const uint32_t lane = threadIdx.x & 31u;
+    DedupWarpCache cache;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < n; i0 += stride) {
+        const uint32_t i = i0 + lane;
+        const bool valid = i < n;
+        unsigned long long key = 0;
+        if (valid) {
+            const unsigned long long e = nodes.ukeys[i];
+            const uint32_t p = uint32_t(e >> 1), bit = uint32_t(e & 1);
+            const double pv = parent.prev[p], cur = parent.cur[p];
+            key = parent.key[p] | ((bit && bit_pos < 64) ? (1ull << bit_pos) : 0ull);
+            na.key[i] = key;
+            na.prev[i] = bit ? __dsub_rn(pv, cur) : cur;
+        }
+        const uint32_t ks = dedup_insert_warp(keys, key, valid, lane, cache);
+        if (valid) na.kslot[i] = ks;
+    }
+}
+
+// Decision records once the level's keys are contracted (values by key slot).
+__global__ void dedup_node_decide_kernel(const uint32_t *count, uint32_t max_ids, const double *__restrict__ value,
+                                         DedupNodeArrays na) {
+    const uint32_t n = min(*count, max_ids);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double cur = value[na.kslot[i]];
+        na.cur[i] = cur;
+        na.rec[i] = node_rec(cur, na.prev[i]);
+    }
+}
+
+struct DedupNodePassArgs {
+    uint64_t seed, first_shot, shots;
+    uint32_t k0_round[10];
+    uint32_t ci, j, out;
+    uint32_t *slot;             // [shots] slot in `cur` (replaced by the slot in `next`)
+    DedupTable cur, next;
+    bool insert_next;
+    const DedupNodeRec *rec;
+    uint32_t *out32;
+    uint64_t out_ld32;
+    unsigned long long *counts;
+    const double *uniforms;
+    uint64_t uniforms_ld, upos;
+    unsigned long long *err;
+};
+
+// One position for every shot: lane = shots s + 32 g (G groups per warp
+// iteration, packed into 64/128-bit output stores by lane 0).
+constexpr int kNodePassG = 4;
+__global__ void __launch_bounds__(256) dedup_node_pass_kernel(const __grid_constant__ DedupNodePassArgs a) {
+    constexpr int G = kNodePassG;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t seed_hi = uint32_t(a.seed >> 32);
+    const uint32_t k2c = uint32_t(kP1c) ^ a.k0_round[1];
+    const uint32_t stream = 0x80000000u ^ (a.ci << 12) ^ a.j;  // sampler.cpp:37-39
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * G;
+    unsigned long long ones = 0;
+    DedupWarpCache cache;
+    const uint64_t shots64 = (a.shots + 63) & ~uint64_t(63);
+    for (uint64_t s0 = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * G; s0 < shots64; s0 += stride) {
+        uint64_t s[G];
+        bool valid[G], bit[G];
+        uint32_t node[G];
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            s[g] = s0 + 32 * g + lane;
+            valid[g] = s[g] < a.shots;
+            node[g] = valid[g] ? __ldg(a.cur.ids + __ldg(a.slot + s[g])) : 0u;
+        }
+        DedupNodeRec r[G];
+        bool need = false;  // a draw is needed unless every node's bit is certain (T = 0 or 2^53, no error)
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            r[g] = a.rec[node[g]];
+            const unsigned long long T = r[g].T & ~kNodeErr;
+            need |= valid[g] && ((r[g].T & kNodeErr) || (T != 0ull && T != (1ull << 53)));
+        }
+        unsigned long long k[G];
+        if (a.uniforms) {
+#pragma unroll
+            for (int g = 0; g < G; g++) k[g] = 0;
+        } else if (__any_sync(kFull, need)) {
+            PhiloxPre pre[G];
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+                const uint64_t shot = a.first_shot + s[g];
+                pre[g] = philox_pre(uint32_t(shot), uint32_t(shot >> 32), a.k0_round[0]);
+            }
+            uint32_t rhi[G], rlo[G];
+            philox_tail<G>(pre, seed_hi ^ stream, a.k0_round, k2c, a.k0_round[9], rhi, rlo);
+#pragma unroll
+            for (int g = 0; g < G; g++) k[g] = ((uint64_t(rhi[g]) << 32) | rlo[g]) >> 11;  // uniform_at = k 2^-53
+        } else {
+#pragma unroll
+            for (int g = 0; g < G; g++) k[g] = 0;  // unused: every T is 0 or 2^53
+        }
+        uint32_t word[G];
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            bit[g] = false;
+            if (valid[g]) {
+                const unsigned long long T = r[g].T & ~kNodeErr;
+                if (a.uniforms) {
+                    const double u = a.uniforms[a.upos * a.uniforms_ld + s[g]];
+                    bit[g] = !(u < r[g].cl);
+                    if (fabs(u - r[g].cl) <= 1e-9 * fmax(r[g].cl, 1e-300)) atomicAdd(&a.err[2], 1ull);
+                } else {
+                    bit[g] = k[g] >= T;
+                    if (T != 0ull && T != (1ull << 53) && k[g] >= r[g].tie_lo && k[g] <= r[g].tie_hi) atomicAdd(&a.err[2], 1ull);
+                }
+                if (r[g].T & kNodeErr) report_ratio_error(a.err, a.first_shot + s[g]);
+            }
+            word[g] = __ballot_sync(kFull, bit[g]);
+        }
+        if (lane == 0) {
+            const uint64_t w0 = s0 >> 5;
+            if (a.out32) {
+                uint32_t *row = a.out32 + a.out * a.out_ld32;
+                if (w0 + G <= a.out_ld32 && (reinterpret_cast<uintptr_t>(row + w0) & 15) == 0) {
+                    *reinterpret_cast<uint4 *>(row + w0) = make_uint4(word[0], word[1], word[2], word[3]);
+                } else {
+#pragma unroll
+                    for (int g = 0; g < G; g++) {
+                        if (w0 + g < a.out_ld32) row[w0 + g] = word[g];
+                    }
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < G; g++) ones += __popc(word[g]);
+        }
+        if (a.insert_next) {
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+                const unsigned long long e = (unsigned long long)node[g] << 1 | (bit[g] ? 1ull : 0ull);
+                const uint32_t ns = dedup_insert_warp(a.next, e, valid[g], lane, cache);
+                if (valid[g]) a.slot[s[g]] = ns;
+            }
+        }
+    }
+    if (a.counts && lane == 0 && ones) atomicAdd(&a.counts[a.out], ones);
+}
+
 // ---- fused chain (short chains): every position's keys are the base keys
 // (f bits) times the patterns of the sampled bits the tensor reads, so all
 // tensors are contracted before any draw and one per-shot kernel runs the

@@ -2106,8 +2106,8 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
     const size_t bytes = al(cap * 8) + al(cap * 4) + al(cap * 8) + 2 * al(size_t(slots) * 8) +
                          al(partial_bytes) + al(nout * 8) + al(4) + al(24) + al(size_t(kDedupRoundKeys) * 8) +
                          (zxs_dev::kDedupMaxFused + 1) * al(size_t(kDedupRoundKeys) * 8) + 4 * per_table +
-                         2 * (3 * al(size_t(max_ids) * 8) + al(size_t(max_ids) * 4) +
-                              al(size_t(max_ids) * sizeof(zxs_dev::DedupNodeRec)));
+                         2 * (3 * al(size_t(slots) * 8) + al(size_t(slots) * 4) +
+                              al(size_t(slots) * sizeof(zxs_dev::DedupNodeRec)));
     if (bytes > s->dd_buf_bytes || slots != s->dd_table_slots) {
         if (s->dd_buf) CK(cudaFree(s->dd_buf));
         s->dd_buf = nullptr;
@@ -2144,11 +2144,11 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
     }
     for (int i = 0; i < 2; i++) {
         zxs_dev::DedupNodeArrays &na = d.nodes[i];
-        na.key = reinterpret_cast<unsigned long long *>(take(size_t(max_ids) * 8));
-        na.prev = reinterpret_cast<double *>(take(size_t(max_ids) * 8));
-        na.cur = reinterpret_cast<double *>(take(size_t(max_ids) * 8));
-        na.kslot = reinterpret_cast<uint32_t *>(take(size_t(max_ids) * 4));
-        na.rec = reinterpret_cast<zxs_dev::DedupNodeRec *>(take(size_t(max_ids) * sizeof(zxs_dev::DedupNodeRec)));
+        na.key = reinterpret_cast<unsigned long long *>(take(size_t(slots) * 8));
+        na.prev = reinterpret_cast<double *>(take(size_t(slots) * 8));
+        na.cur = reinterpret_cast<double *>(take(size_t(slots) * 8));
+        na.kslot = reinterpret_cast<uint32_t *>(take(size_t(slots) * 4));
+        na.rec = reinterpret_cast<zxs_dev::DedupNodeRec *>(take(size_t(slots) * sizeof(zxs_dev::DedupNodeRec)));
     }
     if (s->dd_dirty) {
         for (int i = 0; i < 4; i++) {
@@ -2518,7 +2518,7 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
                 dedup_eval(s, cd.first_tensor + 1 + j, d.table[3].ukeys, d.table[3].uslot, limit, d.value, d.partial,
                            d.partial_bytes, st, d.table[3].count, 1, d.table[3].mask + 1);
                 s->time_begin(4, st, t0);
-                zxs_dev::dedup_node_decide_kernel<<<ngrid, 256, 0, st>>>(cur.count, cur.max_ids, d.value, na);
+                zxs_dev::dedup_node_decide_kernel<<<ngrid, 256, 0, st>>>(cur, d.value, na);
                 CK(cudaGetLastError());
                 s->time_end(4, st, t0);
                 clear(d.table[3]);

@@ -677,7 +677,7 @@ __global__ void __launch_bounds__(256) dedup_ar_kernel(const __grid_constant__ D
 // IEEE ratio, its clamp, the reference's error test, and the integer draw
 // threshold T = ceil(cl 2^53): u = k 2^-53 < cl  <=>  k < T), and one
 // per-shot pass (dedup_node_pass_kernel) reads the shot's node slot, draws,
-// compares k >= T, and inserts the child node (parent id << 1 | bit) for
+// compares k >= T, and inserts the child node (parent slot << 1 | bit) for
 // the next level: 4 B read + 4 B written per shot per position (the
 // step-by-step dedup_ar_kernel moves slot, key and prev per shot).
 struct DedupNodeRec {
@@ -689,11 +689,12 @@ struct DedupNodeRec {
 constexpr unsigned long long kNodeErr = 1ull << 63;
 
 struct DedupNodeArrays {
-    unsigned long long *key;  // [node] key (local parameter bits)
-    double *prev;             // [node] prev marginal
-    double *cur;              // [node] this level's marginal
-    uint32_t *kslot;          // [node] slot of the key in the level's key table
-    DedupNodeRec *rec;        // [node]
+    // indexed by the node's slot in its level's node table
+    unsigned long long *key;  // key (local parameter bits)
+    double *prev;             // prev marginal
+    double *cur;              // this level's marginal
+    uint32_t *kslot;          // slot of the key in the level's key table
+    DedupNodeRec *rec;
 };
 
 __device__ __forceinline__ DedupNodeRec node_rec(double cur, double pv) {
@@ -718,13 +719,13 @@ __global__ void dedup_node_level0_kernel(DedupTable t, const double *__restrict_
                                          DedupNodeArrays na) {
     const uint32_t n = min(*t.count, t.max_ids);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t sl = t.uslot[i];
+        const uint32_t sl = t.uslot[i];  // node arrays are indexed by table slot
         const double pv = value0[sl], cur = value[sl];
-        na.key[i] = t.ukeys[i];
-        na.prev[i] = pv;
-        na.cur[i] = cur;
-        na.kslot[i] = sl;
-        na.rec[i] = node_rec(cur, pv);
+        na.key[sl] = t.ukeys[i];
+        na.prev[sl] = pv;
+        na.cur[sl] = cur;
+        na.kslot[sl] = sl;
+        na.rec[sl] = node_rec(cur, pv);
     }
 }
 
@@ -742,27 +743,29 @@ __global__ void dedup_node_prep_kernel(DedupTable nodes, DedupNodeArrays parent,
         const uint32_t i = i0 + lane;
         const bool valid = i < n;
         unsigned long long key = 0;
+        uint32_t sl = 0;
         if (valid) {
-            const unsigned long long e = nodes.ukeys[i];
+            const unsigned long long e = nodes.ukeys[i];  // parent slot << 1 | bit
             const uint32_t p = uint32_t(e >> 1), bit = uint32_t(e & 1);
             const double pv = parent.prev[p], cur = parent.cur[p];
             key = parent.key[p] | ((bit && bit_pos < 64) ? (1ull << bit_pos) : 0ull);
-            na.key[i] = key;
-            na.prev[i] = bit ? __dsub_rn(pv, cur) : cur;
+            sl = nodes.uslot[i];
+            na.key[sl] = key;
+            na.prev[sl] = bit ? __dsub_rn(pv, cur) : cur;
         }
         const uint32_t ks = dedup_insert_warp(keys, key, valid, lane, cache);
-        if (valid) na.kslot[i] = ks;
+        if (valid) na.kslot[sl] = ks;
     }
 }
 
 // Decision records once the level's keys are contracted (values by key slot).
-__global__ void dedup_node_decide_kernel(const uint32_t *count, uint32_t max_ids, const double *__restrict__ value,
-                                         DedupNodeArrays na) {
-    const uint32_t n = min(*count, max_ids);
+__global__ void dedup_node_decide_kernel(DedupTable nodes, const double *__restrict__ value, DedupNodeArrays na) {
+    const uint32_t n = min(*nodes.count, nodes.max_ids);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const double cur = value[na.kslot[i]];
-        na.cur[i] = cur;
-        na.rec[i] = node_rec(cur, na.prev[i]);
+        const uint32_t sl = nodes.uslot[i];
+        const double cur = value[na.kslot[sl]];
+        na.cur[sl] = cur;
+        na.rec[sl] = node_rec(cur, na.prev[sl]);
     }
 }
 
@@ -803,7 +806,7 @@ __global__ void __launch_bounds__(256) dedup_node_pass_kernel(const __grid_const
         for (int g = 0; g < G; g++) {
             s[g] = s0 + 32 * g + lane;
             valid[g] = s[g] < a.shots;
-            node[g] = valid[g] ? __ldg(a.cur.ids + __ldg(a.slot + s[g])) : 0u;
+            node[g] = valid[g] ? __ldg(a.slot + s[g]) : 0u;  // node arrays are indexed by table slot
         }
         DedupNodeRec r[G];
         bool need = false;  // a draw is needed unless every node's bit is certain (T = 0 or 2^53, no error)

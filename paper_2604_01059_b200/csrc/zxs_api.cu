@@ -2556,9 +2556,29 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
     }
     CK(cudaMemcpyAsync(s->dd_pinned, d.max_count, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (s->dd_pinned[0] > limit || s->dd_pinned[1] > flimit) {  // more keys than the tables hold: redo synchronously
+    if (s->dd_pinned[0] > limit || s->dd_pinned[1] > flimit) {
+        // more distinct keys at some position than the tables hold: distinct keys grow sublinearly
+        // with the batch, so redo the batch as two halves on this path (down to 2^20 shots), and
+        // only then synchronously (whose own fallback is the per-shot mono_kernel)
         s->dd_dirty = true;
         s->dd_stats[0] -= 1;
+        constexpr uint64_t kMinSplit = uint64_t(1) << 20;
+        if (a.shots >= 2 * kMinSplit) {
+            const uint64_t h = (a.shots / 2 + 63) & ~uint64_t(63);  // whole 64-shot record words
+            zxs_dev::LaunchArgs lo = a, hi = a;
+            lo.shots = h;
+            hi.first_shot = a.first_shot + h;
+            hi.shots = a.shots - h;
+            if (hi.out32) hi.out32 = a.out32 + h / 32;
+            if (a.uniforms) hi.uniforms = a.uniforms + h;  // [position][uniforms_ld]: same row stride
+            if (a.heavy_fraw) hi.heavy_fraw = static_cast<char *>(a.heavy_fraw) + h * a.fraw_bytes;
+            hi.heavy_ld32 = a.heavy_ld32;
+            if (a.fcols_spare) hi.fcols_spare = a.fcols_spare + h / 32;
+            s->dd_stats[1] += 1;
+            launch_dedup(s, lo, fcols, fcols_ld32, st);
+            launch_dedup(s, hi, fcols ? fcols + h / 32 : nullptr, fcols_ld32, st);
+            return;
+        }
         if (!fcols) fcols = regen_fcols(s, a, st);
         return launch_dedup_sync(s, a, fcols, fcols_ld32, st);
     }

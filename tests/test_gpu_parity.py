@@ -403,9 +403,10 @@ def test_kernel_timing_counts_launches():
     sample(cd, 5000, 1)
     t = cd.kernel_times()
     cd.kernel_timing(False)
-    # one chain of 5 outputs (6 tensors): 6 evals; init + 6 folds + 5 AR steps + 5 table clears + 5 count resets
+    # one chain of 5 outputs (6 tensors) on node levels: 6 evals; aux = init + 6 folds + level-0 records
+    # + 4 x (node prep + decide + key-table clear and reset) + 5 passes + 5 x (node-table clear and reset)
     assert t["shot_kernel"][1] == 1 and t["mono_kernel"][1] == 0
-    assert t["dedup_eval_kernel"][1] == 6 and t["dedup_aux"][1] == 22
+    assert t["dedup_eval_kernel"][1] == 6 and t["dedup_aux"][1] == 1 + 6 + 1 + 4 * 4 + 5 + 5 * 2
 
 
 # ---------------------------------------------------------------- deduplicated path
@@ -554,3 +555,51 @@ def test_dedup_fused_chain_overflow(name):
     assert np.array_equal(got, orc.sample(shots, 0, fcols=f, uniforms=u))
     b = _heavy_model(name, min_factors="0", mono="1", dedup="0")
     assert np.array_equal(rec, sample(b, 50000, 3, 7))
+
+
+@pytest.mark.skipif(not refdriver.available(), reason="reference library not present")
+@pytest.mark.parametrize("name,scale", [("c2_surface_d3_xmem_t", 0.9), ("c4_color_d5_rz3", 0.75)])
+def test_joint_table_no_hit_fallback(name, scale, tmp_path):
+    """A joint mechanism whose table sums to less than 1: a draw above the
+    running sum hits nothing and the reference keeps outcome 0
+    (sampler.cpp:283-293). Every joint table of the fixture is scaled by
+    `scale`, so the no-hit branch fires for ~(1 - scale) of the draws; the
+    device records equal the reference sampler's on the same model."""
+    from paper_2604_01059_b200 import zxs_format
+    a = zxs_format.load(golden_path(name))
+    tb, tab = a["mech_table_begin"], a["table"].copy()
+    joint = [m for m in range(len(tb) - 1) if tb[m + 1] > tb[m]]
+    assert joint
+    for m in joint:
+        tab[tb[m]:tb[m + 1]] *= scale
+    a["table"] = tab
+    path = str(tmp_path / "nohit.zxs")
+    zxs_format.save(path, a)
+    cs = zx.CompiledSampler.load(path)
+    ref = refdriver.RefModel.load(path)
+    for shots, seed, first in ((20000, 3, 0), (4097, 5, 2**32 - 64)):
+        want = ref.sample_rb(shots, seed, first_shot=first, threads=8)
+        assert np.array_equal(sample(cs, shots, seed, first), want)
+    f_dev = zx.sample_error_batch(cs, 3, 0, 20000)
+    assert np.array_equal(f_dev, ref.sample_error_batch(20000, 3))
+
+
+def test_dedup_overflow_splits_batch():
+    """A batch with more distinct keys at some chain position than the tables
+    hold is redone as halves on the deduplicated path (down to 2^20 shots)
+    before any per-shot fallback: config 3 (frame readout, circuit-level
+    noise) at 2^22 shots with 3,000-key tables; records, counts and dedup
+    statistics against the per-shot path."""
+    import os
+    name = "c3_cultivation_d3_frame"
+    os.environ["ZXS_DEDUP_MAX_KEYS"] = "3000"
+    try:
+        a = _heavy_model(name, min_factors="0", mono="1", dedup="1")
+        a.dedup_stats(reset=True)
+        got = sample(a, 1 << 22, 9, 1 << 30)
+        st = a.dedup_stats()
+    finally:
+        del os.environ["ZXS_DEDUP_MAX_KEYS"]
+    b = _heavy_model(name, min_factors="0", mono="1", dedup="0")
+    assert np.array_equal(got, sample(b, 1 << 22, 9, 1 << 30))
+    assert st["fallbacks"] >= 1  # split (or per-shot) at least once

@@ -113,12 +113,13 @@ class RefModel:
     @classmethod
     def load(cls, path: str) -> "RefModel":
         h = ctypes.c_void_p()
-        if path.endswith(".gz"):  # the C++ loader reads plain .zxs: inflate to a temp file
+        if path.endswith((".gz", ".xz")):  # the C++ loader reads plain .zxs: inflate to a temp file
             import gzip
+            import lzma
             import shutil
             import tempfile
             with tempfile.NamedTemporaryFile(suffix=".zxs") as tmp:
-                with gzip.open(path, "rb") as src:
+                with (gzip.open(path, "rb") if path.endswith(".gz") else lzma.open(path, "rb")) as src:
                     shutil.copyfileobj(src, tmp, 1 << 24)
                 tmp.flush()
                 _check(lib().zr_load(os.fsencode(tmp.name), ctypes.byref(h)))

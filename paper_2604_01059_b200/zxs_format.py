@@ -53,10 +53,14 @@ FIELDS = (
 
 
 def load(path: str) -> dict:
-    """Reads a .zxs file (or a gzip-compressed .zxs.gz)."""
+    """Reads a .zxs file (or a gzip- / xz-compressed .zxs.gz / .zxs.xz)."""
     if path.endswith(".gz"):
         import gzip
         with gzip.open(path, "rb") as fp:
+            data = fp.read()
+    elif path.endswith(".xz"):
+        import lzma
+        with lzma.open(path, "rb") as fp:
             data = fp.read()
     else:
         with open(path, "rb") as fp:

@@ -604,6 +604,8 @@ __global__ void __launch_bounds__(256) dedup_ar_kernel(const __grid_constant__ D
     DedupWarpCache cache;
     // up to the 64-shot boundary: the record's last 64-bit word gets zero tail bits
     const uint64_t shots64 = (a.shots + 63) & ~uint64_t(63);
+    // this batch's record words (a split batch's rows continue past them: out_ld32 is only the stride)
+    const uint64_t out_words = min(a.out_ld32, shots64 / 32);
     for (uint64_t s0 = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * G; s0 < shots64; s0 += stride) {
         uint64_t s[G];
         bool valid[G], bit[G];
@@ -647,7 +649,7 @@ __global__ void __launch_bounds__(256) dedup_ar_kernel(const __grid_constant__ D
             const uint32_t word = __ballot_sync(kFull, bit[g]);
             if (lane == 0) {
                 const uint64_t wi = (s0 >> 5) + g;
-                if (a.out32 && wi < a.out_ld32) a.out32[a.out * a.out_ld32 + wi] = word;
+                if (a.out32 && wi < out_words) a.out32[a.out * a.out_ld32 + wi] = word;
                 ones += __popc(word);
             }
         }
@@ -798,6 +800,8 @@ __global__ void __launch_bounds__(256) dedup_node_pass_kernel(const __grid_const
     unsigned long long ones = 0;
     DedupWarpCache cache;
     const uint64_t shots64 = (a.shots + 63) & ~uint64_t(63);
+    // this batch's record words (a split batch's rows continue past them: out_ld32 is only the stride)
+    const uint64_t out_words = min(a.out_ld32, shots64 / 32);
     for (uint64_t s0 = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * G; s0 < shots64; s0 += stride) {
         uint64_t s[G];
         bool valid[G], bit[G];
@@ -857,12 +861,12 @@ __global__ void __launch_bounds__(256) dedup_node_pass_kernel(const __grid_const
             const uint64_t w0 = s0 >> 5;
             if (a.out32) {
                 uint32_t *row = a.out32 + a.out * a.out_ld32;
-                if (w0 + G <= a.out_ld32 && (reinterpret_cast<uintptr_t>(row + w0) & 15) == 0) {
+                if (w0 + G <= out_words && (reinterpret_cast<uintptr_t>(row + w0) & 15) == 0) {
                     *reinterpret_cast<uint4 *>(row + w0) = make_uint4(word[0], word[1], word[2], word[3]);
                 } else {
 #pragma unroll
                     for (int g = 0; g < G; g++) {
-                        if (w0 + g < a.out_ld32) row[w0 + g] = word[g];
+                        if (w0 + g < out_words) row[w0 + g] = word[g];
                     }
                 }
             }
@@ -933,6 +937,8 @@ __global__ void __launch_bounds__(256) dedup_fused_ar_kernel(const __grid_consta
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * G;
     unsigned long long ones[kDedupMaxFused] = {};
     const uint64_t shots64 = (a.shots + 63) & ~uint64_t(63);
+    // this batch's record words (a split batch's rows continue past them: out_ld32 is only the stride)
+    const uint64_t out_words = min(a.out_ld32, shots64 / 32);
     for (uint64_t s0 = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * G; s0 < shots64; s0 += stride) {
         uint64_t s[G];
         bool valid[G];
@@ -981,7 +987,7 @@ __global__ void __launch_bounds__(256) dedup_fused_ar_kernel(const __grid_consta
                 const uint32_t word = __ballot_sync(kFull, bit[g]);
                 if (lane == 0) {
                     const uint64_t wi = (s0 >> 5) + g;
-                    if (a.out32 && wi < a.out_ld32) a.out32[a.out[j] * a.out_ld32 + wi] = word;
+                    if (a.out32 && wi < out_words) a.out32[a.out[j] * a.out_ld32 + wi] = word;
 #pragma unroll
                     for (uint32_t q = 0; q < kDedupMaxFused; q++) {
                         if (q == j) ones[q] += __popc(word);

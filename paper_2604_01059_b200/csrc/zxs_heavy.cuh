@@ -258,7 +258,9 @@ __global__ void __launch_bounds__(kHeavyWarps * 32, 1) heavy_kernel(const __grid
                     unsigned long long ones = 0;
 #pragma unroll
                     for (int s = 0; s < kHS; s++) {
-                        if (h.out32 && w0 + s < h.out_ld32) h.out32[o * h.out_ld32 + w0 + s] = word[s];
+                        if (h.out32 && w0 + s < min(h.out_ld32, 2 * ((h.shots + 63) / 64))) {
+                            h.out32[o * h.out_ld32 + w0 + s] = word[s];
+                        }
                         ones += __popc(word[s]);
                     }
                     if (h.counts && ones) atomicAdd(&h.counts[o], ones);

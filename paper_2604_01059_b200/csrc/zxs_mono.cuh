@@ -620,7 +620,10 @@ __global__ void __launch_bounds__(MonoCfg<NW>::kWarps * 32, 1) mono_kernel(const
                 const uint32_t o = h.comp_outputs[cd.out_begin + j];
 #pragma unroll
                 for (int i = 0; i < NW; i++) {
-                    if (h.out32 && wrd + i < h.out_ld32) h.out32[o * h.out_ld32 + wrd + i] = word.w[i];
+                    // bounded by this batch's record words (out_ld32 is the row stride)
+                    if (h.out32 && wrd + i < min(h.out_ld32, 2 * ((h.shots + 63) / 64))) {
+                        h.out32[o * h.out_ld32 + wrd + i] = word.w[i];
+                    }
                 }
                 if (h.counts) {
                     uint32_t ones = 0;

@@ -458,16 +458,22 @@ MonoEntry mono_entry(int pa, int pb, int a, int b) {
     return e;
 }
 
-int mono_warps(int nw) { return nw == 2 ? zxs_dev::MonoCfg<2>::kWarps : zxs_dev::MonoCfg<1>::kWarps; }
-
-size_t mono_smem_bytes(uint32_t n_planes, uint32_t max_dict, int nw, uint32_t depth) {
-    return 128 + 2 * size_t(zxs_dev::kMonoChunkWords) * 4 + size_t(max_dict) * 16 +
-           size_t(mono_warps(nw)) * nw * (size_t(depth) * 3 * 128 + size_t(n_planes) * 128);
+// mono_kernel configurations: 2 = two 32-shot words per lane, 12 warps; 1 = one word, 16 warps;
+// 3 = one word, 4 warps (narrow: large dictionaries / many parameter planes)
+int mono_words(int cfg) { return cfg == 2 ? 2 : 1; }
+int mono_warps(int cfg) {
+    return cfg == 2 ? zxs_dev::MonoCfg<2>::kWarps : cfg == 1 ? zxs_dev::MonoCfg<1>::kWarps : 4;
 }
 
-const void *mono_kernel_ptr(int nw) {
-    return nw == 2 ? reinterpret_cast<const void *>(&zxs_dev::mono_kernel<2>)
-                   : reinterpret_cast<const void *>(&zxs_dev::mono_kernel<1>);
+size_t mono_smem_bytes(uint32_t n_planes, uint32_t max_dict, int cfg, uint32_t depth) {
+    return 128 + 2 * size_t(zxs_dev::kMonoChunkWords) * 4 + size_t(max_dict) * 16 +
+           size_t(mono_warps(cfg)) * mono_words(cfg) * (size_t(depth) * 3 * 128 + size_t(n_planes) * 128);
+}
+
+const void *mono_kernel_ptr(int cfg) {
+    return cfg == 2 ? reinterpret_cast<const void *>(&zxs_dev::mono_kernel<2>)
+           : cfg == 1 ? reinterpret_cast<const void *>(&zxs_dev::mono_kernel<1>)
+                      : reinterpret_cast<const void *>(&zxs_dev::mono_kernel<1, 4>);
 }
 
 struct MonoHost {
@@ -827,6 +833,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
         const uint32_t nloc = uint32_t(loc.size());
         bool ok = nf >= heavy_min && H.comps.size() < size_t(zxs_dev::kMaxMonoComps) && nloc + n <= 63 &&
                   all_plane + 2 <= 255;
+        const char *why = ok ? nullptr : (nf < heavy_min ? "small" : "parameters / planes / component count");
         std::vector<uint32_t> to_local(fwid + n, ~0u);  // raw param -> local param
         for (uint32_t i = 0; i < nloc; i++) to_local[loc[i]] = i;
         for (uint32_t j = 0; j < n; j++) to_local[fwid + j] = nloc + j;
@@ -854,7 +861,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             tdb.push_back(uint32_t(dict_base));
             cur_width = nloc + n;  // the local width (reference width f_width + n, compile.cpp:256)
             twid.push_back(cur_width);
-            if (d->tensor_param_width[t] > fwid + n || cur_width > 63) ok = false;  // local forms as 64-bit masks
+            if (d->tensor_param_width[t] > fwid + n || cur_width > 63) { ok = false; if (!why) why = "width"; }  // local forms as 64-bit masks
             // ---- lower every term of tensor t to record tokens (order-free: J and Z commute)
             std::vector<MonoTerm> terms;
             terms.reserve(size_t(d->tensor_term_begin[t + 1] - d->tensor_term_begin[t]));
@@ -865,7 +872,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                 for (uint64_t k = d->term_factor_begin[term]; k < d->term_factor_begin[term + 1]; k++) {
                     const uint32_t tb = d->factor_table[k];
                     if (tb >= d->num_h_tables || tpa[tb] < 0) {
-                        ok = false;
+                        { ok = false; if (!why) why = "table class"; }
                         break;
                     }
                     std::vector<uint32_t> us = sel_list(d->factor_u_bits + d->factor_u_begin[k],
@@ -873,11 +880,11 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                     std::vector<uint32_t> vs = sel_list(d->factor_v_bits + d->factor_v_begin[k],
                                                         d->factor_v_begin[k + 1] - d->factor_v_begin[k]);
                     for (uint32_t &p : us) {
-                        ok &= p < fwid + n && to_local[p] != ~0u;
+                        ok &= p < fwid + n && to_local[p] != ~0u; if (!ok && !why) why = "selector range";
                         p = ok ? to_local[p] : 0;
                     }
                     for (uint32_t &p : vs) {
-                        ok &= p < fwid + n && to_local[p] != ~0u;
+                        ok &= p < fwid + n && to_local[p] != ~0u; if (!ok && !why) why = "selector range";
                         p = ok ? to_local[p] : 0;
                     }
                     if (!ok) break;
@@ -895,7 +902,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                         nnz++;
                         if (mset < 0) mset = en[ab].m;
                         if (oset < 0) oset = en[ab].k & 1;
-                        if (mset != en[ab].m || oset != (en[ab].k & 1)) ok = false;
+                        if (mset != en[ab].m || oset != (en[ab].k & 1)) { ok = false; if (!why) why = "table m/k mismatch"; }
                     }
                     if (!ok) break;
                     if (nnz == 0) {
@@ -924,7 +931,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                         }
                     }
                     if (best < 0) {
-                        ok = false;
+                        { ok = false; if (!why) why = "J polynomial"; }
                         break;
                     }
                     const int d00 = best & 3, al = (best >> 2) & 3, be = (best >> 4) & 3, ga = (best >> 6) & 3;
@@ -934,11 +941,11 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                     for (int ab = 0; ab < 4; ab++) {
                         if (indomain[ab] && zero[ab]) zl |= 1u << ab;
                     }
-                    const uint32_t fa = ua ? dict_form(us) : 0xfffu, fbv = vb ? dict_form(vs) : 0xfffu;
+                    const uint32_t fa = ua ? dict_form(us) : zxs_dev::kFormMask, fbv = vb ? dict_form(vs) : zxs_dev::kFormMask;
                     nsel += us.size() + vs.size();
                     // token: record word | (GEN aux word + 1) << 32
                     auto rec = [&](uint32_t kind, uint32_t a_form, uint32_t b_form, uint64_t aux = 0) {
-                        tw.push_back(uint64_t(kind << 28 | (b_form & 0xfffu) << 16 | (a_form & 0xfffu)) | aux << 32);
+                        tw.push_back(uint64_t(kind << 28 | (b_form & zxs_dev::kFormMask) << zxs_dev::kFormShiftB | (a_form & zxs_dev::kFormMask)) | aux << 32);
                     };
                     const bool jnone = !al && !be && !ga;
                     // Z patterns over the domain points present (bit index a*2+b)
@@ -952,21 +959,21 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                     if (zl == 0) {
                         if (jnone) continue;  // constant factor
                         if (!be && !ga) {
-                            rec(al == 1 ? zxs_dev::kRecAdd : al == 3 ? zxs_dev::kRecSub : zxs_dev::kRecAdd2, fa, 0xfffu);
+                            rec(al == 1 ? zxs_dev::kRecAdd : al == 3 ? zxs_dev::kRecSub : zxs_dev::kRecAdd2, fa, zxs_dev::kFormMask);
                         } else if (!al && !ga) {
                             rec(be == 1 ? zxs_dev::kRecAdd : be == 3 ? zxs_dev::kRecSub : zxs_dev::kRecAdd2,
-                                dict_form(vs), 0xfffu);
+                                dict_form(vs), zxs_dev::kFormMask);
                         } else {
                             rec(zxs_dev::kRecGen, fa, fbv, uint64_t(al | be << 2 | ga << 4) + 1);
                         }
                     } else if (jnone && ua && zis(zA)) {
-                        rec(zxs_dev::kRecZ, fa, 0xfffu);
+                        rec(zxs_dev::kRecZ, fa, zxs_dev::kFormMask);
                     } else if (jnone && ua && zis(zAn)) {
-                        rec(zxs_dev::kRecZn, fa, 0xfffu);
+                        rec(zxs_dev::kRecZn, fa, zxs_dev::kFormMask);
                     } else if (jnone && vb && zis(zB)) {
-                        rec(zxs_dev::kRecZ, dict_form(vs), 0xfffu);
+                        rec(zxs_dev::kRecZ, dict_form(vs), zxs_dev::kFormMask);
                     } else if (jnone && vb && zis(zBn)) {
-                        rec(zxs_dev::kRecZn, dict_form(vs), 0xfffu);
+                        rec(zxs_dev::kRecZn, dict_form(vs), zxs_dev::kFormMask);
                     } else {
                         rec(zxs_dev::kRecGen, fa, fbv, (uint64_t(al | be << 2 | ga << 4) | uint64_t(zl) << 6) + 1);
                     }
@@ -998,22 +1005,22 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             std::vector<uint64_t> usage(form_mask.size(), 0);
             for (const MonoNode &nd : nodes) {
                 for (uint64_t tok : nd.recs) {
-                    const uint32_t r = uint32_t(tok), fa = r & 0xfffu, fbv = (r >> 16) & 0xfffu;
-                    if (fa != 0xfffu && fa < usage.size()) usage[fa]++;
-                    if ((r >> 28) == zxs_dev::kRecGen && fbv != 0xfffu && fbv < usage.size()) usage[fbv]++;
+                    const uint32_t r = uint32_t(tok), fa = r & zxs_dev::kFormMask, fbv = (r >> zxs_dev::kFormShiftB) & zxs_dev::kFormMask;
+                    if (fa != zxs_dev::kFormMask && fa < usage.size()) usage[fa]++;
+                    if ((r >> 28) == zxs_dev::kRecGen && fbv != zxs_dev::kFormMask && fbv < usage.size()) usage[fbv]++;
                 }
             }
-            if (form_mask.size() >= 0xfffu) ok = false;
+            if (form_mask.size() >= zxs_dev::kFormMask) { ok = false; if (!why) why = "forms > 16382"; }
             if (!ok) break;
             std::vector<uint64_t> basis;
             const std::vector<uint32_t> entry_of = finish_dictionary(usage, basis);
             tbb.push_back(uint32_t(H.basis.size() + cb.size()));
             cb.insert(cb.end(), basis.begin(), basis.end());
             auto remap = [&](uint32_t r) {
-                const uint32_t fa = r & 0xfffu, fbv = (r >> 16) & 0xfffu;
-                const uint32_t na = fa == 0xfffu ? 0xfffu : entry_of[fa];
-                const uint32_t nb = fbv == 0xfffu ? 0xfffu : entry_of[fbv];
-                return (r & 0xf000f000u) | (nb << 16) | na;
+                const uint32_t fa = r & zxs_dev::kFormMask, fbv = (r >> zxs_dev::kFormShiftB) & zxs_dev::kFormMask;
+                const uint32_t na = fa == zxs_dev::kFormMask ? zxs_dev::kFormMask : entry_of[fa];
+                const uint32_t nb = fbv == zxs_dev::kFormMask ? zxs_dev::kFormMask : entry_of[fbv];
+                return (r & 0xf0000000u) | (nb << zxs_dev::kFormShiftB) | na;
             };
             uint32_t cur_begin = uint32_t(H.words.size() + w.size()), cur_nodes = 0;
             auto close_chunk = [&]() {
@@ -1025,7 +1032,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                 cur_nodes = 0;
             };
             tcb.push_back(uint32_t(H.chunks.size() + ch.size()));
-            if (H.dict.size() - dict_base >= 0xfffu) ok = false;  // 12-bit form ids
+            if (H.dict.size() - dict_base >= zxs_dev::kFormMask) { ok = false; if (!why) why = "dictionary > 16382"; }  // 14-bit form ids
             comp_max_dict = std::max<uint32_t>(comp_max_dict, uint32_t(H.dict.size() - dict_base));
             // summation segments: contiguous node ranges of about equal cost (records + leaf
             // epilogue), the tensor value being the ordered sum of the segment sums
@@ -1055,7 +1062,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                 // [+ re, im for leaves], then the one-form records grouped by kind, then GEN pairs
                 uint32_t cnt[16] = {};
                 for (uint64_t tok : nd.recs) cnt[uint32_t(tok) >> 28]++;
-                for (int k = 0; k < 16; k++) ok &= cnt[k] < 256;
+                for (int k = 0; k < 16; k++) ok &= cnt[k] < 256; if (!ok && !why) why = "records per node kind >= 256";
                 if (!ok) break;
                 nw.clear();
                 nw.push_back((nd.leaf ? 0x80000000u : 0u) | (seg_start[node_i] ? zxs_dev::kMonoSegStart : 0u) |
@@ -1073,8 +1080,8 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                 // consecutive pairs mostly share a class (mono_kernel's paired straight-line loads)
                 std::vector<uint64_t> recs_sorted(nd.recs.begin(), nd.recs.end());
                 auto cls_of = [&](uint64_t tok) {
-                    const uint32_t r = remap(uint32_t(tok)), fa = r & 0xfffu;
-                    return fa == 0xfffu ? 0u : uint32_t(H.dict[dict_base + fa].x & 0x87u);
+                    const uint32_t r = remap(uint32_t(tok)), fa = r & zxs_dev::kFormMask;
+                    return fa == zxs_dev::kFormMask ? 0u : uint32_t(H.dict[dict_base + fa].x & 0x87u);
                 };
                 std::stable_sort(recs_sorted.begin(), recs_sorted.end(),
                                  [&](uint64_t x, uint64_t y) { return cls_of(x) > cls_of(y); });
@@ -1087,13 +1094,13 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                         nw.push_back(r);
                         if (tok >> 32) nw.push_back(uint32_t((tok >> 32) - 1));
                         recs++;
-                        const uint32_t fa = r & 0xfffu, fbv = (r >> 16) & 0xfffu;
-                        if (fa != 0xfffu) loads += form_size[fa];
-                        if (kind == zxs_dev::kRecGen && fbv != 0xfffu) loads += form_size[fbv];
+                        const uint32_t fa = r & zxs_dev::kFormMask, fbv = (r >> zxs_dev::kFormShiftB) & zxs_dev::kFormMask;
+                        if (fa != zxs_dev::kFormMask) loads += form_size[fa];
+                        if (kind == zxs_dev::kRecGen && fbv != zxs_dev::kFormMask) loads += form_size[fbv];
                     }
                 }
                 if (nw.size() + 4 > zxs_dev::kMonoChunkWords || nd.depth >= zxs_dev::kMonoMaxDepth) {
-                    ok = false;
+                    { ok = false; if (!why) why = "node too large or tree too deep"; }
                     break;
                 }
                 if (H.words.size() + w.size() + nw.size() - cur_begin > zxs_dev::kMonoChunkWords) close_chunk();
@@ -1141,10 +1148,10 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                             q += 3 + ((h0 >> 31) ? 4 : 0);
                             const uint32_t ns = (h1 & 0xffu) + ((h1 >> 8) & 0xffu) + ((h1 >> 16) & 0xffu) + (h1 >> 24) +
                                                 (h2 & 0xffu);
-                            for (uint32_t r = 0; r < ns; r++, q++) sw[q] = (sw[q] & ~0xfffu) | fn(sw[q] & 0xfffu);
+                            for (uint32_t r = 0; r < ns; r++, q++) sw[q] = (sw[q] & ~zxs_dev::kFormMask) | fn(sw[q] & zxs_dev::kFormMask);
                             for (uint32_t gg = 0; gg < (h0 & 0xffu); gg++, q += 2) {
                                 const uint32_t r = sw[q];
-                                sw[q] = (r & 0xf000f000u) | (fn((r >> 16) & 0xfffu) << 16) | fn(r & 0xfffu);
+                                sw[q] = (r & 0xf0000000u) | (fn((r >> zxs_dev::kFormShiftB) & zxs_dev::kFormMask) << zxs_dev::kFormShiftB) | fn(r & zxs_dev::kFormMask);
                             }
                         }
                     }
@@ -1192,9 +1199,15 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             }
             nodes_total += nodes.size();
         }
-        if (ok && mono_smem_bytes(all_plane + max_chain + 2, std::max(comp_max_dict, H.max_dict), 1,
+        // the narrow mono_kernel must fit (the per-shot path is every large component's fallback
+        // and its verification seam); the deduplicated path sizes its own shared memory
+        if (ok && mono_smem_bytes(all_plane + max_chain + 2, std::max(comp_max_dict, H.max_dict), 3,
                                   std::max(comp_depth, H.max_depth)) > 227 * 1024) {
-            ok = false;
+            { ok = false; if (!why) why = "shared memory"; }
+        }
+        if (std::getenv("ZXS_DEBUG_MONO") && nf >= heavy_min) {
+            std::fprintf(stderr, "encode_mono: component %u (%llu factors): %s\n", c, (unsigned long long)nf,
+                         ok ? "monomial path" : (why ? why : "?"));
         }
         if (ok) {
             zxs_dev::HeavyComp hc;
@@ -1887,6 +1900,7 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         s->mono_tensor = MH.tensor_index;
         if (const char *e = std::getenv("ZXS_MONO_WORDS")) s->mono_nw = std::atoi(e) == 1 ? 1 : 2;
         if (mono_smem_bytes(ma.n_planes, ma.max_dict, s->mono_nw, ma.stack_depth) > 227 * 1024) s->mono_nw = 1;
+        if (mono_smem_bytes(ma.n_planes, ma.max_dict, s->mono_nw, ma.stack_depth) > 227 * 1024) s->mono_nw = 3;
         s->mono_smem = mono_smem_bytes(ma.n_planes, ma.max_dict, s->mono_nw, ma.stack_depth);
         s->dd_words = reinterpret_cast<const uint32_t *>(b + o_sw);
         s->dd_segs = reinterpret_cast<const uint4 *>(b + o_sg);
@@ -1904,7 +1918,10 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         s->dd_block_forms = reinterpret_cast<const uint32_t *>(b + o_bf);
         s->dd_block_form_begin = reinterpret_cast<const uint32_t *>(b + o_bfb);
         s->dd_tfb = MH.tensor_first_block;
-        s->dd_table_bytes = uint32_t(std::max<size_t>(size_t(ma.max_dict) * 16, size_t(MH.max_block_forms) * 128));
+        bool all_blocks = true;  // every tensor walks block form tables (the dictionary is never staged whole)
+        for (uint32_t x : MH.tensor_first_block) all_blocks = all_blocks && x != 0xffffffffu;
+        s->dd_table_bytes = uint32_t(std::max<size_t>(all_blocks ? 16 : size_t(ma.max_dict) * 16,
+                                                      size_t(MH.max_block_forms) * 128));
         s->dd_smem = size_t(s->dd_table_bytes) + size_t(MH.all_plane + 2) * 32 * 4 +
                      size_t(zxs_dev::kDedupWarps) * ma.stack_depth * 96 * 4;
         uint32_t max_seg = 0;
@@ -2038,8 +2055,8 @@ void launch_mono(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *f
             }
         }
     }
-    const int nw = s->mono_nw;
-    const uint64_t per_cta = uint64_t(mono_warps(nw)) * 1024 * nw;
+    const int nw = s->mono_nw;  // configuration (mono_kernel_ptr)
+    const uint64_t per_cta = uint64_t(mono_warps(nw)) * 1024 * mono_words(nw);
     h.n_cta_tiles = (a.shots + per_cta - 1) / per_cta;
     if (h.n_cta_tiles == 0) return;
     h.scratch = s->mono_scratch_get(size_t(3) * h.n_cta_tiles * per_cta * 8);

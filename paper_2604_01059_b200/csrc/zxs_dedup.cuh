@@ -300,18 +300,18 @@ __device__ __forceinline__ void mono_walk_fv(const uint32_t *w, uint32_t nnodes,
             const uint32_t n_z = h1 >> 24, n_zn = h2 & 0xffu;
             uint32_t e = q + n_add;
             for (; q < e; q++) {  // J += a
-                const uint32_t x = fv[(w[q] & 0xfffu) * 32];
+                const uint32_t x = fv[(w[q] & kFormMask) * 32];
                 a1 ^= a0 & x;
                 a0 ^= x;
             }
             for (e += n_sub; q < e; q++) {  // J -= a
-                const uint32_t x = fv[(w[q] & 0xfffu) * 32];
+                const uint32_t x = fv[(w[q] & kFormMask) * 32];
                 a1 ^= ~a0 & x;
                 a0 ^= x;
             }
-            for (e += n_add2; q < e; q++) a1 ^= fv[(w[q] & 0xfffu) * 32];  // J += 2a
-            for (e += n_z; q < e; q++) zz |= fv[(w[q] & 0xfffu) * 32];     // Z |= a
-            for (e += n_zn; q < e; q++) zz |= ~fv[(w[q] & 0xfffu) * 32];   // Z |= ~a
+            for (e += n_add2; q < e; q++) a1 ^= fv[(w[q] & kFormMask) * 32];  // J += 2a
+            for (e += n_z; q < e; q++) zz |= fv[(w[q] & kFormMask) * 32];     // Z |= a
+            for (e += n_zn; q < e; q++) zz |= ~fv[(w[q] & kFormMask) * 32];   // Z |= ~a
             z.w[0] = zz;
             j0.w[0] = a0;
             j1.w[0] = a1;
@@ -319,7 +319,7 @@ __device__ __forceinline__ void mono_walk_fv(const uint32_t *w, uint32_t nnodes,
         for (uint32_t g = 0; g < (h0 & 0xffu); g++) {  // two-form records
             const uint32_t r = w[q], gw = w[q + 1];
             q += 2;
-            const uint32_t fa = r & 0xfffu, fb = (r >> 16) & 0xfffu;
+            const uint32_t fa = r & kFormMask, fb = (r >> kFormShiftB) & kFormMask;
             BW<1> a, bb;
             a.w[0] = fa == kMonoNoForm ? 0u : fv[fa * 32];
             bb.w[0] = fb == kMonoNoForm ? 0u : fv[fb * 32];

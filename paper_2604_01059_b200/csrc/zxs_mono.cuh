@@ -57,14 +57,17 @@ struct MonoCfg<2> {
 };
 constexpr int kMonoWarps = 16;               // upper bound of MonoCfg<NW>::kWarps (host sizing)
 constexpr uint32_t kMonoChunkWords = 2048;   // 8 KiB per chunk buffer
-constexpr uint32_t kMonoNoForm = 0xfffu;     // "no form" (parity 0) in the 12-bit form fields
+// record word: kind << 28 | second form << kFormShiftB | first form (14-bit dictionary ids)
+constexpr uint32_t kFormMask = 0x3fffu;
+constexpr int kFormShiftB = 14;
+constexpr uint32_t kMonoNoForm = kFormMask;  // "no form" (parity 0) in the 14-bit form fields
 constexpr int kMaxMonoComps = 8;
 constexpr uint32_t kMonoMaxDepth = 8;        // levels of the shared-prefix term tree
 constexpr uint32_t kMonoSegStart = 1u << 30; // node header flag: first node of a summation segment
 constexpr uint32_t kDedupSegs = 2368;        // summation segments per tensor (148 SMs x 16 warps)
 
-// record kinds (bits 28..31 of a record word; first form in bits 0..11,
-// second form in bits 16..27; ids index the tensor's dictionary)
+// record kinds (bits 28..31 of a record word; first form in bits 0..13,
+// second form in bits 14..27; ids index the tensor's dictionary)
 enum : uint32_t {
     kRecAdd = 0,    // J += a
     kRecSub = 1,    // J -= a
@@ -283,10 +286,10 @@ constexpr bool kMonoQuad = ZXS_MONO_QUAD != 0;
             for (; i_ + 4 <= (N); i_ += 4) {                                             \
                 const uint32_t r0_ = w[q + i_], r1_ = w[q + i_ + 1];                     \
                 const uint32_t r2_ = w[q + i_ + 2], r3_ = w[q + i_ + 3];                 \
-                const BW<NW> x0 = mono_form<NW>(sd, r0_ & 0xfffu, pl);                   \
-                const BW<NW> x1 = mono_form<NW>(sd, r1_ & 0xfffu, pl);                   \
-                const BW<NW> x2 = mono_form<NW>(sd, r2_ & 0xfffu, pl);                   \
-                const BW<NW> x3 = mono_form<NW>(sd, r3_ & 0xfffu, pl);                   \
+                const BW<NW> x0 = mono_form<NW>(sd, r0_ & kFormMask, pl);                   \
+                const BW<NW> x1 = mono_form<NW>(sd, r1_ & kFormMask, pl);                   \
+                const BW<NW> x2 = mono_form<NW>(sd, r2_ & kFormMask, pl);                   \
+                const BW<NW> x3 = mono_form<NW>(sd, r3_ & kFormMask, pl);                   \
                 OP(r0_, x0);                                                             \
                 OP(r1_, x1);                                                             \
                 OP(r2_, x2);                                                             \
@@ -295,7 +298,7 @@ constexpr bool kMonoQuad = ZXS_MONO_QUAD != 0;
         } else {                                                                         \
             for (; i_ + 2 <= (N); i_ += 2) {                                             \
                 const uint32_t r0_ = w[q + i_], r1_ = w[q + i_ + 1];                     \
-                const uint32_t fa_ = r0_ & 0xfffu, fb_ = r1_ & 0xfffu;                   \
+                const uint32_t fa_ = r0_ & kFormMask, fb_ = r1_ & kFormMask;                   \
                 const uint4 ea_ = sd[fa_], eb_ = sd[fb_];                                \
                 BW<NW> x0, x1;                                                           \
                 if (((ea_.x ^ eb_.x) & 0x87u) == 0 && (ea_.x & 0x87u) <= kPairMaxCls) {  \
@@ -310,7 +313,7 @@ constexpr bool kMonoQuad = ZXS_MONO_QUAD != 0;
         }                                                                                \
         for (; i_ < (N); i_++) {                                                         \
             const uint32_t r0_ = w[q + i_];                                              \
-            const BW<NW> x0 = mono_form<NW>(sd, r0_ & 0xfffu, pl);                       \
+            const BW<NW> x0 = mono_form<NW>(sd, r0_ & kFormMask, pl);                       \
             OP(r0_, x0);                                                                 \
         }                                                                                \
         q += (N);                                                                        \
@@ -411,7 +414,7 @@ __device__ __forceinline__ void mono_walk(const uint32_t *w, uint32_t nnodes, co
         for (uint32_t g = 0; g < (h0 & 0xffu); g++) {  // two-form records
             const uint32_t r = w[q], gw = w[q + 1];
             q += 2;
-            const uint32_t fa = r & 0xfffu, fb = (r >> 16) & 0xfffu;
+            const uint32_t fa = r & kFormMask, fb = (r >> kFormShiftB) & kFormMask;
             const BW<NW> a = fa == kMonoNoForm ? bw_zero<NW>() : mono_form<NW>(sd, fa, pl);
             const BW<NW> bb = fb == kMonoNoForm ? bw_zero<NW>() : mono_form<NW>(sd, fb, pl);
             const uint32_t zl = gw >> 6;
@@ -435,9 +438,11 @@ __device__ __forceinline__ void mono_walk(const uint32_t *w, uint32_t nnodes, co
     }
 }
 
-template <int NW>
-__global__ void __launch_bounds__(MonoCfg<NW>::kWarps * 32, 1) mono_kernel(const __grid_constant__ MonoArgs h) {
-    constexpr int kW = MonoCfg<NW>::kWarps;
+// KW warps per CTA: MonoCfg's, or 4 (the narrow variant, for components whose
+// dictionary and parameter planes do not fit the wide CTA's shared memory).
+template <int NW, int KW = MonoCfg<NW>::kWarps>
+__global__ void __launch_bounds__(KW * 32, 1) mono_kernel(const __grid_constant__ MonoArgs h) {
+    constexpr int kW = KW;
     constexpr uint32_t kLaneShots = 32 * NW;
     constexpr uint64_t kWarpShots = 32ull * kLaneShots;
     extern __shared__ __align__(128) uint8_t msm[];

@@ -19,6 +19,7 @@ from oracle import coracle
 from paper_2604_01059_b200 import _native, zxs_format
 
 REC_ADD, REC_SUB, REC_ADD2, REC_Z, REC_ZN, REC_GEN = 0, 1, 2, 3, 4, 15
+FORM_MASK, FORM_SHIFT_B = 0x3FFF, 14  # record word: kind << 28 | form b << 14 | form a (zxs_mono.cuh)
 
 
 def mono_layout(arrays, min_factors=0):
@@ -98,7 +99,7 @@ def apply_node_records(w, q, h0, h1, h2, form, J, Z):
         r = int(w[q])
         q += 1
         kind = r >> 28
-        a = form(r & 0xFFF)
+        a = form(r & FORM_MASK)
         if kind == REC_ADD:
             J += a
         elif kind == REC_SUB:
@@ -114,9 +115,9 @@ def apply_node_records(w, q, h0, h1, h2, form, J, Z):
         r, g = int(w[q]), int(w[q + 1])
         q += 2
         assert r >> 28 == REC_GEN
-        fa, fb = r & 0xFFF, (r >> 16) & 0xFFF
-        a = 0 if fa == 0xFFF else form(fa)
-        b = 0 if fb == 0xFFF else form(fb)
+        fa, fb = r & FORM_MASK, (r >> FORM_SHIFT_B) & FORM_MASK
+        a = 0 if fa == FORM_MASK else form(fa)
+        b = 0 if fb == FORM_MASK else form(fb)
         zl = g >> 6
         Z |= ((zl >> (a * 2 + b)) & 1) == 1
         J += (g & 3) * a + ((g >> 2) & 3) * b + ((g >> 4) & 3) * (a * b)

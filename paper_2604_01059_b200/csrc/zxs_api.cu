@@ -18,7 +18,9 @@
 
 #include <algorithm>
 #include <functional>
+#include <chrono>
 #include <limits>
+#include <unordered_map>
 #include <iterator>
 #include <cmath>
 #include <cstdlib>
@@ -667,16 +669,15 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                               d->term_factor_begin[d->tensor_term_begin[d->comp_tensor_begin[c]]];
         if (nfac >= heavy_min && loc.size() + n <= 63) lf_max = std::max(lf_max, uint32_t(loc.size()));
     }
-    std::map<uint64_t, uint32_t> form_id;  // local mask -> form id (per tensor)
+    std::unordered_map<uint64_t, uint32_t> form_id;  // local mask -> form id (per tensor)
+    form_id.reserve(1 << 14);
     std::vector<uint64_t> form_mask;        // form id -> raw mask
     std::map<uint32_t, uint32_t> form_size; // dictionary entry index -> plane loads
     size_t dict_base = 0;
     // ALL plane (>= every mono tensor's local width); all_plane + 1: ZERO; + 2 + j: raw sampled bit j
     const uint32_t all_plane = lf_max + max_chain;
     uint32_t cur_width = 0;                        // param width of the tensor being encoded
-    auto dict_form = [&](const std::vector<uint32_t> &sel0) -> uint32_t {
-        uint64_t m = 0;
-        for (uint32_t p : sel0) m ^= 1ull << p;
+    auto dict_form = [&](uint64_t m) -> uint32_t {
         auto it = form_id.find(m);
         if (it != form_id.end()) return it->second;
         const uint32_t id = uint32_t(form_mask.size());
@@ -810,16 +811,66 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
         }
         return entry_of;
     };
-    // parity list of a selector range after XOR cancellation, sorted
-    auto sel_list = [](const uint32_t *bits, uint64_t n) {
-        std::vector<uint32_t> v(bits, bits + n);
-        std::sort(v.begin(), v.end());
-        std::vector<uint32_t> r;
-        for (size_t i = 0; i < v.size();) {
-            size_t j = i;
-            while (j < v.size() && v[j] == v[i]) j++;
-            if ((j - i) & 1) r.push_back(v[i]);
-            i = j;
+
+    // Per (h table, u form present, v form present): the factor's exact entries on its domain,
+    // the common m and k mod 2 of its non-zero entries, the cheapest J polynomial
+    // d00 + al a + be b + ga ab (mod 4) matching (k - o)/2 there, and its zero pattern.
+    struct FactorRule {
+        int status = -1;  // -1 unset, 0 record, 1 identically zero, 2 m / k mod 2 differ, 3 no J polynomial
+        int mset = 0, oset = 0, best = 0;
+        uint32_t zl = 0, dm = 0;
+    };
+    std::vector<FactorRule> rules(size_t(std::max<uint32_t>(1, d->num_h_tables)) * 4);
+    auto factor_rule = [&](uint32_t tb, bool ua, bool vb) -> const FactorRule & {
+        FactorRule &r = rules[size_t(tb) * 4 + (ua ? 2 : 0) + (vb ? 1 : 0)];
+        if (r.status >= 0) return r;
+        MonoEntry en[4];
+        int mset = -1, oset = -1, nnz = 0;
+        bool indomain[4], zero[4];
+        r.status = 0;
+        for (int ab = 0; ab < 4; ab++) {
+            const int a = ab >> 1, b = ab & 1;
+            en[ab] = mono_entry(tpa[tb], tpb[tb], a, b);
+            indomain[ab] = (a == 0 || ua) && (b == 0 || vb);
+            zero[ab] = en[ab].zero;
+            if (!indomain[ab] || zero[ab]) continue;
+            nnz++;
+            if (mset < 0) mset = en[ab].m;
+            if (oset < 0) oset = en[ab].k & 1;
+            if (mset != en[ab].m || oset != (en[ab].k & 1)) r.status = 2;
+        }
+        if (r.status) return r;
+        if (nnz == 0) {
+            r.status = 1;
+            return r;
+        }
+        int best = -1, bc = 1 << 30;
+        for (int code = 0; code < 256; code++) {
+            const int d00 = code & 3, al = (code >> 2) & 3, be = (code >> 4) & 3, ga = (code >> 6) & 3;
+            if ((!ua && (al || ga)) || (!vb && (be || ga))) continue;
+            bool fits = true;
+            for (int ab = 0; ab < 4 && fits; ab++) {
+                if (!indomain[ab] || zero[ab]) continue;
+                const int a = ab >> 1, b = ab & 1;
+                fits = ((d00 + al * a + be * b + ga * a * b) & 3) == (((en[ab].k - oset) / 2) & 3);
+            }
+            if (!fits) continue;
+            const int cost = (al != 0) + 4 * (be != 0) + 8 * (ga != 0);
+            if (cost < bc) {
+                bc = cost;
+                best = code;
+            }
+        }
+        if (best < 0) {
+            r.status = 3;
+            return r;
+        }
+        r.mset = mset;
+        r.oset = oset;
+        r.best = best;
+        for (int ab = 0; ab < 4; ab++) {
+            if (indomain[ab] && zero[ab]) r.zl |= 1u << ab;  // zero on the domain (outside: don't-care)
+            r.dm |= indomain[ab] ? 1u << ab : 0u;
         }
         return r;
     };
@@ -875,74 +926,41 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                         { ok = false; if (!why) why = "table class"; }
                         break;
                     }
-                    std::vector<uint32_t> us = sel_list(d->factor_u_bits + d->factor_u_begin[k],
-                                                        d->factor_u_begin[k + 1] - d->factor_u_begin[k]);
-                    std::vector<uint32_t> vs = sel_list(d->factor_v_bits + d->factor_v_begin[k],
-                                                        d->factor_v_begin[k + 1] - d->factor_v_begin[k]);
-                    for (uint32_t &p : us) {
-                        ok &= p < fwid + n && to_local[p] != ~0u; if (!ok && !why) why = "selector range";
-                        p = ok ? to_local[p] : 0;
+                    // the factor's parity forms as masks over local parameters (XOR: repeated
+                    // selectors cancel, phase_terms.cpp:108-121)
+                    uint64_t us = 0, vs = 0;
+                    for (uint64_t x = d->factor_u_begin[k]; ok && x < d->factor_u_begin[k + 1]; x++) {
+                        const uint32_t p = d->factor_u_bits[x];
+                        ok = p < fwid + n && to_local[p] != ~0u;
+                        if (ok) us ^= 1ull << to_local[p];
                     }
-                    for (uint32_t &p : vs) {
-                        ok &= p < fwid + n && to_local[p] != ~0u; if (!ok && !why) why = "selector range";
-                        p = ok ? to_local[p] : 0;
+                    for (uint64_t x = d->factor_v_begin[k]; ok && x < d->factor_v_begin[k + 1]; x++) {
+                        const uint32_t p = d->factor_v_bits[x];
+                        ok = p < fwid + n && to_local[p] != ~0u;
+                        if (ok) vs ^= 1ull << to_local[p];
                     }
+                    if (!ok) {
+                        if (!why) why = "selector range";
+                        break;
+                    }
+                    const bool ua = us != 0, vb = vs != 0;
+                    // the factor's record depends on the (table, ua, vb) triple only: memoised rule
+                    const FactorRule &fr = factor_rule(tb, ua, vb);
+                    if (fr.status == 2) { ok = false; if (!why) why = "table m/k mismatch"; }
+                    if (fr.status == 3) { ok = false; if (!why) why = "J polynomial"; }
                     if (!ok) break;
-                    const bool ua = !us.empty(), vb = !vs.empty();
-                    // domain and non-zero set
-                    MonoEntry en[4];
-                    int mset = -1, oset = -1, nnz = 0;
-                    bool indomain[4], zero[4];
-                    for (int ab = 0; ab < 4; ab++) {
-                        const int a = ab >> 1, b = ab & 1;
-                        en[ab] = mono_entry(tpa[tb], tpb[tb], a, b);
-                        indomain[ab] = (a == 0 || ua) && (b == 0 || vb);
-                        zero[ab] = en[ab].zero;
-                        if (!indomain[ab] || zero[ab]) continue;
-                        nnz++;
-                        if (mset < 0) mset = en[ab].m;
-                        if (oset < 0) oset = en[ab].k & 1;
-                        if (mset != en[ab].m || oset != (en[ab].k & 1)) { ok = false; if (!why) why = "table m/k mismatch"; }
-                    }
-                    if (!ok) break;
-                    if (nnz == 0) {
+                    if (fr.status == 1) {
                         term_dead = true;  // identically zero factor: the term is exactly 0
                         continue;
                     }
-                    M += mset;
-                    K += oset;
-                    // J increment d(a,b) = (k - o)/2 mod 4 on the non-zero domain points:
-                    // cheapest d00 + al*a + be*b + ga*a*b that matches
-                    int best = -1, bc = 1 << 30;
-                    for (int code = 0; code < 256; code++) {
-                        const int d00 = code & 3, al = (code >> 2) & 3, be = (code >> 4) & 3, ga = (code >> 6) & 3;
-                        if ((!ua && (al || ga)) || (!vb && (be || ga))) continue;
-                        bool fits = true;
-                        for (int ab = 0; ab < 4 && fits; ab++) {
-                            if (!indomain[ab] || zero[ab]) continue;
-                            const int a = ab >> 1, b = ab & 1;
-                            fits = ((d00 + al * a + be * b + ga * a * b) & 3) == (((en[ab].k - oset) / 2) & 3);
-                        }
-                        if (!fits) continue;
-                        const int cost = (al != 0) + 4 * (be != 0) + 8 * (ga != 0);
-                        if (cost < bc) {
-                            bc = cost;
-                            best = code;
-                        }
-                    }
-                    if (best < 0) {
-                        { ok = false; if (!why) why = "J polynomial"; }
-                        break;
-                    }
+                    M += fr.mset;
+                    K += fr.oset;
+                    const int best = fr.best;
                     const int d00 = best & 3, al = (best >> 2) & 3, be = (best >> 4) & 3, ga = (best >> 6) & 3;
                     K += 2 * d00;
-                    // zero function on the domain (points outside it are don't-care -> 0)
-                    uint32_t zl = 0;
-                    for (int ab = 0; ab < 4; ab++) {
-                        if (indomain[ab] && zero[ab]) zl |= 1u << ab;
-                    }
+                    const uint32_t zl = fr.zl, dm = fr.dm;
                     const uint32_t fa = ua ? dict_form(us) : zxs_dev::kFormMask, fbv = vb ? dict_form(vs) : zxs_dev::kFormMask;
-                    nsel += us.size() + vs.size();
+                    nsel += uint64_t(__builtin_popcountll(us) + __builtin_popcountll(vs));
                     // token: record word | (GEN aux word + 1) << 32
                     auto rec = [&](uint32_t kind, uint32_t a_form, uint32_t b_form, uint64_t aux = 0) {
                         tw.push_back(uint64_t(kind << 28 | (b_form & zxs_dev::kFormMask) << zxs_dev::kFormShiftB | (a_form & zxs_dev::kFormMask)) | aux << 32);
@@ -953,8 +971,6 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                     const uint32_t zAn = 0x3u;                   // a == 0
                     const uint32_t zB = vb ? 0xAu : 0u;          // b == 1
                     const uint32_t zBn = 0x5u;                   // b == 0
-                    uint32_t dm = 0;
-                    for (int ab = 0; ab < 4; ab++) dm |= indomain[ab] ? 1u << ab : 0u;
                     auto zis = [&](uint32_t pat) { return (pat & dm) == zl; };
                     if (zl == 0) {
                         if (jnone) continue;  // constant factor
@@ -999,7 +1015,9 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             }
             if (!ok) break;
             // ---- shared-prefix tree over the terms in order, emitted in DFS preorder
+            const auto tm0 = std::chrono::steady_clock::now();
             std::vector<MonoNode> nodes = mono_tree(terms);
+            const auto tm1 = std::chrono::steady_clock::now();
             for (const MonoNode &nd : nodes) comp_depth = std::max(comp_depth, nd.depth + 1);
             // basis and dictionary, weighted by the records actually emitted
             std::vector<uint64_t> usage(form_mask.size(), 0);
@@ -1014,6 +1032,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             if (!ok) break;
             std::vector<uint64_t> basis;
             const std::vector<uint32_t> entry_of = finish_dictionary(usage, basis);
+            const auto tm2 = std::chrono::steady_clock::now();
             tbb.push_back(uint32_t(H.basis.size() + cb.size()));
             cb.insert(cb.end(), basis.begin(), basis.end());
             auto remap = [&](uint32_t r) {
@@ -1198,6 +1217,12 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                 }
             }
             nodes_total += nodes.size();
+            if (std::getenv("ZXS_DEBUG_MONO")) {
+                const auto tm3 = std::chrono::steady_clock::now();
+                auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+                std::fprintf(stderr, "encode_mono: tensor %u: %zu terms %zu forms, tree %.2fs dictionary %.2fs streams %.2fs\n",
+                             t, terms.size(), form_mask.size(), sec(tm0, tm1), sec(tm1, tm2), sec(tm2, tm3));
+            }
         }
         // the narrow mono_kernel must fit (the per-shot path is every large component's fallback
         // and its verification seam); the deduplicated path sizes its own shared memory

@@ -157,6 +157,7 @@ typedef struct zxs_sampler_info {
     uint64_t num_mono_records, num_mono_dead_terms;
     uint64_t num_mono_loads;  /* parameter-plane loads per 32-shot word per pass over the mono chains */
     uint64_t num_tab_entries; /* tabulated-chain ratio entries (small components, shot_kernel) */
+    uint64_t num_mono_negligible_terms; /* terms with |c'| < 2^-40 of their tensor's largest (dropped) */
 } zxs_sampler_info;
 
 /* Message of the calling thread's last failed call ("" if none). */

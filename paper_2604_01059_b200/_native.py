@@ -33,7 +33,8 @@ class SamplerInfo(ctypes.Structure):
         ("device_bytes", ctypes.c_uint64), ("device", ctypes.c_int), ("monomial", ctypes.c_int),
         ("num_mono_components", ctypes.c_uint32), ("num_mono_forms", ctypes.c_uint32),
         ("num_mono_records", ctypes.c_uint64), ("num_mono_dead_terms", ctypes.c_uint64),
-        ("num_mono_loads", ctypes.c_uint64), ("num_tab_entries", ctypes.c_uint64)]
+        ("num_mono_loads", ctypes.c_uint64), ("num_tab_entries", ctypes.c_uint64),
+        ("num_mono_negligible_terms", ctypes.c_uint64)]
 
     def as_dict(self) -> dict:
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -177,6 +177,7 @@ struct zxs_sampler {
     std::vector<uint32_t> dd_tsb, dd_tdb, dd_tw, dd_tbb;  // host copies per mono tensor
     std::vector<unsigned long long> dd_key_mask;          // per mono component (local parameters)
     std::vector<uint16_t> dd_param_map;                   // MonoHost::param_map
+    std::vector<unsigned long long> dd_tread;             // per mono tensor: local parameters it reads
     bool dd_identity_map = true;                          // every mono component's local params = raw
     size_t dd_smem = 0;
     uint32_t dd_seg_buf_words = 0;  // per-warp segment copy in dedup_eval_kernel (0: from global)
@@ -488,6 +489,7 @@ struct MonoHost {
     std::map<uint32_t, uint32_t> tensor_index;  // model tensor -> index into tensor_chunk_begin
     uint32_t max_chain = 0;
     uint64_t records = 0, dead_terms = 0, selectors = 0;
+    uint64_t negligible_terms = 0;  // terms with |c'| < 2^-40 of their tensor's largest (dropped)
     uint64_t loads = 0;  // plane loads per 32-shot word for one pass over every mono chain tensor
     uint64_t nodes = 0;
     std::vector<uint32_t> tensor_dict_begin;  // first dictionary entry per mono tensor, then the total
@@ -508,6 +510,7 @@ struct MonoHost {
     // f_width + chain <= 63, else the f columns the component's tensors read.
     std::vector<uint16_t> param_map;
     std::vector<uint64_t> tensor_loads;             // per mono tensor: plane loads per 32-shot word
+    std::vector<unsigned long long> tensor_read_mask;  // per mono tensor: local parameters its forms read
     // block form tables (dedup_eval_kernel): per block of kDedupWarps segments the
     // tensor dictionary entries its records use; segment streams carry block-local ids
     std::vector<uint32_t> block_forms;
@@ -901,9 +904,10 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
         std::vector<uint4> sg;      // segments (word_begin relative to sw)
         std::vector<uint32_t> tsb;  // per tensor: first segment (relative to sg)
         std::vector<uint64_t> tl;   // per tensor: plane loads per 32-shot word
+        std::vector<unsigned long long> trm;  // per tensor: local parameters read
         std::vector<uint32_t> bf, bfb, tfb;  // block forms, block ends (relative), per tensor first block
         uint32_t max_bf = 0;
-        uint64_t recs = 0, dead = 0, nsel = 0, loads = 0, nodes_total = 0;
+        uint64_t recs = 0, dead = 0, nsel = 0, loads = 0, nodes_total = 0, negligible = 0;
         for (uint32_t t = t0; ok && t < t1; t++) {
             form_id.clear();
             form_mask.clear();
@@ -1014,6 +1018,25 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                 terms.push_back(std::move(mt));
             }
             if (!ok) break;
+            // ---- numerically zero terms: a coefficient below 2^-40 of the tensor's largest is the
+            // rounding residue of an exact cancellation in the reference's decomposition weights
+            // (e.g. 1 + e^{i pi} = 1.2e-16 i; cultivation: a third of the terms, 40+ binades below
+            // the rest). They are dropped; the value moves by < 1e-16 relative, the order of the
+            // reference's own rounding (the h entries are already exact here)
+            {
+                double mx = 0.0;
+                for (const MonoTerm &mt : terms) mx = std::max(mx, std::hypot(mt.re, mt.im));
+                const double floor_c = std::ldexp(mx, -40);
+                size_t keep = 0;
+                for (size_t i = 0; i < terms.size(); i++) {
+                    if (std::hypot(terms[i].re, terms[i].im) >= floor_c) {
+                        if (keep != i) terms[keep] = std::move(terms[i]);
+                        keep++;
+                    }
+                }
+                negligible += terms.size() - keep;
+                terms.resize(keep);
+            }
             // ---- shared-prefix tree over the terms in order, emitted in DFS preorder
             const auto tm0 = std::chrono::steady_clock::now();
             std::vector<MonoNode> nodes = mono_tree(terms);
@@ -1131,6 +1154,11 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             }
             if (ok) close_chunk();
             tl.push_back(loads - loads_before);
+            {
+                unsigned long long rm = 0;  // local parameters any of the tensor's forms reads
+                for (uint64_t fm : form_mask) rm |= fm;
+                trm.push_back(rm);
+            }
             // segment streams: each starts with its first node's ancestors (internal nodes,
             // replayed to rebuild the stack), then the segment's own nodes; flags cleared
             tsb.push_back(uint32_t(sg.size()));
@@ -1258,6 +1286,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                 for (uint64_t v : cb) km |= v;
                 H.comp_key_mask.push_back(km);
                 H.tensor_loads.insert(H.tensor_loads.end(), tl.begin(), tl.end());
+                H.tensor_read_mask.insert(H.tensor_read_mask.end(), trm.begin(), trm.end());
                 const uint32_t fb0 = uint32_t(H.block_forms.size()), blk0 = uint32_t(H.block_form_begin.size() - 1);
                 H.block_forms.insert(H.block_forms.end(), bf.begin(), bf.end());
                 for (uint32_t x : bfb) H.block_form_begin.push_back(x + fb0);
@@ -1279,6 +1308,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             H.max_chain = std::max(H.max_chain, n);
             H.records += recs;
             H.dead_terms += dead;
+            H.negligible_terms += negligible;
             H.selectors += nsel;
             H.loads += loads;
             H.nodes += nodes_total;
@@ -1940,6 +1970,7 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
             s->dd_identity_map = s->dd_identity_map && MH.comps[hc].nf == fwid;
         }
         s->dd_tloads = MH.tensor_loads;
+        s->dd_tread = MH.tensor_read_mask;
         s->dd_block_forms = reinterpret_cast<const uint32_t *>(b + o_bf);
         s->dd_block_form_begin = reinterpret_cast<const uint32_t *>(b + o_bfb);
         s->dd_tfb = MH.tensor_first_block;
@@ -1962,6 +1993,7 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     s->info.num_mono_components = uint32_t(MH.comps.size());
     s->info.num_mono_records = MH.records;
     s->info.num_mono_dead_terms = MH.dead_terms;
+    s->info.num_mono_negligible_terms = MH.negligible_terms;
     s->info.num_mono_forms = uint32_t(MH.dict.size());
     s->info.num_mono_loads = MH.loads;
     m.mech_entry_begin = nullptr;
@@ -2554,7 +2586,10 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
                 const uint32_t p = cd.nf + j - 1;
                 const uint32_t bit_pos = (p < 63 && ((s->dd_key_mask[hc] >> p) & 1ull)) ? p : 64u;
                 s->time_begin(4, st, t0);
-                zxs_dev::dedup_node_prep_kernel<<<ngrid, 256, 0, st>>>(cur, d.nodes[(j - 1) & 1], na, bit_pos, d.table[3]);
+                // the level's key table holds the node keys restricted to what tensor j + 1 reads
+                const unsigned long long tmask = s->dd_tread[cd.first_tensor + 1 + j];
+                zxs_dev::dedup_node_prep_kernel<<<ngrid, 256, 0, st>>>(cur, d.nodes[(j - 1) & 1], na, bit_pos, tmask,
+                                                                      d.table[3]);
                 CK(cudaGetLastError());
                 s->time_end(4, st, t0);
                 dedup_eval(s, cd.first_tensor + 1 + j, d.table[3].ukeys, d.table[3].uslot, limit, d.value, d.partial,

@@ -733,10 +733,10 @@ __global__ void dedup_node_level0_kernel(DedupTable t, const double *__restrict_
 
 // Level j + 1's nodes (table entries parent << 1 | bit): key and prev from the
 // parent (prev = bit ? prev - cur : cur, sampler.cpp:95-98), the key extended
-// by the bit when a later tensor reads it (bit_pos < 64), inserted into the
-// level's key table.
+// by the bit when a later tensor reads it (bit_pos < 64); the key restricted to
+// the parameters the level's tensor reads goes into the level's key table.
 __global__ void dedup_node_prep_kernel(DedupTable nodes, DedupNodeArrays parent, DedupNodeArrays na, uint32_t bit_pos,
-                                       DedupTable keys) {
+                                       unsigned long long read_mask, DedupTable keys) {
     const uint32_t n = min(*nodes.count, nodes.max_ids);
     const uint32_t lane = threadIdx.x & 31u;
     DedupWarpCache cache;
@@ -755,7 +755,8 @@ __global__ void dedup_node_prep_kernel(DedupTable nodes, DedupNodeArrays parent,
             na.key[sl] = key;
             na.prev[sl] = bit ? __dsub_rn(pv, cur) : cur;
         }
-        const uint32_t ks = dedup_insert_warp(keys, key, valid, lane, cache);
+        // the value depends only on the parameters the tensor reads: fewer distinct keys to contract
+        const uint32_t ks = dedup_insert_warp(keys, key & read_mask, valid, lane, cache);
         if (valid) na.kslot[sl] = ks;
     }
 }

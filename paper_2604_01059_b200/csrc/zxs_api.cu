@@ -178,6 +178,7 @@ struct zxs_sampler {
     std::vector<unsigned long long> dd_key_mask;          // per mono component (local parameters)
     std::vector<uint16_t> dd_param_map;                   // MonoHost::param_map
     std::vector<unsigned long long> dd_tread;             // per mono tensor: local parameters it reads
+    std::vector<uint32_t> dd_tspw;                        // per mono tensor: segments per warp per eval item
     bool dd_identity_map = true;                          // every mono component's local params = raw
     size_t dd_smem = 0;
     uint32_t dd_seg_buf_words = 0;  // per-warp segment copy in dedup_eval_kernel (0: from global)
@@ -511,6 +512,7 @@ struct MonoHost {
     std::vector<uint16_t> param_map;
     std::vector<uint64_t> tensor_loads;             // per mono tensor: plane loads per 32-shot word
     std::vector<unsigned long long> tensor_read_mask;  // per mono tensor: local parameters its forms read
+    std::vector<uint32_t> tensor_spw;                  // per mono tensor: segments per warp per eval item
     // block form tables (dedup_eval_kernel): per block of kDedupWarps segments the
     // tensor dictionary entries its records use; segment streams carry block-local ids
     std::vector<uint32_t> block_forms;
@@ -679,6 +681,13 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
     size_t dict_base = 0;
     // ALL plane (>= every mono tensor's local width); all_plane + 1: ZERO; + 2 + j: raw sampled bit j
     const uint32_t all_plane = lf_max + max_chain;
+    // Block form tables (dedup_eval_kernel): 128 B of shared memory per form value; the capacity is
+    // what the kernel's 227 KB leave after its parameter planes and the deepest (Z, J0, J1) stacks
+    // (at least kDedupMaxBlockForms)
+    const uint32_t block_form_cap = std::max<uint32_t>(
+        zxs_dev::kDedupMaxBlockForms,
+        uint32_t((227u * 1024u - 1024u - (all_plane + 2) * 128u -
+                  uint32_t(zxs_dev::kDedupWarps) * zxs_dev::kMonoMaxDepth * 384u) / 128u));
     uint32_t cur_width = 0;                        // param width of the tensor being encoded
     auto dict_form = [&](uint64_t m) -> uint32_t {
         auto it = form_id.find(m);
@@ -905,6 +914,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
         std::vector<uint32_t> tsb;  // per tensor: first segment (relative to sg)
         std::vector<uint64_t> tl;   // per tensor: plane loads per 32-shot word
         std::vector<unsigned long long> trm;  // per tensor: local parameters read
+        std::vector<uint32_t> tspw;           // per tensor: segments per warp in a dedup_eval_kernel item
         std::vector<uint32_t> bf, bfb, tfb;  // block forms, block ends (relative), per tensor first block
         uint32_t max_bf = 0;
         uint64_t recs = 0, dead = 0, nsel = 0, loads = 0, nodes_total = 0, negligible = 0;
@@ -1183,12 +1193,17 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                     sg.push_back(make_uint4(b, uint32_t(sw.size()) - b, nn, 0));
                     i = j;
                 }
-                // block form tables: the dictionary entries each block of kDedupWarps segments
-                // uses; its records are rewritten to block-local ids (kept global when a block
-                // needs more than kDedupMaxBlockForms: tensor_first_block = ~0)
+                // block form tables: the dictionary entries each block of kDedupWarps x spw segments
+                // uses (one dedup_eval_kernel item: every warp walks spw consecutive segments); its
+                // records are rewritten to block-local ids (kept global when a block needs more
+                // than the table holds: tensor_first_block = ~0). spw is the largest of 8, 4, 2, 1
+                // whose blocks all fit and leave at least 32 blocks (work items per key group):
+                // the per-item costs (parameter planes, form values, barriers) amortise over
+                // longer walks
                 const uint32_t s0 = tsb.back(), s1 = uint32_t(sg.size());
+                uint32_t bsegs = zxs_dev::kDedupWarps;
                 auto for_forms = [&](uint32_t b0, const std::function<uint32_t(uint32_t)> &fn) {
-                    for (uint32_t g = b0; g < std::min(s1, b0 + uint32_t(zxs_dev::kDedupWarps)); g++) {
+                    for (uint32_t g = b0; g < std::min(s1, b0 + bsegs); g++) {
                         uint32_t q = sg[g].x;
                         for (uint32_t nn2 = 0; nn2 < sg[g].z; nn2++) {
                             const uint32_t h0 = sw[q], h1 = sw[q + 1], h2 = sw[q + 2];
@@ -1204,29 +1219,46 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                     }
                 };
                 std::vector<std::vector<uint32_t>> lists;
-                bool fits = true;
-                for (uint32_t b0 = s0; b0 < s1; b0 += zxs_dev::kDedupWarps) {
-                    std::map<uint32_t, uint32_t> local;
-                    std::vector<uint32_t> list;
-                    for_forms(b0, [&](uint32_t f) {  // identity pass: collect
-                        if (f != zxs_dev::kMonoNoForm && local.emplace(f, uint32_t(list.size())).second) list.push_back(f);
-                        return f;
-                    });
-                    fits = fits && list.size() <= zxs_dev::kDedupMaxBlockForms;
-                    lists.push_back(std::move(list));
+                bool fits = false;
+                uint32_t spw = 8;
+                for (;; spw /= 2) {
+                    bsegs = zxs_dev::kDedupWarps * spw;
+                    lists.clear();
+                    fits = true;
+                    for (uint32_t b0 = s0; b0 < s1; b0 += bsegs) {
+                        std::unordered_map<uint32_t, uint32_t> local;
+                        std::vector<uint32_t> list;
+                        for_forms(b0, [&](uint32_t f) {  // identity pass: collect
+                            if (f != zxs_dev::kMonoNoForm && local.emplace(f, uint32_t(list.size())).second) list.push_back(f);
+                            return f;
+                        });
+                        fits = fits && list.size() <= block_form_cap;
+                        lists.push_back(std::move(list));
+                    }
+                    if (spw == 1 || (fits && lists.size() >= 32)) break;
                 }
+                if (std::getenv("ZXS_DEBUG_MONO")) {
+                    size_t mx = 0, over = 0;
+                    for (const auto &l : lists) {
+                        mx = std::max(mx, l.size());
+                        over += l.size() > block_form_cap;
+                    }
+                    std::fprintf(stderr, "encode_mono: tensor %u: %u segments per warp, %zu blocks, max %zu forms per block, %zu over %u\n",
+                                 t, spw, lists.size(), mx, over, block_form_cap);
+                }
+                tspw.push_back(spw);
                 if (!fits) {
                     tfb.push_back(0xffffffffu);
                 } else {
                     tfb.push_back(uint32_t(bfb.size()));
                     size_t k = 0;
-                    for (uint32_t b0 = s0; b0 < s1; b0 += zxs_dev::kDedupWarps, k++) {
-                        std::map<uint32_t, uint32_t> local;
+                    for (uint32_t b0 = s0; b0 < s1; b0 += bsegs, k++) {
+                        std::unordered_map<uint32_t, uint32_t> local;
                         for (uint32_t i = 0; i < lists[k].size(); i++) local.emplace(lists[k][i], i);
                         for_forms(b0, [&](uint32_t f) { return f == zxs_dev::kMonoNoForm ? f : local.at(f); });
                         // one-form records grouped by kind (ADD, SUB, ADD2, Z, ZN: the header's counts),
                         // so mono_walk_fv runs one fixed operation per loop
-                        for (uint32_t g = b0; g < std::min(s1, b0 + uint32_t(zxs_dev::kDedupWarps)); g++) {
+                        for (uint32_t g = b0; g < std::min(s1, b0 + bsegs); g++) {
                             uint32_t q = sg[g].x;
                             for (uint32_t nn2 = 0; nn2 < sg[g].z; nn2++) {
                                 const uint32_t h0 = sw[q], h1 = sw[q + 1], h2 = sw[q + 2];
@@ -1243,6 +1275,8 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                         bfb.push_back(uint32_t(bf.size()));
                     }
                 }
+            } else {
+                tspw.push_back(1);
             }
             nodes_total += nodes.size();
             if (std::getenv("ZXS_DEBUG_MONO")) {
@@ -1287,6 +1321,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                 H.comp_key_mask.push_back(km);
                 H.tensor_loads.insert(H.tensor_loads.end(), tl.begin(), tl.end());
                 H.tensor_read_mask.insert(H.tensor_read_mask.end(), trm.begin(), trm.end());
+                H.tensor_spw.insert(H.tensor_spw.end(), tspw.begin(), tspw.end());
                 const uint32_t fb0 = uint32_t(H.block_forms.size()), blk0 = uint32_t(H.block_form_begin.size() - 1);
                 H.block_forms.insert(H.block_forms.end(), bf.begin(), bf.end());
                 for (uint32_t x : bfb) H.block_form_begin.push_back(x + fb0);
@@ -1971,6 +2006,7 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         }
         s->dd_tloads = MH.tensor_loads;
         s->dd_tread = MH.tensor_read_mask;
+        s->dd_tspw = MH.tensor_spw;
         s->dd_block_forms = reinterpret_cast<const uint32_t *>(b + o_bf);
         s->dd_block_form_begin = reinterpret_cast<const uint32_t *>(b + o_bfb);
         s->dd_tfb = MH.tensor_first_block;
@@ -2286,13 +2322,15 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const unsigned long long *keys, con
             e.first_block = s->dd_tfb[mt];
             e.stage_entries = s->dd_stage_entries ? 1u : 0u;
         }
+        e.segs_per_warp = mt < s->dd_tspw.size() ? s->dd_tspw[mt] : 1;
         e.n_dev = n_dev;
         e.n_mult = n_mult;
         e.stats = s->dd_dev_stats;
         e.tensor_loads = mt < s->dd_tloads.size() ? s->dd_tloads[mt] : 0;
         s->dd_stats[4] += 1;
+        const uint32_t bsegs = zxs_dev::kDedupWarps * std::max(e.segs_per_warp, 1u);
         const uint64_t items = uint64_t((e.n_keys + zxs_dev::kDedupKeysPerWarp - 1) / zxs_dev::kDedupKeysPerWarp) *
-                               ((ng + zxs_dev::kDedupWarps - 1) / zxs_dev::kDedupWarps);
+                               ((ng + bsegs - 1) / bsegs);
         const unsigned grid = unsigned(std::min<uint64_t>(items, uint64_t(s->sm_count)));
         cudaEvent_t t0 = nullptr;
         s->time_begin(3, st, t0);
@@ -3646,6 +3684,9 @@ zxs_status zxs_debug_mono_layout(const zxs_model_desc *desc, uint64_t min_factor
         blob.insert(blob.end(), H.tensor_first_block.begin(), H.tensor_first_block.end());
         blob.insert(blob.end(), H.block_form_begin.begin(), H.block_form_begin.end());
         blob.insert(blob.end(), H.block_forms.begin(), H.block_forms.end());
+        // segments per warp per eval item, per mono tensor (a block = 16 x spw segments)
+        blob.push_back(uint32_t(H.tensor_spw.size()));
+        blob.insert(blob.end(), H.tensor_spw.begin(), H.tensor_spw.end());
         *needed = blob.size();
         if (out && cap >= blob.size()) std::memcpy(out, blob.data(), blob.size() * 4);
     });

@@ -38,7 +38,7 @@ namespace zxs_dev {
 constexpr unsigned long long kDedupEmpty = ~0ull;  // keys use at most 63 raw parameter bits
 constexpr int kDedupWarps = 16;                    // dedup_eval_kernel: warps per CTA (one segment each)
 constexpr uint32_t kDedupKeysPerWarp = 1024;       // 32 keys per lane (NW = 1)
-constexpr uint32_t kDedupMaxBlockForms = 1024;     // form values per block table (128 B each in shared memory)
+constexpr uint32_t kDedupMaxBlockForms = 1024;     // form values per block table at least (128 B each in shared memory)
 
 struct DedupTable {
     unsigned long long *keys;  // [mask + 1], kDedupEmpty when free
@@ -265,6 +265,7 @@ struct DedupEvalArgs {
     const uint32_t *block_form_begin;
     uint32_t first_block;
     uint32_t table_bytes;  // shared memory before the planes: dictionary or form values
+    uint32_t segs_per_warp;  // block = kDedupWarps x segs_per_warp consecutive segments (block form tables)
     uint32_t stage_entries;  // block tables: stage the forms' first dictionary entries in shared memory
 };
 
@@ -372,7 +373,9 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
         atomicAdd(&h.stats[1], h.tensor_loads * ((n_keys + 31) / 32) * 4);
     }
     const uint32_t n_kg = (n_keys + kDedupKeysPerWarp - 1) / kDedupKeysPerWarp;
-    const uint32_t n_blk = (h.n_segs + kDedupWarps - 1) / kDedupWarps;
+    const uint32_t spw = max(h.segs_per_warp, 1u);  // segments each warp walks per item
+    const uint32_t bsegs = kDedupWarps * spw;       // segments per block (one form table)
+    const uint32_t n_blk = (h.n_segs + bsegs - 1) / bsegs;
     const uint64_t n_items = uint64_t(n_kg) * n_blk;
     uint32_t cur_kg = 0xffffffffu;
     for (uint64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -427,8 +430,9 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
             __syncthreads();
             cur_blk = blk;
         }
-        const uint32_t seg = blk * kDedupWarps + warp;
-        if (seg >= h.n_segs) continue;
+        for (uint32_t si = 0; si < spw; si++) {
+        const uint32_t seg = blk * bsegs + warp * spw + si;
+        if (seg >= h.n_segs) break;
         const uint4 sgd = __ldg(h.segs + seg);
         // the warp's segment into shared memory once (the walk's record loads are
         // warp-uniform and serial: broadcast LDS instead of L1/L2 round trips); a CTA
@@ -459,6 +463,7 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
 #pragma unroll
         for (int s = 0; s < 32; s++) {
             if (k0 + s < n_keys) out[uint64_t(s) * h.n_segs] = acc[s];
+        }
         }
     }
 }

@@ -73,7 +73,10 @@ def mono_layout(arrays, min_factors=0):
     bfb = buf[o:o + n_bfb].astype(np.int64)
     o += n_bfb
     bforms = buf[o:o + n_bf].astype(np.int64)
-    return dict(tfb=tfb, bfb=bfb, bforms=bforms, comps=comps, flags=flags, tcb=tcb, chunks=chunks, dict=dict_, tdb=tdb, twidth=twidth,
+    o += n_bf
+    n_spw = int(buf[o])
+    spw = buf[o + 1:o + 1 + n_spw].astype(np.int64)
+    return dict(tfb=tfb, bfb=bfb, bforms=bforms, spw=spw, comps=comps, flags=flags, tcb=tcb, chunks=chunks, dict=dict_, tdb=tdb, twidth=twidth,
                 tbb=tbb, basis=basis, all_plane=all_plane, words=words, tsb=tsb, segs=segs,
                 seg_words=seg_words, key_mask=key_mask)
 
@@ -188,7 +191,7 @@ def emulate_segments(lay, t, P):
         acc = np.zeros(S)
         fb = int(lay["tfb"][t])
         if fb != 0xFFFFFFFF:  # block-local form ids -> the tensor dictionary's
-            blk = fb + (g - g0) // 16
+            blk = fb + (g - g0) // (16 * int(lay["spw"][t]))  # a block: 16 warps x spw segments
             table = lay["bforms"][lay["bfb"][blk]:lay["bfb"][blk + 1]]
             f = (lambda x, table=table: form(int(table[x])))
         else:

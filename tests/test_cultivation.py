@@ -86,7 +86,8 @@ def test_headline_batch_against_reference(name, path, block, singles):
     assert cs.info["num_mono_components"] == 1
     got = _sample(cs, shots, seed, first)
     ref = _ref(path)
-    want = ref.sample_rb(block, seed, first_shot=first + (shots - block), threads=os.cpu_count())
+    # 64-shot batches: every host thread gets work (the reference's per-shot cost is ~0.7 s here)
+    want = ref.sample_rb(block, seed, first_shot=first + (shots - block), batch_size=64, threads=os.cpu_count())
     w0 = (shots - block) // 64
     assert np.array_equal(got[:, w0:w0 + want.shape[1]], want)
     rng = np.random.default_rng(17)

@@ -684,6 +684,11 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
     // Block form tables (dedup_eval_kernel): 128 B of shared memory per form value; the capacity is
     // what the kernel's 227 KB leave after its parameter planes and the deepest (Z, J0, J1) stacks
     // (at least kDedupMaxBlockForms)
+    // summation segments per tensor at most (the canonical order's granularity; ZXS_DEDUP_SEGS)
+    uint32_t max_segs = zxs_dev::kDedupSegs;
+    if (const char *e = std::getenv("ZXS_DEDUP_SEGS")) {
+        max_segs = uint32_t(std::min<long>(zxs_dev::kDedupSegs, std::max(16L, std::atol(e))));
+    }
     const uint32_t block_form_cap = std::max<uint32_t>(
         zxs_dev::kDedupMaxBlockForms,
         uint32_t((227u * 1024u - 1024u - (all_plane + 2) * 128u -
@@ -1091,7 +1096,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             std::vector<uint8_t> seg_start(nodes.size(), 0);
             {
                 const uint32_t G = std::max<uint32_t>(
-                    1, std::min<uint32_t>(zxs_dev::kDedupSegs, uint32_t(nodes.size() / 8)));
+                    1, std::min<uint32_t>(max_segs, uint32_t(nodes.size() / 8)));
                 uint64_t total = 0;
                 for (const MonoNode &nd : nodes) total += nd.recs.size() + (nd.leaf ? 8 : 1);
                 uint64_t cum = 0, k = 1;

@@ -179,6 +179,7 @@ struct zxs_sampler {
     std::vector<uint16_t> dd_param_map;                   // MonoHost::param_map
     std::vector<unsigned long long> dd_tread;             // per mono tensor: local parameters it reads
     std::vector<uint32_t> dd_tspw;                        // per mono tensor: segments per warp per eval item
+    uint32_t dd_stack_words = 0;                          // dedup_eval_kernel stack area (words)
     bool dd_identity_map = true;                          // every mono component's local params = raw
     size_t dd_smem = 0;
     uint32_t dd_seg_buf_words = 0;  // per-warp segment copy in dedup_eval_kernel (0: from global)
@@ -2019,8 +2020,10 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         for (uint32_t x : MH.tensor_first_block) all_blocks = all_blocks && x != 0xffffffffu;
         s->dd_table_bytes = uint32_t(std::max<size_t>(all_blocks ? 16 : size_t(ma.max_dict) * 16,
                                                       size_t(MH.max_block_forms) * 128));
-        s->dd_smem = size_t(s->dd_table_bytes) + size_t(MH.all_plane + 2) * 32 * 4 +
-                     size_t(zxs_dev::kDedupWarps) * ma.stack_depth * 96 * 4;
+        // stacks: kDedupWarps x depth x (Z, J0, J1) words per lane; between items the same area
+        // holds the key group's 64 raw parameter planes (64 x 33 words)
+        s->dd_stack_words = std::max<uint32_t>(zxs_dev::kDedupWarps * ma.stack_depth * 96, 64 * 33);
+        s->dd_smem = size_t(s->dd_table_bytes) + size_t(MH.all_plane + 2) * 32 * 4 + size_t(s->dd_stack_words) * 4;
         uint32_t max_seg = 0;
         for (const uint4 &g : MH.segs) max_seg = std::max(max_seg, g.y);
         s->dd_seg_buf_words = (max_seg + 3) & ~3u;
@@ -2315,6 +2318,7 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const unsigned long long *keys, con
         e.all_plane = m.all_plane;
         e.n_planes = m.all_plane + 2;
         e.stack_depth = m.stack_depth;
+        e.stack_words = s->dd_stack_words;
         e.keys = keys + r0;
         e.n_keys = std::min(round, n - r0);
         e.key_base = r0;

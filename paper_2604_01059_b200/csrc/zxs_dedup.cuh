@@ -250,6 +250,7 @@ struct DedupEvalArgs {
     uint32_t width;                   // W
     uint32_t all_plane, n_planes;     // plane indices the dictionary uses: [0, W), ALL, ZERO = ALL + 1
     uint32_t stack_depth;
+    uint32_t stack_words;             // stack area (>= kDedupWarps x depth x 96, >= 64 x 33 raw planes)
     const unsigned long long *keys;   // the round's keys
     uint32_t n_keys;                  // keys (n_dev: at most this many, the rest read from n_dev)
     const uint32_t *n_dev;            // device-side key count (the table's), or null
@@ -299,21 +300,65 @@ __device__ __forceinline__ void mono_walk_fv(const uint32_t *w, uint32_t nnodes,
             uint32_t zz = z.w[0], a0 = j0.w[0], a1 = j1.w[0];
             const uint32_t n_add = h1 & 0xffu, n_sub = (h1 >> 8) & 0xffu, n_add2 = (h1 >> 16) & 0xffu;
             const uint32_t n_z = h1 >> 24, n_zn = h2 & 0xffu;
+            // J (mod 4) and Z are order-free sums / ORs: two independent chains per kind (the
+            // form loads of consecutive records overlap), merged at the node's end
+            auto fvr = [&](uint32_t i) { return fv[(w[i] & kFormMask) * 32]; };
             uint32_t e = q + n_add;
-            for (; q < e; q++) {  // J += a
-                const uint32_t x = fv[(w[q] & kFormMask) * 32];
+            uint32_t b0 = 0, b1 = 0;  // J += a, second chain
+            for (; q + 1 < e; q += 2) {
+                const uint32_t x = fvr(q), y = fvr(q + 1);
+                a1 ^= a0 & x;
+                a0 ^= x;
+                b1 ^= b0 & y;
+                b0 ^= y;
+            }
+            if (q < e) {
+                const uint32_t x = fvr(q++);
                 a1 ^= a0 & x;
                 a0 ^= x;
             }
-            for (e += n_sub; q < e; q++) {  // J -= a
-                const uint32_t x = fv[(w[q] & kFormMask) * 32];
-                a1 ^= ~a0 & x;
-                a0 ^= x;
+            uint32_t c0 = 0, c1 = 0, d0 = 0, d1 = 0;  // J -= a: the subtrahends summed in two chains
+            for (e += n_sub; q + 1 < e; q += 2) {
+                const uint32_t x = fvr(q), y = fvr(q + 1);
+                c1 ^= c0 & x;
+                c0 ^= x;
+                d1 ^= d0 & y;
+                d0 ^= y;
             }
-            for (e += n_add2; q < e; q++) a1 ^= fv[(w[q] & kFormMask) * 32];  // J += 2a
-            for (e += n_z; q < e; q++) zz |= fv[(w[q] & kFormMask) * 32];     // Z |= a
-            for (e += n_zn; q < e; q++) zz |= ~fv[(w[q] & kFormMask) * 32];   // Z |= ~a
-            z.w[0] = zz;
+            if (q < e) {
+                const uint32_t x = fvr(q++);
+                c1 ^= c0 & x;
+                c0 ^= x;
+            }
+            uint32_t t1 = 0;  // J += 2a
+            for (e += n_add2; q + 1 < e; q += 2) {
+                a1 ^= fvr(q);
+                t1 ^= fvr(q + 1);
+            }
+            if (q < e) a1 ^= fvr(q++);
+            uint32_t z2 = 0;  // Z |= a, Z |= ~a
+            for (e += n_z; q + 1 < e; q += 2) {
+                zz |= fvr(q);
+                z2 |= fvr(q + 1);
+            }
+            if (q < e) zz |= fvr(q++);
+            for (e += n_zn; q + 1 < e; q += 2) {
+                zz |= ~fvr(q);
+                z2 |= ~fvr(q + 1);
+            }
+            if (q < e) zz |= ~fvr(q++);
+            {  // (a) += (b), (c) += (d), (a) -= (c), mod 4 on two bit planes
+                const uint32_t cy = a0 & b0;
+                a0 ^= b0;
+                a1 ^= b1 ^ cy ^ t1;
+                const uint32_t cd = c0 & d0;
+                c0 ^= d0;
+                c1 ^= d1 ^ cd;
+                const uint32_t br = ~a0 & c0;
+                a0 ^= c0;
+                a1 ^= c1 ^ br;
+            }
+            z.w[0] = zz | z2;
             j0.w[0] = a0;
             j1.w[0] = a1;
         }
@@ -354,8 +399,8 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
     uint32_t *stack_all = planes + h.n_planes * 32;                  // per warp [depth][3][lane]
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     BW<1> *stk = reinterpret_cast<BW<1> *>(stack_all + warp * h.stack_depth * 96) + lane;
-    uint32_t *segbuf = stack_all + kDedupWarps * h.stack_depth * 96 + warp * h.seg_buf_words;
-    uint4 *sent = reinterpret_cast<uint4 *>(stack_all + kDedupWarps * h.stack_depth * 96 + kDedupWarps * h.seg_buf_words);
+    uint32_t *segbuf = stack_all + h.stack_words + warp * h.seg_buf_words;
+    uint4 *sent = reinterpret_cast<uint4 *>(stack_all + h.stack_words + kDedupWarps * h.seg_buf_words);
     uint32_t have_seg = 0xffffffffu;  // segment currently in segbuf
     const char *pl = reinterpret_cast<const char *>(planes + lane);
 
@@ -381,21 +426,30 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
     for (uint64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
         const uint32_t kg = uint32_t(it / n_blk), blk = uint32_t(it % n_blk);
         if (kg != cur_kg) {
-            __syncthreads();  // every warp is done with the previous planes
-            // plane b, lane l, bit s = parity(basis_b & key[kg * 1024 + 32 l + s])
+            __syncthreads();  // every warp is done with the previous planes (and its stack)
+            // plane b, lane l, bit s = parity(basis_b & key[kg * 1024 + 32 l + s]): the key group's
+            // raw parameter planes by warp transposes (row l of 32 keys: lane p gets parameter p's
+            // word), staged in the stack area, then each basis plane as the XOR of its parameters'
+            uint32_t *raw = stack_all;  // [64 parameters][33] (padded: conflict-free)
             for (uint32_t l = warp; l < 32; l += kDedupWarps) {
                 const uint32_t ki = kg * kDedupKeysPerWarp + l * 32 + lane;
                 const unsigned long long key = ki < n_keys ? __ldg(h.keys + ki) : 0ull;
+                raw[lane * 33 + l] = warp_transpose32(uint32_t(key), lane);
+                raw[(32 + lane) * 33 + l] = warp_transpose32(uint32_t(key >> 32), lane);
+            }
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < h.width * 32; i += blockDim.x) {
+                const uint32_t b = i >> 5, l = i & 31u;
+                uint32_t v = 0;
+                for (unsigned long long m = __ldg(h.basis + b); m; m &= m - 1) v ^= raw[(__ffsll((long long)m) - 1) * 33 + l];
+                planes[b * 32 + l] = v;
+            }
+            __syncthreads();
+            if (threadIdx.x < 32) {
                 uint32_t all = 0;
-                for (uint32_t b = 0; b < h.width; b++) {
-                    const uint32_t v = __ballot_sync(kFull, __popcll(key & __ldg(h.basis + b)) & 1);
-                    all ^= v;
-                    if (lane == 0) planes[b * 32 + l] = v;
-                }
-                if (lane == 0) {
-                    planes[h.all_plane * 32 + l] = all;
-                    planes[(h.all_plane + 1) * 32 + l] = 0u;
-                }
+                for (uint32_t b = 0; b < h.width; b++) all ^= planes[b * 32 + threadIdx.x];
+                planes[h.all_plane * 32 + threadIdx.x] = all;
+                planes[(h.all_plane + 1) * 32 + threadIdx.x] = 0u;
             }
             __syncthreads();
             cur_kg = kg;

@@ -3111,10 +3111,10 @@ zxs_status zxs_sample(zxs_sampler *s, uint32_t expected_mode, uint64_t seed, uin
         }
         // chunk: multiple of 64 shots, ~64 MiB of output per buffer (copies overlap the next chunk);
         // on the deduplicated path, whose per-batch contraction amortises, up to 2^28 shots while
-        // a buffer stays within 512 MiB
+        // a buffer stays within 1 GiB
         uint64_t chunk_words = std::max<uint64_t>(1, (uint64_t(64) << 20) / (8ull * nout));
         if (s->has_mono && s->dedup) {
-            chunk_words = std::max<uint64_t>(chunk_words, std::min<uint64_t>(kMaxBatchShots / 64, (uint64_t(512) << 20) / (8ull * nout)));
+            chunk_words = std::max<uint64_t>(chunk_words, std::min<uint64_t>(kMaxBatchShots / 64, (uint64_t(1024) << 20) / (8ull * nout)));
         }
         chunk_words = std::min(chunk_words, words);
         const size_t buf_bytes = size_t(chunk_words) * nout * 8;

@@ -38,6 +38,9 @@ namespace zxs_dev {
 constexpr unsigned long long kDedupEmpty = ~0ull;  // keys use at most 63 raw parameter bits
 constexpr int kDedupWarps = 16;                    // dedup_eval_kernel: warps per CTA (one segment each)
 constexpr uint32_t kDedupKeysPerWarp = 1024;       // 32 keys per lane (NW = 1)
+#ifndef ZXS_WALK_ILP
+#define ZXS_WALK_ILP 0  // 1: two record chains per kind in mono_walk_fv (measured slower: 197 vs 183 ms per 2^28 config-3 batch)
+#endif
 constexpr uint32_t kDedupMaxBlockForms = 1024;     // form values per block table at least (128 B each in shared memory)
 
 struct DedupTable {
@@ -300,9 +303,10 @@ __device__ __forceinline__ void mono_walk_fv(const uint32_t *w, uint32_t nnodes,
             uint32_t zz = z.w[0], a0 = j0.w[0], a1 = j1.w[0];
             const uint32_t n_add = h1 & 0xffu, n_sub = (h1 >> 8) & 0xffu, n_add2 = (h1 >> 16) & 0xffu;
             const uint32_t n_z = h1 >> 24, n_zn = h2 & 0xffu;
+            auto fvr = [&](uint32_t i) { return fv[(w[i] & kFormMask) * 32]; };
+#if ZXS_WALK_ILP
             // J (mod 4) and Z are order-free sums / ORs: two independent chains per kind (the
             // form loads of consecutive records overlap), merged at the node's end
-            auto fvr = [&](uint32_t i) { return fv[(w[i] & kFormMask) * 32]; };
             uint32_t e = q + n_add;
             uint32_t b0 = 0, b1 = 0;  // J += a, second chain
             for (; q + 1 < e; q += 2) {
@@ -359,6 +363,23 @@ __device__ __forceinline__ void mono_walk_fv(const uint32_t *w, uint32_t nnodes,
                 a1 ^= c1 ^ br;
             }
             z.w[0] = zz | z2;
+#else
+            uint32_t e = q + n_add;
+            for (; q < e; q++) {  // J += a
+                const uint32_t x = fvr(q);
+                a1 ^= a0 & x;
+                a0 ^= x;
+            }
+            for (e += n_sub; q < e; q++) {  // J -= a
+                const uint32_t x = fvr(q);
+                a1 ^= ~a0 & x;
+                a0 ^= x;
+            }
+            for (e += n_add2; q < e; q++) a1 ^= fvr(q);  // J += 2a
+            for (e += n_z; q < e; q++) zz |= fvr(q);     // Z |= a
+            for (e += n_zn; q < e; q++) zz |= ~fvr(q);   // Z |= ~a
+            z.w[0] = zz;
+#endif
             j0.w[0] = a0;
             j1.w[0] = a1;
         }

@@ -870,7 +870,11 @@ struct DedupNodePassArgs {
 
 // One position for every shot: lane = shots s + 32 g (G groups per warp
 // iteration, packed into 64/128-bit output stores by lane 0).
-constexpr int kNodePassG = 4;
+#ifndef ZXS_NODE_G
+#define ZXS_NODE_G 4
+#endif
+constexpr int kNodePassG = ZXS_NODE_G;  // 4 or 8
+static_assert(kNodePassG % 4 == 0, "node pass stores 128-bit groups of four 32-shot words");
 __global__ void __launch_bounds__(256) dedup_node_pass_kernel(const __grid_constant__ DedupNodePassArgs a) {
     constexpr int G = kNodePassG;
     const uint32_t lane = threadIdx.x & 31u;
@@ -883,7 +887,15 @@ __global__ void __launch_bounds__(256) dedup_node_pass_kernel(const __grid_const
     const uint64_t shots64 = (a.shots + 63) & ~uint64_t(63);
     // this batch's record words (a split batch's rows continue past them: out_ld32 is only the stride)
     const uint64_t out_words = min(a.out_ld32, shots64 / 32);
-    for (uint64_t s0 = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * G; s0 < shots64; s0 += stride) {
+    // the shots' node slots one iteration ahead (the HBM latency overlaps the previous iteration)
+    uint32_t nxt[G];
+    const uint64_t first_s0 = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * G;
+#pragma unroll
+    for (int g = 0; g < G; g++) {
+        const uint64_t sg = first_s0 + 32 * g + lane;
+        nxt[g] = sg < a.shots ? a.slot[sg] : 0u;
+    }
+    for (uint64_t s0 = first_s0; s0 < shots64; s0 += stride) {
         uint64_t s[G];
         bool valid[G], bit[G];
         uint32_t node[G];
@@ -891,7 +903,9 @@ __global__ void __launch_bounds__(256) dedup_node_pass_kernel(const __grid_const
         for (int g = 0; g < G; g++) {
             s[g] = s0 + 32 * g + lane;
             valid[g] = s[g] < a.shots;
-            node[g] = valid[g] ? __ldg(a.slot + s[g]) : 0u;  // node arrays are indexed by table slot
+            node[g] = valid[g] ? nxt[g] : 0u;  // node arrays are indexed by table slot
+            const uint64_t sn = s[g] + stride;
+            nxt[g] = sn < a.shots ? a.slot[sn] : 0u;
         }
         DedupNodeRec r[G];
         bool need = false;  // a draw is needed unless every node's bit is certain (T = 0 or 2^53, no error)
@@ -943,7 +957,10 @@ __global__ void __launch_bounds__(256) dedup_node_pass_kernel(const __grid_const
             if (a.out32) {
                 uint32_t *row = a.out32 + a.out * a.out_ld32;
                 if (w0 + G <= out_words && (reinterpret_cast<uintptr_t>(row + w0) & 15) == 0) {
-                    *reinterpret_cast<uint4 *>(row + w0) = make_uint4(word[0], word[1], word[2], word[3]);
+#pragma unroll
+                    for (int g = 0; g < G; g += 4) {
+                        *reinterpret_cast<uint4 *>(row + w0 + g) = make_uint4(word[g], word[g + 1], word[g + 2], word[g + 3]);
+                    }
                 } else {
 #pragma unroll
                     for (int g = 0; g < G; g++) {

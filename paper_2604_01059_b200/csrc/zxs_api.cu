@@ -180,13 +180,11 @@ struct zxs_sampler {
     std::vector<unsigned long long> dd_tread;             // per mono tensor: local parameters it reads
     std::vector<uint32_t> dd_tspw;                        // per mono tensor: segments per warp per eval item
     uint32_t dd_stack_words = 0;                          // dedup_eval_kernel stack area (words)
+    std::vector<uint4> dd_t_layout;                       // per mono tensor: {table bytes, segbuf words, stage, smem}
     bool dd_identity_map = true;                          // every mono component's local params = raw
     size_t dd_smem = 0;
-    uint32_t dd_seg_buf_words = 0;  // per-warp segment copy in dedup_eval_kernel (0: from global)
     const uint32_t *dd_block_forms = nullptr, *dd_block_form_begin = nullptr;
     std::vector<uint32_t> dd_tfb;    // per mono tensor: first block form table (~0: dictionary ids)
-    uint32_t dd_table_bytes = 0;
-    bool dd_stage_entries = false;
     int dd_init_occ = 1, dd_ar_occ = 1, dd_fused_occ = 1, dd_raw_occ = 1, dd_node_occ = 1;  // resident blocks per SM (per-shot dedup kernels)
     bool dd_async = true;                 // key counts stay on the device (ZXS_DEDUP_SYNC=1: host round trips)
     bool dd_fused = true;                 // short chains in one per-shot kernel (ZXS_DEDUP_FUSED=0: step by step)
@@ -2016,21 +2014,41 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         s->dd_block_forms = reinterpret_cast<const uint32_t *>(b + o_bf);
         s->dd_block_form_begin = reinterpret_cast<const uint32_t *>(b + o_bfb);
         s->dd_tfb = MH.tensor_first_block;
-        bool all_blocks = true;  // every tensor walks block form tables (the dictionary is never staged whole)
-        for (uint32_t x : MH.tensor_first_block) all_blocks = all_blocks && x != 0xffffffffu;
-        s->dd_table_bytes = uint32_t(std::max<size_t>(all_blocks ? 16 : size_t(ma.max_dict) * 16,
-                                                      size_t(MH.max_block_forms) * 128));
         // stacks: kDedupWarps x depth x (Z, J0, J1) words per lane; between items the same area
         // holds the key group's 64 raw parameter planes (64 x 33 words)
         s->dd_stack_words = std::max<uint32_t>(zxs_dev::kDedupWarps * ma.stack_depth * 96, 64 * 33);
-        s->dd_smem = size_t(s->dd_table_bytes) + size_t(MH.all_plane + 2) * 32 * 4 + size_t(s->dd_stack_words) * 4;
-        uint32_t max_seg = 0;
-        for (const uint4 &g : MH.segs) max_seg = std::max(max_seg, g.y);
-        s->dd_seg_buf_words = (max_seg + 3) & ~3u;
-        if (s->dd_smem + size_t(zxs_dev::kDedupWarps) * s->dd_seg_buf_words * 4 > 227 * 1024) s->dd_seg_buf_words = 0;
-        s->dd_smem += size_t(zxs_dev::kDedupWarps) * s->dd_seg_buf_words * 4;
-        s->dd_stage_entries = MH.max_block_forms > 0 && s->dd_smem + size_t(MH.max_block_forms) * 16 <= 227 * 1024;
-        if (s->dd_stage_entries) s->dd_smem += size_t(MH.max_block_forms) * 16;
+        // dedup_eval_kernel's shared memory, per tensor: its form table (the block form values, or
+        // the whole dictionary when a block does not fit), planes, stacks, then -- when they fit --
+        // a copy of each warp's segment (record words read by LDS instead of L1/L2) and the staged
+        // first dictionary entries of the block's forms
+        const size_t fixed = size_t(MH.all_plane + 2) * 32 * 4 + size_t(s->dd_stack_words) * 4;
+        const size_t nmt = MH.tensor_width.size();
+        s->dd_t_layout.assign(nmt, uint4{0, 0, 0, 0});
+        s->dd_smem = 0;
+        for (size_t t = 0; t < nmt; t++) {
+            uint32_t bforms = 0;
+            const bool blocks = t < MH.tensor_first_block.size() && MH.tensor_first_block[t] != 0xffffffffu;
+            if (blocks) {
+                const uint32_t b0 = MH.tensor_first_block[t];
+                const uint32_t nsg = MH.tensor_seg_begin[t + 1] - MH.tensor_seg_begin[t];
+                const uint32_t bsegs = zxs_dev::kDedupWarps * std::max<uint32_t>(1, MH.tensor_spw[t]);
+                for (uint32_t b = b0; b < b0 + (nsg + bsegs - 1) / bsegs; b++) {
+                    bforms = std::max(bforms, MH.block_form_begin[b + 1] - MH.block_form_begin[b]);
+                }
+            }
+            const uint32_t table = uint32_t(blocks ? std::max<size_t>(16, size_t(bforms) * 128)
+                                                   : size_t(MH.tensor_dict_begin[t + 1] - MH.tensor_dict_begin[t]) * 16);
+            uint32_t max_seg = 0;
+            for (uint32_t g = MH.tensor_seg_begin[t]; g < MH.tensor_seg_begin[t + 1]; g++) max_seg = std::max(max_seg, MH.segs[g].y);
+            size_t smem = table + fixed;
+            uint32_t segbuf = (max_seg + 3) & ~3u;
+            if (smem + size_t(zxs_dev::kDedupWarps) * segbuf * 4 > 227 * 1024) segbuf = 0;
+            smem += size_t(zxs_dev::kDedupWarps) * segbuf * 4;
+            const bool stage = blocks && bforms > 0 && smem + size_t(bforms) * 16 <= 227 * 1024;
+            if (stage) smem += size_t(bforms) * 16;
+            s->dd_t_layout[t] = make_uint4(table, segbuf, stage ? 1u : 0u, uint32_t(smem));
+            s->dd_smem = std::max(s->dd_smem, smem);
+        }
         s->dedup = s->dd_smem <= 227 * 1024 && s->dd_key_mask.size() == MH.comps.size();
         if (const char *e = std::getenv("ZXS_DEDUP")) s->dedup = s->dedup && std::atoi(e) != 0;
     }
@@ -2323,13 +2341,14 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const unsigned long long *keys, con
         e.n_keys = std::min(round, n - r0);
         e.key_base = r0;
         e.partial = partial;
-        e.seg_buf_words = s->dd_seg_buf_words;
-        e.table_bytes = s->dd_table_bytes;
+        const uint4 lay = s->dd_t_layout[mt];  // {table bytes, segment buffer words, stage entries, smem}
+        e.seg_buf_words = lay.y;
+        e.table_bytes = lay.x;
         if (mt < s->dd_tfb.size() && s->dd_tfb[mt] != 0xffffffffu) {
             e.block_forms = s->dd_block_forms;
             e.block_form_begin = s->dd_block_form_begin;
             e.first_block = s->dd_tfb[mt];
-            e.stage_entries = s->dd_stage_entries ? 1u : 0u;
+            e.stage_entries = lay.z;
         }
         e.segs_per_warp = mt < s->dd_tspw.size() ? s->dd_tspw[mt] : 1;
         e.n_dev = n_dev;
@@ -2345,7 +2364,7 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const unsigned long long *keys, con
         s->time_begin(3, st, t0);
         void *args[] = {&e};
         CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_eval_kernel), dim3(grid),
-                            dim3(zxs_dev::kDedupWarps * 32), args, s->dd_smem, st));
+                            dim3(zxs_dev::kDedupWarps * 32), args, lay.w, st));
         s->time_end(3, st, t0);
         s->time_begin(4, st, t0);
         zxs_dev::dedup_reduce_kernel<<<std::min((e.n_keys + 127) / 128, uint32_t(s->sm_count) * 8), 128, 0, st>>>(

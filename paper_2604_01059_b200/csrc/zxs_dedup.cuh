@@ -887,15 +887,7 @@ __global__ void __launch_bounds__(256) dedup_node_pass_kernel(const __grid_const
     const uint64_t shots64 = (a.shots + 63) & ~uint64_t(63);
     // this batch's record words (a split batch's rows continue past them: out_ld32 is only the stride)
     const uint64_t out_words = min(a.out_ld32, shots64 / 32);
-    // the shots' node slots one iteration ahead (the HBM latency overlaps the previous iteration)
-    uint32_t nxt[G];
-    const uint64_t first_s0 = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * G;
-#pragma unroll
-    for (int g = 0; g < G; g++) {
-        const uint64_t sg = first_s0 + 32 * g + lane;
-        nxt[g] = sg < a.shots ? a.slot[sg] : 0u;
-    }
-    for (uint64_t s0 = first_s0; s0 < shots64; s0 += stride) {
+    for (uint64_t s0 = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * G; s0 < shots64; s0 += stride) {
         uint64_t s[G];
         bool valid[G], bit[G];
         uint32_t node[G];
@@ -903,9 +895,9 @@ __global__ void __launch_bounds__(256) dedup_node_pass_kernel(const __grid_const
         for (int g = 0; g < G; g++) {
             s[g] = s0 + 32 * g + lane;
             valid[g] = s[g] < a.shots;
-            node[g] = valid[g] ? nxt[g] : 0u;  // node arrays are indexed by table slot
-            const uint64_t sn = s[g] + stride;
-            nxt[g] = sn < a.shots ? a.slot[sn] : 0u;
+            // node arrays are indexed by table slot (measured: prefetching the next iteration's slots,
+            // or 8 shots per lane, is slower)
+            node[g] = valid[g] ? __ldg(a.slot + s[g]) : 0u;
         }
         DedupNodeRec r[G];
         bool need = false;  // a draw is needed unless every node's bit is certain (T = 0 or 2^53, no error)

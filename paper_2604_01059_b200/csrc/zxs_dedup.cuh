@@ -261,7 +261,7 @@ struct DedupEvalArgs {
     uint32_t key_base;                // first key of this round (keys / partials are relative to it)
     unsigned long long *stats;        // device counters {keys, plane-load bytes} (nullable)
     unsigned long long tensor_loads;  // plane loads per 32-key word of this tensor
-    double *partial;                  // [keys][n_segs]
+    double *partial;                  // [n_segs][keys of the round, even stride]
     uint32_t seg_buf_words;           // per-warp shared-memory copy of its segment (0: walk from global)
     // block form tables (null: records carry tensor dictionary ids): the forms block
     // `first_block + blk` of kDedupWarps segments uses, as tensor dictionary entries
@@ -533,11 +533,20 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
         } else {
             mono_walk<1, false>(w, sgd.z, sd, pl, stk, acc, nullptr);
         }
+        // partial sums [segment][key] (key stride = the round's capacity, even): a lane's 32 keys are
+        // consecutive, so the warp's stores are contiguous
         const uint32_t k0 = kg * kDedupKeysPerWarp + lane * 32;
-        double *out = h.partial + uint64_t(k0) * h.n_segs + seg;  // [key][segment]
+        const uint64_t stride = (uint64_t(h.n_keys) + 1) & ~uint64_t(1);
+        double *out = h.partial + uint64_t(seg) * stride + k0;
+        if (k0 + 32 <= n_keys) {
+            double2 *o2 = reinterpret_cast<double2 *>(out);
 #pragma unroll
-        for (int s = 0; s < 32; s++) {
-            if (k0 + s < n_keys) out[uint64_t(s) * h.n_segs] = acc[s];
+            for (int s = 0; s < 16; s++) o2[s] = make_double2(acc[2 * s], acc[2 * s + 1]);
+        } else {
+#pragma unroll
+            for (int s = 0; s < 32; s++) {
+                if (k0 + s < n_keys) out[s] = acc[s];
+            }
         }
         }
     }
@@ -545,32 +554,27 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
 
 // value[slot of key k] = ((0 + S_0[k]) + S_1[k]) + ... in segment order (values
 // are stored by table slot, or densely for expanded keys). Thread = key: it
-// streams its own row of segment sums (16 B loads, eight in flight) and adds
-// them in order.
+// reads its segment sums down a [segment][key] column (a warp's loads are
+// contiguous, eight in flight) and adds them in order.
 __global__ void dedup_reduce_kernel(const double *__restrict__ partial, uint32_t n_segs, uint32_t max_keys,
                                     const uint32_t *n_dev, uint32_t n_mult, uint32_t key_base,
                                     const uint32_t *__restrict__ uslot, double *__restrict__ value) {
     const uint64_t dev_keys = n_dev ? uint64_t(*n_dev) * max(n_mult, 1u) : 0;
     const uint32_t n_keys = n_dev ? uint32_t(min(dev_keys > key_base ? dev_keys - key_base : uint64_t(0), uint64_t(max_keys)))
                                   : max_keys;
+    const uint64_t stride = (uint64_t(max_keys) + 1) & ~uint64_t(1);  // partials [segment][key]
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n_keys; k += gridDim.x * blockDim.x) {
-        const double *row = partial + uint64_t(k) * n_segs;
+        const double *col = partial + k;  // consecutive threads read consecutive keys
         double v = 0.0;
         uint32_t g = 0;
-        if (!(n_segs & 1u)) {  // rows are 16-byte aligned
-            const double2 *r2 = reinterpret_cast<const double2 *>(row);
-            for (; g + 16 <= n_segs; g += 16) {
-                double2 x[8];
+        for (; g + 8 <= n_segs; g += 8) {
+            double x[8];
 #pragma unroll
-                for (int i = 0; i < 8; i++) x[i] = __ldg(r2 + (g >> 1) + i);
+            for (int i = 0; i < 8; i++) x[i] = __ldg(col + uint64_t(g + i) * stride);
 #pragma unroll
-                for (int i = 0; i < 8; i++) {
-                    v = __dadd_rn(v, x[i].x);
-                    v = __dadd_rn(v, x[i].y);
-                }
-            }
+            for (int i = 0; i < 8; i++) v = __dadd_rn(v, x[i]);
         }
-        for (; g < n_segs; g++) v = __dadd_rn(v, __ldg(row + g));
+        for (; g < n_segs; g++) v = __dadd_rn(v, __ldg(col + uint64_t(g) * stride));
         value[uslot ? uslot[k] : k] = v;
     }
 }

@@ -1090,14 +1090,22 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
             tcb.push_back(uint32_t(H.chunks.size() + ch.size()));
             if (H.dict.size() - dict_base >= zxs_dev::kFormMask) { ok = false; if (!why) why = "dictionary > 16382"; }  // 14-bit form ids
             comp_max_dict = std::max<uint32_t>(comp_max_dict, uint32_t(H.dict.size() - dict_base));
-            // summation segments: contiguous node ranges of about equal cost (records + leaf
-            // epilogue), the tensor value being the ordered sum of the segment sums
+            // summation segments: contiguous node ranges of about equal cost, the tensor value
+            // being the ordered sum of the segment sums. Cost in issued instructions per 32-key
+            // word of the walk (mono_walk_fv SASS): a node's header and stack ~30, a one-form
+            // record ~4, a two-form record ~25, a leaf's epilogue ~140 (32 keys); the warps of a
+            // dedup_eval_kernel item wait for the slowest at the next barrier
             std::vector<uint8_t> seg_start(nodes.size(), 0);
             {
                 const uint32_t G = std::max<uint32_t>(
                     1, std::min<uint32_t>(max_segs, uint32_t(nodes.size() / 8)));
+                auto cost = [](const MonoNode &nd) {
+                    uint64_t c = 30 + (nd.leaf ? 140 : 0);
+                    for (uint64_t tok : nd.recs) c += (uint32_t(tok) >> 28) == zxs_dev::kRecGen ? 25 : 4;
+                    return c;
+                };
                 uint64_t total = 0;
-                for (const MonoNode &nd : nodes) total += nd.recs.size() + (nd.leaf ? 8 : 1);
+                for (const MonoNode &nd : nodes) total += cost(nd);
                 uint64_t cum = 0, k = 1;
                 for (size_t i = 0; i < nodes.size(); i++) {
                     if (i == 0) seg_start[i] = 1;
@@ -1105,7 +1113,7 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                         seg_start[i] = 1;
                         while (k < G && cum * G >= total * k) k++;
                     }
-                    cum += nodes[i].recs.size() + (nodes[i].leaf ? 8 : 1);
+                    cum += cost(nodes[i]);
                 }
             }
             const uint64_t loads_before = loads;
@@ -1251,6 +1259,16 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                                  t, spw, lists.size(), mx, over, block_form_cap);
                 }
                 tspw.push_back(spw);
+                // the canonical summation groups are runs of spw consecutive segments (one warp's
+                // walk in dedup_eval_kernel, accumulated without a reset): only a group's first
+                // segment folds in the per-shot stream
+                if (spw > 1) {
+                    uint32_t si = 0;
+                    for (size_t x = 0; x < nodes.size(); x++) {
+                        if (!seg_start[x]) continue;
+                        if (si++ % spw != 0) w[node_off[x]] &= ~zxs_dev::kMonoSegStart;
+                    }
+                }
                 if (!fits) {
                     tfb.push_back(0xffffffffu);
                 } else {
@@ -1271,6 +1289,13 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                                                     (h1 >> 24) + (h2 & 0xffu);
                                 std::stable_sort(sw.begin() + q, sw.begin() + q + ns,
                                                  [](uint32_t x, uint32_t y) { return (x >> 28) < (y >> 28); });
+                                // the kind is implied by the position; the word becomes the form value's
+                                // byte offset in the block table (fv[form][lane]: 128 B per form)
+                                for (uint32_t r = q; r < q + ns; r++) {
+                                    const uint32_t f = sw[r] & zxs_dev::kFormMask;
+                                    if (f == zxs_dev::kMonoNoForm) { ok = false; if (!why) why = "one-form record without a form"; }
+                                    sw[r] = f * zxs_dev::kFvFormBytes;
+                                }
                                 q += ns + 2 * (h0 & 0xffu);
                             }
                         }
@@ -2014,9 +2039,10 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         s->dd_block_forms = reinterpret_cast<const uint32_t *>(b + o_bf);
         s->dd_block_form_begin = reinterpret_cast<const uint32_t *>(b + o_bfb);
         s->dd_tfb = MH.tensor_first_block;
-        // stacks: kDedupWarps x depth x (Z, J0, J1) words per lane; between items the same area
-        // holds the key group's 64 raw parameter planes (64 x 33 words)
-        s->dd_stack_words = std::max<uint32_t>(zxs_dev::kDedupWarps * ma.stack_depth * 96, 64 * 33);
+        // stacks: kDedupWarps x depth x (Z, J0, J1) words per lane, then two 8-double leaf tables
+        // per warp; between items the same area holds the key group's 64 raw parameter planes
+        // (64 x 33 words)
+        s->dd_stack_words = std::max<uint32_t>(zxs_dev::kDedupWarps * (ma.stack_depth * 96 + 32), 64 * 33);
         // dedup_eval_kernel's shared memory, per tensor: its form table (the block form values, or
         // the whole dictionary when a block does not fit), planes, stacks, then -- when they fit --
         // a copy of each warp's segment (record words read by LDS instead of L1/L2) and the staged
@@ -2319,8 +2345,11 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const unsigned long long *keys, con
         return;
     }
     const zxs_dev::MonoArgs &m = s->mono;
-    // keys per round: as many as the partial buffer holds for this tensor's segments (whole key groups)
-    const uint64_t fit = partial_bytes / (uint64_t(ng) * 8);
+    // partial sums: one per summation group (spw consecutive segments, walked by one warp)
+    const uint32_t spw = std::max<uint32_t>(1, mt < s->dd_tspw.size() ? s->dd_tspw[mt] : 1);
+    const uint32_t ngroups = (ng + spw - 1) / spw;
+    // keys per round: as many as the partial buffer holds for this tensor's groups (whole key groups)
+    const uint64_t fit = partial_bytes / (uint64_t(ngroups) * 8);
     const uint32_t round = uint32_t(std::max<uint64_t>(zxs_dev::kDedupKeysPerWarp,
                                                        std::min<uint64_t>(n, fit) / zxs_dev::kDedupKeysPerWarp *
                                                            zxs_dev::kDedupKeysPerWarp));
@@ -2350,7 +2379,7 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const unsigned long long *keys, con
             e.first_block = s->dd_tfb[mt];
             e.stage_entries = lay.z;
         }
-        e.segs_per_warp = mt < s->dd_tspw.size() ? s->dd_tspw[mt] : 1;
+        e.segs_per_warp = spw;
         e.n_dev = n_dev;
         e.n_mult = n_mult;
         e.stats = s->dd_dev_stats;
@@ -2368,7 +2397,7 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const unsigned long long *keys, con
         s->time_end(3, st, t0);
         s->time_begin(4, st, t0);
         zxs_dev::dedup_reduce_kernel<<<std::min((e.n_keys + 127) / 128, uint32_t(s->sm_count) * 8), 128, 0, st>>>(
-            partial, ng, e.n_keys, n_dev, n_mult, r0, uslot ? uslot + r0 : nullptr, uslot ? value : value + r0);
+            partial, ngroups, e.n_keys, n_dev, n_mult, r0, uslot ? uslot + r0 : nullptr, uslot ? value : value + r0);
         CK(cudaGetLastError());
         s->time_end(4, st, t0);
     }
@@ -2640,10 +2669,12 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
                    st, d.table[0].count, 1, d.table[0].mask + 1);
         const unsigned ngrid = unsigned(s->sm_count) * 4;
         s->time_begin(4, st, t0);
-        zxs_dev::dedup_node_level0_kernel<<<ngrid, 256, 0, st>>>(d.table[0], d.value0, d.value, d.nodes[0]);
+        auto node_table = [&](uint32_t j) -> const zxs_dev::DedupTable & { return j == 0 ? d.table[0] : d.table[1 + ((j - 1) & 1)]; };
+        // a node whose bit is certain gets its only child in the next level's (clear) table here
+        zxs_dev::dedup_node_level0_kernel<<<ngrid, 256, 0, st>>>(d.table[0], d.value0, d.value, d.nodes[0], node_table(1),
+                                                                 cd.n_out > 1);
         CK(cudaGetLastError());
         s->time_end(4, st, t0);
-        auto node_table = [&](uint32_t j) -> const zxs_dev::DedupTable & { return j == 0 ? d.table[0] : d.table[1 + ((j - 1) & 1)]; };
         for (uint32_t j = 0; j < cd.n_out; j++) {
             const zxs_dev::DedupTable &cur = node_table(j);
             const zxs_dev::DedupNodeArrays &na = d.nodes[j & 1];
@@ -2661,7 +2692,8 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
                 dedup_eval(s, cd.first_tensor + 1 + j, d.table[3].ukeys, d.table[3].uslot, limit, d.value, d.partial,
                            d.partial_bytes, st, d.table[3].count, 1, d.table[3].mask + 1);
                 s->time_begin(4, st, t0);
-                zxs_dev::dedup_node_decide_kernel<<<ngrid, 256, 0, st>>>(cur, d.value, na);
+                zxs_dev::dedup_node_decide_kernel<<<ngrid, 256, 0, st>>>(cur, d.value, na, node_table(j + 1),
+                                                                        j + 1 < cd.n_out);
                 CK(cudaGetLastError());
                 s->time_end(4, st, t0);
                 clear(d.table[3]);

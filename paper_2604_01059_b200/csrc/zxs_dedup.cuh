@@ -253,7 +253,7 @@ struct DedupEvalArgs {
     uint32_t width;                   // W
     uint32_t all_plane, n_planes;     // plane indices the dictionary uses: [0, W), ALL, ZERO = ALL + 1
     uint32_t stack_depth;
-    uint32_t stack_words;             // stack area (>= kDedupWarps x depth x 96, >= 64 x 33 raw planes)
+    uint32_t stack_words;             // stack area (>= kDedupWarps x (depth x 96 + 32), >= 64 x 33 raw planes)
     const unsigned long long *keys;   // the round's keys
     uint32_t n_keys;                  // keys (n_dev: at most this many, the rest read from n_dev)
     const uint32_t *n_dev;            // device-side key count (the table's), or null
@@ -273,13 +273,53 @@ struct DedupEvalArgs {
     uint32_t stage_entries;  // block tables: stage the forms' first dictionary entries in shared memory
 };
 
+#ifndef ZXS_LEAF_LDS
+#define ZXS_LEAF_LDS 1
+#endif
+// mono_leaf for one 32-key word per lane through a per-warp table of the leaf's
+// five possible contributions, indexed by the key's (J mod 4, Z) code:
+// {re, -im, -re, im, +0, +0, +0, +0}. A zero-flagged key adds +0.0 instead of
+// skipping the add -- the same double (the accumulators start at +0.0 and
+// round to nearest, so they are never -0.0) -- so the sums equal mono_leaf's
+// bit for bit. Per key: one byte extract, one LDS.64 (five distinct addresses:
+// broadcast) and the DADD, instead of mono_leaf's selects on the ALU pipe;
+// the codes of four keys are built together (nibble x spread constant).
+// Two tables per warp alternate, so one __syncwarp per leaf orders the writes
+// after the previous leaf's reads.
+__device__ __forceinline__ void dedup_leaf_lds(double (&acc)[32], uint32_t z, uint32_t j0, uint32_t j1, double re,
+                                               double im, double *ltab, uint32_t lane, uint32_t &lbuf) {
+    double *tab = ltab + lbuf * 8;
+    if (lane < 8) {
+        const double v = (lane & 1u) ? im : re;          // J odd: the imaginary part
+        const double sv = ((lane + 1u) & 2u) ? -v : v;   // J = 1, 2: negated
+        tab[lane] = lane < 4 ? sv : 0.0;
+    }
+    __syncwarp();
+    lbuf ^= 1u;
+    const char *tb = reinterpret_cast<const char *>(tab);
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+        // byte k of c = 8 x (j0 | j1 << 1 | z << 2) of key 4r + k: bit k of a nibble times
+        // sum_m 2^(7m + sh) lands on bit 8k + sh (no two terms share a position: no carries)
+        const uint32_t n0 = (j0 >> (4 * r)) & 0xfu, n1 = (j1 >> (4 * r)) & 0xfu, nz = (z >> (4 * r)) & 0xfu;
+        const uint32_t c = ((n0 * 0x01020408u) & 0x08080808u) | ((n1 * 0x02040810u) & 0x10101010u) |
+                           ((nz * 0x04081020u) & 0x20202020u);
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const uint32_t off = __byte_perm(c, 0u, 0x4440u | uint32_t(k));
+            acc[4 * r + k] = __dadd_rn(acc[4 * r + k], *reinterpret_cast<const double *>(tb + off));
+        }
+    }
+}
+
 // mono_walk for one 32-key word per lane when every form value of the block
 // is precomputed in shared memory (fv[local form * 32 + lane]): a form costs
 // one conflict-free LDS instead of its dictionary entry and selector loads.
 __device__ __forceinline__ void mono_walk_fv(const uint32_t *w, uint32_t nnodes, const uint32_t *fv, BW<1> *stk,
-                                             double (&acc)[32]) {
+                                             double (&acc)[32], double *ltab, uint32_t lane) {
     constexpr int NW = 1;
     uint32_t q = 0;
+    uint32_t lbuf = 0;
     for (uint32_t nn = 0; nn < nnodes; nn++) {
         const uint32_t h0 = w[q], h1 = w[q + 1], h2 = w[q + 2];
         const uint32_t depth = (h0 >> 24) & 0x3fu;
@@ -303,7 +343,8 @@ __device__ __forceinline__ void mono_walk_fv(const uint32_t *w, uint32_t nnodes,
             uint32_t zz = z.w[0], a0 = j0.w[0], a1 = j1.w[0];
             const uint32_t n_add = h1 & 0xffu, n_sub = (h1 >> 8) & 0xffu, n_add2 = (h1 >> 16) & 0xffu;
             const uint32_t n_z = h1 >> 24, n_zn = h2 & 0xffu;
-            auto fvr = [&](uint32_t i) { return fv[(w[i] & kFormMask) * 32]; };
+            // one-form record word = the form value's byte offset in the block table (host: encode_mono)
+            auto fvr = [&](uint32_t i) { return *reinterpret_cast<const uint32_t *>(reinterpret_cast<const char *>(fv) + w[i]); };
 #if ZXS_WALK_ILP
             // J (mod 4) and Z are order-free sums / ORs: two independent chains per kind (the
             // form loads of consecutive records overlap), merged at the node's end
@@ -404,7 +445,11 @@ __device__ __forceinline__ void mono_walk_fv(const uint32_t *w, uint32_t nnodes,
             nsp[64] = j1;
             continue;
         }
+#if ZXS_LEAF_LDS
+        dedup_leaf_lds(acc, z.w[0], j0.w[0], j1.w[0], re, im, ltab, lane, lbuf);
+#else
         mono_leaf<1>(acc, z, j0, j1, re, im);
+#endif
     }
 }
 
@@ -420,6 +465,8 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
     uint32_t *stack_all = planes + h.n_planes * 32;                  // per warp [depth][3][lane]
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     BW<1> *stk = reinterpret_cast<BW<1> *>(stack_all + warp * h.stack_depth * 96) + lane;
+    // the warp's two leaf tables (dedup_leaf_lds) after every warp's stack
+    double *ltab = reinterpret_cast<double *>(stack_all + kDedupWarps * h.stack_depth * 96) + warp * 16;
     uint32_t *segbuf = stack_all + h.stack_words + warp * h.seg_buf_words;
     uint4 *sent = reinterpret_cast<uint4 *>(stack_all + h.stack_words + kDedupWarps * h.seg_buf_words);
     uint32_t have_seg = 0xffffffffu;  // segment currently in segbuf
@@ -505,39 +552,44 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
             __syncthreads();
             cur_blk = blk;
         }
-        for (uint32_t si = 0; si < spw; si++) {
-        const uint32_t seg = blk * bsegs + warp * spw + si;
-        if (seg >= h.n_segs) break;
-        const uint4 sgd = __ldg(h.segs + seg);
-        // the warp's segment into shared memory once (the walk's record loads are
-        // warp-uniform and serial: broadcast LDS instead of L1/L2 round trips); a CTA
-        // keeps its segment block across key groups
-        const uint32_t *w = h.words + sgd.x;
-        if (sgd.y <= h.seg_buf_words) {
-            if (have_seg != seg) {
-                const uint32_t *src = h.words + sgd.x;
-#pragma unroll 4
-                for (uint32_t i = lane; i < sgd.y; i += 32) segbuf[i] = __ldg(src + i);
-                __syncwarp();
-                have_seg = seg;
-            }
-            w = segbuf;
-        }
+        // the warp's summation group: spw consecutive segments accumulated without a reset
+        // (the per-shot stream folds only at a group's first segment, encode_mono)
+        const uint32_t group = blk * kDedupWarps + warp;
+        if (group * spw >= h.n_segs) continue;
         double acc[32];
 #pragma unroll
         for (int s = 0; s < 32; s++) acc[s] = 0.0;
-        if (fvm && w == segbuf) {  // record words in shared memory: LDS (a separate instantiation)
-            mono_walk_fv(segbuf, sgd.z, fv + lane, stk, acc);
-        } else if (fvm) {
-            mono_walk_fv(h.words + sgd.x, sgd.z, fv + lane, stk, acc);
-        } else {
-            mono_walk<1, false>(w, sgd.z, sd, pl, stk, acc, nullptr);
+        for (uint32_t si = 0; si < spw; si++) {
+            const uint32_t seg = group * spw + si;
+            if (seg >= h.n_segs) break;
+            const uint4 sgd = __ldg(h.segs + seg);
+            // the warp's segment into shared memory once (the walk's record loads are
+            // warp-uniform and serial: broadcast LDS instead of L1/L2 round trips); a CTA
+            // keeps its segment block across key groups
+            const uint32_t *w = h.words + sgd.x;
+            if (sgd.y <= h.seg_buf_words) {
+                if (have_seg != seg) {
+                    const uint32_t *src = h.words + sgd.x;
+#pragma unroll 4
+                    for (uint32_t i = lane; i < sgd.y; i += 32) segbuf[i] = __ldg(src + i);
+                    __syncwarp();
+                    have_seg = seg;
+                }
+                w = segbuf;
+            }
+            if (fvm && w == segbuf) {  // record words in shared memory: LDS (a separate instantiation)
+                mono_walk_fv(segbuf, sgd.z, fv + lane, stk, acc, ltab, lane);
+            } else if (fvm) {
+                mono_walk_fv(h.words + sgd.x, sgd.z, fv + lane, stk, acc, ltab, lane);
+            } else {
+                mono_walk<1, false>(w, sgd.z, sd, pl, stk, acc, nullptr);
+            }
         }
-        // partial sums [segment][key] (key stride = the round's capacity, even): a lane's 32 keys are
+        // partial sums [group][key] (key stride = the round's capacity, even): a lane's 32 keys are
         // consecutive, so the warp's stores are contiguous
         const uint32_t k0 = kg * kDedupKeysPerWarp + lane * 32;
         const uint64_t stride = (uint64_t(h.n_keys) + 1) & ~uint64_t(1);
-        double *out = h.partial + uint64_t(seg) * stride + k0;
+        double *out = h.partial + uint64_t(group) * stride + k0;
         if (k0 + 32 <= n_keys) {
             double2 *o2 = reinterpret_cast<double2 *>(out);
 #pragma unroll
@@ -547,7 +599,6 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
             for (int s = 0; s < 32; s++) {
                 if (k0 + s < n_keys) out[s] = acc[s];
             }
-        }
         }
     }
 }
@@ -766,13 +817,18 @@ __global__ void __launch_bounds__(256) dedup_ar_kernel(const __grid_constant__ D
 // compares k >= T, and inserts the child node (parent slot << 1 | bit) for
 // the next level: 4 B read + 4 B written per shot per position (the
 // step-by-step dedup_ar_kernel moves slot, key and prev per shot).
-struct DedupNodeRec {
+struct __align__(16) DedupNodeRec {
     unsigned long long T;       // bit = (k >= T); bit 63: ratio outside (-1e-6, 1 + 1e-6)
-    unsigned long long tie_lo;  // near-tie draws: k in [tie_lo, tie_hi]
-    unsigned long long tie_hi;
+    unsigned long long tie_lo;  // near-tie draws: k - tie_lo <= tie_w (2^62: none)
     double cl;                  // clamped ratio (injected-uniform mode)
+    uint32_t tie_w;
+    // certain bit (T = 0 or 2^53, no error): the slot of the only child in the next
+    // level's table, inserted by the decide kernel (kNodeNoChild on the last level);
+    // kNodeDraw otherwise (the pass draws and inserts the child)
+    uint32_t child;
 };
 constexpr unsigned long long kNodeErr = 1ull << 63;
+constexpr uint32_t kNodeDraw = 0xffffffffu, kNodeNoChild = 0xfffffffeu;
 
 struct DedupNodeArrays {
     // indexed by the node's slot in its level's node table
@@ -783,7 +839,8 @@ struct DedupNodeArrays {
     DedupNodeRec *rec;
 };
 
-__device__ __forceinline__ DedupNodeRec node_rec(double cur, double pv) {
+__device__ __forceinline__ DedupNodeRec node_rec(double cur, double pv, uint32_t sl, const DedupTable &next,
+                                                 bool insert_next) {
     // sampler.cpp:84-99, per node: the same division, test and clamp as per shot
     const double ratio = __ddiv_rn(cur, pv);
     const bool err = !(ratio > -1e-6 && ratio < 1.0 + 1e-6);
@@ -791,18 +848,27 @@ __device__ __forceinline__ DedupNodeRec node_rec(double cur, double pv) {
     cl = (cl < 1.0) ? cl : 1.0;
     DedupNodeRec r;
     r.cl = cl;
-    r.T = (unsigned long long)ceil(cl * 0x1.0p53) | (err ? kNodeErr : 0ull);  // cl 2^53 is exact
+    const unsigned long long T = (unsigned long long)ceil(cl * 0x1.0p53);  // cl 2^53 is exact
+    r.T = T | (err ? kNodeErr : 0ull);
     const double w = 1e-9 * fmax(cl, 1e-300);
     const double lo = fmax(cl - w, 0.0) * 0x1.0p53, hi = fmin(cl + w, 1.0) * 0x1.0p53;
-    r.tie_lo = (unsigned long long)ceil(lo);
-    r.tie_hi = (unsigned long long)floor(hi);
+    const unsigned long long tlo = (unsigned long long)ceil(lo), thi = (unsigned long long)floor(hi);
+    const bool certain = T == 0ull || T == (1ull << 53);
+    // the window's width is below 2^32 (1e-9 2^53); an empty window or a certain bit never counts
+    r.tie_lo = (certain || thi < tlo) ? (1ull << 62) : tlo;
+    r.tie_w = (certain || thi < tlo) ? 0u : uint32_t(thi - tlo);
+    r.child = kNodeDraw;
+    if (certain && !err) {
+        // every shot at this node takes the same bit (k < 2^53 <= T, or k >= 0 = T)
+        r.child = insert_next ? dedup_insert(next, (unsigned long long)sl << 1 | (T == 0ull ? 1ull : 0ull)) : kNodeNoChild;
+    }
     return r;
 }
 
 // Level 0: the nodes are the base keys (table ids), already contracted for the
 // normalization (value0) and the first marginal (value), both by table slot.
 __global__ void dedup_node_level0_kernel(DedupTable t, const double *__restrict__ value0, const double *__restrict__ value,
-                                         DedupNodeArrays na) {
+                                         DedupNodeArrays na, DedupTable next, bool insert_next) {
     const uint32_t n = min(*t.count, t.max_ids);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t sl = t.uslot[i];  // node arrays are indexed by table slot
@@ -811,7 +877,7 @@ __global__ void dedup_node_level0_kernel(DedupTable t, const double *__restrict_
         na.prev[sl] = pv;
         na.cur[sl] = cur;
         na.kslot[sl] = sl;
-        na.rec[sl] = node_rec(cur, pv);
+        na.rec[sl] = node_rec(cur, pv, sl, next, insert_next);
     }
 }
 
@@ -846,13 +912,14 @@ __global__ void dedup_node_prep_kernel(DedupTable nodes, DedupNodeArrays parent,
 }
 
 // Decision records once the level's keys are contracted (values by key slot).
-__global__ void dedup_node_decide_kernel(DedupTable nodes, const double *__restrict__ value, DedupNodeArrays na) {
+__global__ void dedup_node_decide_kernel(DedupTable nodes, const double *__restrict__ value, DedupNodeArrays na,
+                                         DedupTable next, bool insert_next) {
     const uint32_t n = min(*nodes.count, nodes.max_ids);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t sl = nodes.uslot[i];
         const double cur = value[na.kslot[sl]];
         na.cur[sl] = cur;
-        na.rec[sl] = node_rec(cur, na.prev[sl]);
+        na.rec[sl] = node_rec(cur, na.prev[sl], sl, next, insert_next);
     }
 }
 
@@ -908,8 +975,7 @@ __global__ void __launch_bounds__(256) dedup_node_pass_kernel(const __grid_const
 #pragma unroll
         for (int g = 0; g < G; g++) {
             r[g] = a.rec[node[g]];
-            const unsigned long long T = r[g].T & ~kNodeErr;
-            need |= valid[g] && ((r[g].T & kNodeErr) || (T != 0ull && T != (1ull << 53)));
+            need |= valid[g] && r[g].child == kNodeDraw;
         }
         unsigned long long k[G];
         if (a.uniforms) {
@@ -942,7 +1008,7 @@ __global__ void __launch_bounds__(256) dedup_node_pass_kernel(const __grid_const
                     if (fabs(u - r[g].cl) <= 1e-9 * fmax(r[g].cl, 1e-300)) atomicAdd(&a.err[2], 1ull);
                 } else {
                     bit[g] = k[g] >= T;
-                    if (T != 0ull && T != (1ull << 53) && k[g] >= r[g].tie_lo && k[g] <= r[g].tie_hi) atomicAdd(&a.err[2], 1ull);
+                    if (k[g] - r[g].tie_lo <= r[g].tie_w) atomicAdd(&a.err[2], 1ull);
                 }
                 if (r[g].T & kNodeErr) report_ratio_error(a.err, a.first_shot + s[g]);
             }
@@ -971,8 +1037,11 @@ __global__ void __launch_bounds__(256) dedup_node_pass_kernel(const __grid_const
 #pragma unroll
             for (int g = 0; g < G; g++) {
                 const unsigned long long e = (unsigned long long)node[g] << 1 | (bit[g] ? 1ull : 0ull);
-                const uint32_t ns = dedup_insert_warp(a.next, e, valid[g], lane, cache);
-                if (valid[g]) a.slot[s[g]] = ns;
+                // a certain bit's child was inserted by the decide kernel (an injected uniform
+                // outside [0, 1) can still take the other bit)
+                const bool known = r[g].child < kNodeNoChild && bit[g] == ((r[g].T & ~kNodeErr) == 0ull);
+                const uint32_t ns = dedup_insert_warp(a.next, e, valid[g] && !known, lane, cache);
+                if (valid[g]) a.slot[s[g]] = known ? r[g].child : ns;
             }
         }
     }

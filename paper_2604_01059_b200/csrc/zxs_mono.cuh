@@ -60,6 +60,7 @@ constexpr uint32_t kMonoChunkWords = 2048;   // 8 KiB per chunk buffer
 // record word: kind << 28 | second form << kFormShiftB | first form (14-bit dictionary ids)
 constexpr uint32_t kFormMask = 0x3fffu;
 constexpr int kFormShiftB = 14;
+constexpr uint32_t kFvFormBytes = 32 * 4;  // block form table (dedup_eval_kernel): fv[form][lane], 32-bit words
 constexpr uint32_t kMonoNoForm = kFormMask;  // "no form" (parity 0) in the 14-bit form fields
 constexpr int kMaxMonoComps = 8;
 constexpr uint32_t kMonoMaxDepth = 8;        // levels of the shared-prefix term tree

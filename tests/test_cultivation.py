@@ -137,3 +137,15 @@ def test_noiseless_outcome_is_certain_on_device():
         cs = _model(path)
         p = zx.probability_of_at(cs, [0] * cs.num_outputs, [0] * cs.f_width)
         assert abs(p - 1.0) < 1e-9, (path, p)
+
+
+def test_decoded_dedup_equals_per_shot():
+    """The decoded model's summation groups span several segments (spw = 2, 4): the
+    deduplicated path and the per-shot mono_kernel (ZXS_DEDUP=0) give the same
+    records bit for bit on a batch with many distinct keys per position."""
+    if not os.path.exists(BIG):
+        pytest.skip(f"{BIG} absent")
+    shots, seed, first = 1 << 13, 11, 5 << 20
+    got = _sample(_model(BIG), shots, seed, first)
+    want = _sample(_model(BIG, ZXS_DEDUP="0"), shots, seed, first)
+    assert np.array_equal(got, want)

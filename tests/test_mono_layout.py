@@ -94,15 +94,23 @@ def form_sel(dict_, f):
         f += 1
 
 
-def apply_node_records(w, q, h0, h1, h2, form, J, Z):
+FV_FORM_BYTES = 128  # block form tables: a one-form record word is the form's byte offset (fv[form][lane])
+
+
+def apply_node_records(w, q, h0, h1, h2, form, J, Z, block=False):
     """mono_kernel's one-form records (any kind order) and two-form records on (J, Z);
-    returns the new position."""
-    ns = (h1 & 0xFF) + ((h1 >> 8) & 0xFF) + ((h1 >> 16) & 0xFF) + (h1 >> 24) + (h2 & 0xFF)
-    for _ in range(ns):
+    returns the new position. block: dedup_eval_kernel's block-table segments, whose
+    one-form records are grouped by kind (the header's counts) and hold fv byte offsets."""
+    counts = (h1 & 0xFF, (h1 >> 8) & 0xFF, (h1 >> 16) & 0xFF, h1 >> 24, h2 & 0xFF)
+    kinds = [k for k, n in zip((REC_ADD, REC_SUB, REC_ADD2, REC_Z, REC_ZN), counts) for _ in range(n)]
+    for kind_by_pos in kinds:
         r = int(w[q])
         q += 1
-        kind = r >> 28
-        a = form(r & FORM_MASK)
+        if block:
+            assert r % FV_FORM_BYTES == 0
+            kind, a = kind_by_pos, form(r // FV_FORM_BYTES)
+        else:
+            kind, a = r >> 28, form(r & FORM_MASK)
         if kind == REC_ADD:
             J += a
         elif kind == REC_SUB:
@@ -130,7 +138,7 @@ def apply_node_records(w, q, h0, h1, h2, form, J, Z):
 SEG_START = 1 << 30
 
 
-def walk_nodes(w, nnodes, form, S, stack, acc, tot, stats=None):
+def walk_nodes(w, nnodes, form, S, stack, acc, tot, stats=None, block=False):
     """mono_walk: nnodes nodes of stream w; FOLD when tot is given (segment starts
     fold the running sum into tot)."""
     q = 0
@@ -149,7 +157,7 @@ def walk_nodes(w, nnodes, form, S, stack, acc, tot, stats=None):
             J, Z = stack[depth - 1][0].copy(), stack[depth - 1][1].copy()
         else:
             J, Z = np.zeros(S, np.int64), np.zeros(S, bool)
-        q = apply_node_records(w, q, h0, h1, h2, form, J, Z)
+        q = apply_node_records(w, q, h0, h1, h2, form, J, Z, block)
         if stats is not None:
             stats["nodes"] = stats.get("nodes", 0) + 1
         if not leaf:
@@ -180,15 +188,20 @@ def tensor_forms(lay, t, P):
 
 
 def emulate_segments(lay, t, P):
-    """dedup_eval_kernel + dedup_reduce_kernel: every summation segment walked on its
-    own (ancestors replayed), segment sums folded in order."""
+    """dedup_eval_kernel + dedup_reduce_kernel: every segment walked on its own
+    (ancestors replayed); a summation group (spw consecutive segments, one warp)
+    accumulates without a reset; group sums folded in order."""
     form = tensor_forms(lay, t, P)
     S = P.shape[0]
     tot = np.zeros(S)
     g0 = lay["tsb"][t]
+    spw = max(1, int(lay["spw"][t]))
+    acc = np.zeros(S)
     for g in range(g0, lay["tsb"][t + 1]):
         wb, nw, nn = lay["segs"][g, :3]
-        acc = np.zeros(S)
+        if (g - g0) % spw == 0:
+            tot += acc
+            acc = np.zeros(S)
         fb = int(lay["tfb"][t])
         if fb != 0xFFFFFFFF:  # block-local form ids -> the tensor dictionary's
             blk = fb + (g - g0) // (16 * int(lay["spw"][t]))  # a block: 16 warps x spw segments
@@ -196,9 +209,8 @@ def emulate_segments(lay, t, P):
             f = (lambda x, table=table: form(int(table[x])))
         else:
             f = form
-        walk_nodes(lay["seg_words"][wb:wb + nw], nn, f, S, {}, acc, None)
-        tot += acc
-    return tot
+        walk_nodes(lay["seg_words"][wb:wb + nw], nn, f, S, {}, acc, None, block=fb != 0xFFFFFFFF)
+    return tot + acc
 
 
 def emulate_tensor(lay, t, P, stats=None):
@@ -287,7 +299,8 @@ def test_mono_values_match_oracle(name):
 
 def test_summation_segments():
     """Segments partition each tensor's node stream, every segment stream starts at
-    the root (depth 0) and the key mask covers every basis vector."""
+    the root (depth 0), the per-shot stream folds once per summation group (spw
+    segments) and the key mask covers every basis vector."""
     arrays = zxs_format.load(golden_path("surface_d3_xmem_9t"))
     lay = mono_layout(arrays)
     nt = len(lay["tcb"]) - 1
@@ -304,7 +317,8 @@ def test_summation_segments():
                 starts += bool(h0 & SEG_START)
                 q += 3 + (4 if h0 >> 31 else 0)
                 q += (h1 & 0xFF) + ((h1 >> 8) & 0xFF) + ((h1 >> 16) & 0xFF) + (h1 >> 24) + (h2 & 0xFF) + 2 * (h0 & 0xFF)
-        assert starts == g1 - g0
+        spw = max(1, int(lay["spw"][t]))
+        assert starts == (g1 - g0 + spw - 1) // spw
         for g in range(g0, g1):
             wb = lay["segs"][g, 0]
             assert (int(lay["seg_words"][wb]) >> 24) & 0x3F == 0

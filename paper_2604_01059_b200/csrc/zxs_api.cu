@@ -2216,11 +2216,13 @@ void launch_mono(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *f
 
 // ---- deduplicated large-chi path (zxs_dedup.cuh)
 constexpr uint32_t kDedupRoundKeys = 65536;  // fused chains: expanded keys per position (one round)
-// Segment partial sums of one evaluation round live in one buffer of at most this many bytes; a
-// tensor of G segments is evaluated in rounds of about budget / (8 G) keys, each round reading the
-// device key count (rounds past it exit at once), so no host round trip decides how many run.
+// Group partial sums of one evaluation round live in one buffer of at most this many bytes (4 GB
+// of the 180 GB: config 3 then needs 38 evaluation rounds per 2^28 shots instead of 91 at 1 GB);
+// a tensor of G summation groups is evaluated in rounds of about budget / (8 G) keys, each round
+// reading the device key count (rounds past it exit at once), so no host round trip decides how
+// many run.
 size_t dedup_partial_budget() {
-    size_t mb = 1024;
+    size_t mb = 4096;
     if (const char *e = std::getenv("ZXS_DEDUP_PARTIAL_MB")) mb = size_t(std::max(64L, std::atol(e)));
     return mb << 20;
 }
@@ -2350,8 +2352,10 @@ void dedup_eval(zxs_sampler *s, uint32_t mt, const unsigned long long *keys, con
     const uint32_t ngroups = (ng + spw - 1) / spw;
     // keys per round: as many as the partial buffer holds for this tensor's groups (whole key groups)
     const uint64_t fit = partial_bytes / (uint64_t(ngroups) * 8);
+    uint64_t cap = fit;
+    if (const char *e = std::getenv("ZXS_DEDUP_ROUND_KEYS")) cap = std::min<uint64_t>(cap, uint64_t(std::max(1L, std::atol(e))));
     const uint32_t round = uint32_t(std::max<uint64_t>(zxs_dev::kDedupKeysPerWarp,
-                                                       std::min<uint64_t>(n, fit) / zxs_dev::kDedupKeysPerWarp *
+                                                       std::min<uint64_t>(n, cap) / zxs_dev::kDedupKeysPerWarp *
                                                            zxs_dev::kDedupKeysPerWarp));
     for (uint32_t r0 = 0; r0 < n; r0 += round) {
         zxs_dev::DedupEvalArgs e{};

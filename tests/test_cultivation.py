@@ -149,3 +149,22 @@ def test_decoded_dedup_equals_per_shot():
     got = _sample(_model(BIG), shots, seed, first)
     want = _sample(_model(BIG, ZXS_DEDUP="0"), shots, seed, first)
     assert np.array_equal(got, want)
+
+
+def test_decoded_evaluation_rounds_identical():
+    """Evaluation rounds of 4096 keys (ZXS_DEDUP_ROUND_KEYS; the default is as many as
+    the 4 GB partial buffer holds, all of a batch's keys here) give the same records."""
+    if not os.path.exists(BIG):
+        pytest.skip(f"{BIG} absent")
+    shots, seed, first = 1 << 22, 13, 7 << 26
+    cs = _model(BIG)
+    want = _sample(cs, shots, seed, first)
+    cs.dedup_stats(reset=True)
+    os.environ["ZXS_DEDUP_ROUND_KEYS"] = "4096"  # read per evaluation
+    try:
+        got = _sample(cs, shots, seed, first)
+    finally:
+        del os.environ["ZXS_DEDUP_ROUND_KEYS"]
+    stats = cs.dedup_stats()
+    assert stats["eval_launches"] > 2 * 16, stats  # several rounds per tensor
+    assert np.array_equal(got, want)

@@ -499,7 +499,7 @@ def test_dedup_sync_and_async_paths_identical():
         assert np.array_equal(sample(a, shots, seed, first), sample(b, shots, seed, first))
     orc = coracle.OracleModel.load(golden_path(name))
     rng = np.random.default_rng(47)
-    shots = 40000  # random f: ~40000 distinct keys > one round of 16384
+    shots = 40000  # random f: ~40000 distinct keys
     f = rng.integers(0, 2**63, size=(orc.f_width, (shots + 63) // 64), dtype=np.uint64)
     f[:, -1] &= np.uint64((1 << (shots & 63)) - 1)
     u = rng.random((orc.num_positions, shots))

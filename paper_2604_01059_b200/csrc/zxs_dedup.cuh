@@ -273,6 +273,9 @@ struct DedupEvalArgs {
     uint32_t stage_entries;  // block tables: stage the forms' first dictionary entries in shared memory
 };
 
+#ifndef ZXS_REC_UNROLL
+#define ZXS_REC_UNROLL 0
+#endif
 #ifndef ZXS_LEAF_LDS
 #define ZXS_LEAF_LDS 1
 #endif
@@ -405,20 +408,38 @@ __device__ __forceinline__ void mono_walk_fv(const uint32_t *w, uint32_t nnodes,
             }
             z.w[0] = zz | z2;
 #else
+            // ZXS_REC_UNROLL > 0: the kind loops unrolled by hand with a rolled tail (the
+            // compiler's own unroll by 8 adds remainder blocks of 4, 2 and 1 per loop)
+#if ZXS_REC_UNROLL > 0
+#define ZXS_REC_LOOP(END, BODY)                                                     \
+    for (; q + ZXS_REC_UNROLL <= (END); q += ZXS_REC_UNROLL) {                      \
+        _Pragma("unroll") for (int u_ = 0; u_ < ZXS_REC_UNROLL; u_++) {             \
+            const uint32_t x = fvr(q + u_);                                         \
+            BODY                                                                    \
+        }                                                                           \
+    }                                                                               \
+    _Pragma("unroll 1") for (; q < (END); q++) {                                    \
+        const uint32_t x = fvr(q);                                                  \
+        BODY                                                                        \
+    }
+#else
+#define ZXS_REC_LOOP(END, BODY) \
+    for (; q < (END); q++) {    \
+        const uint32_t x = fvr(q); \
+        BODY                    \
+    }
+#endif
             uint32_t e = q + n_add;
-            for (; q < e; q++) {  // J += a
-                const uint32_t x = fvr(q);
-                a1 ^= a0 & x;
-                a0 ^= x;
-            }
-            for (e += n_sub; q < e; q++) {  // J -= a
-                const uint32_t x = fvr(q);
-                a1 ^= ~a0 & x;
-                a0 ^= x;
-            }
-            for (e += n_add2; q < e; q++) a1 ^= fvr(q);  // J += 2a
-            for (e += n_z; q < e; q++) zz |= fvr(q);     // Z |= a
-            for (e += n_zn; q < e; q++) zz |= ~fvr(q);   // Z |= ~a
+            ZXS_REC_LOOP(e, a1 ^= a0 & x; a0 ^= x;)  // J += a
+            e += n_sub;
+            ZXS_REC_LOOP(e, a1 ^= ~a0 & x; a0 ^= x;)  // J -= a
+            e += n_add2;
+            ZXS_REC_LOOP(e, a1 ^= x;)  // J += 2a
+            e += n_z;
+            ZXS_REC_LOOP(e, zz |= x;)  // Z |= a
+            e += n_zn;
+            ZXS_REC_LOOP(e, zz |= ~x;)  // Z |= ~a
+#undef ZXS_REC_LOOP
             z.w[0] = zz;
 #endif
             j0.w[0] = a0;

@@ -1,5 +1,6 @@
 """profiles/r02/traffic.json from an ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum CSV:
-per-launch DRAM bytes of a kernel over a bench step (bench.py's roofline.traffic)."""
+per-launch DRAM bytes of a kernel over a bench step (bench.py's roofline.traffic).
+usage: traffic_json.py CSV WORKLOAD KERNEL SHOTS [LAUNCHES_PER_STEP]"""
 import csv
 import json
 import os
@@ -22,9 +23,14 @@ def main():
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1024, "MB": 1 << 20, "GB": 1 << 30}.get(unit, 1)
         byid[d["ID"]][d["Metric Name"]] = v * scale
         names[d["ID"]] = d["Kernel Name"]
-    launches = len(byid)
-    rd = sum(m.get("dram__bytes_read.sum", 0) for m in byid.values())
-    wr = sum(m.get("dram__bytes_write.sum", 0) for m in byid.values())
+    # the timed step's launches: the first `per_step` of the kernel in launch order (bench.py
+    # --steps 1 --warmup 0 runs the step before its end-to-end leg)
+    ids = sorted(byid, key=int)
+    if len(sys.argv) > 5:
+        ids = ids[:int(sys.argv[5])]
+    launches = len(ids)
+    rd = sum(byid[i].get("dram__bytes_read.sum", 0) for i in ids)
+    wr = sum(byid[i].get("dram__bytes_write.sum", 0) for i in ids)
     out_path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r02", "traffic.json")
     data = json.load(open(out_path)) if os.path.exists(out_path) else {}
     data[workload] = {"kernel": kernel, "shots": shots, "launches_per_step": launches,

@@ -549,7 +549,10 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
             const uint32_t f0 = __ldg(h.block_form_begin + h.first_block + blk);
             const uint32_t nf = __ldg(h.block_form_begin + h.first_block + blk + 1) - f0;
             __syncthreads();  // every warp is done with the previous block's values
-            if (h.stage_entries) {
+#ifndef ZXS_FV_REG_ONLY
+#define ZXS_FV_REG_ONLY 0
+#endif
+            if (h.stage_entries && !ZXS_FV_REG_ONLY) {
                 // first dictionary entry of every form, gathered once (L2 -> shared)
                 for (uint32_t i = threadIdx.x; i < nf; i += blockDim.x) sent[i] = __ldg(h.dict + __ldg(h.block_forms + f0 + i));
                 __syncthreads();
@@ -566,8 +569,30 @@ __global__ void __launch_bounds__(kDedupWarps * 32, 1) dedup_eval_kernel(const _
                     fv[f * 32 + lane] = v.w[0];
                 }
             } else {
-                for (uint32_t f = warp; f < nf; f += kDedupWarps) {
-                    fv[f * 32 + lane] = mono_form<1>(h.dict, __ldg(h.block_forms + f0 + f), pl).w[0];
+                // no room to stage them in shared memory: staged in registers instead -- lane i
+                // fetches the first entry of the warp's form w + 16 i (32 dependent L2 round trips
+                // in flight instead of one), each broadcast by shuffle when its form is computed
+                for (uint32_t fb = warp; fb < nf; fb += kDedupWarps * 32) {
+                    const uint32_t mf = fb + kDedupWarps * lane;
+                    const uint32_t mgi = mf < nf ? __ldg(h.block_forms + f0 + mf) : 0u;
+                    const uint4 me = mf < nf ? __ldg(h.dict + mgi) : make_uint4(0, 0, 0, 0);
+                    const uint32_t nk = min(32u, (nf - fb + kDedupWarps - 1) / kDedupWarps);
+                    for (uint32_t k = 0; k < nk; k++) {
+                        uint4 e;
+                        e.x = __shfl_sync(kFull, me.x, k);
+                        e.y = __shfl_sync(kFull, me.y, k);
+                        e.z = __shfl_sync(kFull, me.z, k);
+                        e.w = __shfl_sync(kFull, me.w, k);
+                        BW<1> v = mono_entry<1>(e, pl);
+                        if (e.x & 0x80u) {  // continuation entries (forms of more than 15 selectors)
+                            uint32_t gi = __shfl_sync(kFull, mgi, k);
+                            do {
+                                e = __ldg(h.dict + ++gi);
+                                v = bw_xor<1>(v, mono_entry<1>(e, pl));
+                            } while (e.x & 0x80u);
+                        }
+                        fv[(fb + kDedupWarps * k) * 32 + lane] = v.w[0];
+                    }
                 }
             }
             __syncthreads();

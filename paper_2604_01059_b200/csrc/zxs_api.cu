@@ -2050,6 +2050,9 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         const size_t fixed = size_t(MH.all_plane + 2) * 32 * 4 + size_t(s->dd_stack_words) * 4;
         const size_t nmt = MH.tensor_width.size();
         s->dd_t_layout.assign(nmt, uint4{0, 0, 0, 0});
+        // ZXS_DEDUP_STAGE=0: block form values from register-staged entries only (tests)
+        const char *stage_env = std::getenv("ZXS_DEDUP_STAGE");
+        const bool stage_ok = !stage_env || std::atoi(stage_env) != 0;
         s->dd_smem = 0;
         for (size_t t = 0; t < nmt; t++) {
             uint32_t bforms = 0;
@@ -2070,7 +2073,7 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
             uint32_t segbuf = (max_seg + 3) & ~3u;
             if (smem + size_t(zxs_dev::kDedupWarps) * segbuf * 4 > 227 * 1024) segbuf = 0;
             smem += size_t(zxs_dev::kDedupWarps) * segbuf * 4;
-            const bool stage = blocks && bforms > 0 && smem + size_t(bforms) * 16 <= 227 * 1024;
+            const bool stage = blocks && bforms > 0 && smem + size_t(bforms) * 16 <= 227 * 1024 && stage_ok;
             if (stage) smem += size_t(bforms) * 16;
             s->dd_t_layout[t] = make_uint4(table, segbuf, stage ? 1u : 0u, uint32_t(smem));
             s->dd_smem = std::max(s->dd_smem, smem);

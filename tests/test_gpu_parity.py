@@ -431,6 +431,28 @@ def test_dedup_bit_identical_to_per_shot(name):
     assert np.array_equal(zx.count_outputs(a, 50000, seed=9), zx.count_outputs(b, 50000, seed=9))
 
 
+@pytest.mark.parametrize("name", ["surface_d3_xmem_9t", "steane_inject", "surface_d5_r5_xmem_rz3"])
+def test_dedup_register_staged_forms_identical(name):
+    """Block form values computed from register-staged dictionary entries (the path of
+    tensors whose staged entries do not fit shared memory; ZXS_DEDUP_STAGE=0 forces it)
+    equal the per-shot path's bit for bit."""
+    import os
+    os.environ["ZXS_DEDUP_STAGE"] = "0"
+    try:
+        a = _heavy_model(name, min_factors="0", mono="1", dedup="1")
+    finally:
+        del os.environ["ZXS_DEDUP_STAGE"]
+    b = _heavy_model(name, min_factors="0", mono="1", dedup="0")
+    orc = coracle.OracleModel.load(golden_path(name))
+    rng = np.random.default_rng(43)
+    shots = 20000
+    f = rng.integers(0, 2**63, size=(orc.f_width, (shots + 63) // 64), dtype=np.uint64)
+    f[:, -1] &= np.uint64((1 << (shots & 63)) - 1)
+    u = rng.random((orc.num_positions, shots))
+    assert np.array_equal(zx.sample_given_f(a, f, shots, uniforms=u), zx.sample_given_f(b, f, shots, uniforms=u))
+    assert np.array_equal(sample(a, 70000, 5, 11), sample(b, 70000, 5, 11))
+
+
 def test_imag_health_check():
     """SURVEY finding 3: the reference never checks that P is real. Clean
     compiles report rounding-level ratios; a model whose magic component's

@@ -26,7 +26,8 @@ def run(cs, shots, seed=1, first=0):
 
 
 for name in ("surface_d3_xmem_9t", "c4_color_d5_rz3", "surface_d5_r5_xmem_rz3", "steane_inject"):
-    for env in ({}, {"ZXS_DEDUP_FUSED": 0}, {"ZXS_DEDUP_MAX_KEYS": 64}, {"ZXS_DEDUP": 0}, {"ZXS_DEDUP_SYNC": 1}):
+    for env in ({}, {"ZXS_DEDUP_FUSED": 0}, {"ZXS_DEDUP_MAX_KEYS": 64}, {"ZXS_DEDUP": 0}, {"ZXS_DEDUP_SYNC": 1},
+                {"ZXS_DEDUP_STAGE": 0}):
         cs = load(name, ZXS_HEAVY_MIN_FACTORS=0, ZXS_MONO=1, **env)
         print(name, env, run(cs, 40000, 1, 12345), zx.count_outputs(cs, 20000, seed=3).sum(), flush=True)
         cs.close()

@@ -178,6 +178,8 @@ struct zxs_sampler {
     std::vector<unsigned long long> dd_key_mask;          // per mono component (local parameters)
     std::vector<uint16_t> dd_param_map;                   // MonoHost::param_map
     std::vector<unsigned long long> dd_tread;             // per mono tensor: local parameters it reads
+    const unsigned long long *dd_null = nullptr;          // device: null pairs of every mono tensor
+    std::vector<uint32_t> dd_null_begin;                  // per mono tensor: first pair (2 words each), then the end
     std::vector<uint32_t> dd_tspw;                        // per mono tensor: segments per warp per eval item
     uint32_t dd_stack_words = 0;                          // dedup_eval_kernel stack area (words)
     std::vector<uint4> dd_t_layout;                       // per mono tensor: {table bytes, segbuf words, stage, smem}
@@ -511,6 +513,11 @@ struct MonoHost {
     std::vector<uint16_t> param_map;
     std::vector<uint64_t> tensor_loads;             // per mono tensor: plane loads per 32-shot word
     std::vector<unsigned long long> tensor_read_mask;  // per mono tensor: local parameters its forms read
+    // per mono tensor: the null space of its forms inside the read mask, as pairs {1 << q, n_q}
+    // (q a free parameter, n_q the null vector with bit q and otherwise pivot bits only); keys
+    // that differ by a null vector give every form the same value, hence the same tensor value
+    std::vector<uint32_t> tensor_null_begin{0};
+    std::vector<unsigned long long> tensor_null;
     std::vector<uint32_t> tensor_spw;                  // per mono tensor: segments per warp per eval item
     // block form tables (dedup_eval_kernel): per block of kDedupWarps segments the
     // tensor dictionary entries its records use; segment streams carry block-local ids
@@ -918,6 +925,8 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
         std::vector<uint32_t> tsb;  // per tensor: first segment (relative to sg)
         std::vector<uint64_t> tl;   // per tensor: plane loads per 32-shot word
         std::vector<unsigned long long> trm;  // per tensor: local parameters read
+        std::vector<uint32_t> tnb;            // per tensor: null pairs (end, relative to tn)
+        std::vector<unsigned long long> tn;   // null pairs of this component's tensors
         std::vector<uint32_t> tspw;           // per tensor: segments per warp in a dedup_eval_kernel item
         std::vector<uint32_t> bf, bfb, tfb;  // block forms, block ends (relative), per tensor first block
         uint32_t max_bf = 0;
@@ -1180,6 +1189,35 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                 unsigned long long rm = 0;  // local parameters any of the tensor's forms reads
                 for (uint64_t fm : form_mask) rm |= fm;
                 trm.push_back(rm);
+                // reduced row echelon form of the forms (pivot = highest bit), then one null
+                // vector per free parameter q of rm: e_q + the pivots of the rows holding q
+                std::vector<uint64_t> rows;
+                std::vector<int> piv;
+                for (uint64_t fm : form_mask) {
+                    uint64_t v = fm;
+                    for (size_t r = 0; r < rows.size(); r++) {
+                        if ((v >> piv[r]) & 1) v ^= rows[r];
+                    }
+                    if (!v) continue;
+                    const int pb = 63 - __builtin_clzll(v);
+                    for (uint64_t &row : rows) {
+                        if ((row >> pb) & 1) row ^= v;
+                    }
+                    rows.push_back(v);
+                    piv.push_back(pb);
+                }
+                uint64_t pivm = 0;
+                for (int pb : piv) pivm |= 1ull << pb;
+                for (uint64_t fr = rm & ~pivm; fr; fr &= fr - 1) {
+                    const int q = __builtin_ctzll(fr);
+                    uint64_t nv = 1ull << q;
+                    for (size_t r = 0; r < rows.size(); r++) {
+                        if ((rows[r] >> q) & 1) nv |= 1ull << piv[r];
+                    }
+                    tn.push_back(1ull << q);
+                    tn.push_back(nv);
+                }
+                tnb.push_back(uint32_t(tn.size()));
             }
             // segment streams: each starts with its first node's ancestors (internal nodes,
             // replayed to rebuild the stack), then the segment's own nodes; flags cleared
@@ -1350,6 +1388,9 @@ MonoHost encode_mono(const zxs_model_desc *d, uint32_t max_chain, uint64_t heavy
                 H.comp_key_mask.push_back(km);
                 H.tensor_loads.insert(H.tensor_loads.end(), tl.begin(), tl.end());
                 H.tensor_read_mask.insert(H.tensor_read_mask.end(), trm.begin(), trm.end());
+                const uint32_t nb0 = uint32_t(H.tensor_null.size());
+                H.tensor_null.insert(H.tensor_null.end(), tn.begin(), tn.end());
+                for (uint32_t x : tnb) H.tensor_null_begin.push_back(x + nb0);
                 H.tensor_spw.insert(H.tensor_spw.end(), tspw.begin(), tspw.end());
                 const uint32_t fb0 = uint32_t(H.block_forms.size()), blk0 = uint32_t(H.block_form_begin.size() - 1);
                 H.block_forms.insert(H.block_forms.end(), bf.begin(), bf.end());
@@ -1915,6 +1956,8 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
     if (MH.segs.empty()) MH.segs.push_back(make_uint4(0, 0, 0, 0));
     size_t o_sw = ar.add(MH.seg_words);
     size_t o_sg = ar.add(MH.segs);
+    if (MH.tensor_null.empty()) MH.tensor_null.assign(2, 0ull);
+    size_t o_null = ar.add(MH.tensor_null);
 
     CK(cudaMalloc(&s->dev_model, ar.host.size()));
     s->dev_model_bytes = ar.host.size();
@@ -2035,6 +2078,11 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
         }
         s->dd_tloads = MH.tensor_loads;
         s->dd_tread = MH.tensor_read_mask;
+        s->dd_null = reinterpret_cast<const unsigned long long *>(b + o_null);
+        s->dd_null_begin = MH.tensor_null_begin;
+        if (const char *e = std::getenv("ZXS_DEDUP_NULL")) {
+            if (std::atoi(e) == 0) s->dd_null_begin.assign(s->dd_null_begin.size(), 0u);
+        }
         s->dd_tspw = MH.tensor_spw;
         s->dd_block_forms = reinterpret_cast<const uint32_t *>(b + o_bf);
         s->dd_block_form_begin = reinterpret_cast<const uint32_t *>(b + o_bfb);
@@ -2691,9 +2739,12 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
                 const uint32_t bit_pos = (p < 63 && ((s->dd_key_mask[hc] >> p) & 1ull)) ? p : 64u;
                 s->time_begin(4, st, t0);
                 // the level's key table holds the node keys restricted to what tensor j + 1 reads
-                const unsigned long long tmask = s->dd_tread[cd.first_tensor + 1 + j];
+                // and reduced to one representative per coset of the forms' null space
+                const uint32_t tj = cd.first_tensor + 1 + j;
+                const unsigned long long tmask = s->dd_tread[tj];
+                const uint32_t nb = s->dd_null_begin[tj], ne = s->dd_null_begin[tj + 1];
                 zxs_dev::dedup_node_prep_kernel<<<ngrid, 256, 0, st>>>(cur, d.nodes[(j - 1) & 1], na, bit_pos, tmask,
-                                                                      d.table[3]);
+                                                                      s->dd_null + nb, (ne - nb) / 2, d.table[3]);
                 CK(cudaGetLastError());
                 s->time_end(4, st, t0);
                 dedup_eval(s, cd.first_tensor + 1 + j, d.table[3].ukeys, d.table[3].uslot, limit, d.value, d.partial,
@@ -3754,6 +3805,12 @@ zxs_status zxs_debug_mono_layout(const zxs_model_desc *desc, uint64_t min_factor
         // segments per warp per eval item, per mono tensor (a block = 16 x spw segments)
         blob.push_back(uint32_t(H.tensor_spw.size()));
         blob.insert(blob.end(), H.tensor_spw.begin(), H.tensor_spw.end());
+        // per mono tensor: read mask and null-space pairs (dedup_node_prep_kernel's key reduction)
+        blob.insert(blob.end(), {uint32_t(H.tensor_read_mask.size()), uint32_t(H.tensor_null_begin.size()),
+                                 uint32_t(H.tensor_null.size())});
+        for (unsigned long long x : H.tensor_read_mask) blob.insert(blob.end(), {uint32_t(x), uint32_t(x >> 32)});
+        blob.insert(blob.end(), H.tensor_null_begin.begin(), H.tensor_null_begin.end());
+        for (unsigned long long x : H.tensor_null) blob.insert(blob.end(), {uint32_t(x), uint32_t(x >> 32)});
         *needed = blob.size();
         if (out && cap >= blob.size()) std::memcpy(out, blob.data(), blob.size() * 4);
     });

@@ -931,8 +931,23 @@ __global__ void dedup_node_level0_kernel(DedupTable t, const double *__restrict_
 // parent (prev = bit ? prev - cur : cur, sampler.cpp:95-98), the key extended
 // by the bit when a later tensor reads it (bit_pos < 64); the key restricted to
 // the parameters the level's tensor reads goes into the level's key table.
+// That key is first reduced modulo the null space of the tensor's forms
+// (null[2i] = 1 << q_i, null[2i + 1] = the null vector with free bit q_i;
+// encode_mono): keys of one coset give every form -- so every record and the
+// tensor -- the same value, and the representative with no free bit set is
+// evaluated once for all of them.
+__device__ __forceinline__ unsigned long long dedup_null_reduce(unsigned long long k,
+                                                                const unsigned long long *__restrict__ null,
+                                                                uint32_t n_null) {
+    for (uint32_t i = 0; i < n_null; i++) {
+        if (k & __ldg(null + 2 * i)) k ^= __ldg(null + 2 * i + 1);
+    }
+    return k;
+}
+
 __global__ void dedup_node_prep_kernel(DedupTable nodes, DedupNodeArrays parent, DedupNodeArrays na, uint32_t bit_pos,
-                                       unsigned long long read_mask, DedupTable keys) {
+                                       unsigned long long read_mask, const unsigned long long *__restrict__ null,
+                                       uint32_t n_null, DedupTable keys) {
     const uint32_t n = min(*nodes.count, nodes.max_ids);
     const uint32_t lane = threadIdx.x & 31u;
     DedupWarpCache cache;
@@ -952,7 +967,7 @@ __global__ void dedup_node_prep_kernel(DedupTable nodes, DedupNodeArrays parent,
             na.prev[sl] = bit ? __dsub_rn(pv, cur) : cur;
         }
         // the value depends only on the parameters the tensor reads: fewer distinct keys to contract
-        const uint32_t ks = dedup_insert_warp(keys, key & read_mask, valid, lane, cache);
+        const uint32_t ks = dedup_insert_warp(keys, dedup_null_reduce(key & read_mask, null, n_null), valid, lane, cache);
         if (valid) na.kslot[sl] = ks;
     }
 }

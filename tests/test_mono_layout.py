@@ -76,7 +76,16 @@ def mono_layout(arrays, min_factors=0):
     o += n_bf
     n_spw = int(buf[o])
     spw = buf[o + 1:o + 1 + n_spw].astype(np.int64)
-    return dict(tfb=tfb, bfb=bfb, bforms=bforms, spw=spw, comps=comps, flags=flags, tcb=tcb, chunks=chunks, dict=dict_, tdb=tdb, twidth=twidth,
+    o += 1 + n_spw
+    n_rm, n_nb, n_null = (int(x) for x in buf[o:o + 3])
+    o += 3
+    u64 = lambda a: [int(a[2 * i]) | (int(a[2 * i + 1]) << 32) for i in range(len(a) // 2)]  # noqa: E731
+    read_mask = u64(buf[o:o + 2 * n_rm])
+    o += 2 * n_rm
+    null_begin = buf[o:o + n_nb].astype(np.int64)
+    o += n_nb
+    null = u64(buf[o:o + 2 * n_null])
+    return dict(read_mask=read_mask, null_begin=null_begin, null=null, tfb=tfb, bfb=bfb, bforms=bforms, spw=spw, comps=comps, flags=flags, tcb=tcb, chunks=chunks, dict=dict_, tdb=tdb, twidth=twidth,
                 tbb=tbb, basis=basis, all_plane=all_plane, words=words, tsb=tsb, segs=segs,
                 seg_words=seg_words, key_mask=key_mask)
 
@@ -340,3 +349,37 @@ def test_mono_min_factors_gate():
     arrays = zxs_format.load(golden_path("c2_surface_d3_xmem_t"))
     lay = mono_layout(arrays, min_factors=10 ** 9)
     assert not lay["comps"] and not lay["flags"].any()
+
+
+def test_null_space_keys():
+    """dedup_node_prep_kernel evaluates one key per coset of the null space of a
+    tensor's forms (encode_mono): every pair {1 << q, n_q} has n_q inside the read
+    mask with bit q set and no other free bit, and adding n_q to the parameters
+    leaves the deduplicated path's value unchanged bit for bit (every form keeps
+    its value)."""
+    rng = np.random.default_rng(11)
+    with_null = 0
+    for name in MONO_FIXTURES:
+        arrays = zxs_format.load(golden_path(name))
+        lay = mono_layout(arrays)
+        nt = len(lay["tcb"]) - 1
+        assert len(lay["read_mask"]) == nt and len(lay["null_begin"]) == nt + 1
+        for t in range(nt):
+            pairs = lay["null"][lay["null_begin"][t]:lay["null_begin"][t + 1]]
+            rm = lay["read_mask"][t]
+            qs = pairs[0::2]
+            free = 0
+            for q in qs:
+                free |= q
+            for q, n in zip(pairs[0::2], pairs[1::2]):
+                assert q & (q - 1) == 0 and n & q and n & ~rm == 0 and n & free == q
+            if not qs:
+                continue
+            with_null += 1
+            P = rng.integers(0, 2, (64, 64)).astype(np.int64)
+            P[:, [p for p in range(64) if not (rm >> p) & 1]] = 0
+            base = emulate_segments(lay, t, P)
+            for n in pairs[1::2]:
+                bits = np.array([(n >> p) & 1 for p in range(64)], np.int64)
+                assert np.array_equal(emulate_segments(lay, t, P ^ bits), base), (name, t, hex(n))
+    assert with_null, "no fixture tensor has a null space"

@@ -180,6 +180,17 @@ struct zxs_sampler {
     std::vector<unsigned long long> dd_tread;             // per mono tensor: local parameters it reads
     const unsigned long long *dd_null = nullptr;          // device: null pairs of every mono tensor
     std::vector<uint32_t> dd_null_begin;                  // per mono tensor: first pair (2 words each), then the end
+    // main-lineage speculation (dedup_init_spec_kernel): per mono component, the node
+    // records of the all-zero key's likelier-bit chain, computed on first use
+    struct Lineage {
+        bool done = false, ok = false;
+        uint32_t bits = 0;
+        unsigned long long T[zxs_dev::kSpecMaxChain], tie_lo[zxs_dev::kSpecMaxChain];
+        uint32_t tie_w[zxs_dev::kSpecMaxChain];
+    };
+    std::vector<Lineage> dd_lineage;
+    bool dd_spec = false;                                 // ZXS_DEDUP_SPEC=1: main-lineage speculation
+    char *dd_spec_dev = nullptr;                          // 64 B: one key, one value, one node record
     std::vector<uint32_t> dd_tspw;                        // per mono tensor: segments per warp per eval item
     uint32_t dd_stack_words = 0;                          // dedup_eval_kernel stack area (words)
     std::vector<uint4> dd_t_layout;                       // per mono tensor: {table bytes, segbuf words, stage, smem}
@@ -187,7 +198,7 @@ struct zxs_sampler {
     size_t dd_smem = 0;
     const uint32_t *dd_block_forms = nullptr, *dd_block_form_begin = nullptr;
     std::vector<uint32_t> dd_tfb;    // per mono tensor: first block form table (~0: dictionary ids)
-    int dd_init_occ = 1, dd_ar_occ = 1, dd_fused_occ = 1, dd_raw_occ = 1, dd_node_occ = 1;  // resident blocks per SM (per-shot dedup kernels)
+    int dd_init_occ = 1, dd_ar_occ = 1, dd_fused_occ = 1, dd_raw_occ = 1, dd_node_occ = 1, dd_node_act_occ = 1;  // resident blocks per SM (per-shot dedup kernels)
     bool dd_async = true;                 // key counts stay on the device (ZXS_DEDUP_SYNC=1: host round trips)
     bool dd_fused = true;                 // short chains in one per-shot kernel (ZXS_DEDUP_FUSED=0: step by step)
     unsigned long long *dd_dev_stats = nullptr;  // {keys, plane-load bytes} accumulated by dedup_eval_kernel
@@ -2213,7 +2224,10 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &s->dd_ar_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_ar_kernel), 256, 0));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &s->dd_node_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_node_pass_kernel), 256, 0));
+                &s->dd_node_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_node_pass_kernel<false>), 256, 0));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &s->dd_node_act_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_node_pass_kernel<true>), 256, 0));
+            if (const char *e = std::getenv("ZXS_DEDUP_SPEC")) s->dd_spec = std::atoi(e) != 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &s->dd_fused_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_fused_ar_kernel), 256, 0));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
@@ -2280,6 +2294,8 @@ size_t dedup_partial_budget() {
 
 struct DedupBufs {
     unsigned long long *key;
+    uint32_t *active;    // main-lineage speculation: active shots (aliases key, unused on that path)
+    uint32_t *n_active;
     uint32_t *slot;
     double *prev, *value0, *value, *partial;
     size_t partial_bytes;
@@ -2319,7 +2335,7 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
     const size_t partial_bytes = std::max(size_t(max_segs) * kDedupRoundKeys * 8,
                                           std::min(dedup_partial_budget(), size_t(max_segs) * max_ids * 8));
     const size_t bytes = al(cap * 8) + al(cap * 4) + al(cap * 8) + 2 * al(size_t(slots) * 8) +
-                         al(partial_bytes) + al(nout * 8) + al(4) + al(24) + al(size_t(kDedupRoundKeys) * 8) +
+                         al(partial_bytes) + al(nout * 8) + al(4) + al(8) + al(24) + al(size_t(kDedupRoundKeys) * 8) +
                          (zxs_dev::kDedupMaxFused + 1) * al(size_t(kDedupRoundKeys) * 8) + 4 * per_table +
                          2 * (3 * al(size_t(slots) * 8) + al(size_t(slots) * 4) +
                               al(size_t(slots) * sizeof(zxs_dev::DedupNodeRec)));
@@ -2344,6 +2360,8 @@ DedupBufs dedup_reserve(zxs_sampler *s, uint64_t shots) {
     d.partial_bytes = partial_bytes;
     d.counts = reinterpret_cast<unsigned long long *>(take(nout * 8));
     d.max_count = reinterpret_cast<unsigned int *>(take(8));
+    d.active = reinterpret_cast<uint32_t *>(d.key);
+    d.n_active = reinterpret_cast<uint32_t *>(take(8));
     d.err = reinterpret_cast<unsigned long long *>(take(24));
     d.xkeys = reinterpret_cast<unsigned long long *>(take(size_t(kDedupRoundKeys) * 8));
     for (uint32_t i = 0; i <= zxs_dev::kDedupMaxFused; i++) d.fvals[i] = reinterpret_cast<double *>(take(size_t(kDedupRoundKeys) * 8));
@@ -2588,6 +2606,57 @@ const uint32_t *regen_fcols(zxs_sampler *s, const zxs_dev::LaunchArgs &a, cudaSt
 // count is checked once at the end; a batch that needed more rounds (or
 // overflowed the tables) is redone on the synchronous path, which overwrites
 // every output it wrote (counts are staged, so nothing is added twice).
+//
+// dedup_lineage: the main lineage of component hc for dedup_init_spec_kernel --
+// the all-zero key's node at each level, contracted one key at a time with the
+// same dedup_eval, its record from the same node_rec (dedup_main_rec_kernel),
+// the likelier bit taken (P(bit = 1) = 1 - T 2^-53). Computed once per sampler
+// (the values depend only on the model); ok = false (no speculation) when a
+// level's ratio is out of range, which the node passes must report per shot.
+const zxs_sampler::Lineage *dedup_lineage(zxs_sampler *s, uint32_t hc, const DedupBufs &d, cudaStream_t st) {
+    if (s->dd_lineage.size() < s->mono.n_comps) s->dd_lineage.resize(s->mono.n_comps);
+    zxs_sampler::Lineage &L = s->dd_lineage[hc];
+    if (L.done) return &L;
+    L.done = true;
+    const zxs_dev::HeavyComp cd = s->mono.comps[hc];
+    if (!s->dd_spec_dev) CK(cudaMalloc(&s->dd_spec_dev, 64));
+    auto *kdev = reinterpret_cast<unsigned long long *>(s->dd_spec_dev);
+    auto *vdev = reinterpret_cast<double *>(s->dd_spec_dev + 8);               // cur, pv
+    auto *rdev = reinterpret_cast<zxs_dev::DedupNodeRec *>(s->dd_spec_dev + 32);
+    auto value = [&](uint32_t tj, unsigned long long key) {
+        key &= s->dd_tread[tj];
+        CK(cudaMemcpyAsync(kdev, &key, 8, cudaMemcpyHostToDevice, st));
+        dedup_eval(s, tj, kdev, nullptr, 1, vdev, d.partial, d.partial_bytes, st, nullptr, 1, 1);
+        double v = 0;
+        CK(cudaMemcpyAsync(&v, vdev, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return v;
+    };
+    double pv = value(cd.first_tensor, 0ull);
+    unsigned long long key = 0;
+    for (uint32_t j = 0; j < cd.n_out; j++) {
+        const double cur = value(cd.first_tensor + 1 + j, key);
+        const double in[2] = {cur, pv};
+        CK(cudaMemcpyAsync(vdev, in, 16, cudaMemcpyHostToDevice, st));
+        zxs_dev::dedup_main_rec_kernel<<<1, 1, 0, st>>>(vdev, rdev);
+        CK(cudaGetLastError());
+        zxs_dev::DedupNodeRec r;
+        CK(cudaMemcpyAsync(&r, rdev, sizeof r, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (r.T & zxs_dev::kNodeErr) return &L;
+        const uint32_t b = r.T < (1ull << 52) ? 1u : 0u;
+        L.T[j] = r.T;
+        L.tie_lo[j] = r.tie_lo;
+        L.tie_w[j] = r.tie_w;
+        L.bits |= b << j;
+        pv = b ? pv - cur : cur;  // sampler.cpp:95-98 (dedup_node_prep_kernel's __dsub_rn)
+        const uint32_t p = cd.nf + j;
+        if (b && p < 63 && ((s->dd_key_mask[hc] >> p) & 1ull)) key |= 1ull << p;
+    }
+    L.ok = true;
+    return &L;
+}
+
 void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *fcols, uint64_t fcols_ld32,
                   cudaStream_t st) {
     if (a.shots == 0) return;
@@ -2648,8 +2717,44 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
         const uint64_t iwarps = (a.shots + 1023) / 1024;
         const unsigned igrid = unsigned(std::min<uint64_t>((iwarps + zxs_dev::kDedupInitWarps - 1) / zxs_dev::kDedupInitWarps,
                                                            uint64_t(s->sm_count) * std::max(1, s->dd_init_occ)));
+        // main-lineage speculation: zero-key shots that stay on the lineage skip the node passes
+        const bool spec_ok = s->dd_spec && !fused && a.heavy_fraw && !a.uniforms && cd.n_out >= 1 &&
+                             cd.n_out <= zxs_dev::kSpecMaxChain && s->dd_identity_map;
+        const zxs_sampler::Lineage *lin = spec_ok ? dedup_lineage(s, hc, d, st) : nullptr;
+        const bool spec = lin && lin->ok;
         s->time_begin(4, st, t0);
-        if (a.heavy_fraw) {  // per-shot f words from shot_kernel (identity parameter maps only)
+        if (spec) {
+            const unsigned long long fm = s->dd_key_mask[hc] & (cd.nf >= 63 ? (1ull << 63) - 1 : (1ull << cd.nf) - 1);
+            zxs_dev::DedupSpecArgs sa{};
+            sa.seed = a.seed;
+            sa.first_shot = a.first_shot;
+            sa.shots = a.shots;
+            for (int i = 0; i < 10; i++) sa.k0_round[i] = a.k0_round[i];
+            sa.ci = cd.ci;
+            sa.n_out = cd.n_out;
+            sa.main_bits = lin->bits;
+            for (uint32_t j = 0; j < cd.n_out; j++) {
+                sa.T[j] = lin->T[j];
+                sa.tie_lo[j] = lin->tie_lo[j];
+                sa.tie_w[j] = lin->tie_w[j];
+                sa.out[j] = s->comp_outputs[cd.out_begin + j];
+            }
+            sa.out32 = a.out32;
+            sa.out_ld32 = a.ld32;
+            sa.err = d.err;
+            sa.active = d.active;
+            sa.n_active = d.n_active;
+            CK(cudaMemsetAsync(d.n_active, 0, 4, st));
+            const unsigned rgrid = unsigned(std::min<uint64_t>((a.shots + 255) / 256, uint64_t(s->sm_count) * 8));
+            if (a.fraw_bytes == 4) {
+                zxs_dev::dedup_init_spec_kernel<uint32_t><<<rgrid, 256, 0, st>>>(
+                    static_cast<const uint32_t *>(a.heavy_fraw), fm, d.slot, d.table[0], sa);
+            } else {
+                zxs_dev::dedup_init_spec_kernel<unsigned long long><<<rgrid, 256, 0, st>>>(
+                    static_cast<const unsigned long long *>(a.heavy_fraw), fm, d.slot, d.table[0], sa);
+            }
+            CK(cudaGetLastError());
+        } else if (a.heavy_fraw) {  // per-shot f words from shot_kernel (identity parameter maps only)
             const unsigned long long fm = s->dd_key_mask[hc] & (cd.nf >= 63 ? (1ull << 63) - 1 : (1ull << cd.nf) - 1);
             const unsigned rgrid =
                 unsigned(std::min<uint64_t>((a.shots + 255) / 256, uint64_t(s->sm_count) * std::max(1, s->dd_raw_occ)));
@@ -2714,22 +2819,42 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
             continue;
         }
         // ---- node levels (zxs_dedup.cuh): level 0's nodes are the base keys
-        dedup_eval(s, cd.first_tensor, d.table[0].ukeys, d.table[0].uslot, limit, d.value0, d.partial, d.partial_bytes, st,
-                   d.table[0].count, 1, d.table[0].mask + 1);
+        const unsigned ngrid = unsigned(s->sm_count) * 4;
         if (cd.n_out == 0) {
+            dedup_eval(s, cd.first_tensor, d.table[0].ukeys, d.table[0].uslot, limit, d.value0, d.partial, d.partial_bytes,
+                       st, d.table[0].count, 1, d.table[0].mask + 1);
             clear(d.table[0]);
             continue;
         }
-        dedup_eval(s, cd.first_tensor + 1, d.table[0].ukeys, d.table[0].uslot, limit, d.value, d.partial, d.partial_bytes,
-                   st, d.table[0].count, 1, d.table[0].mask + 1);
-        const unsigned ngrid = unsigned(s->sm_count) * 4;
+        // tensors 0 and 1 on the base keys restricted to what each reads and reduced modulo its
+        // null space (dedup_key_restrict_kernel; table 3, kslot in the level-1 node arrays)
+        uint32_t *kslot0 = d.nodes[1].kslot;
+        for (uint32_t pos = 0; pos < 2; pos++) {
+            const uint32_t tj = cd.first_tensor + pos;
+            const uint32_t nb = s->dd_null_begin[tj], ne = s->dd_null_begin[tj + 1];
+            s->time_begin(4, st, t0);
+            zxs_dev::dedup_key_restrict_kernel<<<ngrid, 256, 0, st>>>(d.table[0], s->dd_tread[tj], s->dd_null + nb,
+                                                                     (ne - nb) / 2, d.table[3], kslot0);
+            CK(cudaGetLastError());
+            s->time_end(4, st, t0);
+            dedup_eval(s, tj, d.table[3].ukeys, d.table[3].uslot, limit, d.value, d.partial, d.partial_bytes, st,
+                       d.table[3].count, 1, d.table[3].mask + 1);
+            if (pos == 0) {
+                s->time_begin(4, st, t0);
+                zxs_dev::dedup_gather_kernel<<<ngrid, 256, 0, st>>>(d.table[0], d.value, kslot0, d.value0);
+                CK(cudaGetLastError());
+                s->time_end(4, st, t0);
+                clear(d.table[3]);
+            }
+        }
         s->time_begin(4, st, t0);
         auto node_table = [&](uint32_t j) -> const zxs_dev::DedupTable & { return j == 0 ? d.table[0] : d.table[1 + ((j - 1) & 1)]; };
         // a node whose bit is certain gets its only child in the next level's (clear) table here
-        zxs_dev::dedup_node_level0_kernel<<<ngrid, 256, 0, st>>>(d.table[0], d.value0, d.value, d.nodes[0], node_table(1),
-                                                                 cd.n_out > 1);
+        zxs_dev::dedup_node_level0_kernel<<<ngrid, 256, 0, st>>>(d.table[0], d.value0, d.value, kslot0, d.nodes[0],
+                                                                 node_table(1), cd.n_out > 1);
         CK(cudaGetLastError());
         s->time_end(4, st, t0);
+        clear(d.table[3]);
         for (uint32_t j = 0; j < cd.n_out; j++) {
             const zxs_dev::DedupTable &cur = node_table(j);
             const zxs_dev::DedupNodeArrays &na = d.nodes[j & 1];
@@ -2780,8 +2905,13 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
             void *rargs[] = {&ra};
             const unsigned agrid = unsigned(std::min<uint64_t>(
                 (a.shots + 256 * zxs_dev::kNodePassG - 1) / (256 * zxs_dev::kNodePassG),
-                uint64_t(s->sm_count) * std::max(1, s->dd_node_occ)));
-            CK(cudaLaunchKernel(reinterpret_cast<const void *>(&zxs_dev::dedup_node_pass_kernel), dim3(agrid), dim3(256),
+                uint64_t(s->sm_count) * std::max(1, spec ? s->dd_node_act_occ : s->dd_node_occ)));
+            ra.active = spec ? d.active : nullptr;
+            ra.n_active = d.n_active;
+            ra.main_bit = spec ? (lin->bits >> j) & 1u : 0u;
+            const void *pk = spec ? reinterpret_cast<const void *>(&zxs_dev::dedup_node_pass_kernel<true>)
+                                  : reinterpret_cast<const void *>(&zxs_dev::dedup_node_pass_kernel<false>);
+            CK(cudaLaunchKernel(pk, dim3(agrid), dim3(256),
                                 rargs, 0, st));
             s->time_end(4, st, t0);
             clear(cur);
@@ -3007,6 +3137,7 @@ void zxs_sampler_destroy(zxs_sampler *s) {
     if (s->dev_flip_out) cudaFree(s->dev_flip_out);
     if (s->mono_scratch) cudaFree(s->mono_scratch);
     if (s->dd_buf) cudaFree(s->dd_buf);
+    if (s->dd_spec_dev) cudaFree(s->dd_spec_dev);
     if (s->dd_pinned) cudaFreeHost(s->dd_pinned);
     if (s->dd_dev_stats) cudaFree(s->dd_dev_stats);
     for (auto &t : s->timed) {

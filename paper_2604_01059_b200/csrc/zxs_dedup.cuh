@@ -243,6 +243,85 @@ __global__ void __launch_bounds__(256) dedup_init_raw_kernel(const FW *__restric
     }
 }
 
+// ---- main-lineage speculation (node levels, raw f words). The main lineage is
+// the chain of nodes of the all-zero key that always takes the likelier bit;
+// its decision records are the same node_rec a node pass would read (computed
+// once per sampler, launch_dedup). A shot whose key is 0 draws its chain
+// uniforms here (the same Philox draws as the node passes, sampler.cpp:37-39,
+// 84-99) and compares them with the lineage's thresholds; while every bit is
+// the lineage's the shot is done: its bits are the lineage's, already in the
+// record words this kernel writes for every shot. The other shots -- a nonzero
+// key, or a draw off the lineage -- go to the active list and through the
+// node passes (ACT), which flip their bits where they differ.
+constexpr uint32_t kSpecMaxChain = 32;
+struct DedupSpecArgs {
+    uint64_t seed, first_shot, shots;
+    uint32_t k0_round[10];
+    uint32_t ci, n_out;
+    uint32_t main_bits;                      // bit j: the lineage's bit at position j
+    unsigned long long T[kSpecMaxChain];     // bit = (k >= T), node_rec
+    unsigned long long tie_lo[kSpecMaxChain];
+    uint32_t tie_w[kSpecMaxChain];
+    uint32_t out[kSpecMaxChain];             // record row of position j
+    uint32_t *out32;
+    uint64_t out_ld32;
+    unsigned long long *err;                 // err[2]: near-tie draws
+    uint32_t *active;                        // [shots] active shots (compacted)
+    uint32_t *n_active;
+};
+
+template <typename FW>
+__global__ void __launch_bounds__(256) dedup_init_spec_kernel(const FW *__restrict__ fraw, unsigned long long f_mask,
+                                                              uint32_t *slot_out, DedupTable table,
+                                                              const __grid_constant__ DedupSpecArgs a) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t seed_hi = uint32_t(a.seed >> 32);
+    const uint32_t k2c = uint32_t(kP1c) ^ a.k0_round[1];
+    DedupWarpCache cache;
+    const uint64_t shots64 = (a.shots + 63) & ~uint64_t(63);
+    const uint64_t out_words = min(a.out_ld32, shots64 / 32);
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t s0 = uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); s0 < shots64; s0 += stride) {
+        const uint64_t s = s0 + lane;
+        const bool valid = s < a.shots;
+        const unsigned long long k = valid ? ((unsigned long long)__ldg(fraw + s) & f_mask) : 0ull;
+        bool on = valid && k == 0ull;  // on the main lineage so far
+        uint32_t ties = 0;             // counted once the shot is done (an active shot's passes count its own)
+        const uint64_t shot = a.first_shot + s;
+        const PhiloxPre pre[1] = {philox_pre(uint32_t(shot), uint32_t(shot >> 32), a.k0_round[0])};
+        for (uint32_t j = 0; j < a.n_out; j++) {
+            if (!__any_sync(kFull, on)) break;
+            const uint32_t stream = 0x80000000u ^ (a.ci << 12) ^ j;  // sampler.cpp:37-39
+            uint32_t rhi[1], rlo[1];
+            philox_tail<1>(pre, seed_hi ^ stream, a.k0_round, k2c, a.k0_round[9], rhi, rlo);
+            const unsigned long long kk = ((uint64_t(rhi[0]) << 32) | rlo[0]) >> 11;  // uniform_at = kk 2^-53
+            if (on) {
+                ties += kk - a.tie_lo[j] <= a.tie_w[j] ? 1u : 0u;
+                on = uint32_t(kk >= a.T[j]) == ((a.main_bits >> j) & 1u);
+            }
+        }
+        if (on && ties) atomicAdd(&a.err[2], (unsigned long long)ties);
+        // every shot's record words start with the lineage's bits (zero tails)
+        const uint32_t vm = __ballot_sync(kFull, valid);
+        if (a.out32 && lane < a.n_out && (s0 >> 5) < out_words) {
+            a.out32[a.out[lane] * a.out_ld32 + (s0 >> 5)] = ((a.main_bits >> lane) & 1u) ? vm : 0u;
+        }
+        const bool act = valid && !on;
+        const uint32_t am = __ballot_sync(kFull, act);
+        if (am) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(a.n_active, uint32_t(__popc(am)));
+            base = __shfl_sync(kFull, base, 0);
+            const uint32_t i = base + __popc(am & ((1u << lane) - 1u));
+            const uint32_t sl = dedup_insert_warp(table, k, act, lane, cache);
+            if (act) {
+                a.active[i] = uint32_t(s);
+                slot_out[i] = sl;
+            }
+        }
+    }
+}
+
 struct DedupEvalArgs {
     const uint32_t *words;  // segment streams
     const uint4 *segs;      // this tensor's segments {word_begin, n_words, n_nodes, 0}
@@ -911,14 +990,22 @@ __device__ __forceinline__ DedupNodeRec node_rec(double cur, double pv, uint32_t
     return r;
 }
 
+// One node record from (cur, pv) = v[0], v[1] (main-lineage speculation, launch_dedup).
+__global__ void dedup_main_rec_kernel(const double *v, DedupNodeRec *out) {
+    DedupTable none{};
+    *out = node_rec(v[0], v[1], 0u, none, false);
+}
+
 // Level 0: the nodes are the base keys (table ids), already contracted for the
-// normalization (value0) and the first marginal (value), both by table slot.
+// normalization (value0, by node slot) and the first marginal (value, by the
+// slot kslot[node slot] of the node's reduced key; kslot null: by node slot).
 __global__ void dedup_node_level0_kernel(DedupTable t, const double *__restrict__ value0, const double *__restrict__ value,
-                                         DedupNodeArrays na, DedupTable next, bool insert_next) {
+                                         const uint32_t *__restrict__ kslot, DedupNodeArrays na, DedupTable next,
+                                         bool insert_next) {
     const uint32_t n = min(*t.count, t.max_ids);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t sl = t.uslot[i];  // node arrays are indexed by table slot
-        const double pv = value0[sl], cur = value[sl];
+        const double pv = value0[sl], cur = value[kslot ? kslot[sl] : sl];
         na.key[sl] = t.ukeys[i];
         na.prev[sl] = pv;
         na.cur[sl] = cur;
@@ -927,15 +1014,10 @@ __global__ void dedup_node_level0_kernel(DedupTable t, const double *__restrict_
     }
 }
 
-// Level j + 1's nodes (table entries parent << 1 | bit): key and prev from the
-// parent (prev = bit ? prev - cur : cur, sampler.cpp:95-98), the key extended
-// by the bit when a later tensor reads it (bit_pos < 64); the key restricted to
-// the parameters the level's tensor reads goes into the level's key table.
-// That key is first reduced modulo the null space of the tensor's forms
-// (null[2i] = 1 << q_i, null[2i + 1] = the null vector with free bit q_i;
-// encode_mono): keys of one coset give every form -- so every record and the
-// tensor -- the same value, and the representative with no free bit set is
-// evaluated once for all of them.
+// A key reduced modulo the null space of a tensor's forms (null[2i] = 1 << q_i,
+// null[2i + 1] = the null vector with free bit q_i; encode_mono): keys of one
+// coset give every form -- so every record and the tensor -- the same value,
+// and the representative with no free bit set is evaluated once for all of them.
 __device__ __forceinline__ unsigned long long dedup_null_reduce(unsigned long long k,
                                                                 const unsigned long long *__restrict__ null,
                                                                 uint32_t n_null) {
@@ -945,6 +1027,39 @@ __device__ __forceinline__ unsigned long long dedup_null_reduce(unsigned long lo
     return k;
 }
 
+// Level 0's key tables: the base keys restricted to what tensor 0 (or 1) reads
+// and reduced modulo its null space; kslot[node slot] = the reduced key's slot.
+__global__ void dedup_key_restrict_kernel(DedupTable nodes, unsigned long long read_mask,
+                                          const unsigned long long *__restrict__ null, uint32_t n_null, DedupTable keys,
+                                          uint32_t *__restrict__ kslot) {
+    const uint32_t n = min(*nodes.count, nodes.max_ids);
+    const uint32_t lane = threadIdx.x & 31u;
+    DedupWarpCache cache;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < n; i0 += stride) {
+        const uint32_t i = i0 + lane;
+        const bool valid = i < n;
+        const unsigned long long key = valid ? dedup_null_reduce(nodes.ukeys[i] & read_mask, null, n_null) : 0ull;
+        const uint32_t ks = dedup_insert_warp(keys, key, valid, lane, cache);
+        if (valid) kslot[nodes.uslot[i]] = ks;
+    }
+}
+
+// dst[node slot] = src[kslot[node slot]] for every node of the table.
+__global__ void dedup_gather_kernel(DedupTable nodes, const double *__restrict__ src, const uint32_t *__restrict__ kslot,
+                                    double *__restrict__ dst) {
+    const uint32_t n = min(*nodes.count, nodes.max_ids);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t sl = nodes.uslot[i];
+        dst[sl] = src[kslot[sl]];
+    }
+}
+
+// Level j + 1's nodes (table entries parent << 1 | bit): key and prev from the
+// parent (prev = bit ? prev - cur : cur, sampler.cpp:95-98), the key extended
+// by the bit when a later tensor reads it (bit_pos < 64); the key restricted to
+// the parameters the level's tensor reads and reduced modulo its null space
+// goes into the level's key table.
 __global__ void dedup_node_prep_kernel(DedupTable nodes, DedupNodeArrays parent, DedupNodeArrays na, uint32_t bit_pos,
                                        unsigned long long read_mask, const unsigned long long *__restrict__ null,
                                        uint32_t n_null, DedupTable keys) {
@@ -998,6 +1113,12 @@ struct DedupNodePassArgs {
     const double *uniforms;
     uint64_t uniforms_ld, upos;
     unsigned long long *err;
+    // main-lineage speculation (dedup_init_spec_kernel): the pass visits only the active
+    // shots (active[i], slot[i] for i < *n_active); every record word already holds the
+    // main lineage's bit main_bit, an active shot whose bit differs flips its own bit
+    const uint32_t *active;
+    const uint32_t *n_active;
+    uint32_t main_bit;
 };
 
 // One position for every shot: lane = shots s + 32 g (G groups per warp
@@ -1007,6 +1128,7 @@ struct DedupNodePassArgs {
 #endif
 constexpr int kNodePassG = ZXS_NODE_G;  // 4 or 8
 static_assert(kNodePassG % 4 == 0, "node pass stores 128-bit groups of four 32-shot words");
+template <bool ACT>
 __global__ void __launch_bounds__(256) dedup_node_pass_kernel(const __grid_constant__ DedupNodePassArgs a) {
     constexpr int G = kNodePassG;
     const uint32_t lane = threadIdx.x & 31u;
@@ -1019,17 +1141,25 @@ __global__ void __launch_bounds__(256) dedup_node_pass_kernel(const __grid_const
     const uint64_t shots64 = (a.shots + 63) & ~uint64_t(63);
     // this batch's record words (a split batch's rows continue past them: out_ld32 is only the stride)
     const uint64_t out_words = min(a.out_ld32, shots64 / 32);
-    for (uint64_t s0 = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * G; s0 < shots64; s0 += stride) {
-        uint64_t s[G];
+    const uint64_t n_items = ACT ? uint64_t(*a.n_active) : shots64;
+    int delta = 0;  // ACT: ones minus the main lineage's, this lane's shots
+    for (uint64_t s0 = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * G; s0 < n_items; s0 += stride) {
+        uint64_t s[G], idx[G];
         bool valid[G], bit[G];
         uint32_t node[G];
 #pragma unroll
         for (int g = 0; g < G; g++) {
-            s[g] = s0 + 32 * g + lane;
-            valid[g] = s[g] < a.shots;
+            idx[g] = s0 + 32 * g + lane;
+            if (ACT) {
+                valid[g] = idx[g] < n_items;
+                s[g] = valid[g] ? __ldg(a.active + idx[g]) : 0ull;
+            } else {
+                s[g] = idx[g];
+                valid[g] = s[g] < a.shots;
+            }
             // node arrays are indexed by table slot (measured: prefetching the next iteration's slots,
             // or 8 shots per lane, is slower)
-            node[g] = valid[g] ? __ldg(a.slot + s[g]) : 0u;
+            node[g] = valid[g] ? __ldg(a.slot + idx[g]) : 0u;
         }
         DedupNodeRec r[G];
         bool need = false;  // a draw is needed unless every node's bit is certain (T = 0 or 2^53, no error)
@@ -1073,9 +1203,19 @@ __global__ void __launch_bounds__(256) dedup_node_pass_kernel(const __grid_const
                 }
                 if (r[g].T & kNodeErr) report_ratio_error(a.err, a.first_shot + s[g]);
             }
-            word[g] = __ballot_sync(kFull, bit[g]);
+            if (!ACT) word[g] = __ballot_sync(kFull, bit[g]);
         }
-        if (lane == 0) {
+        if (ACT) {
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+                if (valid[g] && uint32_t(bit[g]) != a.main_bit) {
+                    delta += bit[g] ? 1 : -1;
+                    if (a.out32 && (s[g] >> 5) < out_words) {
+                        atomicXor(a.out32 + a.out * a.out_ld32 + (s[g] >> 5), 1u << (s[g] & 31));
+                    }
+                }
+            }
+        } else if (lane == 0) {
             const uint64_t w0 = s0 >> 5;
             if (a.out32) {
                 uint32_t *row = a.out32 + a.out * a.out_ld32;
@@ -1102,11 +1242,18 @@ __global__ void __launch_bounds__(256) dedup_node_pass_kernel(const __grid_const
                 // outside [0, 1) can still take the other bit)
                 const bool known = r[g].child < kNodeNoChild && bit[g] == ((r[g].T & ~kNodeErr) == 0ull);
                 const uint32_t ns = dedup_insert_warp(a.next, e, valid[g] && !known, lane, cache);
-                if (valid[g]) a.slot[s[g]] = known ? r[g].child : ns;
+                if (valid[g]) a.slot[idx[g]] = known ? r[g].child : ns;
             }
         }
     }
-    if (a.counts && lane == 0 && ones) atomicAdd(&a.counts[a.out], ones);
+    if (ACT) {
+        // every shot's word was written with the main lineage's bit: shots x main_bit, then the deltas
+        if (a.counts && blockIdx.x == 0 && threadIdx.x == 0 && a.main_bit) atomicAdd(&a.counts[a.out], a.shots);
+        const int d = __reduce_add_sync(kFull, delta);
+        if (a.counts && lane == 0 && d) atomicAdd(&a.counts[a.out], (unsigned long long)(long long)d);
+    } else if (a.counts && lane == 0 && ones) {
+        atomicAdd(&a.counts[a.out], ones);
+    }
 }
 
 // ---- fused chain (short chains): every position's keys are the base keys

@@ -168,3 +168,23 @@ def test_decoded_evaluation_rounds_identical():
     stats = cs.dedup_stats()
     assert stats["eval_launches"] > 2 * 16, stats  # several rounds per tensor
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("shots,first", [(1 << 24, 3 << 26), (1_000_037, (1 << 32) - 500_000)])
+def test_main_lineage_speculation_identical(shots, first):
+    """Main-lineage speculation (ZXS_DEDUP_SPEC=1, dedup_init_spec_kernel: zero-key shots that stay on
+    the all-zero key's likelier-bit chain skip the node passes; the passes visit
+    only the active shots and flip their bits) gives the records, the per-output
+    counts and the near-tie count of every shot going through the node passes
+    (ZXS_DEDUP_SPEC=0) -- including a ragged batch that crosses 2^32."""
+    if not os.path.exists(BIG):
+        pytest.skip(f"{BIG} absent")
+    seed = 17
+    on, off = _model(BIG, ZXS_DEDUP_SPEC="1"), _model(BIG, ZXS_DEDUP_SPEC="0")
+    on.tie_count(reset=True)
+    off.tie_count(reset=True)
+    got = _sample(on, shots, seed, first)
+    want = _sample(off, shots, seed, first)
+    assert np.array_equal(got, want)
+    assert on.tie_count(reset=True) == off.tie_count(reset=True)
+    assert np.array_equal(on.count(seed, first, shots), off.count(seed, first, shots))

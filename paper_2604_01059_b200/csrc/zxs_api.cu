@@ -189,7 +189,7 @@ struct zxs_sampler {
         uint32_t tie_w[zxs_dev::kSpecMaxChain];
     };
     std::vector<Lineage> dd_lineage;
-    bool dd_spec = false;                                 // ZXS_DEDUP_SPEC=1: main-lineage speculation
+    bool dd_spec = true;                                  // ZXS_DEDUP_SPEC=0: every shot through the node passes
     char *dd_spec_dev = nullptr;                          // 64 B: one key, one value, one node record
     std::vector<uint32_t> dd_tspw;                        // per mono tensor: segments per warp per eval item
     uint32_t dd_stack_words = 0;                          // dedup_eval_kernel stack area (words)

@@ -198,7 +198,7 @@ struct zxs_sampler {
     size_t dd_smem = 0;
     const uint32_t *dd_block_forms = nullptr, *dd_block_form_begin = nullptr;
     std::vector<uint32_t> dd_tfb;    // per mono tensor: first block form table (~0: dictionary ids)
-    int dd_init_occ = 1, dd_ar_occ = 1, dd_fused_occ = 1, dd_raw_occ = 1, dd_node_occ = 1, dd_node_act_occ = 1;  // resident blocks per SM (per-shot dedup kernels)
+    int dd_init_occ = 1, dd_ar_occ = 1, dd_fused_occ = 1, dd_raw_occ = 1, dd_node_occ = 1, dd_node_act_occ = 1, dd_spec_occ = 1;  // resident blocks per SM (per-shot dedup kernels)
     bool dd_async = true;                 // key counts stay on the device (ZXS_DEDUP_SYNC=1: host round trips)
     bool dd_fused = true;                 // short chains in one per-shot kernel (ZXS_DEDUP_FUSED=0: step by step)
     unsigned long long *dd_dev_stats = nullptr;  // {keys, plane-load bytes} accumulated by dedup_eval_kernel
@@ -2227,6 +2227,8 @@ void build(zxs_sampler *s, const zxs_model_desc *d) {
                 &s->dd_node_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_node_pass_kernel<false>), 256, 0));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &s->dd_node_act_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_node_pass_kernel<true>), 256, 0));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &s->dd_spec_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_init_spec_kernel<unsigned long long>), 256, 0));
             if (const char *e = std::getenv("ZXS_DEDUP_SPEC")) s->dd_spec = std::atoi(e) != 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &s->dd_fused_occ, reinterpret_cast<const void *>(&zxs_dev::dedup_fused_ar_kernel), 256, 0));
@@ -2745,7 +2747,8 @@ void launch_dedup(zxs_sampler *s, const zxs_dev::LaunchArgs &a, const uint32_t *
             sa.active = d.active;
             sa.n_active = d.n_active;
             CK(cudaMemsetAsync(d.n_active, 0, 4, st));
-            const unsigned rgrid = unsigned(std::min<uint64_t>((a.shots + 255) / 256, uint64_t(s->sm_count) * 8));
+            const unsigned rgrid = unsigned(std::min<uint64_t>((a.shots + 256 * zxs_dev::kSpecG - 1) / (256 * zxs_dev::kSpecG),
+                                                               uint64_t(s->sm_count) * std::max(1, s->dd_spec_occ)));
             if (a.fraw_bytes == 4) {
                 zxs_dev::dedup_init_spec_kernel<uint32_t><<<rgrid, 256, 0, st>>>(
                     static_cast<const uint32_t *>(a.heavy_fraw), fm, d.slot, d.table[0], sa);

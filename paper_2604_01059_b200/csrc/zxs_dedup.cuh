@@ -270,53 +270,79 @@ struct DedupSpecArgs {
     uint32_t *n_active;
 };
 
+#ifndef ZXS_SPEC_G
+#define ZXS_SPEC_G 4
+#endif
+constexpr int kSpecG = ZXS_SPEC_G;  // 32-shot groups per warp iteration (independent Philox chains per lane)
 template <typename FW>
 __global__ void __launch_bounds__(256) dedup_init_spec_kernel(const FW *__restrict__ fraw, unsigned long long f_mask,
                                                               uint32_t *slot_out, DedupTable table,
                                                               const __grid_constant__ DedupSpecArgs a) {
+    constexpr int G = kSpecG;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t seed_hi = uint32_t(a.seed >> 32);
     const uint32_t k2c = uint32_t(kP1c) ^ a.k0_round[1];
     DedupWarpCache cache;
     const uint64_t shots64 = (a.shots + 63) & ~uint64_t(63);
     const uint64_t out_words = min(a.out_ld32, shots64 / 32);
-    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-    for (uint64_t s0 = uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); s0 < shots64; s0 += stride) {
-        const uint64_t s = s0 + lane;
-        const bool valid = s < a.shots;
-        const unsigned long long k = valid ? ((unsigned long long)__ldg(fraw + s) & f_mask) : 0ull;
-        bool on = valid && k == 0ull;  // on the main lineage so far
-        uint32_t ties = 0;             // counted once the shot is done (an active shot's passes count its own)
-        const uint64_t shot = a.first_shot + s;
-        const PhiloxPre pre[1] = {philox_pre(uint32_t(shot), uint32_t(shot >> 32), a.k0_round[0])};
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * G;
+    for (uint64_t s0 = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * G; s0 < shots64; s0 += stride) {
+        uint64_t s[G];
+        bool valid[G], on[G];  // on: on the main lineage so far
+        unsigned long long k[G];
+        uint32_t ties[G];      // counted once the shot is done (an active shot's passes count its own)
+        PhiloxPre pre[G];
+        bool any_on = false;
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            s[g] = s0 + 32 * g + lane;
+            valid[g] = s[g] < a.shots;
+            k[g] = valid[g] ? ((unsigned long long)__ldg(fraw + s[g]) & f_mask) : 0ull;
+            on[g] = valid[g] && k[g] == 0ull;
+            any_on |= on[g];
+            ties[g] = 0;
+            const uint64_t shot = a.first_shot + s[g];
+            pre[g] = philox_pre(uint32_t(shot), uint32_t(shot >> 32), a.k0_round[0]);
+        }
         for (uint32_t j = 0; j < a.n_out; j++) {
-            if (!__any_sync(kFull, on)) break;
+            if (!__any_sync(kFull, any_on)) break;
+            // a certain lineage bit (T = 0: k >= 0; T = 2^53: k < 2^53) needs no draw, has no near ties
+            if (a.T[j] == 0ull || a.T[j] == (1ull << 53)) continue;
             const uint32_t stream = 0x80000000u ^ (a.ci << 12) ^ j;  // sampler.cpp:37-39
-            uint32_t rhi[1], rlo[1];
-            philox_tail<1>(pre, seed_hi ^ stream, a.k0_round, k2c, a.k0_round[9], rhi, rlo);
-            const unsigned long long kk = ((uint64_t(rhi[0]) << 32) | rlo[0]) >> 11;  // uniform_at = kk 2^-53
-            if (on) {
-                ties += kk - a.tie_lo[j] <= a.tie_w[j] ? 1u : 0u;
-                on = uint32_t(kk >= a.T[j]) == ((a.main_bits >> j) & 1u);
+            uint32_t rhi[G], rlo[G];
+            philox_tail<G>(pre, seed_hi ^ stream, a.k0_round, k2c, a.k0_round[9], rhi, rlo);
+            any_on = false;
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+                const unsigned long long kk = ((uint64_t(rhi[g]) << 32) | rlo[g]) >> 11;  // uniform_at = kk 2^-53
+                if (on[g]) {
+                    ties[g] += kk - a.tie_lo[j] <= a.tie_w[j] ? 1u : 0u;
+                    on[g] = uint32_t(kk >= a.T[j]) == ((a.main_bits >> j) & 1u);
+                }
+                any_on |= on[g];
             }
         }
-        if (on && ties) atomicAdd(&a.err[2], (unsigned long long)ties);
-        // every shot's record words start with the lineage's bits (zero tails)
-        const uint32_t vm = __ballot_sync(kFull, valid);
-        if (a.out32 && lane < a.n_out && (s0 >> 5) < out_words) {
-            a.out32[a.out[lane] * a.out_ld32 + (s0 >> 5)] = ((a.main_bits >> lane) & 1u) ? vm : 0u;
-        }
-        const bool act = valid && !on;
-        const uint32_t am = __ballot_sync(kFull, act);
-        if (am) {
-            uint32_t base = 0;
-            if (lane == 0) base = atomicAdd(a.n_active, uint32_t(__popc(am)));
-            base = __shfl_sync(kFull, base, 0);
-            const uint32_t i = base + __popc(am & ((1u << lane) - 1u));
-            const uint32_t sl = dedup_insert_warp(table, k, act, lane, cache);
-            if (act) {
-                a.active[i] = uint32_t(s);
-                slot_out[i] = sl;
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            if (on[g] && ties[g]) atomicAdd(&a.err[2], (unsigned long long)ties[g]);
+            // every shot's record words start with the lineage's bits (zero tails)
+            const uint32_t vm = __ballot_sync(kFull, valid[g]);
+            const uint64_t w = (s0 >> 5) + g;
+            if (a.out32 && lane < a.n_out && w < out_words) {
+                a.out32[a.out[lane] * a.out_ld32 + w] = ((a.main_bits >> lane) & 1u) ? vm : 0u;
+            }
+            const bool act = valid[g] && !on[g];
+            const uint32_t am = __ballot_sync(kFull, act);
+            if (am) {
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(a.n_active, uint32_t(__popc(am)));
+                base = __shfl_sync(kFull, base, 0);
+                const uint32_t i = base + __popc(am & ((1u << lane) - 1u));
+                const uint32_t sl = dedup_insert_warp(table, k[g], act, lane, cache);
+                if (act) {
+                    a.active[i] = uint32_t(s[g]);
+                    slot_out[i] = sl;
+                }
             }
         }
     }

@@ -24,11 +24,19 @@
 //      values looked up by key: for short chains every position's keys are
 //      expanded over the sampled-bit patterns up front and one kernel runs
 //      the whole chain (dedup_expand_kernel, dedup_fused_ar_kernel);
-//      otherwise one dedup_ar_kernel per position inserts the extended keys
-//      for the next tensor.
+//      otherwise the chain runs as node levels (a shot's state before
+//      position j is a node: key + prev marginal; per level the distinct
+//      node keys are contracted, one decision record per node, one pass per
+//      shot: dedup_node_*_kernel; dedup_ar_kernel is the synchronous path).
+// A level's keys are restricted to the parameters its tensor reads and
+// reduced modulo the null space of its parity forms (dedup_null_reduce):
+// one contraction per coset. Shots whose key is 0 and whose draws stay on
+// the all-zero key's likelier-bit chain (the main lineage, contracted once
+// per sampler) are finished by dedup_init_spec_kernel; only the others go
+// through the node passes.
 // Key counts stay on the device; the host checks once per batch and redoes
-// a batch that needed more than one evaluation round synchronously. Every
-// step is recomputed per batch (nothing is cached across calls).
+// an overflowing batch as two halves. Every step except the main lineage is
+// recomputed per batch.
 #pragma once
 
 #include "zxs_mono.cuh"

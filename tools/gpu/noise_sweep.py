@@ -21,11 +21,12 @@ from tools.noise_scale import scale  # noqa: E402
 path = sys.argv[1] if len(sys.argv) > 1 else "data/c3_cultivation_d3.zxs.xz"
 dedup_shots = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 26
 mono_shots = int(sys.argv[3]) if len(sys.argv) > 3 else 1 << 14
+paths = ("1",) if len(sys.argv) > 4 and sys.argv[4] == "dedup-only" else ("1", "0")
 base = zxs_format.load(path)
 dev = torch.device("cuda", 0)
 for r in (0.1, 1.0, 3.0, 10.0):
     arrays = scale(base, r)
-    for dedup in ("1", "0"):
+    for dedup in paths:
         os.environ["ZXS_DEDUP"] = dedup
         cs = zx.CompiledSampler(arrays)
         shots = dedup_shots if dedup == "1" else mono_shots

@@ -1162,8 +1162,11 @@ struct DedupNodePassArgs {
 #endif
 constexpr int kNodePassG = ZXS_NODE_G;  // 4 or 8
 static_assert(kNodePassG % 4 == 0, "node pass stores 128-bit groups of four 32-shot words");
+#ifndef ZXS_NODE_ACT_MINB
+#define ZXS_NODE_ACT_MINB 1
+#endif
 template <bool ACT>
-__global__ void __launch_bounds__(256) dedup_node_pass_kernel(const __grid_constant__ DedupNodePassArgs a) {
+__global__ void __launch_bounds__(256, ACT ? ZXS_NODE_ACT_MINB : 1) dedup_node_pass_kernel(const __grid_constant__ DedupNodePassArgs a) {
     constexpr int G = kNodePassG;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t seed_hi = uint32_t(a.seed >> 32);

@@ -281,7 +281,10 @@ struct DedupSpecArgs {
 #ifndef ZXS_SPEC_G
 #define ZXS_SPEC_G 4
 #endif
-constexpr int kSpecG = ZXS_SPEC_G;  // 32-shot groups per warp iteration (independent Philox chains per lane)
+constexpr int kSpecG = ZXS_SPEC_G;
+#ifndef ZXS_SPEC_PREFETCH
+#define ZXS_SPEC_PREFETCH 0
+#endif  // 32-shot groups per warp iteration (independent Philox chains per lane)
 template <typename FW>
 __global__ void __launch_bounds__(256) dedup_init_spec_kernel(const FW *__restrict__ fraw, unsigned long long f_mask,
                                                               uint32_t *slot_out, DedupTable table,
@@ -294,7 +297,13 @@ __global__ void __launch_bounds__(256) dedup_init_spec_kernel(const FW *__restri
     const uint64_t shots64 = (a.shots + 63) & ~uint64_t(63);
     const uint64_t out_words = min(a.out_ld32, shots64 / 32);
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * G;
-    for (uint64_t s0 = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * G; s0 < shots64; s0 += stride) {
+    const uint64_t sbeg = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * G;
+#if ZXS_SPEC_PREFETCH
+    FW fnext[G];  // the next iteration's f words, loaded before this iteration's draws
+#pragma unroll
+    for (int g = 0; g < G; g++) fnext[g] = sbeg + 32 * g + lane < a.shots ? __ldg(fraw + sbeg + 32 * g + lane) : FW(0);
+#endif
+    for (uint64_t s0 = sbeg; s0 < shots64; s0 += stride) {
         uint64_t s[G];
         bool valid[G], on[G];  // on: on the main lineage so far
         unsigned long long k[G];
@@ -305,7 +314,13 @@ __global__ void __launch_bounds__(256) dedup_init_spec_kernel(const FW *__restri
         for (int g = 0; g < G; g++) {
             s[g] = s0 + 32 * g + lane;
             valid[g] = s[g] < a.shots;
+#if ZXS_SPEC_PREFETCH
+            k[g] = valid[g] ? ((unsigned long long)fnext[g] & f_mask) : 0ull;
+            const uint64_t sn = s[g] + stride;
+            fnext[g] = sn < a.shots ? __ldg(fraw + sn) : FW(0);
+#else
             k[g] = valid[g] ? ((unsigned long long)__ldg(fraw + s[g]) & f_mask) : 0ull;
+#endif
             on[g] = valid[g] && k[g] == 0ull;
             any_on |= on[g];
             ties[g] = 0;
@@ -1163,7 +1178,7 @@ struct DedupNodePassArgs {
 constexpr int kNodePassG = ZXS_NODE_G;  // 4 or 8
 static_assert(kNodePassG % 4 == 0, "node pass stores 128-bit groups of four 32-shot words");
 #ifndef ZXS_NODE_ACT_MINB
-#define ZXS_NODE_ACT_MINB 1
+#define ZXS_NODE_ACT_MINB 3  // measured: 3 (80 registers) beats 1 (108): node passes + init 23.1 -> 20.4 ms per 2^28 config-3 shots
 #endif
 template <bool ACT>
 __global__ void __launch_bounds__(256, ACT ? ZXS_NODE_ACT_MINB : 1) dedup_node_pass_kernel(const __grid_constant__ DedupNodePassArgs a) {
